@@ -1,0 +1,143 @@
+/*
+ * pmg_b200.h -- C-ABI of libpmg_b200.so, the B200 (sm_100a) V-cycle / FMG
+ * hot path of the level-set geometric multigrid Poisson solver
+ * (arXiv 2205.09411; reference C++ implementation "poissonmg").
+ *
+ * Plain pointers and sizes only; no C++ or torch types.  Every entry point
+ * returns a pmg_status (include/pmg_types.h); pmg_b200_last_error() holds the
+ * message, which for solver failures is the reference's exception text.
+ *
+ * Conventions follow the reference exactly: 1-based levels, block ids in the
+ * caller's mesh order, dir = 2*axis + side (core.hpp:79-83), padded field
+ * slices of (N+2)^D doubles with lin(i) = sum_k (i_k+1)(N+2)^k
+ * (mesh.hpp:128-137), interior slices of N^D doubles x-fastest.
+ *
+ * Each function cites the reference interface it replaces.  A maintainer binds
+ * these from the reference's C++ through include/pmg_b200/solver.hpp (a
+ * header-only pmg::b200::MgSolver<D> with MgSolver's exact public surface) and
+ * from Python through paper_2205_09411_b200/_lib.py (ctypes); see INTEGRATION.md.
+ */
+#ifndef PMG_B200_H
+#define PMG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "pmg_types.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pmg_b200_ctx pmg_b200_ctx;
+
+/* Field layouts for upload/download. */
+enum pmg_layout {
+  PMG_LAYOUT_PADDED = 0,   /* (N+2)^D per block, Block::data var slice (mesh.hpp:47,118-125) */
+  PMG_LAYOUT_INTERIOR = 1  /* N^D per block, x fastest (for_box order, core.hpp:85-97) */
+};
+
+/* ---- context ------------------------------------------------------------ */
+/* replaces: TreeMesh<Dim>::TreeMesh(lo, hi, block_size) (mesh.hpp:66-82) for the
+ * parts the solver reads; binds CUDA device `device`. Returns NULL only on OOM;
+ * check pmg_b200_last_error(ctx) for argument errors. */
+pmg_b200_ctx* pmg_b200_create(int dim, int N, const double* lo, const double* hi, int device);
+void pmg_b200_destroy(pmg_b200_ctx* ctx);
+const char* pmg_b200_last_error(pmg_b200_ctx* ctx);
+/* cudaStream_t the context launches on (for events / interop) */
+void* pmg_b200_stream(pmg_b200_ctx* ctx);
+
+/* ---- mesh ----------------------------------------------------------------- */
+/* replaces: the Block table of TreeMesh (mesh.hpp:37-55) + rebuild_topology
+ * neighbour tables (mesh.hpp:429-469).  Arrays are indexed by block id:
+ * level[nb], coords[nb*3], origin[nb*3], dx[nb], parent[nb], children[nb*8],
+ * nbr[nb*6], cnbr[nb*6] (trailing unused entries ignored). */
+int pmg_b200_set_mesh(pmg_b200_ctx* ctx, int n_blocks, const int32_t* level,
+                      const int32_t* coords, const double* origin, const double* dx,
+                      const int32_t* parent, const int32_t* children, const int32_t* nbr,
+                      const int32_t* cnbr);
+/* replaces: TreeMesh::face_bc[dir] (mesh.hpp:148, FaceBc mesh.hpp:22-32).
+ * values: NULL (value 0) or, for every block with a physical face `dir`
+ * (nbr == cnbr == -1) in increasing block id, N^(D-1) values bc(x_f) at the
+ * face centres x_f = cell_center(b, i1) + 0.5 dx sign(dir) e_axis
+ * (mesh.hpp:540-550), transverse index lower axis fastest. */
+int pmg_b200_set_face_bc(pmg_b200_ctx* ctx, int dir, int type, const double* values);
+
+/* ---- stencils ------------------------------------------------------------- */
+/* replaces: StencilSet<Dim> (stencil.hpp:196-205) handed to MgSolver's ctor.
+ * boundary[nb], row_count[nb]; row_of[nb*N^D] (entries of non-boundary blocks
+ * ignored); rows concatenated in block-id order as SoA:
+ * center[R], nb[R*2D], bc[R*2D], d[R*2D], obj[R*2D], mask[R], pin_obj[R], lin[R];
+ * phi_b[n_obj] = BoundaryValues::phi_b (stencil.hpp:12-18). */
+int pmg_b200_set_stencils(pmg_b200_ctx* ctx, const int32_t* boundary, const int32_t* row_count,
+                          const int32_t* row_of, const double* center, const double* nb,
+                          const double* bc, const double* d, const int8_t* obj,
+                          const uint8_t* mask, const int8_t* pin_obj, const int32_t* lin,
+                          int n_obj, const double* phi_b);
+/* replaces: build_stencils(mesh, lsf, cfg) (stencil.hpp:207-222) -- runs on the
+ * GPU (level-set line searches + thin-object rescue, levelset.hpp:151-382). */
+int pmg_b200_build_stencils(pmg_b200_ctx* ctx, const pmg_lsf_t* lsf, int n_lsf,
+                            const pmg_stencil_cfg_t* cfg);
+/* read back the current StencilSet; summary returns total rows R (>= 0) */
+int pmg_b200_stencil_summary(pmg_b200_ctx* ctx, int32_t* boundary, int32_t* row_count);
+int pmg_b200_get_stencils(pmg_b200_ctx* ctx, int32_t* row_of, double* center, double* nb,
+                          double* bc, double* d, int8_t* obj, uint8_t* mask, int8_t* pin_obj,
+                          int32_t* lin);
+/* replaces: StencilSet::set_boundary_value (stencil.hpp:201-204) */
+int pmg_b200_set_boundary_value(pmg_b200_ctx* ctx, int obj, double value);
+
+/* ---- fields --------------------------------------------------------------- */
+/* replaces: writes/reads through TreeMesh::field(id, var) (mesh.hpp:118-125).
+ * All blocks, block-id order.  Ghost values on download are the filled ghosts
+ * (PHI, OLD); other vars report 0 in ghost slots. */
+int pmg_b200_upload_field(pmg_b200_ctx* ctx, int var, const double* host, int layout);
+int pmg_b200_download_field(pmg_b200_ctx* ctx, int var, double* host, int layout);
+/* one level only, blocks in TreeMesh::level_blocks(level) order (mesh.hpp:101-105) */
+int pmg_b200_upload_level_field(pmg_b200_ctx* ctx, int var, int level, const double* host,
+                                int layout);
+int pmg_b200_download_level_field(pmg_b200_ctx* ctx, int var, int level, double* host,
+                                  int layout);
+
+/* ---- solver (MgSolver<Dim>, multigrid.hpp:292-792) ------------------------ */
+/* replaces: MgSolver(mesh, stencils, cfg) -- cfg.validate() then init() (:295-299) */
+int pmg_b200_solver_create(pmg_b200_ctx* ctx, const pmg_mg_cfg_t* cfg);
+/* replaces: MgSolver::init (:304-311) */
+int pmg_b200_init(pmg_b200_ctx* ctx);
+/* replaces: v_cycle (:318-323), fmg_cycle (:325-350), measure_residual (:353-360) */
+int pmg_b200_v_cycle(pmg_b200_ctx* ctx, pmg_cycle_stats_t* out);
+int pmg_b200_fmg_cycle(pmg_b200_ctx* ctx, pmg_cycle_stats_t* out);
+int pmg_b200_measure_residual(pmg_b200_ctx* ctx, pmg_cycle_stats_t* out);
+/* asynchronous variants: enqueue on pmg_b200_stream(); pmg_b200_cycle_result
+ * waits and returns the stats (and the coarse-solve status) of the last one */
+int pmg_b200_v_cycle_async(pmg_b200_ctx* ctx);
+int pmg_b200_fmg_cycle_async(pmg_b200_ctx* ctx);
+int pmg_b200_cycle_result(pmg_b200_ctx* ctx, pmg_cycle_stats_t* out);
+/* op-level API (public MgSolver members) */
+int pmg_b200_gsrb_sweep(pmg_b200_ctx* ctx, int level, int parity);       /* :365-370 */
+int pmg_b200_fill_ghosts(pmg_b200_ctx* ctx, int level, int var);          /* mesh.hpp:217-221 (ghosts are always current: no-op) */
+int pmg_b200_apply_pins(pmg_b200_ctx* ctx, int level);                     /* stencil.hpp:225-237 */
+int pmg_b200_residual_level(pmg_b200_ctx* ctx, int level);                 /* :510-517 -> VAR_RES */
+int pmg_b200_restrict_level(pmg_b200_ctx* ctx, int level);                 /* :374-398 (residual fused) */
+int pmg_b200_restrict_level_no_guess(pmg_b200_ctx* ctx, int level);        /* :403-418 */
+int pmg_b200_prolong_correction(pmg_b200_ctx* ctx, int level);             /* :422-428 */
+int pmg_b200_prolong_full(pmg_b200_ctx* ctx, int level);                   /* :432-438 */
+int pmg_b200_coarse_solve(pmg_b200_ctx* ctx);                              /* :442-472 */
+int pmg_b200_set_have_guess(pmg_b200_ctx* ctx, int v);                     /* :480 */
+/* replaces: coarse_system() (:474) -- CoarseSystem (:41-57) of level 1 */
+int pmg_b200_coarse_sizes(pmg_b200_ctx* ctx, int32_t* n, int32_t* nnz, int32_t* n_obj);
+int pmg_b200_coarse_get(pmg_b200_ctx* ctx, int32_t* rp, int32_t* ci, double* val, double* c0,
+                        double* cobj, int32_t* unk_block, int32_t* unk_lin);
+
+/* ---- introspection -------------------------------------------------------- */
+/* kernels launched by one cycle of the given kind (0 = V, 1 = FMG, 2 = measure) */
+int pmg_b200_cycle_kernel_count(pmg_b200_ctx* ctx, int kind);
+/* number of refinement levels and blocks per level (after set_mesh) */
+int pmg_b200_n_levels(pmg_b200_ctx* ctx);
+int pmg_b200_level_size(pmg_b200_ctx* ctx, int level);
+int pmg_b200_synchronize(pmg_b200_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PMG_B200_H */

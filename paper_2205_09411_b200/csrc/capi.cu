@@ -1,0 +1,1021 @@
+// capi.cu -- host orchestration of the B200 multigrid hot path and the C-ABI
+// (include/pmg_b200.h).
+//
+// The cycle structure is MgSolver's (multigrid.hpp:318-350, 483-508); each
+// reference phase maps to one or more kernels (see kernels.cuh) and every
+// cycle type is captured once into a CUDA graph and replayed.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+
+#include "ctx.h"
+
+using namespace pmghost;
+using pmgdev::LevelView;
+
+struct pmg_b200_ctx {
+  Ctx c;
+};
+
+namespace pmghost {
+
+Ctx::~Ctx() {
+  g_v.reset();
+  g_fmg[0].reset();
+  g_fmg[1].reset();
+  g_measure.reset();
+  if (h_out) cudaFreeHost(h_out);
+  if (h_status) cudaFreeHost(h_status);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+static void require(bool cond, const std::string& msg, int code = PMG_ERR_INVALID_ARG) {
+  if (!cond) throw PmgError(code, msg);
+}
+
+static uint64_t morton(const int32_t* c, int dim) {
+  uint64_t m = 0;
+  for (int b = 0; b < 21; ++b)
+    for (int k = 0; k < dim; ++k) m |= (uint64_t)((c[k] >> b) & 1) << (b * dim + k);
+  return m;
+}
+
+static void set_views(Ctx& c) {
+  for (int l = 1; l <= c.mesh.L; ++l) {
+    LevelDev& d = *c.lev[(size_t)l];
+    LevelView& v = d.view;
+    v.nb = d.nb;
+    v.level = l;
+    const double dx = c.mesh.dx[(size_t)c.mesh.slots[(size_t)l][0]];
+    v.dx = dx;
+    v.h2 = dx * dx;
+    v.w = 1.0 / (dx * dx);
+    v.nbr = d.nbr.p;
+    v.cnbr = d.cnbr.p;
+    v.coords = d.coords.p;
+    v.parent = d.parent.p;
+    v.child = d.child.p;
+    v.leaf = d.leaf.p;
+    v.kind = d.kind.p;
+    v.srow = d.srow.p;
+    v.bcoff = d.bcoff.p;
+    v.bcval = d.bcval.p;
+    v.phi = d.phi.p;
+    v.rhs = d.rhs.p;
+    v.old = d.old.p;
+    v.res = d.res.p;
+    v.row_of = d.row_of.p;
+    v.r_center = d.r_center.p;
+    v.r_nb = d.r_nb.p;
+    v.r_bc = d.r_bc.p;
+    v.r_obj = d.r_obj.p;
+    v.r_mask = d.r_mask.p;
+    v.r_pin = d.r_pin.p;
+    v.cfold = d.cfold.p;
+    v.cfoff = d.has_cfold ? d.cfoff.p : nullptr;
+    for (int k = 0; k < 6; ++k) v.bctype[k] = c.bctype[k];
+  }
+}
+
+static void invalidate_graphs(Ctx& c) {
+  c.g_v.reset();
+  c.g_fmg[0].reset();
+  c.g_fmg[1].reset();
+  c.g_measure.reset();
+}
+
+// colour-split entry address of interior cell ii (x-fastest) within a block
+static inline int cs_addr(int ii, int N, int dim, int H) {
+  const int i = ii % N, j = (ii / N) % N, k = dim == 3 ? ii / (N * N) : 0;
+  return ((i + j + k) & 1) * H + (ii >> 1);
+}
+
+static void upload_bc(Ctx& c) {
+  const HostMesh& m = c.mesh;
+  for (int l = 1; l <= m.L; ++l) {
+    LevelDev& d = *c.lev[(size_t)l];
+    std::vector<int32_t> off((size_t)d.nb * c.F, -1);
+    std::vector<double> vals;
+    for (int s = 0; s < d.nb; ++s) {
+      const int id = m.slots[(size_t)l][(size_t)s];
+      for (int f = 0; f < c.F; ++f) {
+        const int32_t o = c.face_off[f].empty() ? -1 : c.face_off[f][(size_t)id];
+        if (o < 0) continue;
+        off[(size_t)s * c.F + f] = (int32_t)vals.size();
+        vals.insert(vals.end(), c.face_vals[f].begin() + o, c.face_vals[f].begin() + o + c.NT);
+      }
+    }
+    d.bcoff.upload(off, c.stream);
+    d.bcval.upload(vals, c.stream);
+  }
+}
+
+static void upload_stencils(Ctx& c) {
+  const HostMesh& m = c.mesh;
+  const HostStencils& st = c.st;
+  const int NI = c.NI, H = NI / 2, F = c.F;
+  for (int l = 1; l <= m.L; ++l) {
+    LevelDev& d = *c.lev[(size_t)l];
+    std::vector<int32_t> srow((size_t)d.nb, -1), row_of;
+    std::vector<uint8_t> kind((size_t)d.nb, pmgdev::KIND_UNIFORM), mask;
+    std::vector<double> center, nbv, bcv;
+    std::vector<int8_t> obj, pin;
+    int n_if = 0;
+    for (int s = 0; s < d.nb; ++s) {
+      const int id = m.slots[(size_t)l][(size_t)s];
+      if (!st.valid || !st.boundary[(size_t)id]) continue;
+      srow[(size_t)s] = n_if++;
+      const int base = (int)center.size();
+      const int r0 = st.row_start[(size_t)id];
+      const int rc = st.row_count[(size_t)id];
+      bool all_inside = true;
+      row_of.resize((size_t)n_if * NI, -1);
+      int32_t* page = row_of.data() + (size_t)(n_if - 1) * NI;
+      for (int ii = 0; ii < NI; ++ii) {
+        const int32_t r = st.row_of[(size_t)id * NI + ii];
+        require(r < rc, "stencil row_of entry out of range");
+        page[cs_addr(ii, c.N, c.dim, H)] = r < 0 ? -1 : base + r;
+        if (r < 0 || st.mask[(size_t)(r0 + r)] != PMG_INSIDE) all_inside = false;
+      }
+      for (int r = 0; r < rc; ++r) {
+        const size_t q = (size_t)(r0 + r);
+        center.push_back(st.center[q]);
+        mask.push_back(st.mask[q]);
+        pin.push_back(st.pin[q]);
+        for (int f = 0; f < F; ++f) {
+          nbv.push_back(st.nb[q * F + f]);
+          bcv.push_back(st.bc[q * F + f]);
+          obj.push_back(st.obj[q * F + f]);
+        }
+      }
+      kind[(size_t)s] = all_inside ? pmgdev::KIND_ALL_INSIDE : pmgdev::KIND_IFACE;
+    }
+    d.srow.upload(srow, c.stream);
+    d.kind.upload(kind, c.stream);
+    d.row_of.upload(row_of, c.stream);
+    d.r_center.upload(center, c.stream);
+    d.r_nb.upload(nbv, c.stream);
+    d.r_bc.upload(bcv, c.stream);
+    d.r_obj.upload(obj, c.stream);
+    d.r_mask.upload(mask, c.stream);
+    d.r_pin.upload(pin, c.stream);
+  }
+  std::vector<double> pb = st.phi_b;
+  if (pb.empty()) pb.push_back(0.0);
+  c.phi_b.upload(pb, c.stream);
+}
+
+static void default_stencils(Ctx& c) {
+  HostStencils& st = c.st;
+  st = HostStencils{};
+  st.valid = true;
+  st.boundary.assign((size_t)c.mesh.nb, 0);
+  st.row_count.assign((size_t)c.mesh.nb, 0);
+  st.row_start.assign((size_t)c.mesh.nb + 1, 0);
+  st.row_of.assign((size_t)c.mesh.nb * c.NI, -1);
+}
+
+// ---------------------------------------------------------------- coarse assembly
+// Restates assemble_level(mesh, set, 1) (multigrid.hpp:62-190) for the single
+// root block of level 1: unknowns = non-inside cells in x-fastest order,
+// physical faces folded into diag / c0, pinned neighbours and cut directions
+// into cobj, rows sorted by column.
+static void assemble_coarse(Ctx& c) {
+  const HostMesh& m = c.mesh;
+  const HostStencils& st = c.st;
+  const int N = c.N, D = c.dim, NI = c.NI, F = c.F, H = NI / 2;
+  const int id = m.slots[1][0];
+  const int n_obj = (int)st.phi_b.size();
+  HostCoarse& cs = c.coarse;
+  cs = HostCoarse{};
+  std::vector<int> unk((size_t)NI, -1);
+  const bool bnd = st.boundary[(size_t)id] != 0;
+  const int r0 = st.row_start[(size_t)id];
+  auto row_ptr = [&](int ii) -> int {
+    if (!bnd) return -1;
+    const int r = st.row_of[(size_t)id * NI + ii];
+    return r < 0 ? -1 : r0 + r;
+  };
+  auto inside = [&](int ii) {
+    const int r = row_ptr(ii);
+    return r >= 0 && st.mask[(size_t)r] == PMG_INSIDE;
+  };
+  const int s1 = N + 2;
+  auto lin = [&](int i, int j, int k) { return (i + 1) + (j + 1) * s1 + (D == 3 ? (k + 1) * s1 * s1 : 0); };
+  for (int ii = 0; ii < NI; ++ii) {
+    if (inside(ii)) continue;
+    unk[(size_t)ii] = cs.n++;
+    const int i = ii % N, j = (ii / N) % N, k = D == 3 ? ii / (N * N) : 0;
+    cs.unk_block.push_back(id);
+    cs.unk_lin.push_back(lin(i, j, k));
+    cs.uaddr.push_back(cs_addr(ii, N, D, H));  // slot 0
+  }
+  cs.c0.assign((size_t)cs.n, 0.0);
+  cs.cobj.assign((size_t)n_obj * cs.n, 0.0);
+  std::vector<std::vector<std::pair<int, double>>> rows((size_t)cs.n);
+  const double bdx = m.dx[(size_t)id];
+  const double w = 1.0 / (bdx * bdx);
+  for (int ii = 0; ii < NI; ++ii) {
+    const int row = unk[(size_t)ii];
+    if (row < 0) continue;
+    const int ic[3] = {ii % N, (ii / N) % N, D == 3 ? ii / (N * N) : 0};
+    double diag;
+    double an[6];
+    const int rp = row_ptr(ii);
+    if (rp >= 0) {
+      diag = st.center[(size_t)rp];
+      for (int f = 0; f < F; ++f) {
+        an[f] = st.nb[(size_t)rp * F + f];
+        const double b = st.bc[(size_t)rp * F + f];
+        if (b != 0) cs.cobj[(size_t)st.obj[(size_t)rp * F + f] * cs.n + row] -= b;
+      }
+    } else {
+      diag = -2.0 * D * w;
+      for (int f = 0; f < F; ++f) an[f] = w;
+    }
+    auto& r = rows[(size_t)row];
+    for (int f = 0; f < F; ++f) {
+      const double a = an[f];
+      if (a == 0) continue;
+      const int axis = f >> 1, sgn = (f & 1) ? 1 : -1;
+      int ni[3] = {ic[0], ic[1], ic[2]};
+      ni[axis] += sgn;
+      if (ni[axis] < 0 || ni[axis] >= N) {
+        // level 1 is the root block: every face is physical (mesh.hpp:455)
+        if (c.bctype[f] == PMG_BC_NEUMANN_ZERO) {
+          diag += a;
+        } else {
+          diag -= a;
+          double bcv = 0.0;
+          if (!c.face_off[f].empty() && c.face_off[f][(size_t)id] >= 0) {
+            int t;
+            if (D == 2) t = axis == 0 ? ic[1] : ic[0];
+            else t = axis == 0 ? ic[1] + N * ic[2] : (axis == 1 ? ic[0] + N * ic[2] : ic[0] + N * ic[1]);
+            bcv = c.face_vals[f][(size_t)c.face_off[f][(size_t)id] + t];
+          }
+          cs.c0[(size_t)row] -= 2.0 * a * bcv;
+        }
+        continue;
+      }
+      const int nii = ni[0] + N * (ni[1] + N * ni[2]);
+      const int col = unk[(size_t)nii];
+      if (col < 0) {
+        const int po = st.pin[(size_t)row_ptr(nii)];
+        cs.cobj[(size_t)po * cs.n + row] -= a;
+        continue;
+      }
+      r.emplace_back(col, a);
+    }
+    r.emplace_back(row, diag);
+  }
+  cs.rp.assign((size_t)cs.n + 1, 0);
+  for (int r = 0; r < cs.n; ++r) {
+    auto& row = rows[(size_t)r];
+    std::sort(row.begin(), row.end());
+    cs.rp[(size_t)r + 1] = cs.rp[(size_t)r] + (int)row.size();
+    for (auto& [col, v] : row) {
+      cs.ci.push_back(col);
+      cs.val.push_back(v);
+    }
+  }
+  // Jacobi preconditioner (multigrid.hpp:213-217)
+  cs.dinv.assign((size_t)cs.n, 1.0);
+  for (int r = 0; r < cs.n; ++r)
+    for (int q = cs.rp[(size_t)r]; q < cs.rp[(size_t)r + 1]; ++q)
+      if (cs.ci[(size_t)q] == r && cs.val[(size_t)q] != 0) cs.dinv[(size_t)r] = 1.0 / cs.val[(size_t)q];
+  c.c_rp.upload(cs.rp, c.stream);
+  c.c_ci.upload(cs.ci, c.stream);
+  c.c_val.upload(cs.val, c.stream);
+  c.c_dinv.upload(cs.dinv, c.stream);
+  c.c_c0.upload(cs.c0, c.stream);
+  c.c_cobj.upload(cs.cobj, c.stream);
+  c.c_uaddr.upload(cs.uaddr, c.stream);
+  c.c_scratch.alloc((size_t)10 * std::max(cs.n, 1));
+}
+
+// ---------------------------------------------------------------- cycle sequences
+static void enq_restrict_level(Ctx& c, int l) {
+  // residual_level(l) + restrict_level(l): fused unless level l has
+  // coarse-fine faces (their ghosts read level l-1 cells being restricted)
+  if (c.lev[(size_t)l]->has_cf) {
+    c.ops->residual(c, l);
+    c.ops->restrict_(c, l, pmgdev::RM_RES);
+  } else {
+    c.ops->restrict_(c, l, pmgdev::RM_FUSED);
+  }
+  c.ops->fas(c, l - 1, true);
+  if (c.lev[(size_t)(l - 1)]->has_cfold) c.ops->cfold(c, l - 1);
+}
+static void enq_restrict_level_no_guess(Ctx& c, int l) {
+  c.ops->restrict_(c, l, pmgdev::RM_RHS);
+  c.ops->fas(c, l - 1, false);
+  if (c.lev[(size_t)(l - 1)]->has_cfold) c.ops->cfold(c, l - 1);
+}
+static void enq_smooth(Ctx& c, int l, int steps) {
+  for (int s = 0; s < steps; ++s) {
+    c.ops->gs(c, l, 0);
+    c.ops->gs(c, l, 1);
+  }
+}
+static void enq_coarse(Ctx& c) { c.ops->coarse(c); }
+static void enq_v_span(Ctx& c, int top) {
+  if (top == 1) {
+    enq_coarse(c);
+    return;
+  }
+  for (int l = top; l >= 2; --l) {
+    enq_smooth(c, l, c.cfg.n_down);
+    enq_restrict_level(c, l);
+  }
+  enq_coarse(c);
+  for (int l = 2; l <= top; ++l) {
+    c.ops->prolong(c, l, false);
+    enq_smooth(c, l, c.cfg.n_up);
+    c.ops->record(c, l);
+  }
+}
+static void enq_reset_records(Ctx& c) {
+  PMG_CUDA(cudaMemsetAsync(c.rec.p, 0, c.rec.n * sizeof(pmgdev::Rec), c.stream));
+}
+static void enq_finish(Ctx& c) {
+  pmgdev::k_combine<<<1, 32, 0, c.stream>>>(c.rec.p, c.mesh.L, c.stats.p);
+  PMG_CUDA(cudaGetLastError());
+  PMG_CUDA(cudaMemcpyAsync(c.h_out, c.stats.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  PMG_CUDA(cudaMemcpyAsync(c.h_out + 2, c.diag.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  PMG_CUDA(cudaMemcpyAsync(c.h_status, c.status.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+}
+static void enq_clear_status(Ctx& c) {
+  PMG_CUDA(cudaMemsetAsync(c.status.p, 0, sizeof(int), c.stream));
+}
+
+enum CycleKind { CK_V = 0, CK_FMG_NOGUESS = 1, CK_FMG_GUESS = 2, CK_MEASURE = 3 };
+
+static void enq_cycle(Ctx& c, int kind) {
+  const int L = c.mesh.L;
+  enq_clear_status(c);
+  enq_reset_records(c);
+  if (kind == CK_V) {
+    enq_v_span(c, L);
+  } else if (kind == CK_MEASURE) {
+    for (int l = 1; l <= L; ++l) c.ops->record(c, l);
+  } else {
+    const bool guess = kind == CK_FMG_GUESS;
+    for (int l = L; l >= 2; --l) {
+      if (guess) enq_restrict_level(c, l);
+      else enq_restrict_level_no_guess(c, l);
+    }
+    enq_coarse(c);
+    for (int l = 2; l <= L; ++l) {
+      c.ops->prolong(c, l, !guess);
+      enq_v_span(c, l);
+    }
+  }
+  enq_finish(c);
+}
+
+static Graph& graph_for(Ctx& c, int kind) {
+  Graph& g = kind == CK_V ? c.g_v : kind == CK_MEASURE ? c.g_measure : c.g_fmg[kind == CK_FMG_GUESS];
+  if (g.exec) return g;
+  cudaGraph_t graph;
+  PMG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    enq_cycle(c, kind);
+  } catch (...) {
+    cudaStreamEndCapture(c.stream, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    throw;
+  }
+  PMG_CUDA(cudaStreamEndCapture(c.stream, &graph));
+  size_t nn = 0;
+  PMG_CUDA(cudaGraphGetNodes(graph, nullptr, &nn));
+  std::vector<cudaGraphNode_t> nodes(nn);
+  PMG_CUDA(cudaGraphGetNodes(graph, nodes.data(), &nn));
+  int kernels = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType t;
+    PMG_CUDA(cudaGraphNodeGetType(nd, &t));
+    if (t == cudaGraphNodeTypeKernel) ++kernels;
+  }
+  PMG_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
+  cudaGraphDestroy(graph);
+  g.kernels = kernels;
+  return g;
+}
+
+static void launch_cycle(Ctx& c, int kind) {
+  require(c.solver, "solver not created (call pmg_b200_solver_create)", PMG_ERR_STATE);
+  Graph& g = graph_for(c, kind);
+  PMG_CUDA(cudaGraphLaunch(g.exec, c.stream));
+  if (kind != CK_MEASURE) c.have_guess = true;
+}
+
+static void cycle_result(Ctx& c, pmg_cycle_stats_t* out) {
+  PMG_CUDA(cudaStreamSynchronize(c.stream));
+  const int st = *c.h_status;
+  if (st == 3) {
+    char buf[64];
+    const std::string rel = std::to_string(c.h_out[2]);
+    (void)buf;
+    throw PmgError(PMG_ERR_COARSE_STALL,
+                   "coarse solve failed: BiCGStab stalled at relative residual " + rel +
+                       " after " + std::to_string((int)c.h_out[3]) + " iterations on " +
+                       std::to_string(c.coarse.n) + " unknowns");
+  }
+  if (st == 4) throw PmgError(PMG_ERR_COARSE_STALL, "coarse solve failed: smoothing fallback stalled");
+  if (out) {
+    out->max_resid = c.h_out[0];
+    out->l2_resid = c.h_out[1];
+  }
+}
+
+static void do_init(Ctx& c) {
+  for (int l = 1; l <= c.mesh.L; ++l) c.ops->pins(c, l);
+  assemble_coarse(c);
+  enq_reset_records(c);
+  c.have_guess = false;
+  invalidate_graphs(c);
+  PMG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+static void need_mesh(Ctx& c) { require(c.have_mesh, "mesh not set (call pmg_b200_set_mesh)", PMG_ERR_STATE); }
+static void need_level(Ctx& c, int l, int lo = 1) {
+  need_mesh(c);
+  require(l >= lo && l <= c.mesh.L, "level out of range");
+}
+
+static void set_mesh(Ctx& c, int nb, const int32_t* level, const int32_t* coords,
+                     const double* origin, const double* dx, const int32_t* parent,
+                     const int32_t* children, const int32_t* nbr, const int32_t* cnbr) {
+  require(nb >= 1, "mesh needs at least one block");
+  HostMesh& m = c.mesh;
+  m = HostMesh{};
+  m.nb = nb;
+  m.level.assign(level, level + nb);
+  m.coords.assign(coords, coords + (size_t)nb * 3);
+  m.origin.assign(origin, origin + (size_t)nb * 3);
+  m.dx.assign(dx, dx + nb);
+  m.parent.assign(parent, parent + nb);
+  m.children.assign(children, children + (size_t)nb * 8);
+  m.nbr.assign(nbr, nbr + (size_t)nb * 6);
+  m.cnbr.assign(cnbr, cnbr + (size_t)nb * 6);
+  m.L = *std::max_element(m.level.begin(), m.level.end());
+  require(m.L < pmgdev::kMaxLevels, "too many levels");
+  m.slots.assign((size_t)m.L + 1, {});
+  m.ref_order.assign((size_t)m.L + 1, {});
+  m.slot_of.assign((size_t)nb, -1);
+  for (int id = 0; id < nb; ++id) {
+    require(m.level[(size_t)id] >= 1, "block level must be >= 1");
+    m.slots[(size_t)m.level[(size_t)id]].push_back(id);
+  }
+  require(m.slots[1].size() == 1, "level 1 must hold exactly the root block");
+  const int D = c.dim;
+  for (int l = 1; l <= m.L; ++l) {
+    auto& v = m.slots[(size_t)l];
+    require(!v.empty(), "every level 1..L must hold blocks");
+    m.ref_order[(size_t)l] = v;
+    std::sort(m.ref_order[(size_t)l].begin(), m.ref_order[(size_t)l].end(), [&](int a, int b) {
+      for (int k = 0; k < D; ++k)
+        if (m.coords[(size_t)a * 3 + k] != m.coords[(size_t)b * 3 + k])
+          return m.coords[(size_t)a * 3 + k] < m.coords[(size_t)b * 3 + k];
+      return false;
+    });
+    std::stable_sort(v.begin(), v.end(), [&](int a, int b) {
+      return morton(&m.coords[(size_t)a * 3], D) < morton(&m.coords[(size_t)b * 3], D);
+    });
+    for (size_t s = 0; s < v.size(); ++s) m.slot_of[(size_t)v[s]] = (int)s;
+    for (int id : v)
+      require(m.dx[(size_t)id] == m.dx[(size_t)v[0]], "blocks of one level must share dx");
+  }
+  // topology per level, in slot order
+  c.lev.clear();
+  c.lev.resize((size_t)m.L + 1);
+  const int F = c.F, NC = 1 << D;
+  for (int l = 1; l <= m.L; ++l) {
+    c.lev[(size_t)l] = std::make_unique<LevelDev>();
+    LevelDev& d = *c.lev[(size_t)l];
+    const auto& v = m.slots[(size_t)l];
+    d.nb = (int)v.size();
+    std::vector<int32_t> nbrs((size_t)d.nb * F), cnbrs((size_t)d.nb * F), crd((size_t)d.nb * D),
+        par((size_t)d.nb), chl((size_t)d.nb * NC), sid((size_t)d.nb), rpos((size_t)d.nb),
+        cfoff((size_t)d.nb * F, -1);
+    std::vector<uint8_t> leaf((size_t)d.nb);
+    for (size_t s = 0; s < v.size(); ++s) {
+      const int id = v[s];
+      sid[s] = id;
+      for (int k = 0; k < D; ++k) crd[s * D + k] = m.coords[(size_t)id * 3 + k];
+      const int p = m.parent[(size_t)id];
+      require(l == 1 ? p < 0 : (p >= 0 && m.level[(size_t)p] == l - 1), "bad parent link");
+      par[s] = p < 0 ? -1 : m.slot_of[(size_t)p];
+      bool lf = true;
+      for (int ch = 0; ch < NC; ++ch) {
+        const int cid = m.children[(size_t)id * 8 + ch];
+        chl[s * NC + ch] = cid < 0 ? -1 : m.slot_of[(size_t)cid];
+        if (ch == 0) lf = cid < 0;
+      }
+      leaf[s] = lf ? 1 : 0;
+      for (int f = 0; f < F; ++f) {
+        const int nid = m.nbr[(size_t)id * 6 + f];
+        const int cid = m.cnbr[(size_t)id * 6 + f];
+        nbrs[s * F + f] = nid < 0 ? -1 : m.slot_of[(size_t)nid];
+        cnbrs[s * F + f] = -1;
+        if (nid >= 0) require(m.level[(size_t)nid] == l, "nbr must be on the same level", PMG_ERR_TOPOLOGY);
+        if (nid < 0 && cid >= 0) {
+          require(m.level[(size_t)cid] == l - 1, "coarse nbr must be one level up", PMG_ERR_TOPOLOGY);
+          cnbrs[s * F + f] = m.slot_of[(size_t)cid];
+          d.has_cf = true;
+          // transverse faces of the coarse neighbour must not be coarse-fine
+          // (2:1 corner balance, mesh.hpp:252-290)
+          for (int g = 0; g < F; ++g) {
+            if ((g >> 1) == (f >> 1)) continue;
+            require(!(m.nbr[(size_t)cid * 6 + g] < 0 && m.cnbr[(size_t)cid * 6 + g] >= 0),
+                    "mesh is not 2:1 corner balanced at a coarse-fine face", PMG_ERR_TOPOLOGY);
+          }
+        }
+      }
+    }
+    const auto& ro = m.ref_order[(size_t)l];
+    for (size_t q = 0; q < ro.size(); ++q) rpos[(size_t)m.slot_of[(size_t)ro[q]]] = (int32_t)q;
+    d.nbr.upload(nbrs, c.stream);
+    d.cnbr.upload(cnbrs, c.stream);
+    d.coords.upload(crd, c.stream);
+    d.parent.upload(par, c.stream);
+    d.child.upload(chl, c.stream);
+    d.leaf.upload(leaf, c.stream);
+    d.slot_id.upload(sid, c.stream);
+    d.ref_slot.upload(rpos, c.stream);
+    const size_t cells = (size_t)d.nb * c.NI;
+    d.phi.alloc(cells);
+    d.rhs.alloc(cells);
+    d.old.alloc(cells);
+    d.res.alloc(cells);
+    PMG_CUDA(cudaMemsetAsync(d.phi.p, 0, cells * 8, c.stream));
+    PMG_CUDA(cudaMemsetAsync(d.rhs.p, 0, cells * 8, c.stream));
+    PMG_CUDA(cudaMemsetAsync(d.old.p, 0, cells * 8, c.stream));
+    PMG_CUDA(cudaMemsetAsync(d.res.p, 0, cells * 8, c.stream));
+  }
+  // VAR_OLD coarse-fine ghost tables: needed on level l-1 blocks that are
+  // parents of level-l blocks and have a coarse-fine face
+  for (int l = 1; l <= m.L; ++l) {
+    LevelDev& d = *c.lev[(size_t)l];
+    std::vector<int32_t> cfo((size_t)d.nb * F, -1);
+    int n = 0;
+    for (int s = 0; s < d.nb; ++s) {
+      const int id = m.slots[(size_t)l][(size_t)s];
+      for (int f = 0; f < F; ++f)
+        if (m.nbr[(size_t)id * 6 + f] < 0 && m.cnbr[(size_t)id * 6 + f] >= 0) {
+          cfo[(size_t)s * F + f] = n;
+          n += c.NT;
+        }
+    }
+    d.has_cfold = n > 0;
+    d.cfoff.upload(cfo, c.stream);
+    d.cfold.alloc((size_t)std::max(n, 1));
+  }
+  for (int f = 0; f < 6; ++f) {
+    c.face_vals[f].clear();
+    c.face_off[f].clear();
+  }
+  int maxnb = 0;
+  for (int l = 1; l <= m.L; ++l) maxnb = std::max(maxnb, c.lev[(size_t)l]->nb);
+  c.partial.alloc((size_t)maxnb);
+  c.rec.alloc(pmgdev::kMaxLevels + 1);
+  c.counter.alloc(1);
+  PMG_CUDA(cudaMemsetAsync(c.counter.p, 0, sizeof(unsigned), c.stream));
+  c.stats.alloc(2);
+  c.status.alloc(1);
+  c.diag.alloc(2);
+  c.have_mesh = true;
+  c.solver = false;
+  default_stencils(c);
+  upload_bc(c);
+  upload_stencils(c);
+  set_views(c);
+  invalidate_graphs(c);
+  PMG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+static void set_face_bc(Ctx& c, int dir, int type, const double* values) {
+  need_mesh(c);
+  require(dir >= 0 && dir < c.F, "face direction out of range");
+  require(type == PMG_BC_DIRICHLET || type == PMG_BC_NEUMANN_ZERO, "bad face bc type");
+  c.bctype[dir] = type;
+  c.face_vals[dir].clear();
+  c.face_off[dir].assign((size_t)c.mesh.nb, -1);
+  if (values) {
+    size_t q = 0;
+    for (int id = 0; id < c.mesh.nb; ++id) {
+      if (c.mesh.nbr[(size_t)id * 6 + dir] >= 0 || c.mesh.cnbr[(size_t)id * 6 + dir] >= 0) continue;
+      c.face_off[dir][(size_t)id] = (int32_t)c.face_vals[dir].size();
+      c.face_vals[dir].insert(c.face_vals[dir].end(), values + q, values + q + c.NT);
+      q += (size_t)c.NT;
+    }
+  }
+  upload_bc(c);
+  set_views(c);
+  invalidate_graphs(c);
+  PMG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+static double* staging(Ctx& c, size_t n) {
+  if (c.staging.n < n) c.staging.alloc(n);
+  return c.staging.p;
+}
+
+static double* var_ptr(LevelDev& d, int var) {
+  switch (var) {
+    case PMG_VAR_PHI: return d.phi.p;
+    case PMG_VAR_RHS: return d.rhs.p;
+    case PMG_VAR_RES: return d.res.p;
+    case PMG_VAR_OLD: return d.old.p;
+    default: throw PmgError(PMG_ERR_INVALID_ARG, "unsupported field variable");
+  }
+}
+
+static void upload_field(Ctx& c, int var, int level, const double* host, int layout) {
+  need_mesh(c);
+  require(layout == PMG_LAYOUT_PADDED || layout == PMG_LAYOUT_INTERIOR, "bad layout");
+  const size_t per = layout == PMG_LAYOUT_PADDED ? (size_t)c.S : (size_t)c.NI;
+  const size_t nblk = level > 0 ? (size_t)c.lev[(size_t)level]->nb : (size_t)c.mesh.nb;
+  double* stg = staging(c, nblk * per);
+  PMG_CUDA(cudaMemcpyAsync(stg, host, nblk * per * 8, cudaMemcpyHostToDevice, c.stream));
+  for (int l = 1; l <= c.mesh.L; ++l) {
+    if (level > 0 && l != level) continue;
+    LevelDev& d = *c.lev[(size_t)l];
+    c.ops->scatter(c, l, var_ptr(d, var), stg, level > 0 ? d.ref_slot.p : d.slot_id.p, layout);
+  }
+}
+
+static void download_field(Ctx& c, int var, int level, double* host, int layout) {
+  need_mesh(c);
+  require(layout == PMG_LAYOUT_PADDED || layout == PMG_LAYOUT_INTERIOR, "bad layout");
+  require(var >= 0 && var <= 3, "unsupported field variable");
+  const size_t per = layout == PMG_LAYOUT_PADDED ? (size_t)c.S : (size_t)c.NI;
+  const size_t nblk = level > 0 ? (size_t)c.lev[(size_t)level]->nb : (size_t)c.mesh.nb;
+  double* stg = staging(c, nblk * per);
+  for (int l = 1; l <= c.mesh.L; ++l) {
+    if (level > 0 && l != level) continue;
+    LevelDev& d = *c.lev[(size_t)l];
+    c.ops->gather(c, l, var, stg, level > 0 ? d.ref_slot.p : d.slot_id.p, layout);
+  }
+  PMG_CUDA(cudaMemcpyAsync(host, stg, nblk * per * 8, cudaMemcpyDeviceToHost, c.stream));
+  PMG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+static void set_stencils(Ctx& c, const int32_t* boundary, const int32_t* row_count,
+                         const int32_t* row_of, const double* center, const double* nb,
+                         const double* bc, const double* d, const int8_t* obj,
+                         const uint8_t* mask, const int8_t* pin, const int32_t* lin, int n_obj,
+                         const double* phi_b) {
+  need_mesh(c);
+  require(n_obj >= 0 && n_obj <= 127, "at most 127 boundary objects (int8 ids)");
+  HostStencils& st = c.st;
+  st = HostStencils{};
+  const int nbk = c.mesh.nb, F = c.F;
+  st.boundary.assign(boundary, boundary + nbk);
+  st.row_count.assign(row_count, row_count + nbk);
+  st.row_start.assign((size_t)nbk + 1, 0);
+  for (int i = 0; i < nbk; ++i) st.row_start[(size_t)i + 1] = st.row_start[(size_t)i] + st.row_count[(size_t)i];
+  const size_t R = (size_t)st.row_start[(size_t)nbk];
+  st.row_of.assign((size_t)nbk * c.NI, -1);
+  for (int i = 0; i < nbk; ++i)
+    if (st.boundary[(size_t)i])
+      std::copy(row_of + (size_t)i * c.NI, row_of + (size_t)(i + 1) * c.NI,
+                st.row_of.begin() + (long)i * c.NI);
+  st.center.assign(center, center + R);
+  st.nb.assign(nb, nb + R * F);
+  st.bc.assign(bc, bc + R * F);
+  st.d.assign(d, d + R * F);
+  st.obj.assign(obj, obj + R * F);
+  st.mask.assign(mask, mask + R);
+  st.pin.assign(pin, pin + R);
+  st.lin.assign(lin, lin + R);
+  st.phi_b.assign(phi_b, phi_b + n_obj);
+  for (size_t r = 0; r < R; ++r) {
+    if (st.mask[r] == PMG_INSIDE) require(st.pin[r] >= 0 && st.pin[r] < n_obj, "pin_obj out of range");
+    for (int f = 0; f < F; ++f)
+      if (st.bc[r * F + f] != 0)
+        require(st.obj[r * F + f] >= 0 && st.obj[r * F + f] < n_obj, "stencil object id out of range");
+  }
+  st.valid = true;
+  upload_stencils(c);
+  set_views(c);
+  c.solver = false;
+  invalidate_graphs(c);
+  PMG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+}  // namespace pmghost
+
+// ============================================================================ C ABI
+template <typename Fn>
+static int guard(pmg_b200_ctx* h, Fn&& fn) {
+  if (!h) return PMG_ERR_STATE;
+  try {
+    h->c.err.clear();
+    PMG_CUDA(cudaSetDevice(h->c.device));
+    fn(h->c);
+    return PMG_OK;
+  } catch (const PmgError& e) {
+    h->c.err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    h->c.err = e.what();
+    return PMG_ERR_INVALID_ARG;
+  }
+}
+
+extern "C" {
+
+pmg_b200_ctx* pmg_b200_create(int dim, int N, const double* lo, const double* hi, int device) {
+  auto* h = new (std::nothrow) pmg_b200_ctx;
+  if (!h) return nullptr;
+  Ctx& c = h->c;
+  try {
+    require(dim == 2 || dim == 3, "dim must be 2 or 3");
+    require(N >= 4 && (N & (N - 1)) == 0, "block size N must be a power of two and at least 4");
+    c.dim = dim;
+    c.N = N;
+    c.F = 2 * dim;
+    c.NI = dim == 2 ? N * N : N * N * N;
+    c.S = dim == 2 ? (N + 2) * (N + 2) : (N + 2) * (N + 2) * (N + 2);
+    c.NT = dim == 2 ? N : N * N;
+    const double ext = hi[0] - lo[0];
+    for (int k = 0; k < dim; ++k) {
+      c.lo[k] = lo[k];
+      c.hi[k] = hi[k];
+      require(std::abs((hi[k] - lo[k]) - ext) <= 1e-12 * std::abs(ext), "domain must be square/cubic");
+    }
+    require(ext > 0, "domain extent must be positive");
+    c.device = device;
+    PMG_CUDA(cudaSetDevice(device));
+    PMG_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    PMG_CUDA(cudaMallocHost(&c.h_out, 4 * sizeof(double)));
+    PMG_CUDA(cudaMallocHost(&c.h_status, sizeof(int)));
+    c.ops = make_ops(dim, N);
+  } catch (const std::exception& e) {
+    c.err = e.what();
+  }
+  return h;
+}
+
+void pmg_b200_destroy(pmg_b200_ctx* h) {
+  if (!h) return;
+  cudaSetDevice(h->c.device);
+  if (h->c.stream) cudaStreamSynchronize(h->c.stream);
+  delete h;
+}
+
+const char* pmg_b200_last_error(pmg_b200_ctx* h) { return h ? h->c.err.c_str() : "null context"; }
+void* pmg_b200_stream(pmg_b200_ctx* h) { return h ? (void*)h->c.stream : nullptr; }
+
+int pmg_b200_set_mesh(pmg_b200_ctx* h, int n_blocks, const int32_t* level, const int32_t* coords,
+                      const double* origin, const double* dx, const int32_t* parent,
+                      const int32_t* children, const int32_t* nbr, const int32_t* cnbr) {
+  return guard(h, [&](Ctx& c) {
+    require(c.ops != nullptr, c.err.empty() ? "context not initialised" : c.err);
+    set_mesh(c, n_blocks, level, coords, origin, dx, parent, children, nbr, cnbr);
+  });
+}
+int pmg_b200_set_face_bc(pmg_b200_ctx* h, int dir, int type, const double* values) {
+  return guard(h, [&](Ctx& c) { set_face_bc(c, dir, type, values); });
+}
+int pmg_b200_set_stencils(pmg_b200_ctx* h, const int32_t* boundary, const int32_t* row_count,
+                          const int32_t* row_of, const double* center, const double* nb,
+                          const double* bc, const double* d, const int8_t* obj,
+                          const uint8_t* mask, const int8_t* pin_obj, const int32_t* lin,
+                          int n_obj, const double* phi_b) {
+  return guard(h, [&](Ctx& c) {
+    set_stencils(c, boundary, row_count, row_of, center, nb, bc, d, obj, mask, pin_obj, lin, n_obj,
+                 phi_b);
+  });
+}
+int pmg_b200_build_stencils(pmg_b200_ctx* h, const pmg_lsf_t* lsf, int n_lsf,
+                            const pmg_stencil_cfg_t* cfg) {
+  return guard(h, [&](Ctx& c) {
+    need_mesh(c);
+    require(lsf && n_lsf >= 1 && cfg, "bad level-set description");
+    c.ops->build_stencils(c, lsf, n_lsf, cfg);
+    upload_stencils(c);
+    set_views(c);
+    c.solver = false;
+    invalidate_graphs(c);
+    PMG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+int pmg_b200_stencil_summary(pmg_b200_ctx* h, int32_t* boundary, int32_t* row_count) {
+  int total = 0;
+  int rc = guard(h, [&](Ctx& c) {
+    need_mesh(c);
+    for (int i = 0; i < c.mesh.nb; ++i) {
+      if (boundary) boundary[i] = c.st.boundary[(size_t)i];
+      if (row_count) row_count[i] = c.st.row_count[(size_t)i];
+    }
+    total = c.st.row_start.empty() ? 0 : c.st.row_start.back();
+  });
+  return rc == 0 ? total : -rc;
+}
+int pmg_b200_get_stencils(pmg_b200_ctx* h, int32_t* row_of, double* center, double* nb,
+                          double* bc, double* d, int8_t* obj, uint8_t* mask, int8_t* pin_obj,
+                          int32_t* lin) {
+  return guard(h, [&](Ctx& c) {
+    need_mesh(c);
+    const HostStencils& st = c.st;
+    for (int i = 0; i < c.mesh.nb; ++i)
+      for (int q = 0; q < c.NI; ++q)
+        row_of[(size_t)i * c.NI + q] = st.boundary[(size_t)i] ? st.row_of[(size_t)i * c.NI + q] : -1;
+    std::copy(st.center.begin(), st.center.end(), center);
+    std::copy(st.nb.begin(), st.nb.end(), nb);
+    std::copy(st.bc.begin(), st.bc.end(), bc);
+    std::copy(st.d.begin(), st.d.end(), d);
+    std::copy(st.obj.begin(), st.obj.end(), obj);
+    std::copy(st.mask.begin(), st.mask.end(), mask);
+    std::copy(st.pin.begin(), st.pin.end(), pin_obj);
+    std::copy(st.lin.begin(), st.lin.end(), lin);
+  });
+}
+int pmg_b200_set_boundary_value(pmg_b200_ctx* h, int obj, double value) {
+  return guard(h, [&](Ctx& c) {
+    need_mesh(c);
+    require(obj >= 0 && obj < (int)c.st.phi_b.size(), "boundary object out of range");
+    c.st.phi_b[(size_t)obj] = value;
+    PMG_CUDA(cudaMemcpyAsync(c.phi_b.p + obj, &c.st.phi_b[(size_t)obj], sizeof(double),
+                             cudaMemcpyHostToDevice, c.stream));
+    PMG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+int pmg_b200_upload_field(pmg_b200_ctx* h, int var, const double* host, int layout) {
+  return guard(h, [&](Ctx& c) { upload_field(c, var, 0, host, layout); });
+}
+int pmg_b200_download_field(pmg_b200_ctx* h, int var, double* host, int layout) {
+  return guard(h, [&](Ctx& c) { download_field(c, var, 0, host, layout); });
+}
+int pmg_b200_upload_level_field(pmg_b200_ctx* h, int var, int level, const double* host, int layout) {
+  return guard(h, [&](Ctx& c) {
+    need_level(c, level);
+    upload_field(c, var, level, host, layout);
+  });
+}
+int pmg_b200_download_level_field(pmg_b200_ctx* h, int var, int level, double* host, int layout) {
+  return guard(h, [&](Ctx& c) {
+    need_level(c, level);
+    download_field(c, var, level, host, layout);
+  });
+}
+int pmg_b200_solver_create(pmg_b200_ctx* h, const pmg_mg_cfg_t* cfg) {
+  return guard(h, [&](Ctx& c) {
+    need_mesh(c);
+    require(cfg != nullptr, "null MgConfig");
+    // MgConfig::validate (multigrid.hpp:22-27)
+    require(cfg->n_down >= 1 && cfg->n_up >= 1, "n_up and n_down must be at least 1");
+    require(cfg->coarse_rel_tol > 0 && cfg->coarse_rel_tol < 1, "coarse_rel_tol must be in (0, 1)");
+    require(cfg->threads >= 1, "thread count must be at least 1");
+    c.cfg = *cfg;
+    c.solver = true;
+    do_init(c);
+  });
+}
+int pmg_b200_init(pmg_b200_ctx* h) {
+  return guard(h, [&](Ctx& c) {
+    require(c.solver, "solver not created", PMG_ERR_STATE);
+    do_init(c);
+  });
+}
+int pmg_b200_v_cycle_async(pmg_b200_ctx* h) {
+  return guard(h, [&](Ctx& c) { launch_cycle(c, CK_V); });
+}
+int pmg_b200_fmg_cycle_async(pmg_b200_ctx* h) {
+  return guard(h, [&](Ctx& c) { launch_cycle(c, c.have_guess ? CK_FMG_GUESS : CK_FMG_NOGUESS); });
+}
+int pmg_b200_cycle_result(pmg_b200_ctx* h, pmg_cycle_stats_t* out) {
+  return guard(h, [&](Ctx& c) { cycle_result(c, out); });
+}
+int pmg_b200_v_cycle(pmg_b200_ctx* h, pmg_cycle_stats_t* out) {
+  return guard(h, [&](Ctx& c) {
+    launch_cycle(c, CK_V);
+    cycle_result(c, out);
+  });
+}
+int pmg_b200_fmg_cycle(pmg_b200_ctx* h, pmg_cycle_stats_t* out) {
+  return guard(h, [&](Ctx& c) {
+    launch_cycle(c, c.have_guess ? CK_FMG_GUESS : CK_FMG_NOGUESS);
+    cycle_result(c, out);
+  });
+}
+int pmg_b200_measure_residual(pmg_b200_ctx* h, pmg_cycle_stats_t* out) {
+  return guard(h, [&](Ctx& c) {
+    launch_cycle(c, CK_MEASURE);
+    cycle_result(c, out);
+  });
+}
+int pmg_b200_gsrb_sweep(pmg_b200_ctx* h, int level, int parity) {
+  return guard(h, [&](Ctx& c) {
+    need_level(c, level);
+    require(parity == 0 || parity == 1, "parity must be 0 or 1");
+    c.ops->gs(c, level, parity);
+    PMG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+int pmg_b200_fill_ghosts(pmg_b200_ctx* h, int level, int var) {
+  return guard(h, [&](Ctx& c) {
+    need_level(c, level);
+    (void)var;  // ghost layers are evaluated on read: always current
+  });
+}
+int pmg_b200_apply_pins(pmg_b200_ctx* h, int level) {
+  return guard(h, [&](Ctx& c) {
+    need_level(c, level);
+    c.ops->pins(c, level);
+    PMG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+int pmg_b200_residual_level(pmg_b200_ctx* h, int level) {
+  return guard(h, [&](Ctx& c) {
+    need_level(c, level);
+    c.ops->residual(c, level);
+    PMG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+int pmg_b200_restrict_level(pmg_b200_ctx* h, int level) {
+  return guard(h, [&](Ctx& c) {
+    need_level(c, level, 2);
+    enq_restrict_level(c, level);
+    PMG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+int pmg_b200_restrict_level_no_guess(pmg_b200_ctx* h, int level) {
+  return guard(h, [&](Ctx& c) {
+    need_level(c, level, 2);
+    enq_restrict_level_no_guess(c, level);
+    PMG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+int pmg_b200_prolong_correction(pmg_b200_ctx* h, int level) {
+  return guard(h, [&](Ctx& c) {
+    need_level(c, level, 2);
+    c.ops->prolong(c, level, false);
+    PMG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+int pmg_b200_prolong_full(pmg_b200_ctx* h, int level) {
+  return guard(h, [&](Ctx& c) {
+    need_level(c, level, 2);
+    c.ops->prolong(c, level, true);
+    PMG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+int pmg_b200_coarse_solve(pmg_b200_ctx* h) {
+  return guard(h, [&](Ctx& c) {
+    require(c.solver, "solver not created", PMG_ERR_STATE);
+    enq_clear_status(c);
+    enq_coarse(c);
+    PMG_CUDA(cudaMemcpyAsync(c.h_out + 2, c.diag.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    PMG_CUDA(cudaMemcpyAsync(c.h_status, c.status.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    cycle_result(c, nullptr);
+  });
+}
+int pmg_b200_set_have_guess(pmg_b200_ctx* h, int v) {
+  return guard(h, [&](Ctx& c) { c.have_guess = v != 0; });
+}
+int pmg_b200_coarse_sizes(pmg_b200_ctx* h, int32_t* n, int32_t* nnz, int32_t* n_obj) {
+  return guard(h, [&](Ctx& c) {
+    require(c.solver, "solver not created", PMG_ERR_STATE);
+    *n = c.coarse.n;
+    *nnz = (int32_t)c.coarse.val.size();
+    *n_obj = (int32_t)c.st.phi_b.size();
+  });
+}
+int pmg_b200_coarse_get(pmg_b200_ctx* h, int32_t* rp, int32_t* ci, double* val, double* c0,
+                        double* cobj, int32_t* ub, int32_t* ul) {
+  return guard(h, [&](Ctx& c) {
+    require(c.solver, "solver not created", PMG_ERR_STATE);
+    const HostCoarse& cs = c.coarse;
+    std::copy(cs.rp.begin(), cs.rp.end(), rp);
+    std::copy(cs.ci.begin(), cs.ci.end(), ci);
+    std::copy(cs.val.begin(), cs.val.end(), val);
+    std::copy(cs.c0.begin(), cs.c0.end(), c0);
+    std::copy(cs.cobj.begin(), cs.cobj.end(), cobj);
+    std::copy(cs.unk_block.begin(), cs.unk_block.end(), ub);
+    std::copy(cs.unk_lin.begin(), cs.unk_lin.end(), ul);
+  });
+}
+int pmg_b200_cycle_kernel_count(pmg_b200_ctx* h, int kind) {
+  int k = -1;
+  int rc = guard(h, [&](Ctx& c) {
+    require(c.solver, "solver not created", PMG_ERR_STATE);
+    const int ck = kind == 0 ? CK_V : kind == 2 ? CK_MEASURE : (c.have_guess ? CK_FMG_GUESS : CK_FMG_NOGUESS);
+    k = graph_for(c, ck).kernels;
+  });
+  return rc == 0 ? k : -rc;
+}
+int pmg_b200_n_levels(pmg_b200_ctx* h) { return h && h->c.have_mesh ? h->c.mesh.L : 0; }
+int pmg_b200_level_size(pmg_b200_ctx* h, int level) {
+  if (!h || !h->c.have_mesh || level < 1 || level > h->c.mesh.L) return 0;
+  return h->c.lev[(size_t)level]->nb;
+}
+int pmg_b200_synchronize(pmg_b200_ctx* h) {
+  return guard(h, [&](Ctx& c) { PMG_CUDA(cudaStreamSynchronize(c.stream)); });
+}
+
+}  // extern "C"

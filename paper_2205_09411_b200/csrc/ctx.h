@@ -1,0 +1,167 @@
+// ctx.h -- host-side state of one solver context (one mesh on one device).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pmg_b200.h"
+#include "kernels.cuh"
+
+namespace pmghost {
+
+struct PmgError : std::runtime_error {
+  int code;
+  PmgError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define PMG_CUDA(x)                                                                    \
+  do {                                                                                 \
+    cudaError_t e_ = (x);                                                              \
+    if (e_ != cudaSuccess)                                                             \
+      throw ::pmghost::PmgError(PMG_ERR_CUDA, std::string("CUDA error: ") +            \
+                                                  cudaGetErrorString(e_) + " at " #x); \
+  } while (0)
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    release();
+    if (count == 0) count = 1;
+    PMG_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void upload(const std::vector<T>& v, cudaStream_t s) {
+    alloc(v.size());
+    if (!v.empty()) PMG_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+};
+
+struct HostMesh {
+  int nb = 0;
+  int L = 0;
+  std::vector<int32_t> level, coords, parent, children, nbr, cnbr;  // coords nb*3, children nb*8, nbr nb*6
+  std::vector<double> origin, dx;
+  std::vector<std::vector<int32_t>> slots;      // per level: block ids in device slot (Morton) order
+  std::vector<std::vector<int32_t>> ref_order;  // per level: block ids in level_blocks (x-major) order
+  std::vector<int32_t> slot_of;                 // block id -> slot within its level
+};
+
+struct HostStencils {
+  bool valid = false;
+  std::vector<int32_t> boundary, row_count, row_start, row_of;  // row_of nb*NI
+  std::vector<double> center, nb, bc, d;
+  std::vector<int8_t> obj, pin;
+  std::vector<uint8_t> mask;
+  std::vector<int32_t> lin;
+  std::vector<double> phi_b;
+};
+
+struct HostCoarse {
+  int n = 0;
+  std::vector<int32_t> rp, ci;
+  std::vector<double> val, c0, cobj;  // cobj n_obj*n
+  std::vector<int32_t> unk_block, unk_lin, uaddr;
+  std::vector<double> dinv;
+};
+
+struct LevelDev {
+  int nb = 0;
+  DevBuf<int32_t> nbr, cnbr, coords, parent, child, srow, bcoff, cfoff, row_of, slot_id;
+  DevBuf<uint8_t> leaf, kind, r_mask;
+  DevBuf<double> phi, rhs, old, res, bcval, cfold, r_center, r_nb, r_bc;
+  DevBuf<int8_t> r_obj, r_pin;
+  DevBuf<int32_t> ref_slot;  // level_blocks order position -> slot
+  bool has_cf = false;       // some block has a coarse-fine face
+  bool has_cfold = false;
+  pmgdev::LevelView view{};
+};
+
+struct Ctx;
+
+// Launchers, templated on (Dim, N) inside ops.cu.
+struct Ops {
+  virtual ~Ops() = default;
+  virtual void gs(Ctx& c, int l, int parity) = 0;
+  virtual void residual(Ctx& c, int l) = 0;
+  virtual void restrict_(Ctx& c, int l, int mode) = 0;
+  virtual void fas(Ctx& c, int lc, bool fas) = 0;
+  virtual void cfold(Ctx& c, int lc) = 0;
+  virtual void prolong(Ctx& c, int l, bool full) = 0;
+  virtual void record(Ctx& c, int l) = 0;
+  virtual void pins(Ctx& c, int l) = 0;
+  virtual void coarse(Ctx& c) = 0;
+  virtual void scatter(Ctx& c, int l, double* dst, const double* staging, const int32_t* slot_id,
+                       int layout) = 0;
+  virtual void gather(Ctx& c, int l, int var, double* staging, const int32_t* slot_id,
+                      int layout) = 0;
+  virtual void build_stencils(Ctx& c, const pmg_lsf_t* lsf, int n_lsf,
+                              const pmg_stencil_cfg_t* cfg) = 0;
+};
+std::unique_ptr<Ops> make_ops(int dim, int N);
+
+struct Graph {
+  cudaGraphExec_t exec = nullptr;
+  int kernels = 0;
+  void reset() {
+    if (exec) cudaGraphExecDestroy(exec);
+    exec = nullptr;
+    kernels = 0;
+  }
+  ~Graph() { reset(); }
+};
+
+struct Ctx {
+  int dim = 3, N = 16, F = 6, NI = 0, S = 0, NT = 0;
+  double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+
+  HostMesh mesh;
+  bool have_mesh = false;
+  int bctype[6] = {0, 0, 0, 0, 0, 0};
+  std::vector<double> face_vals[6];  // per dir, concatenated over physical-face blocks in id order
+  std::vector<int32_t> face_off[6];  // per dir, per block: offset into face_vals[dir] or -1
+
+  HostStencils st;
+  HostCoarse coarse;
+  std::vector<std::unique_ptr<LevelDev>> lev;  // index 0 unused
+  DevBuf<double> phi_b;
+  DevBuf<pmgdev::Rec> rec, partial;
+  DevBuf<unsigned int> counter;
+  DevBuf<double> stats;
+  DevBuf<int> status;
+  DevBuf<double> diag;
+  DevBuf<double> staging;
+  // coarse system on device
+  DevBuf<int32_t> c_rp, c_ci, c_uaddr;
+  DevBuf<double> c_val, c_dinv, c_c0, c_cobj, c_scratch;
+
+  double* h_out = nullptr;  // pinned: stats[2], diag[2]
+  int* h_status = nullptr;  // pinned
+
+  pmg_mg_cfg_t cfg{2, 2, 1e-6, 2000, 1};
+  bool solver = false;
+  bool have_guess = false;
+  std::unique_ptr<Ops> ops;
+  Graph g_v, g_fmg[2], g_measure;
+  bool graphs_dirty = true;
+
+  ~Ctx();
+};
+
+}  // namespace pmghost
