@@ -1,0 +1,362 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 V-cycle hot path on BASELINE config 2 (the headline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config cfg2] [--no-cpu-baseline]
+
+Workload (BASELINE.json configs[1]): 3D [0,1]^3, 256^3 fp64 cells in 16^3
+blocks (L=5), sphere c=(.5,.5,.5) R=0.2 with phi=1, phi=0 on the outer faces,
+g = seeded 1e-2*U[-1,1); setup + GPU stencil build + FMG, then a STEP is one
+V-cycle (2+2 GS-RB) over the whole mesh.  Inputs are synthetic, generated on
+the host (configs.py) and resident in HBM when the timed region starts.
+The finest level alone (phi + rhs = 268 MB) exceeds the 126 MB L2, so no
+explicit L2 flush is needed between steps.
+
+N > 1 (torchrun): every rank solves its own replica of the workload (weak
+scaling, no data-path collective); time = max over ranks.  The
+Morton-partitioned single-problem path is the next row.
+``--impl reference`` times the reference's own CPU solver (oracle/_ref,
+compiled from /root/reference) on the host's cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "V-cycle unknowns/sec (fp64) and % of HBM peak; residual reduction/cycle"
+UNIT = "unknowns/s"
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def vcycle_bytes(mesh, N, dim, nu1=2, nu2=2):
+    """Algorithmic bytes of one V-cycle:
+    B_V = sum_{l=2..L} [(24(nu1+nu2)+32) n_l + 32 n_l/2^D + 32 n_{l-1}] + 16 sum_l leaf_l."""
+    NI = N ** dim
+    L = mesh.n_levels
+    n = [0] + [len(mesh.level_blocks(l)) * NI for l in range(1, L + 1)]
+    leaf = [0] + [sum(1 for b in mesh.level_blocks(l) if mesh.is_leaf(b)) * NI
+                  for l in range(1, L + 1)]
+    B = 0
+    for l in range(2, L + 1):
+        B += (24 * (nu1 + nu2) + 32) * n[l] + 32 * n[l] / (1 << dim) + 32 * n[l - 1]
+    B += 16 * sum(leaf)
+    return B
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        for line in getattr(self, "out", "").splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                                "sw_power_cap"), f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_reference_run(case, steps, warmup, budget_s=None, threads=None):
+    """The reference's own MgSolver (oracle/_ref/libpmgref.so) on host cores."""
+    from oracle.oc import REF_SO, PORT_SO, Oracle
+    from paper_2205_09411_b200 import configs as cfgs
+    kind = "reference" if os.path.exists(REF_SO) else "port"
+    threads = threads or os.cpu_count() or 1
+    mesh = case.build_mesh()
+    o = Oracle(case.dim, case.N, case.lo[:case.dim], case.hi[:case.dim],
+               "ref" if kind == "reference" else "port")
+    o.build_uniform(case.levels)
+    if case.amr_band > 0:
+        o.refine_band(case.lsf.as_descs(), case.amr_band, case.max_level)
+    t0 = time.perf_counter()
+    o.build_stencils(case.lsf.as_descs(), w_min=case.w_min)
+    t_st = time.perf_counter() - t0
+    g = case.rhs_fields(mesh)
+    o.set_field(1, cfgs.padded_from_interior(g, case.dim, case.N))
+    o.solver_create(threads=threads)
+    if case.fmg_first:
+        o.fmg_cycle()
+    times = []
+    t_start = time.perf_counter()
+    for k in range(warmup + steps):
+        t = time.perf_counter()
+        o.v_cycle()
+        dt = time.perf_counter() - t
+        if k >= warmup:
+            times.append(dt)
+        if budget_s and time.perf_counter() - t_start > budget_s and len(times) >= 3:
+            break
+    leaf = case.leaf_cells(mesh)
+    return dict(kind=kind, threads=threads, times=times, leaf=leaf, stencil_s=t_st)
+
+
+def run_reference(args, case):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    r = cpu_reference_run(case, args.steps, args.warmup)
+    t = sum(r["times"])
+    k = len(r["times"])
+    value = r["leaf"] * k / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+        "steps": k, "warmup": args.warmup, "ms_per_step": 1e3 * t / k, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{case.name}: {case.notes}; step = one V-cycle (after FMG)",
+                   "leaf_cells": r["leaf"], "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["threads"], "kind": r["kind"],
+                         "sample": f"{k} V-cycles of {case.name} after FMG "
+                                   f"(median {1e3 * statistics.median(r['times']):.1f} ms)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_b200(args, case):
+    import torch
+    from paper_2205_09411_b200 import (DeviceMesh, MgConfig, MgSolver, StencilBuildConfig,
+                                       build_stencils)
+    from paper_2205_09411_b200.mesh import VAR_RHS
+    from paper_2205_09411_b200.solver import LAYOUT_INTERIOR
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev_id = local
+    torch.cuda.set_device(dev_id)
+
+    t0 = time.perf_counter()
+    mesh = case.build_mesh()
+    t_mesh = time.perf_counter() - t0
+    dev = DeviceMesh(mesh, device=dev_id)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    st = build_stencils(dev, case.lsf, StencilBuildConfig(w_min=case.w_min))
+    t_stencil = time.perf_counter() - t0
+    g = case.rhs_fields(mesh)
+    dev.set_field(VAR_RHS, g, layout=LAYOUT_INTERIOR)
+    sol = MgSolver(dev, None, MgConfig())
+    L = mesh.n_levels
+    stream = torch.cuda.ExternalStream(dev.stream, device=dev_id)
+
+    r0 = sol.measure_residual().max_resid
+    hist = [r0]
+    t_fmg = None
+    if case.fmg_first:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        sol.fmg_cycle_async()
+        e1.record(stream)
+        hist.append(sol.cycle_result().max_resid)
+        t_fmg = e0.elapsed_time(e1)
+    for _ in range(case.v_cycles):  # the config's own plan: FMG + 8 V
+        hist.append(sol.v_cycle().max_resid)
+    plan_v = hist[-case.v_cycles - 1:]
+    red = [plan_v[i] / plan_v[i + 1] for i in range(len(plan_v) - 1) if plan_v[i + 1] > 0]
+    reduction = math.exp(sum(math.log(x) for x in red) / len(red)) if red else None
+
+    # warmup (untimed)
+    for _ in range(args.warmup):
+        sol.v_cycle_async()
+    sol.cycle_result()
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev_id) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            sol.v_cycle_async()
+        e1.record(stream)
+        stats = sol.cycle_result()
+        torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    ms_total = e0.elapsed_time(e1)
+    if ws > 1:
+        tt = torch.tensor([ms_total], device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms_total = float(tt.item())
+    ms_step = ms_total / args.steps
+    leaf = case.leaf_cells(mesh)
+    value = leaf * ws * args.steps / (ms_total * 1e-3)
+
+    # dominant kernel: GS-RB half-sweep of the finest level (12 B/cell algorithmic)
+    peak, peak_kind = measured_peaks()
+    reps = 20
+    gs_ms = sol.time_op(0, L, reps)
+    n_fine = len(mesh.level_blocks(L)) * case.N ** case.dim
+    gs_bytes = 12.0 * n_fine
+    gs_gbs = gs_bytes / (gs_ms * 1e-3) / 1e9
+    phases = {
+        "gs_half_sweep_finest_ms": gs_ms,
+        "restrict_finest_ms": sol.time_op(1, L, reps),
+        "prolong_finest_ms": sol.time_op(2, L, reps),
+        "record_finest_ms": sol.time_op(3, L, reps),
+        "coarse_solve_ms": sol.time_op(4, 0, reps),
+    }
+    BV = vcycle_bytes(mesh, case.N, case.dim)
+    vc_gbs = BV / (ms_step * 1e-3) / 1e9
+
+    # end-to-end through the public API: h2d of the step's input (finest-level
+    # rhs from pinned host memory) + V-cycle + d2h of the step's result (stats)
+    gL = np.ascontiguousarray(g[np.array(mesh.level_blocks(L))])
+    pinned = torch.empty(gL.size, dtype=torch.float64, pin_memory=True)
+    pinned.numpy()[:] = gL.reshape(-1)
+    pin_np = pinned.numpy()
+    import ctypes as C
+    ptr = C.c_void_p(pinned.data_ptr())
+
+    def e2e_step():
+        dev._check(dev.lib.pmg_b200_upload_level_field(dev.h, VAR_RHS, L, ptr, LAYOUT_INTERIOR))
+        sol.v_cycle_async()
+        return sol.cycle_result()
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if ws > 1:
+        tt = torch.tensor([e2e_s], device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    e2e_val = leaf * ws * args.steps / e2e_s
+    kernels = sol.kernel_count(0)
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        r = cpu_reference_run(case, steps=40, warmup=1, budget_s=20.0)
+        cpu = {"value": r["leaf"] * len(r["times"]) / sum(r["times"]), "unit": UNIT,
+               "cores": r["threads"], "kind": r["kind"],
+               "sample": f"{len(r['times'])} V-cycles of {case.name} after FMG on the host "
+                         f"(reference MgSolver, {r['threads']} threads; median "
+                         f"{1e3 * statistics.median(r['times']):.1f} ms/V-cycle)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{case.name}: {case.notes}; step = one V-cycle (after FMG)",
+                       "leaf_cells": leaf, "levels": L, "blocks": mesh.n_blocks,
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
+                       "l2_flush": "none needed: finest phi+rhs = "
+                                   f"{2 * 8 * n_fine / 1e6:.0f} MB > 126 MB L2"},
+            "roofline": {"bound": "hbm", "kernel": f"k_gs<{case.dim},{case.N}> finest half-sweep",
+                         "achieved": gs_gbs, "peak": peak, "unit": "GB/s",
+                         "frac": gs_gbs / peak, "traffic": None,
+                         "bytes_per_launch": gs_bytes, "peak_kind": peak_kind},
+            "vcycle_roofline": {"algorithmic_bytes": BV, "achieved": vc_gbs, "peak": peak,
+                                "unit": "GB/s", "frac": vc_gbs / peak,
+                                "bytes_per_unknown": BV / leaf},
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(gL.nbytes),
+                    "d2h_bytes_per_step": 16 + 16 + 4},
+            "gpu_launches": kernels * args.steps,
+            "kernels_per_step": kernels,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "fmg_ms": t_fmg,
+            "residual_reduction_per_cycle": reduction,
+            "residual_history": hist,
+            "phases_ms": phases,
+            "setup_s": {"mesh": t_mesh, "stencil_build_gpu": t_stencil},
+            "final_max_resid": stats.max_resid,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    from paper_2205_09411_b200 import configs as cfgs
+    case = cfgs.get_case(args.config)
+    if args.impl == "reference":
+        return run_reference(args, case)
+    return run_b200(args, case)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -135,6 +135,16 @@ int pmg_b200_cycle_kernel_count(pmg_b200_ctx* ctx, int kind);
 int pmg_b200_n_levels(pmg_b200_ctx* ctx);
 int pmg_b200_level_size(pmg_b200_ctx* ctx, int level);
 int pmg_b200_synchronize(pmg_b200_ctx* ctx);
+/* Average device time (CUDA events on pmg_b200_stream) of `reps` back-to-back
+ * launches of one phase, after one untimed launch:
+ *   op 0: GS-RB half-sweep on `level` (parities alternate)
+ *   op 1: residual+restriction of `level` (+ FAS/OLD on level-1), as in the V-cycle
+ *   op 2: prolong_correction of `level`
+ *   op 3: leaf-residual record of `level`
+ *   op 4: coarse solve
+ *   op 5: one V-cycle (graph)        op 6: one FMG cycle (graph, with guess)
+ * Ops 1-6 modify the solution exactly as the solver would. */
+int pmg_b200_time_op(pmg_b200_ctx* ctx, int op, int level, int reps, double* ms_avg);
 
 #ifdef __cplusplus
 }

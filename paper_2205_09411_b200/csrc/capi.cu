@@ -1014,6 +1014,38 @@ int pmg_b200_level_size(pmg_b200_ctx* h, int level) {
   if (!h || !h->c.have_mesh || level < 1 || level > h->c.mesh.L) return 0;
   return h->c.lev[(size_t)level]->nb;
 }
+int pmg_b200_time_op(pmg_b200_ctx* h, int op, int level, int reps, double* ms_avg) {
+  return guard(h, [&](Ctx& c) {
+    require(c.solver, "solver not created", PMG_ERR_STATE);
+    require(reps >= 1 && op >= 0 && op <= 6, "bad op/reps");
+    if (op <= 3) need_level(c, level, op == 0 || op == 3 ? 1 : 2);
+    auto one = [&](int k) {
+      switch (op) {
+        case 0: c.ops->gs(c, level, k & 1); break;
+        case 1: enq_restrict_level(c, level); break;
+        case 2: c.ops->prolong(c, level, false); break;
+        case 3: c.ops->record(c, level); break;
+        case 4: enq_coarse(c); break;
+        case 5: PMG_CUDA(cudaGraphLaunch(graph_for(c, CK_V).exec, c.stream)); break;
+        default: PMG_CUDA(cudaGraphLaunch(graph_for(c, CK_FMG_GUESS).exec, c.stream)); break;
+      }
+    };
+    one(0);
+    cudaEvent_t e0, e1;
+    PMG_CUDA(cudaEventCreate(&e0));
+    PMG_CUDA(cudaEventCreate(&e1));
+    PMG_CUDA(cudaEventRecord(e0, c.stream));
+    for (int k = 0; k < reps; ++k) one(k + 1);
+    PMG_CUDA(cudaEventRecord(e1, c.stream));
+    PMG_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    PMG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (op >= 5) c.have_guess = true;
+    *ms_avg = (double)ms / reps;
+  });
+}
 int pmg_b200_synchronize(pmg_b200_ctx* h) {
   return guard(h, [&](Ctx& c) { PMG_CUDA(cudaStreamSynchronize(c.stream)); });
 }

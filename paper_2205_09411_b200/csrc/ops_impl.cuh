@@ -1,0 +1,125 @@
+// ops_impl.cuh -- kernel launchers (OpsImpl<Dim,N>); instantiated once per
+// (Dim, N) in ops_<D>_<N>.cu so the variants compile in parallel.
+#pragma once
+#include "ctx.h"
+#include "stencil_build.cuh"
+
+namespace pmghost {
+
+using namespace pmgdev;
+
+static inline unsigned grid_for(long long n, int threads = kThreads) {
+  return (unsigned)((n + threads - 1) / threads);
+}
+
+template <int D, int N>
+struct OpsImpl final : Ops {
+  using G = Geo<D, N>;
+  const LevelView& V(Ctx& c, int l) { return c.lev[(size_t)l]->view; }
+  const LevelView& Vc(Ctx& c, int l) { return c.lev[(size_t)(l > 1 ? l - 1 : l)]->view; }
+
+  void check() { PMG_CUDA(cudaGetLastError()); }
+
+  void gs(Ctx& c, int l, int parity) override {
+    const LevelView& L = V(c, l);
+    k_gs<D, N><<<grid_for((long long)L.nb * G::H), kThreads, 0, c.stream>>>(L, Vc(c, l), c.phi_b.p,
+                                                                           parity);
+    check();
+  }
+  void residual(Ctx& c, int l) override {
+    const LevelView& L = V(c, l);
+    k_residual<D, N><<<grid_for((long long)L.nb * G::NI), kThreads, 0, c.stream>>>(L, Vc(c, l),
+                                                                                  c.phi_b.p);
+    check();
+  }
+  void restrict_(Ctx& c, int l, int mode) override {
+    const LevelView& Lf = V(c, l);
+    const unsigned g = grid_for((long long)Lf.nb * (G::NI / G::NC));
+    if (mode == RM_RES)
+      k_restrict<D, N, RM_RES><<<g, kThreads, 0, c.stream>>>(Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
+    else if (mode == RM_RHS)
+      k_restrict<D, N, RM_RHS><<<g, kThreads, 0, c.stream>>>(Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
+    else
+      k_restrict<D, N, RM_FUSED><<<g, kThreads, 0, c.stream>>>(Lf, Vc(c, l), V(c, l - 1),
+                                                             c.phi_b.p);
+    check();
+  }
+  void fas(Ctx& c, int lc, bool f) override {
+    const LevelView& L = V(c, lc);
+    const unsigned g = grid_for((long long)L.nb * G::NI);
+    if (f)
+      k_fas<D, N, true><<<g, kThreads, 0, c.stream>>>(L, Vc(c, lc), c.phi_b.p);
+    else
+      k_fas<D, N, false><<<g, kThreads, 0, c.stream>>>(L, Vc(c, lc), c.phi_b.p);
+    check();
+  }
+  void cfold(Ctx& c, int lc) override {
+    const LevelView& L = V(c, lc);
+    k_cfold<D, N><<<grid_for((long long)L.nb * G::F * G::NT), kThreads, 0, c.stream>>>(L, Vc(c, lc));
+    check();
+  }
+  void prolong(Ctx& c, int l, bool full) override {
+    const LevelView& Lf = V(c, l);
+    const LevelView& Lp = V(c, l - 1);
+    const LevelView& Lpp = Vc(c, l - 1);
+    const unsigned g = grid_for((long long)Lf.nb * G::NI);
+    if (full)
+      k_prolong<D, N, true><<<g, kThreads, 0, c.stream>>>(Lf, Lp, Lpp);
+    else
+      k_prolong<D, N, false><<<g, kThreads, 0, c.stream>>>(Lf, Lp, Lpp);
+    check();
+  }
+  void record(Ctx& c, int l) override {
+    const LevelView& L = V(c, l);
+    k_record<D, N><<<L.nb, kThreads, 0, c.stream>>>(L, Vc(c, l), c.phi_b.p, c.partial.p, c.rec.p,
+                                                    c.counter.p);
+    check();
+  }
+  void pins(Ctx& c, int l) override {
+    const LevelView& L = V(c, l);
+    k_pins<D, N><<<grid_for((long long)L.nb * G::NI), kThreads, 0, c.stream>>>(L, c.phi_b.p);
+    check();
+  }
+  void coarse(Ctx& c) override {
+    CoarseDev C{};
+    C.n = c.coarse.n;
+    C.nnz = (int)c.coarse.val.size();
+    C.n_obj = (int)c.st.phi_b.size();
+    C.rp = c.c_rp.p;
+    C.ci = c.c_ci.p;
+    C.val = c.c_val.p;
+    C.dinv = c.c_dinv.p;
+    C.c0 = c.c_c0.p;
+    C.cobj = c.c_cobj.p;
+    C.uaddr = c.c_uaddr.p;
+    C.scratch = c.c_scratch.p;
+    C.rel_tol = c.cfg.coarse_rel_tol;
+    C.max_iters = c.cfg.coarse_max_iters;
+    int lim = 1;
+    for (int k = 0; k < D; ++k) lim *= 8;
+    C.fallback_ok = c.coarse.n <= lim + 1;
+    k_coarse<D, N><<<1, 1024, 0, c.stream>>>(V(c, 1), C, c.phi_b.p, c.rec.p, c.status.p, c.diag.p);
+    check();
+  }
+  void scatter(Ctx& c, int l, double* dst, const double* staging, const int32_t* slot_id,
+               int layout) override {
+    const LevelView& L = V(c, l);
+    k_scatter<D, N><<<grid_for((long long)L.nb * G::NI), kThreads, 0, c.stream>>>(
+        L.nb, dst, staging, slot_id, layout);
+    check();
+  }
+  void gather(Ctx& c, int l, int var, double* staging, const int32_t* slot_id,
+              int layout) override {
+    const LevelView& L = V(c, l);
+    const long long per = layout == 0 ? c.S : G::NI;
+    k_gather<D, N><<<grid_for((long long)L.nb * per), kThreads, 0, c.stream>>>(
+        L, Vc(c, l), var, staging, slot_id, layout);
+    check();
+  }
+  void build_stencils(Ctx& c, const pmg_lsf_t* lsf, int n_lsf,
+                      const pmg_stencil_cfg_t* cfg) override {
+    run_stencil_build<D, N>(c, lsf, n_lsf, cfg);
+  }
+};
+
+}  // namespace pmghost

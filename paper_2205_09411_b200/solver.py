@@ -305,6 +305,12 @@ class MgSolver:
             self.dev._check(-k)
         return k
 
+    def time_op(self, op, level=0, reps=10):
+        """Average device ms of one phase (pmg_b200_time_op)."""
+        ms = C.c_double()
+        self.dev._check(self.lib.pmg_b200_time_op(self.h, op, level, reps, C.byref(ms)))
+        return ms.value
+
     def coarse_system(self):
         n, nnz, no = C.c_int32(), C.c_int32(), C.c_int32()
         self.dev._check(self.lib.pmg_b200_coarse_sizes(self.h, C.byref(n), C.byref(nnz), C.byref(no)))
