@@ -135,6 +135,9 @@ int pmg_b200_cycle_kernel_count(pmg_b200_ctx* ctx, int kind);
 int pmg_b200_n_levels(pmg_b200_ctx* ctx);
 int pmg_b200_level_size(pmg_b200_ctx* ctx, int level);
 int pmg_b200_synchronize(pmg_b200_ctx* ctx);
+/* BiCGStab iterations and final relative residual of the most recent coarse
+ * solve (KrylovResult, multigrid.hpp:200-204; the reference discards it) */
+int pmg_b200_coarse_info(pmg_b200_ctx* ctx, int32_t* iters, double* rel);
 /* Average device time (CUDA events on pmg_b200_stream) of `reps` back-to-back
  * launches of one phase, after one untimed launch:
  *   op 0: GS-RB half-sweep on `level` (parities alternate)

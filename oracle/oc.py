@@ -138,6 +138,8 @@ def load(path):
     lib.oc_coarse_sizes.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                     C.POINTER(C.c_int32)]
     lib.oc_coarse_get.argtypes = [vp, _i32p, _i32p, _f64p, _f64p, _f64p, _i32p, _i32p]
+    lib.oc_bicgstab_probe.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                      C.POINTER(C.c_double)]
     _LIBS[path] = lib
     return lib
 
@@ -323,6 +325,11 @@ class Oracle:
 
     def set_have_guess(self, v):
         self._check(self.lib.oc_set_have_guess(self.h, int(bool(v))))
+
+    def bicgstab_probe(self):
+        c, it, rel = C.c_int32(), C.c_int32(), C.c_double()
+        self._check(self.lib.oc_bicgstab_probe(self.h, C.byref(c), C.byref(it), C.byref(rel)))
+        return bool(c.value), it.value, rel.value
 
     def coarse_system(self):
         n, nnz, no = C.c_int32(), C.c_int32(), C.c_int32()

@@ -91,6 +91,9 @@ int oc_set_have_guess(oc_ctx* h, int v);
 int oc_coarse_sizes(oc_ctx* h, int32_t* n, int32_t* nnz, int32_t* n_obj);
 int oc_coarse_get(oc_ctx* h, int32_t* rp, int32_t* ci, double* val, double* c0,
                   double* cobj, int32_t* unk_block, int32_t* unk_lin);
+/* KrylovResult of the BiCGStab that coarse_solve() would run on the current
+ * state (b and x0 assembled as in multigrid.hpp:443-453), without changing it */
+int oc_bicgstab_probe(oc_ctx* h, int32_t* converged, int32_t* iters, double* rel);
 
 #ifdef __cplusplus
 }

@@ -53,6 +53,7 @@ struct Base {
   virtual int op(int which, int a, int b, pmg_cycle_stats_t* out) = 0;
   virtual int coarse_sizes(int32_t*, int32_t*, int32_t*) = 0;
   virtual int coarse_get(int32_t*, int32_t*, double*, double*, double*, int32_t*, int32_t*) = 0;
+  virtual int probe(int32_t*, int32_t*, double*) = 0;
 };
 
 enum Op {
@@ -270,6 +271,8 @@ struct Impl final : Base {
     mg.coarse_rel_tol = c->coarse_rel_tol;
     mg.coarse_max_iters = c->coarse_max_iters;
     mg.threads = c->threads;
+    tol = c->coarse_rel_tol;
+    max_iters = c->coarse_max_iters;
     solver.reset();
     solver = std::make_unique<MgSolver<D>>(mesh, set, mg);
     return 0;
@@ -331,6 +334,26 @@ struct Impl final : Base {
     }
     return 0;
   }
+  int probe(int32_t* conv, int32_t* iters, double* rel) override {
+    if (!solver) return PMG_ERR_STATE;
+    const CoarseSystem& cs = solver->coarse_system();
+    const size_t n = static_cast<size_t>(cs.n);
+    std::vector<double> b(n), x(n);
+    for (size_t u = 0; u < n; ++u) {
+      const auto& [id, lin] = cs.unknown_cell[u];
+      b[u] = mesh.field(id, VAR_RHS)[lin] + cs.c0[u];
+      x[u] = mesh.field(id, VAR_PHI)[lin];
+    }
+    for (size_t o = 0; o < set.bv.phi_b.size(); ++o)
+      for (size_t u = 0; u < n; ++u) b[u] += cs.cobj[o][u] * set.bv.phi_b[o];
+    auto res = detail::bicgstab(cs, b, x, tol, max_iters);
+    *conv = res.converged ? 1 : 0;
+    *iters = res.iters;
+    *rel = res.rel;
+    return 0;
+  }
+  double tol = 1e-6;
+  int max_iters = 2000;
 };
 
 template <typename Fn>
@@ -466,6 +489,10 @@ int oc_coarse_sizes(oc_ctx* h, int32_t* n, int32_t* nnz, int32_t* nobj) {
 int oc_coarse_get(oc_ctx* h, int32_t* rp, int32_t* ci, double* val, double* c0, double* cobj,
                   int32_t* ub, int32_t* ul) {
   return guard(h, [&](Base& b) { return b.coarse_get(rp, ci, val, c0, cobj, ub, ul); });
+}
+
+int oc_bicgstab_probe(oc_ctx* h, int32_t* conv, int32_t* iters, double* rel) {
+  return guard(h, [&](Base& b) { return b.probe(conv, iters, rel); });
 }
 
 }  // extern "C"

@@ -67,7 +67,7 @@ EXPORTS = [
     "pmg_b200_prolong_correction", "pmg_b200_prolong_full", "pmg_b200_coarse_solve",
     "pmg_b200_set_have_guess", "pmg_b200_coarse_sizes", "pmg_b200_coarse_get",
     "pmg_b200_cycle_kernel_count", "pmg_b200_n_levels", "pmg_b200_level_size",
-    "pmg_b200_synchronize", "pmg_b200_time_op",
+    "pmg_b200_synchronize", "pmg_b200_time_op", "pmg_b200_coarse_info",
 ]
 
 _lib = None
@@ -121,6 +121,7 @@ def load():
                                           C.POINTER(C.c_int32)]
     lib.pmg_b200_coarse_get.argtypes = [vp, i32p, i32p, f64p, f64p, f64p, i32p, i32p]
     lib.pmg_b200_time_op.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
+    lib.pmg_b200_coarse_info.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_double)]
     _lib = lib
     return lib
 

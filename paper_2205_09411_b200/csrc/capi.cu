@@ -76,6 +76,8 @@ static void set_views(Ctx& c) {
     v.cfold = d.cfold.p;
     v.cfoff = d.has_cfold ? d.cfoff.p : nullptr;
     for (int k = 0; k < 6; ++k) v.bctype[k] = c.bctype[k];
+    const char* ex = getenv("PMG_EXP");
+    v.exp = ex ? atoi(ex) : 0;
   }
 }
 
@@ -293,6 +295,70 @@ static void assemble_coarse(Ctx& c) {
   c.c_cobj.upload(cs.cobj, c.stream);
   c.c_uaddr.upload(cs.uaddr, c.stream);
   c.c_scratch.alloc((size_t)10 * std::max(cs.n, 1));
+
+  // cell-indexed form for the on-chip solver (coarse.cuh): per cell the diagonal,
+  // a mask of neighbours whose coefficient is w, or an explicit special row
+  std::vector<uint8_t> fl((size_t)NI, 0);
+  std::vector<double> dg((size_t)NI, 0.0), c0c((size_t)NI, 0.0), spc, obv;
+  std::vector<int16_t> sp((size_t)NI, -1);
+  std::vector<int32_t> obs((size_t)NI + 1, 0);
+  std::vector<int8_t> obo;
+  const int offs[6] = {-1, 1, -N, N, -N * N, N * N};
+  std::vector<int> cell_of_unk((size_t)cs.n);
+  for (int ii = 0; ii < NI; ++ii)
+    if (unk[(size_t)ii] >= 0) cell_of_unk[(size_t)unk[(size_t)ii]] = ii;
+  for (int u = 0; u < cs.n; ++u) {
+    const int ii = cell_of_unk[(size_t)u];
+    double coef[6] = {0, 0, 0, 0, 0, 0};
+    bool special = false;
+    for (int q = cs.rp[(size_t)u]; q < cs.rp[(size_t)u + 1]; ++q) {
+      const int col = cs.ci[(size_t)q];
+      if (col == u) {
+        dg[(size_t)ii] = cs.val[(size_t)q];
+        continue;
+      }
+      const int dj = cell_of_unk[(size_t)col] - ii;
+      int dir = -1;
+      for (int f = 0; f < F; ++f)
+        if (offs[f] == dj) dir = f;
+      require(dir >= 0, "coarse operator is not a face stencil");
+      coef[dir] = cs.val[(size_t)q];
+      if (coef[dir] != w) special = true;
+    }
+    uint8_t f8 = 0x40;
+    if (special) {
+      f8 |= 0x80;
+      sp[(size_t)ii] = (int16_t)(spc.size() / F);
+      for (int f = 0; f < F; ++f) spc.push_back(coef[f]);
+    } else {
+      for (int f = 0; f < F; ++f)
+        if (coef[f] != 0) f8 |= (uint8_t)(1u << f);
+    }
+    fl[(size_t)ii] = f8;
+    c0c[(size_t)ii] = cs.c0[(size_t)u];
+  }
+  for (int ii = 0; ii < NI; ++ii) {
+    obs[(size_t)ii + 1] = obs[(size_t)ii];
+    const int u = unk[(size_t)ii];
+    if (u < 0) continue;
+    for (int o = 0; o < n_obj; ++o) {
+      const double v = cs.cobj[(size_t)o * cs.n + u];
+      if (v == 0) continue;
+      obo.push_back((int8_t)o);
+      obv.push_back(v);
+      obs[(size_t)ii + 1]++;
+    }
+  }
+  require(spc.size() / std::max(F, 1) < 32767, "too many special coarse rows");
+  c.cf_flags.upload(fl, c.stream);
+  c.cf_diag.upload(dg, c.stream);
+  c.cf_spec.upload(sp, c.stream);
+  c.cf_spec_c.upload(spc, c.stream);
+  c.cf_c0.upload(c0c, c.stream);
+  c.cf_ob_start.upload(obs, c.stream);
+  c.cf_ob_obj.upload(obo, c.stream);
+  c.cf_ob_val.upload(obv, c.stream);
+  c.cf_w = w;
 }
 
 // ---------------------------------------------------------------- cycle sequences
@@ -751,6 +817,7 @@ pmg_b200_ctx* pmg_b200_create(int dim, int N, const double* lo, const double* hi
     c.device = device;
     PMG_CUDA(cudaSetDevice(device));
     PMG_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    PMG_CUDA(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, device));
     PMG_CUDA(cudaMallocHost(&c.h_out, 4 * sizeof(double)));
     PMG_CUDA(cudaMallocHost(&c.h_status, sizeof(int)));
     c.ops = make_ops(dim, N);
@@ -1044,6 +1111,13 @@ int pmg_b200_time_op(pmg_b200_ctx* h, int op, int level, int reps, double* ms_av
     cudaEventDestroy(e1);
     if (op >= 5) c.have_guess = true;
     *ms_avg = (double)ms / reps;
+  });
+}
+int pmg_b200_coarse_info(pmg_b200_ctx* h, int32_t* iters, double* rel) {
+  return guard(h, [&](Ctx& c) {
+    PMG_CUDA(cudaStreamSynchronize(c.stream));
+    *iters = (int32_t)c.h_out[3];
+    *rel = c.h_out[2];
   });
 }
 int pmg_b200_synchronize(pmg_b200_ctx* h) {

@@ -128,6 +128,7 @@ struct Ctx {
   int dim = 3, N = 16, F = 6, NI = 0, S = 0, NT = 0;
   double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
   int device = 0;
+  int sms = 148;  // multiprocessors of `device`
   cudaStream_t stream = nullptr;
   std::string err;
 
@@ -150,6 +151,13 @@ struct Ctx {
   // coarse system on device
   DevBuf<int32_t> c_rp, c_ci, c_uaddr;
   DevBuf<double> c_val, c_dinv, c_c0, c_cobj, c_scratch;
+  // cell-indexed level-1 operator for the on-chip BiCGStab (coarse.cuh)
+  DevBuf<uint8_t> cf_flags;
+  DevBuf<double> cf_diag, cf_spec_c, cf_c0, cf_ob_val;
+  DevBuf<int16_t> cf_spec;
+  DevBuf<int32_t> cf_ob_start;
+  DevBuf<int8_t> cf_ob_obj;
+  double cf_w = 0;
 
   double* h_out = nullptr;  // pinned: stats[2], diag[2]
   int* h_status = nullptr;  // pinned

@@ -1,8 +1,11 @@
 // ops_impl.cuh -- kernel launchers (OpsImpl<Dim,N>); instantiated once per
 // (Dim, N) in ops_<D>_<N>.cu so the variants compile in parallel.
 #pragma once
+#include <algorithm>
 #include "ctx.h"
 #include "stencil_build.cuh"
+#include "tile_kernels.cuh"
+#include "coarse.cuh"
 
 namespace pmghost {
 
@@ -15,6 +18,10 @@ static inline unsigned grid_for(long long n, int threads = kThreads) {
 template <int D, int N>
 struct OpsImpl final : Ops {
   using G = Geo<D, N>;
+  using TT = Tile<D, N>;
+  // shared-memory tiles fit the static 48 KB limit (3D N=32 keeps the per-cell kernels)
+  static constexpr bool TILE = 2 * TT::SIZE * 8 + 1024 <= 48 * 1024;
+  static constexpr bool FASTC = G::NI <= 4096;
   const LevelView& V(Ctx& c, int l) { return c.lev[(size_t)l]->view; }
   const LevelView& Vc(Ctx& c, int l) { return c.lev[(size_t)(l > 1 ? l - 1 : l)]->view; }
 
@@ -22,8 +29,20 @@ struct OpsImpl final : Ops {
 
   void gs(Ctx& c, int l, int parity) override {
     const LevelView& L = V(c, l);
-    k_gs<D, N><<<grid_for((long long)L.nb * G::H), kThreads, 0, c.stream>>>(L, Vc(c, l), c.phi_b.p,
-                                                                           parity);
+    if constexpr (TILE)
+    {
+      // persistent, software-pipelined sweep: fill every SM to its occupancy
+      static int occ = 0;
+      if (!occ) PMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gs_pers<D, N>, TT::THREADS, 0));
+      const int grid = std::min(L.nb, std::max(1, occ) * c.sms);
+      if (L.exp & 8)
+        k_gs_pers<D, N><<<grid, TT::THREADS, 0, c.stream>>>(L, Vc(c, l), c.phi_b.p, parity);
+      else
+        k_gs_tile<D, N><<<L.nb, TT::THREADS, 0, c.stream>>>(L, Vc(c, l), c.phi_b.p, parity);
+    }
+    else
+      k_gs<D, N><<<grid_for((long long)L.nb * G::H), kThreads, 0, c.stream>>>(L, Vc(c, l),
+                                                                             c.phi_b.p, parity);
     check();
   }
   void residual(Ctx& c, int l) override {
@@ -35,6 +54,16 @@ struct OpsImpl final : Ops {
   void restrict_(Ctx& c, int l, int mode) override {
     const LevelView& Lf = V(c, l);
     const unsigned g = grid_for((long long)Lf.nb * (G::NI / G::NC));
+    if constexpr (TILE) {
+      if (mode == RM_RES)
+        k_restrict_tile<D, N, RM_RES><<<Lf.nb, TT::THREADS, 0, c.stream>>>(Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
+      else if (mode == RM_RHS)
+        k_restrict_tile<D, N, RM_RHS><<<Lf.nb, TT::THREADS, 0, c.stream>>>(Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
+      else
+        k_restrict_tile<D, N, RM_FUSED><<<Lf.nb, TT::THREADS, 0, c.stream>>>(Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
+      check();
+      return;
+    }
     if (mode == RM_RES)
       k_restrict<D, N, RM_RES><<<g, kThreads, 0, c.stream>>>(Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
     else if (mode == RM_RHS)
@@ -47,6 +76,14 @@ struct OpsImpl final : Ops {
   void fas(Ctx& c, int lc, bool f) override {
     const LevelView& L = V(c, lc);
     const unsigned g = grid_for((long long)L.nb * G::NI);
+    if constexpr (TILE) {
+      if (f)
+        k_fas_tile<D, N, true><<<L.nb, TT::THREADS, 0, c.stream>>>(L, Vc(c, lc), c.phi_b.p);
+      else
+        k_fas_tile<D, N, false><<<L.nb, TT::THREADS, 0, c.stream>>>(L, Vc(c, lc), c.phi_b.p);
+      check();
+      return;
+    }
     if (f)
       k_fas<D, N, true><<<g, kThreads, 0, c.stream>>>(L, Vc(c, lc), c.phi_b.p);
     else
@@ -63,6 +100,14 @@ struct OpsImpl final : Ops {
     const LevelView& Lp = V(c, l - 1);
     const LevelView& Lpp = Vc(c, l - 1);
     const unsigned g = grid_for((long long)Lf.nb * G::NI);
+    if constexpr (TILE) {
+      if (full)
+        k_prolong_tile<D, N, true><<<Lf.nb, TT::THREADS, 0, c.stream>>>(Lf, Lp, Lpp);
+      else
+        k_prolong_tile<D, N, false><<<Lf.nb, TT::THREADS, 0, c.stream>>>(Lf, Lp, Lpp);
+      check();
+      return;
+    }
     if (full)
       k_prolong<D, N, true><<<g, kThreads, 0, c.stream>>>(Lf, Lp, Lpp);
     else
@@ -71,6 +116,12 @@ struct OpsImpl final : Ops {
   }
   void record(Ctx& c, int l) override {
     const LevelView& L = V(c, l);
+    if constexpr (TILE) {
+      k_record_tile<D, N><<<L.nb, TT::THREADS, 0, c.stream>>>(L, Vc(c, l), c.phi_b.p, c.partial.p,
+                                                              c.rec.p, c.counter.p);
+      check();
+      return;
+    }
     k_record<D, N><<<L.nb, kThreads, 0, c.stream>>>(L, Vc(c, l), c.phi_b.p, c.partial.p, c.rec.p,
                                                     c.counter.p);
     check();
@@ -81,6 +132,34 @@ struct OpsImpl final : Ops {
     check();
   }
   void coarse(Ctx& c) override {
+    if constexpr (FASTC) {
+      CoarseFast F{};
+      F.flags = c.cf_flags.p;
+      F.diag = c.cf_diag.p;
+      F.spec = c.cf_spec.p;
+      F.spec_c = c.cf_spec_c.p;
+      F.c0 = c.cf_c0.p;
+      F.ob_start = c.cf_ob_start.p;
+      F.ob_obj = c.cf_ob_obj.p;
+      F.ob_val = c.cf_ob_val.p;
+      F.w = c.cf_w;
+      F.rel_tol = c.cfg.coarse_rel_tol;
+      F.max_iters = c.cfg.coarse_max_iters;
+      int lim = 1;
+      for (int k = 0; k < D; ++k) lim *= 8;
+      F.fallback_ok = c.coarse.n <= lim + 1;
+      F.n_unknowns = c.coarse.n;
+      constexpr size_t smem = coarse_fast_smem<D, N>();
+      static bool attr = false;
+      if (!attr) {
+        PMG_CUDA(cudaFuncSetAttribute(k_coarse_fast<D, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+      }
+      k_coarse_fast<D, N><<<1, kCoarseThreads, smem, c.stream>>>(V(c, 1), F, c.phi_b.p, c.rec.p,
+                                                                   c.status.p, c.diag.p);
+      check();
+      return;
+    }
     CoarseDev C{};
     C.n = c.coarse.n;
     C.nnz = (int)c.coarse.val.size();

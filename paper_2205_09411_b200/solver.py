@@ -305,6 +305,12 @@ class MgSolver:
             self.dev._check(-k)
         return k
 
+    def coarse_info(self):
+        """(iterations, relative residual) of the last BiCGStab coarse solve."""
+        it, rel = C.c_int32(), C.c_double()
+        self.dev._check(self.lib.pmg_b200_coarse_info(self.h, C.byref(it), C.byref(rel)))
+        return it.value, rel.value
+
     def time_op(self, op, level=0, reps=10):
         """Average device ms of one phase (pmg_b200_time_op)."""
         ms = C.c_double()

@@ -120,6 +120,27 @@ def test_cycles_match_oracle(name):
     assert hist[-1][0].max_resid < hist[0][0].max_resid
 
 
+@pytest.mark.parametrize("name", ["cfg2@3", "cfg4@3", "cfg1@3"])
+def test_coarse_bicgstab_iterations_match(name):
+    """The on-chip BiCGStab replays detail::bicgstab (multigrid.hpp:208-280):
+    same state in, same iteration count (+-1 for reassociated dot products),
+    same converged solution within the solve tolerance."""
+    case = cfgs.get_case(name)
+    mesh = case.build_mesh()
+    phi, g = _random_fields(case, mesh, 11)
+    o, dev, sol, mesh, st = setup_pair(case, rhs=g, phi=phi)
+    conv, it_ref, rel_ref = o.bicgstab_probe()
+    sol.coarse_solve()
+    o.coarse_solve()
+    it, rel = sol.coarse_info()
+    assert conv
+    assert abs(it - it_ref) <= 1, (it, it_ref)
+    assert rel <= 1e-6 and rel_ref <= 1e-6
+    a = _lvl(mesh, dev.get_field(VAR_PHI, layout=LAYOUT_INTERIOR), 1)
+    b = _lvl(mesh, interior(o, VAR_PHI, case.dim, case.N), 1)
+    assert max_rel_diff(a, b) < 1e-9
+
+
 def test_coarse_solve_single_level():
     """multigrid test 'single-level v_cycle is the coarse solve' (test_multigrid.cpp:382-396)."""
     from paper_2205_09411_b200 import DeviceMesh, MgConfig, MgSolver, build_uniform
