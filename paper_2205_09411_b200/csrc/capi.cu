@@ -29,6 +29,9 @@ Ctx::~Ctx() {
   if (h_out) cudaFreeHost(h_out);
   if (h_status) cudaFreeHost(h_status);
   if (stream) cudaStreamDestroy(stream);
+  if (side) cudaStreamDestroy(side);
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
 }
 
 static void require(bool cond, const std::string& msg, int code = PMG_ERR_INVALID_ARG) {
@@ -78,6 +81,9 @@ static void set_views(Ctx& c) {
     for (int k = 0; k < 6; ++k) v.bctype[k] = c.bctype[k];
     const char* ex = getenv("PMG_EXP");
     v.exp = ex ? atoi(ex) : 0;
+    v.dense = d.dense ? 1 : 0;
+    v.nside = 1 << (l - 1);
+    v.bczero = d.bczero ? 1 : 0;
   }
 }
 
@@ -111,6 +117,7 @@ static void upload_bc(Ctx& c) {
     }
     d.bcoff.upload(off, c.stream);
     d.bcval.upload(vals, c.stream);
+    d.bczero = vals.empty();
   }
 }
 
@@ -156,6 +163,20 @@ static void upload_stencils(Ctx& c) {
     }
     d.srow.upload(srow, c.stream);
     d.kind.upload(kind, c.stream);
+    // block classes for the specialised kernels
+    {
+      std::vector<int32_t> fast, slow;
+      for (int s = 0; s < d.nb; ++s) {
+        const int id = m.slots[(size_t)l][(size_t)s];
+        bool all_same = true;
+        for (int f = 0; f < F; ++f) all_same = all_same && m.nbr[(size_t)id * 6 + f] >= 0;
+        (kind[(size_t)s] == pmgdev::KIND_UNIFORM && all_same ? fast : slow).push_back(s);
+      }
+      d.n_fast = (int)fast.size();
+      d.n_slow = (int)slow.size();
+      d.fast_list.upload(fast, c.stream);
+      d.slow_list.upload(slow, c.stream);
+    }
     d.row_of.upload(row_of, c.stream);
     d.r_center.upload(center, c.stream);
     d.r_nb.upload(nbv, c.stream);
@@ -601,6 +622,15 @@ static void set_mesh(Ctx& c, int nb, const int32_t* level, const int32_t* coords
         }
       }
     }
+    {  // dense level: every block present and its slot equals its Morton code
+      const long nside = 1L << (l - 1);
+      long full = 1;
+      for (int k = 0; k < D; ++k) full *= nside;
+      bool dense = d.nb == full && nside <= 1024;
+      for (size_t s = 0; dense && s < v.size(); ++s)
+        dense = morton(&m.coords[(size_t)v[s] * 3], D) == (uint64_t)s;
+      d.dense = dense;
+    }
     const auto& ro = m.ref_order[(size_t)l];
     for (size_t q = 0; q < ro.size(); ++q) rpos[(size_t)m.slot_of[(size_t)ro[q]]] = (int32_t)q;
     d.nbr.upload(nbrs, c.stream);
@@ -818,6 +848,9 @@ pmg_b200_ctx* pmg_b200_create(int dim, int N, const double* lo, const double* hi
     PMG_CUDA(cudaSetDevice(device));
     PMG_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
     PMG_CUDA(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, device));
+    PMG_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+    PMG_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
+    PMG_CUDA(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
     PMG_CUDA(cudaMallocHost(&c.h_out, 4 * sizeof(double)));
     PMG_CUDA(cudaMallocHost(&c.h_status, sizeof(int)));
     c.ops = make_ops(dim, N);

@@ -1,0 +1,254 @@
+// coarse_cluster.cuh -- K6 on a thread-block cluster (3D levels with N <= 16).
+//
+// Same algorithm and row arithmetic as coarse.cuh (a replica of
+// detail::bicgstab, multigrid.hpp:208-280), distributed over a cluster of N
+// CTAs: CTA z owns plane z of the root block, one cell per thread, every
+// per-cell vector lives in registers.  The vectors the SpMV gathers (x, p^,
+// s^) are kept as zero-padded planes in each CTA's shared memory; the z-1 and
+// z+1 values are read from the neighbouring CTAs through distributed shared
+// memory.  Each dot product is reduced inside the CTA, its partial broadcast
+// to every CTA of the cluster by DSMEM stores, and after one cluster barrier
+// every CTA sums the N partials in rank order -- deterministic, and identical
+// in every CTA, so all CTAs take the same branch at every breakdown/stopping
+// test.  Five cluster barriers per iteration.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "coarse.cuh"
+
+namespace pmgdev {
+
+namespace cg = cooperative_groups;
+
+template <int N>
+struct CC {
+  static constexpr int P = N + 2;           // padded plane extent
+  static constexpr int PP = P * P;
+  static constexpr int THR = N * N;         // one thread per cell of the plane
+  static constexpr int NW = (THR + 31) / 32;
+  static constexpr int NSTAGE = 6;          // reduction stages per iteration (+ setup)
+};
+
+template <int N>
+__device__ __forceinline__ double cc_row(const CoarseFast& C, const double* __restrict__ G,
+                                         const double* __restrict__ Gm,
+                                         const double* __restrict__ Gp, uint8_t f, double dg,
+                                         int pi, int ii) {
+  // sorted column order: z-, y-, x-, diag, x+, y+, z+ (coarse.cuh); absent
+  // terms are exact zeros (0*x with x finite) and change nothing
+  constexpr int P = N + 2;
+  double s = 0;
+  if (f & 0x80) {
+    const double* sc = C.spec_c + (size_t)C.spec[ii] * 6;
+    s += sc[4] * Gm[pi];
+    s += sc[2] * G[pi - P];
+    s += sc[0] * G[pi - 1];
+    s += dg * G[pi];
+    s += sc[1] * G[pi + 1];
+    s += sc[3] * G[pi + P];
+    s += sc[5] * Gp[pi];
+    return s;
+  }
+  const double w = C.w;
+  s += ((f & 16) ? w : 0.0) * Gm[pi];
+  s += ((f & 4) ? w : 0.0) * G[pi - P];
+  s += ((f & 1) ? w : 0.0) * G[pi - 1];
+  s += dg * G[pi];
+  s += ((f & 2) ? w : 0.0) * G[pi + 1];
+  s += ((f & 8) ? w : 0.0) * G[pi + P];
+  s += ((f & 32) ? w : 0.0) * Gp[pi];
+  return s;
+}
+
+template <int N>
+__global__ void __launch_bounds__(CC<N>::THR) k_coarse_cluster(LevelView L, CoarseFast C,
+                                                               const double* __restrict__ phi_b,
+                                                               Rec* rec, int* status,
+                                                               double* diag_out) {
+  using G = Geo<3, N>;
+  using K = CC<N>;
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ double Gx[K::PP];                  // own plane of the gathered vector
+  __shared__ double part[K::NSTAGE][N][2];      // partials of every CTA, per stage
+  __shared__ double wred[K::NW][2];
+  const int z = (int)cl.block_rank();
+  const int t = threadIdx.x;
+  const int lane = t & 31, wid = t >> 5;
+  const int x = t % N, y = t / N;
+  const int ii = x + N * (y + N * z);
+  const int pi = (x + 1) + (y + 1) * K::P;
+  // neighbour planes (z-1, z+1); out-of-block planes alias our own (coefficient 0)
+  const double* Gm = z > 0 ? cl.map_shared_rank(Gx, z - 1) : Gx;
+  const double* Gp = z < N - 1 ? cl.map_shared_rank(Gx, z + 1) : Gx;
+  for (int q = t; q < K::PP; q += K::THR) Gx[q] = 0.0;
+  __syncthreads();
+  // ---- per-cell data (multigrid.hpp:213-217, 445-453)
+  const uint8_t f = C.flags[ii];
+  const double dg = C.diag[ii];
+  const double dinv = (dg != 0) ? 1.0 / dg : 1.0;
+  const bool unk = (f & 0x40) != 0;
+  const size_t a = G::addr(0, x, y, z);
+  double xv = unk ? L.phi[a] : 0.0;
+  double bv = 0;
+  if (unk) {
+    bv = L.rhs[a] + C.c0[ii];
+    for (int q = C.ob_start[ii]; q < C.ob_start[ii + 1]; ++q) bv += C.ob_val[q] * phi_b[C.ob_obj[q]];
+  }
+  // cluster-wide deterministic sum of (a, b): CTA tree, DSMEM broadcast, rank-ordered sum
+  auto csum = [&](int stage, double& va, double& vb) {
+    va = warp_sum(va);
+    vb = warp_sum(vb);
+    if (lane == 0) {
+      wred[wid][0] = va;
+      wred[wid][1] = vb;
+    }
+    __syncthreads();
+    if (t == 0) {
+      double sa = 0, sb = 0;
+      for (int w = 0; w < K::NW; ++w) {
+        sa += wred[w][0];
+        sb += wred[w][1];
+      }
+      for (int r = 0; r < (int)cl.num_blocks(); ++r) {
+        double* dst = cl.map_shared_rank(&part[stage][z][0], r);
+        dst[0] = sa;
+        dst[1] = sb;
+      }
+    }
+    cl.sync();
+    double sa = 0, sb = 0;
+    for (int r = 0; r < N; ++r) {
+      sa += part[stage][r][0];
+      sb += part[stage][r][1];
+    }
+    va = sa;
+    vb = sb;
+  };
+  Gx[pi] = xv;
+  cl.sync();  // every plane of x published
+  double r = 0;
+  if (unk) r = bv - cc_row<N>(C, Gx, Gm, Gp, f, dg, pi, ii);
+  const double r0 = r;
+  double n2 = unk ? r * r : 0.0, rho1 = unk ? r0 * r : 0.0;
+  csum(0, n2, rho1);
+  const double norm0 = sqrt(n2);
+  bool converged = false;
+  double rel = 1.0;
+  int iters = 0;
+  double p = 0, v = 0, s = 0, tv = 0;
+  if (norm0 == 0 || norm0 < 1e-300) {
+    converged = true;
+    rel = 0;
+  } else {
+    const double target = C.rel_tol * norm0;
+    double rho = 1, alpha = 1, omega = 1;
+    for (int it = 0; it < C.max_iters; ++it) {
+      if (rho1 == 0) break;
+      const double beta = it == 0 ? 0.0 : (rho1 / rho) * (alpha / omega);
+      if (unk) p = it == 0 ? r : r + beta * (p - omega * v);
+      const double ph = unk ? dinv * p : 0.0;
+      Gx[pi] = ph;
+      cl.sync();  // B1: p^ planes visible
+      v = unk ? cc_row<N>(C, Gx, Gm, Gp, f, dg, pi, ii) : 0.0;
+      double r0v = unk ? r0 * v : 0.0, dummy = 0;
+      csum(1, r0v, dummy);  // B2
+      if (r0v == 0) break;
+      alpha = rho1 / r0v;
+      s = unk ? r - alpha * v : 0.0;
+      double ss = s * s;
+      Gx[pi] = unk ? dinv * s : 0.0;  // s^ (neighbours finished reading p^ before B2)
+      const double sh = Gx[pi];
+      csum(2, ss, dummy);  // B3: also publishes s^
+      const double ns = sqrt(ss);
+      if (ns <= target) {
+        if (unk) xv += alpha * ph;
+        converged = true;
+        iters = it + 1;
+        rel = ns / norm0;
+        break;
+      }
+      tv = unk ? cc_row<N>(C, Gx, Gm, Gp, f, dg, pi, ii) : 0.0;
+      double ts = tv * s, tt = tv * tv;
+      csum(3, ts, tt);  // B4
+      if (tt == 0) break;
+      omega = ts / tt;
+      if (unk) {
+        xv += alpha * ph + omega * sh;
+        r = s - omega * tv;
+      }
+      double rr = unk ? r * r : 0.0, r0r = unk ? r0 * r : 0.0;
+      csum(4, rr, r0r);  // B5
+      rho = rho1;
+      iters = it + 1;
+      rel = sqrt(rr) / norm0;
+      if (rel <= C.rel_tol) {
+        converged = true;
+        break;
+      }
+      if (omega == 0) break;
+      rho1 = r0r;
+    }
+  }
+  const bool wb = converged || C.fallback_ok;
+  if (unk && wb) L.phi[a] = xv;
+  cl.sync();  // write-back complete in every plane before the tail
+  if (z != 0) return;
+  // ---- tail on rank 0 (whole root block): fallback, pins, level-1 record
+  __shared__ double sm[72];
+  if (t == 0) {
+    status[0] = wb ? 0 : 3;
+    diag_out[0] = rel;
+    diag_out[1] = (double)iters;
+  }
+  if (!converged && C.fallback_ok) {
+    double r0m = -1;
+    bool ok = false;
+    for (int it = 0; it < 20000 && !ok; ++it) {
+      for (int par = 0; par < 2; ++par) {
+        __threadfence_block();
+        for (int e = t; e < G::H; e += blockDim.x) gs_cell<3, N>(L, L, phi_b, 0, par, e);
+        __syncthreads();
+      }
+      if (it % 50 == 0) {
+        double m = 0;
+        for (int ce = t; ce < G::NI; ce += blockDim.x) {
+          bool ins;
+          const double rr = resid_cell<3, N>(L, L, phi_b, 0, ce / G::H, ce % G::H, &ins);
+          if (!ins) m = fmax(m, fabs(rr));
+        }
+        m = block_max(m, sm);
+        if (r0m < 0) r0m = m;
+        if (m <= C.rel_tol * r0m || m < 1e-300) ok = true;
+      }
+    }
+    if (!ok && t == 0) status[0] = 4;
+    __syncthreads();
+  }
+  if (L.srow[0] >= 0)
+    for (int ce = t; ce < G::NI; ce += blockDim.x) {
+      const int rr = L.row_of[(size_t)L.srow[0] * G::NI + ce];
+      if (rr >= 0 && L.r_mask[rr] == 1) L.phi[ce] = phi_b[L.r_pin[rr]];
+    }
+  __syncthreads();
+  double mx = 0, ss = 0, cnt = 0;
+  if (L.leaf[0]) {
+    for (int ce = t; ce < G::NI; ce += blockDim.x) {
+      bool ins;
+      const double rr = resid_cell<3, N>(L, L, phi_b, 0, ce / G::H, ce % G::H, &ins);
+      if (ins) continue;
+      mx = fmax(mx, fabs(rr));
+      ss += rr * rr;
+      cnt += 1;
+    }
+  }
+  mx = block_max(mx, sm);
+  ss = block_sum(ss, sm);
+  cnt = block_sum(cnt, sm);
+  if (t == 0) {
+    rec[1].max = mx;
+    rec[1].sumsq = ss;
+    rec[1].count = (long long)cnt;
+  }
+}
+
+}  // namespace pmgdev

@@ -85,8 +85,14 @@ struct LevelDev {
   DevBuf<double> phi, rhs, old, res, bcval, cfold, r_center, r_nb, r_bc;
   DevBuf<int8_t> r_obj, r_pin;
   DevBuf<int32_t> ref_slot;  // level_blocks order position -> slot
+  // block classes: "fast" = uniform stencil and all 2D faces same-level
+  // (served by the lean kernels), "slow" = everything else
+  DevBuf<int32_t> fast_list, slow_list;
+  int n_fast = 0, n_slow = 0;
   bool has_cf = false;       // some block has a coarse-fine face
   bool has_cfold = false;
+  bool dense = false;   // all blocks present, slot == Morton code
+  bool bczero = true;   // no Dirichlet face values (all zero)
   pmgdev::LevelView view{};
 };
 
@@ -130,6 +136,8 @@ struct Ctx {
   int device = 0;
   int sms = 148;  // multiprocessors of `device`
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // forked branch for concurrent block classes
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::string err;
 
   HostMesh mesh;

@@ -6,6 +6,7 @@
 #include "stencil_build.cuh"
 #include "tile_kernels.cuh"
 #include "coarse.cuh"
+#include "coarse_cluster.cuh"
 
 namespace pmghost {
 
@@ -35,10 +36,24 @@ struct OpsImpl final : Ops {
       static int occ = 0;
       if (!occ) PMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gs_pers<D, N>, TT::THREADS, 0));
       const int grid = std::min(L.nb, std::max(1, occ) * c.sms);
-      if (L.exp & 8)
-        k_gs_pers<D, N><<<grid, TT::THREADS, 0, c.stream>>>(L, Vc(c, l), c.phi_b.p, parity);
-      else
-        k_gs_tile<D, N><<<L.nb, TT::THREADS, 0, c.stream>>>(L, Vc(c, l), c.phi_b.p, parity);
+      (void)grid;
+      const LevelDev& d = *c.lev[(size_t)l];
+      // the latency-bound general blocks run on a forked branch concurrently
+      // with the bandwidth-bound lean blocks (both write disjoint cells)
+      const bool fork = d.n_fast > 0 && d.n_slow > 0;
+      if (fork) {
+        PMG_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+        PMG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+      }
+      if (d.n_slow > 0)
+        k_gs_tile<D, N><<<d.n_slow, TT::THREADS, 0, fork ? c.side : c.stream>>>(
+            L, Vc(c, l), c.phi_b.p, parity, d.slow_list.p);
+      if (d.n_fast > 0)
+        k_gs_lean<D, N><<<d.n_fast, Lean<D, N>::THR, 0, c.stream>>>(L, parity, d.fast_list.p);
+      if (fork) {
+        PMG_CUDA(cudaEventRecord(c.ev_join, c.side));
+        PMG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
+      }
     }
     else
       k_gs<D, N><<<grid_for((long long)L.nb * G::H), kThreads, 0, c.stream>>>(L, Vc(c, l),
@@ -149,6 +164,33 @@ struct OpsImpl final : Ops {
       for (int k = 0; k < D; ++k) lim *= 8;
       F.fallback_ok = c.coarse.n <= lim + 1;
       F.n_unknowns = c.coarse.n;
+      if constexpr (D == 3 && (N == 8 || N == 16)) {
+        if (!(V(c, 1).exp & 32)) {
+          // one CTA per z-plane of the root block, as one thread-block cluster
+          static bool cattr = false;
+          if (!cattr) {
+            PMG_CUDA(cudaFuncSetAttribute(k_coarse_cluster<N>,
+                                          cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            cattr = true;
+          }
+          cudaLaunchConfig_t cfgl = {};
+          cfgl.gridDim = dim3(N, 1, 1);
+          cfgl.blockDim = dim3(CC<N>::THR, 1, 1);
+          cfgl.dynamicSmemBytes = 0;
+          cfgl.stream = c.stream;
+          cudaLaunchAttribute at[1];
+          at[0].id = cudaLaunchAttributeClusterDimension;
+          at[0].val.clusterDim.x = N;
+          at[0].val.clusterDim.y = 1;
+          at[0].val.clusterDim.z = 1;
+          cfgl.attrs = at;
+          cfgl.numAttrs = 1;
+          PMG_CUDA(cudaLaunchKernelEx(&cfgl, k_coarse_cluster<N>, V(c, 1), F, (const double*)c.phi_b.p,
+                                      c.rec.p, c.status.p, c.diag.p));
+          check();
+          return;
+        }
+      }
       constexpr size_t smem = coarse_fast_smem<D, N>();
       static bool attr = false;
       if (!attr) {

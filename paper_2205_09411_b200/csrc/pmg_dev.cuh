@@ -61,7 +61,68 @@ struct LevelView {
   const int32_t* cfoff;   // [nb*2D] offset into cfold or -1
   int bctype[6];          // per domain face: 0 Dirichlet, 1 Neumann-zero (mesh.hpp:22-32)
   int exp;                // performance-experiment switches (PMG_EXP, 0 in production)
+  int dense;              // 1: all (2^(l-1))^D blocks present and slot == Morton code
+  int nside;              // blocks per axis on this level (dense levels)
+  int bczero;             // 1: no Dirichlet face values on this level (all zero)
 };
+
+// Morton (Z-order) helpers: on a dense level the slot of a block is the
+// interleave of its coordinates, so face neighbours need no table lookup.
+__device__ __forceinline__ unsigned m_part3(unsigned x) {  // 10 bits -> every 3rd bit
+  x &= 0x3ffu;
+  x = (x | (x << 16)) & 0x030000ffu;
+  x = (x | (x << 8)) & 0x0300f00fu;
+  x = (x | (x << 4)) & 0x030c30c3u;
+  x = (x | (x << 2)) & 0x09249249u;
+  return x;
+}
+__device__ __forceinline__ unsigned m_comp3(unsigned x) {
+  x &= 0x09249249u;
+  x = (x | (x >> 2)) & 0x030c30c3u;
+  x = (x | (x >> 4)) & 0x0300f00fu;
+  x = (x | (x >> 8)) & 0x030000ffu;
+  x = (x | (x >> 16)) & 0x3ffu;
+  return x;
+}
+__device__ __forceinline__ unsigned m_part2(unsigned x) {  // 16 bits -> every 2nd bit
+  x &= 0xffffu;
+  x = (x | (x << 8)) & 0x00ff00ffu;
+  x = (x | (x << 4)) & 0x0f0f0f0fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x;
+}
+__device__ __forceinline__ unsigned m_comp2(unsigned x) {
+  x &= 0x55555555u;
+  x = (x | (x >> 1)) & 0x33333333u;
+  x = (x | (x >> 2)) & 0x0f0f0f0fu;
+  x = (x | (x >> 4)) & 0x00ff00ffu;
+  x = (x | (x >> 8)) & 0xffffu;
+  return x;
+}
+// same-level neighbour slot across face dir of a dense level, -1 at the domain boundary
+template <int D>
+__device__ __forceinline__ int dense_nbr(int slot, int dir, int nside) {
+  const unsigned s = (unsigned)slot;
+  int c[3];
+  if (D == 3) {
+    c[0] = (int)m_comp3(s);
+    c[1] = (int)m_comp3(s >> 1);
+    c[2] = (int)m_comp3(s >> 2);
+  } else {
+    c[0] = (int)m_comp2(s);
+    c[1] = (int)m_comp2(s >> 1);
+  }
+  c[dir >> 1] += (dir & 1) ? 1 : -1;
+  if (c[dir >> 1] < 0 || c[dir >> 1] >= nside) return -1;
+  if (D == 3) return (int)(m_part3(c[0]) | (m_part3(c[1]) << 1) | (m_part3(c[2]) << 2));
+  return (int)(m_part2(c[0]) | (m_part2(c[1]) << 1));
+}
+// neighbour slot via the table, or arithmetically on dense levels
+template <int D>
+__device__ __forceinline__ int nbr_slot(const LevelView& L, int slot, int dir) {
+  return L.dense ? dense_nbr<D>(slot, dir, L.nside) : L.nbr[slot * 2 * D + dir];
+}
 
 template <int D>
 struct Ipow {

@@ -72,9 +72,9 @@ struct Halo {
     for (int u = 0; u < PER; ++u) {
       const int q = threadIdx.x + u * Tile<D, N>::THREADS;
       const int f = slot * G::F + q / HT;
-      ns[u] = q < NQ ? L.nbr[f] : -2;
-      cn[u] = q < NQ ? L.cnbr[f] : -1;
-      bo[u] = q < NQ ? L.bcoff[f] : -1;
+      ns[u] = q < NQ ? nbr_slot<D>(L, slot, q / HT) : -2;
+      cn[u] = (q < NQ && !L.dense) ? L.cnbr[f] : -1;
+      bo[u] = (q < NQ && !L.bczero) ? L.bcoff[f] : -1;
     }
   }
   template <int AXIS, int SIDE>
@@ -147,12 +147,13 @@ struct Halo {
 template <int D, int N>
 __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_gs_tile(LevelView L, LevelView Lc,
                                                                  const double* __restrict__ phi_b,
-                                                                 int parity) {
+                                                                 int parity,
+                                                                 const int32_t* __restrict__ list) {
   using G = Geo<D, N>;
   using TT = Tile<D, N>;
   using O = Own<D, N>;
   __shared__ double T[TT::SIZE];
-  const int slot = blockIdx.x;
+  const int slot = list ? list[blockIdx.x] : blockIdx.x;
   const int c = parity, X = 1 - c;
   const size_t base = (size_t)slot * G::NI;
   Halo<D, N> h;
@@ -209,6 +210,119 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_gs_tile(LevelView L, Le
     double p[2 * D];
     nbrs_at<D, N>(T, B, (c + j + k) & 1, p);
     dst[e] = gs_value<D>(L, phi_b, kind, r, p, gv[q]);
+  }
+}
+
+// ------------------------------------------------------------------ lean GS-RB for interior blocks
+// Blocks whose stencil is uniform and whose 2D faces all have a same-level
+// neighbour (about two thirds of a uniform level) need none of the physical /
+// coarse-fine / interface machinery: the halo is a plain gather and the
+// update is the constant-coefficient formula.  Fewer registers per thread let
+// more CTAs share an SM, which is what hides the DRAM latency here.
+template <int D, int N>
+struct Lean {
+  using G = Geo<D, N>;
+  static constexpr int THR = G::H < 512 ? G::H : 512;
+  static constexpr int PER = G::H / THR;
+  static constexpr int HN = N / 2;
+  static constexpr int RS = THR / HN;
+  static constexpr int HT = G::NT / 2;
+  static constexpr int HQ = G::F * HT;
+  static constexpr int HPER = (HQ + THR - 1) / THR;
+};
+
+template <int D, int N, int AXIS, int SIDE>
+__device__ __forceinline__ double lean_halo(const LevelView& L, int ns, int X, int r, int& tix) {
+  using G = Geo<D, N>;
+  using TT = Tile<D, N>;
+  constexpr int AC = SIDE ? N - 1 : 0;
+  int c3[3] = {0, 0, 0};
+  if (D == 2) {
+    c3[AXIS] = AC;
+    c3[1 - AXIS] = 2 * r + ((1 - X + AC) & 1);
+  } else {
+    constexpr int A0 = AXIS == 0 ? 1 : 0;
+    constexpr int A1 = AXIS == 2 ? 1 : 2;
+    const int t1 = r / (N / 2);
+    c3[AXIS] = AC;
+    c3[A1] = t1;
+    c3[A0] = 2 * (r % (N / 2)) + ((1 - X + AC + t1) & 1);
+  }
+  int p3[3] = {c3[0] + 1, c3[1] + 1, c3[2] + 1};
+  p3[AXIS] = SIDE ? N + 1 : 0;
+  tix = TT::idx(p3[0], p3[1], p3[2]);
+  c3[AXIS] = SIDE ? 0 : N - 1;
+  return L.phi[(size_t)ns * G::NI + (size_t)X * G::H + G::entry(c3[0], c3[1], c3[2])];
+}
+
+template <int D, int N>
+__global__ void __launch_bounds__(Lean<D, N>::THR) k_gs_lean(LevelView L, int parity,
+                                                            const int32_t* __restrict__ list) {
+  using G = Geo<D, N>;
+  using TT = Tile<D, N>;
+  using LN = Lean<D, N>;
+  __shared__ double T[TT::SIZE];
+  const int slot = list[blockIdx.x];
+  const int c = parity, X = 1 - c;
+  const int t = threadIdx.x;
+  const size_t base = (size_t)slot * G::NI;
+  int ns[LN::HPER];
+#pragma unroll
+  for (int u = 0; u < LN::HPER; ++u) {
+    const int q = t + u * LN::THR;
+    ns[u] = q < LN::HQ ? nbr_slot<D>(L, slot, q / LN::HT) : 0;
+  }
+  double ov[LN::PER], gv[LN::PER];
+#pragma unroll
+  for (int q = 0; q < LN::PER; ++q) {
+    ov[q] = L.phi[base + (size_t)X * G::H + t + q * LN::THR];
+    gv[q] = L.rhs[base + (size_t)c * G::H + t + q * LN::THR];
+  }
+  double hv[LN::HPER];
+  int hix[LN::HPER];
+#pragma unroll
+  for (int u = 0; u < LN::HPER; ++u) {
+    const int q = t + u * LN::THR;
+    hix[u] = -1;
+    if (q >= LN::HQ) continue;
+    const int dir = q / LN::HT, r = q % LN::HT;
+    switch (dir) {
+      case 0: hv[u] = lean_halo<D, N, 0, 0>(L, ns[u], X, r, hix[u]); break;
+      case 1: hv[u] = lean_halo<D, N, 0, 1>(L, ns[u], X, r, hix[u]); break;
+      case 2: hv[u] = lean_halo<D, N, 1, 0>(L, ns[u], X, r, hix[u]); break;
+      case 3: hv[u] = lean_halo<D, N, 1, 1>(L, ns[u], X, r, hix[u]); break;
+      case 4: if (D == 3) hv[u] = lean_halo<D, N, 2 % D, 0>(L, ns[u], X, r, hix[u]); break;
+      default: if (D == 3) hv[u] = lean_halo<D, N, 2 % D, 1>(L, ns[u], X, r, hix[u]); break;
+    }
+  }
+  const int m = t % LN::HN;
+  const int row0 = t / LN::HN;
+#pragma unroll
+  for (int q = 0; q < LN::PER; ++q) {
+    const int row = row0 + LN::RS * q;
+    const int j = row % N, k = D == 3 ? row / N : 0;
+    const int B = (D == 3 ? ((k + 1) * TT::P + (j + 1)) : (j + 1)) * TT::RW + m;
+    T[B + ((X + j + k) & 1)] = ov[q];
+  }
+#pragma unroll
+  for (int u = 0; u < LN::HPER; ++u)
+    if (hix[u] >= 0) T[hix[u]] = hv[u];
+  __syncthreads();
+  double* __restrict__ dst = L.phi + base + (size_t)c * G::H;
+  const double h2 = L.h2;
+#pragma unroll
+  for (int q = 0; q < LN::PER; ++q) {
+    const int row = row0 + LN::RS * q;
+    const int j = row % N, k = D == 3 ? row / N : 0;
+    const int B = (D == 3 ? ((k + 1) * TT::P + (j + 1)) : (j + 1)) * TT::RW + m;
+    const int o = (c + j + k) & 1;
+    double v;
+    if (D == 3)  // multigrid.hpp:651-653
+      v = div6(T[B] + T[B + 1] + T[B + o - TT::RW] + T[B + o + TT::RW] + T[B + o - TT::RW * TT::P] +
+               T[B + o + TT::RW * TT::P] - h2 * gv[q]);
+    else  // multigrid.hpp:640-641
+      v = 0.25 * (T[B] + T[B + 1] + T[B + o - TT::RW] + T[B + o + TT::RW] - h2 * gv[q]);
+    dst[t + q * LN::THR] = v;
   }
 }
 

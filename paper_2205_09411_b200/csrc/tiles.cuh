@@ -39,9 +39,10 @@ __device__ __forceinline__ double div6(double x) {
   const double q = __dmul_rn(x, y);
   const double r = __fma_rn(-q, 6.0, x);
   const double q1 = __fma_rn(r, y, q);
-  const double aq = fabs(q);
-  if (__builtin_expect(aq > 1e-300 && aq < 1e300, 1)) return q1;
-  return div6_slow(x);
+  const double ax = fabs(x);
+  if (__builtin_expect(ax > 1e-290 && ax < 1e300, 1)) return q1;
+  if (x == 0.0) return q;  // +-0 * RN(1/6) = +-0 = x / 6
+  return div6_slow(x);     // subnormal / huge / inf / nan
 }
 
 // Face-ghost loader for one face (AXIS, SIDE compile-time): ghost cells of
@@ -191,7 +192,7 @@ __device__ __forceinline__ double gs_value(const LevelView& L, const double* __r
                                           uint8_t kind, int r, const double* p, double g) {
   const double h2 = L.h2;
   if (kind == KIND_UNIFORM) {
-    if (D == 3) return (p[0] + p[1] + p[2] + p[3] + p[4] + p[5] - h2 * g) / 6.0;
+    if (D == 3) return div6(p[0] + p[1] + p[2] + p[3] + p[4] + p[5] - h2 * g);
     return 0.25 * (p[0] + p[1] + p[2] + p[3] - h2 * g);
   }
   if (r < 0) {
