@@ -165,17 +165,34 @@ static void upload_stencils(Ctx& c) {
     d.kind.upload(kind, c.stream);
     // block classes for the specialised kernels
     {
-      std::vector<int32_t> fast, slow;
+      std::vector<int32_t> fast, slow, ufast, uslow, fix[2];
       for (int s = 0; s < d.nb; ++s) {
         const int id = m.slots[(size_t)l][(size_t)s];
-        bool all_same = true;
-        for (int f = 0; f < F; ++f) all_same = all_same && m.nbr[(size_t)id * 6 + f] >= 0;
-        (kind[(size_t)s] == pmgdev::KIND_UNIFORM && all_same ? fast : slow).push_back(s);
+        bool no_cf = true;  // lean kernels handle same-level and physical faces
+        for (int f = 0; f < F; ++f)
+          no_cf = no_cf && !(m.nbr[(size_t)id * 6 + f] < 0 && m.cnbr[(size_t)id * 6 + f] >= 0);
+        (no_cf ? fast : slow).push_back(s);
+        (no_cf && kind[(size_t)s] == pmgdev::KIND_UNIFORM ? ufast : uslow).push_back(s);
+        // special rows of lean interface blocks, per colour, for k_gs_fix
+        if (no_cf && kind[(size_t)s] == pmgdev::KIND_IFACE) {
+          const int32_t* page = row_of.data() + (size_t)srow[(size_t)s] * NI;
+          for (int cc = 0; cc < 2; ++cc)
+            for (int e = 0; e < H; ++e)
+              if (page[cc * H + e] >= 0) fix[cc].push_back(s), fix[cc].push_back(e);
+        }
       }
       d.n_fast = (int)fast.size();
       d.n_slow = (int)slow.size();
       d.fast_list.upload(fast, c.stream);
       d.slow_list.upload(slow, c.stream);
+      d.n_ufast = (int)ufast.size();
+      d.n_uslow = (int)uslow.size();
+      d.ufast_list.upload(ufast, c.stream);
+      d.uslow_list.upload(uslow, c.stream);
+      for (int cc = 0; cc < 2; ++cc) {
+        d.n_fix[cc] = (int)fix[cc].size() / 2;
+        d.fix_list[cc].upload(fix[cc], c.stream);
+      }
     }
     d.row_of.upload(row_of, c.stream);
     d.r_center.upload(center, c.stream);

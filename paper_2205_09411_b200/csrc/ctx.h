@@ -89,6 +89,11 @@ struct LevelDev {
   // (served by the lean kernels), "slow" = everything else
   DevBuf<int32_t> fast_list, slow_list;
   int n_fast = 0, n_slow = 0;
+  // residual-family classes: lean = uniform stencil without coarse-fine faces
+  DevBuf<int32_t> ufast_list, uslow_list;
+  int n_ufast = 0, n_uslow = 0;
+  DevBuf<int32_t> fix_list[2];  // (slot, entry) pairs of special rows in lean interface blocks
+  int n_fix[2] = {0, 0};
   bool has_cf = false;       // some block has a coarse-fine face
   bool has_cfold = false;
   bool dense = false;   // all blocks present, slot == Morton code

@@ -50,6 +50,9 @@ struct OpsImpl final : Ops {
             L, Vc(c, l), c.phi_b.p, parity, d.slow_list.p);
       if (d.n_fast > 0)
         k_gs_lean<D, N><<<d.n_fast, Lean<D, N>::THR, 0, c.stream>>>(L, parity, d.fast_list.p);
+      if (d.n_fix[parity] > 0)
+        k_gs_fix<D, N><<<grid_for(d.n_fix[parity]), 256, 0, c.stream>>>(
+            L, Vc(c, l), c.phi_b.p, parity, (const int2*)d.fix_list[parity].p, d.n_fix[parity]);
       if (fork) {
         PMG_CUDA(cudaEventRecord(c.ev_join, c.side));
         PMG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
@@ -132,8 +135,22 @@ struct OpsImpl final : Ops {
   void record(Ctx& c, int l) override {
     const LevelView& L = V(c, l);
     if constexpr (TILE) {
-      k_record_tile<D, N><<<L.nb, TT::THREADS, 0, c.stream>>>(L, Vc(c, l), c.phi_b.p, c.partial.p,
-                                                              c.rec.p, c.counter.p);
+      const LevelDev& d = *c.lev[(size_t)l];
+      const bool fork = d.n_ufast > 0 && d.n_uslow > 0;
+      if (fork) {
+        PMG_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+        PMG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+      }
+      if (d.n_uslow > 0)
+        k_record_tile<D, N><<<d.n_uslow, TT::THREADS, 0, fork ? c.side : c.stream>>>(
+            L, Vc(c, l), c.phi_b.p, c.partial.p, c.rec.p, c.counter.p, d.uslow_list.p);
+      if (d.n_ufast > 0)
+        k_record_lean<D, N><<<d.n_ufast, TT::THREADS, 0, c.stream>>>(L, c.partial.p, c.rec.p,
+                                                                     c.counter.p, d.ufast_list.p);
+      if (fork) {
+        PMG_CUDA(cudaEventRecord(c.ev_join, c.side));
+        PMG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
+      }
       check();
       return;
     }

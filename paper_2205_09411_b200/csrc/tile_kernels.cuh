@@ -232,7 +232,8 @@ struct Lean {
 };
 
 template <int D, int N, int AXIS, int SIDE>
-__device__ __forceinline__ double lean_halo(const LevelView& L, int ns, int X, int r, int& tix) {
+__device__ __forceinline__ double lean_halo(const LevelView& L, int ns, int X, int r, int& tix,
+                                            int slot) {
   using G = Geo<D, N>;
   using TT = Tile<D, N>;
   constexpr int AC = SIDE ? N - 1 : 0;
@@ -251,6 +252,17 @@ __device__ __forceinline__ double lean_halo(const LevelView& L, int ns, int X, i
   int p3[3] = {c3[0] + 1, c3[1] + 1, c3[2] + 1};
   p3[AXIS] = SIDE ? N + 1 : 0;
   tix = TT::idx(p3[0], p3[1], p3[2]);
+  if (ns < 0) {  // physical face: Dirichlet 2 bc - f1 / Neumann f1 (mesh.hpp:538-552)
+    constexpr int DIR = 2 * AXIS + SIDE;
+    const double self = L.phi[(size_t)slot * G::NI + (size_t)(1 - X) * G::H + G::entry(c3[0], c3[1], c3[2])];
+    if (L.bctype[DIR] == 1) return self;
+    double bcv = 0.0;
+    if (!L.bczero) {
+      const int bo = L.bcoff[slot * G::F + DIR];
+      if (bo >= 0) bcv = L.bcval[bo + G::tindex(AXIS, c3[0], c3[1], c3[2])];
+    }
+    return 2.0 * bcv - self;
+  }
   c3[AXIS] = SIDE ? 0 : N - 1;
   return L.phi[(size_t)ns * G::NI + (size_t)X * G::H + G::entry(c3[0], c3[1], c3[2])];
 }
@@ -262,15 +274,17 @@ __global__ void __launch_bounds__(Lean<D, N>::THR) k_gs_lean(LevelView L, int pa
   using TT = Tile<D, N>;
   using LN = Lean<D, N>;
   __shared__ double T[TT::SIZE];
-  const int slot = list[blockIdx.x];
+  const int slot = (L.exp & 128) ? (int)blockIdx.x : list[blockIdx.x];
   const int c = parity, X = 1 - c;
   const int t = threadIdx.x;
   const size_t base = (size_t)slot * G::NI;
+  const uint8_t kind = L.kind[slot];
   int ns[LN::HPER];
 #pragma unroll
   for (int u = 0; u < LN::HPER; ++u) {
     const int q = t + u * LN::THR;
-    ns[u] = q < LN::HQ ? nbr_slot<D>(L, slot, q / LN::HT) : 0;
+    ns[u] = q < LN::HQ ? nbr_slot<D>(L, slot, q / LN::HT) : 0;  // -1: physical face
+    if (L.exp & 64) ns[u] = 0;
   }
   double ov[LN::PER], gv[LN::PER];
 #pragma unroll
@@ -287,12 +301,12 @@ __global__ void __launch_bounds__(Lean<D, N>::THR) k_gs_lean(LevelView L, int pa
     if (q >= LN::HQ) continue;
     const int dir = q / LN::HT, r = q % LN::HT;
     switch (dir) {
-      case 0: hv[u] = lean_halo<D, N, 0, 0>(L, ns[u], X, r, hix[u]); break;
-      case 1: hv[u] = lean_halo<D, N, 0, 1>(L, ns[u], X, r, hix[u]); break;
-      case 2: hv[u] = lean_halo<D, N, 1, 0>(L, ns[u], X, r, hix[u]); break;
-      case 3: hv[u] = lean_halo<D, N, 1, 1>(L, ns[u], X, r, hix[u]); break;
-      case 4: if (D == 3) hv[u] = lean_halo<D, N, 2 % D, 0>(L, ns[u], X, r, hix[u]); break;
-      default: if (D == 3) hv[u] = lean_halo<D, N, 2 % D, 1>(L, ns[u], X, r, hix[u]); break;
+      case 0: hv[u] = lean_halo<D, N, 0, 0>(L, ns[u], X, r, hix[u], slot); break;
+      case 1: hv[u] = lean_halo<D, N, 0, 1>(L, ns[u], X, r, hix[u], slot); break;
+      case 2: hv[u] = lean_halo<D, N, 1, 0>(L, ns[u], X, r, hix[u], slot); break;
+      case 3: hv[u] = lean_halo<D, N, 1, 1>(L, ns[u], X, r, hix[u], slot); break;
+      case 4: if (D == 3) hv[u] = lean_halo<D, N, 2 % D, 0>(L, ns[u], X, r, hix[u], slot); break;
+      default: if (D == 3) hv[u] = lean_halo<D, N, 2 % D, 1>(L, ns[u], X, r, hix[u], slot); break;
     }
   }
   const int m = t % LN::HN;
@@ -310,20 +324,62 @@ __global__ void __launch_bounds__(Lean<D, N>::THR) k_gs_lean(LevelView L, int pa
   __syncthreads();
   double* __restrict__ dst = L.phi + base + (size_t)c * G::H;
   const double h2 = L.h2;
+  if (kind == KIND_ALL_INSIDE) return;  // every cell pinned
+  if (kind == KIND_UNIFORM) {
+#pragma unroll
+    for (int q = 0; q < LN::PER; ++q) {
+      const int row = row0 + LN::RS * q;
+      const int j = row % N, k = D == 3 ? row / N : 0;
+      const int B = (D == 3 ? ((k + 1) * TT::P + (j + 1)) : (j + 1)) * TT::RW + m;
+      const int o = (c + j + k) & 1;
+      double v;
+      if (D == 3)  // multigrid.hpp:651-653
+        v = div6(T[B] + T[B + 1] + T[B + o - TT::RW] + T[B + o + TT::RW] + T[B + o - TT::RW * TT::P] +
+                 T[B + o + TT::RW * TT::P] - h2 * gv[q]);
+      else  // multigrid.hpp:640-641
+        v = 0.25 * (T[B] + T[B + 1] + T[B + o - TT::RW] + T[B + o + TT::RW] - h2 * gv[q]);
+      dst[t + q * LN::THR] = v;
+    }
+    return;
+  }
+  // interface block: the uniform-row formula of multigrid.hpp:667-672 for every
+  // cell; its special (cut / inside) rows are redone by k_gs_fix afterwards
 #pragma unroll
   for (int q = 0; q < LN::PER; ++q) {
     const int row = row0 + LN::RS * q;
     const int j = row % N, k = D == 3 ? row / N : 0;
     const int B = (D == 3 ? ((k + 1) * TT::P + (j + 1)) : (j + 1)) * TT::RW + m;
     const int o = (c + j + k) & 1;
-    double v;
-    if (D == 3)  // multigrid.hpp:651-653
-      v = div6(T[B] + T[B + 1] + T[B + o - TT::RW] + T[B + o + TT::RW] + T[B + o - TT::RW * TT::P] +
-               T[B + o + TT::RW * TT::P] - h2 * gv[q]);
-    else  // multigrid.hpp:640-641
-      v = 0.25 * (T[B] + T[B + 1] + T[B + o - TT::RW] + T[B + o + TT::RW] - h2 * gv[q]);
-    dst[t + q * LN::THR] = v;
+    double sv = -h2 * gv[q];
+    sv += T[B];
+    sv += T[B + 1];
+    sv += T[B + o - TT::RW];
+    sv += T[B + o + TT::RW];
+    if (D == 3) {
+      sv += T[B + o - TT::RW * TT::P];
+      sv += T[B + o + TT::RW * TT::P];
+    }
+    dst[t + q * LN::THR] = -sv * (-1.0 / (2.0 * D));
   }
+}
+
+// Special rows of interface blocks after k_gs_lean: cut rows get their
+// boundary-modified update (multigrid.hpp:674-684), inside rows their pinned
+// value back.  One thread per special cell of the active colour.
+template <int D, int N>
+__global__ void __launch_bounds__(256) k_gs_fix(LevelView L, LevelView Lc,
+                                               const double* __restrict__ phi_b, int parity,
+                                               const int2* __restrict__ cells, int n) {
+  using G = Geo<D, N>;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int2 se = cells[i];
+  const int r = L.row_of[(size_t)L.srow[se.x] * G::NI + parity * G::H + se.y];
+  if (L.r_mask[r] == 1) {
+    L.phi[(size_t)se.x * G::NI + (size_t)parity * G::H + se.y] = phi_b[L.r_pin[r]];
+    return;
+  }
+  gs_cell<D, N>(L, Lc, phi_b, se.x, parity, se.y);
 }
 
 // ------------------------------------------------------------------ persistent GS-RB half-sweep
@@ -707,11 +763,53 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_prolong_tile(LevelView 
 }
 
 // ------------------------------------------------------------------ residual record
+// Per-block partials (max |r|, sum r^2, count) of the leaf cells, written by
+// one or two kernels (lean + general block classes, possibly concurrent); the
+// CTA that completes the level's count reduces all partials in slot order
+// (deterministic, multigrid.hpp:555-561).
+__device__ __forceinline__ void record_finish(const LevelView& L, Rec* __restrict__ partial,
+                                              Rec* rec, unsigned int* counter, int slot,
+                                              double mx, double ss, double cnt, double* sm,
+                                              bool* last) {
+  mx = block_max(mx, sm);
+  ss = block_sum(ss, sm);
+  cnt = block_sum(cnt, sm);
+  if (threadIdx.x == 0) {
+    partial[slot].max = mx;
+    partial[slot].sumsq = ss;
+    partial[slot].count = (long long)cnt;
+    __threadfence();
+    *last = atomicAdd(counter, 1u) == (unsigned)L.nb - 1;
+  }
+  __syncthreads();
+  if (!*last) return;
+  __threadfence();
+  mx = 0;
+  ss = 0;
+  double cc = 0;
+  for (int b = threadIdx.x; b < L.nb; b += blockDim.x) {
+    const volatile Rec* p = partial + b;
+    mx = fmax(mx, p->max);
+    ss += p->sumsq;
+    cc += (double)p->count;
+  }
+  mx = block_max(mx, sm);
+  ss = block_sum(ss, sm);
+  cc = block_sum(cc, sm);
+  if (threadIdx.x == 0) {
+    rec[L.level].max = mx;
+    rec[L.level].sumsq = ss;
+    rec[L.level].count = (long long)cc;
+    *counter = 0;
+  }
+}
+
 template <int D, int N>
 __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_record_tile(LevelView L, LevelView Lc,
                                                                      const double* __restrict__ phi_b,
                                                                      Rec* __restrict__ partial,
-                                                                     Rec* rec, unsigned int* counter) {
+                                                                     Rec* rec, unsigned int* counter,
+                                                                     const int32_t* __restrict__ list) {
   using G = Geo<D, N>;
   using TT = Tile<D, N>;
   using O = Own<D, N>;
@@ -719,7 +817,7 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_record_tile(LevelView L
   __shared__ double T1[TT::SIZE];
   __shared__ double sm[72];
   __shared__ bool last;
-  const int slot = blockIdx.x;
+  const int slot = list ? list[blockIdx.x] : blockIdx.x;
   const size_t base = (size_t)slot * G::NI;
   double mx = 0, ss = 0, cnt = 0;
   const bool leaf = L.leaf[slot] != 0;
@@ -758,37 +856,103 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_record_tile(LevelView L
       }
     }
   }
-  mx = block_max(mx, sm);
-  ss = block_sum(ss, sm);
-  cnt = block_sum(cnt, sm);
-  if (threadIdx.x == 0) {
-    partial[slot].max = mx;
-    partial[slot].sumsq = ss;
-    partial[slot].count = (long long)cnt;
-    __threadfence();
-    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  record_finish(L, partial, rec, counter, slot, mx, ss, cnt, sm, &last);
+}
+
+// Lean record for interior uniform blocks: both colours asynchronously into
+// shared memory, halos gathered from the same-level neighbours, uniform
+// residual g - (sum_6 - 2D phi) w (stencil.hpp:336-342) for every cell.
+template <int D, int N>
+__global__ void __launch_bounds__(Tile<D, N>::THREADS) k_record_lean(LevelView L,
+                                                                     Rec* __restrict__ partial,
+                                                                     Rec* rec, unsigned int* counter,
+                                                                     const int32_t* __restrict__ list) {
+  using G = Geo<D, N>;
+  using TT = Tile<D, N>;
+  using O = Own<D, N>;
+  using LN = Lean<D, N>;
+  constexpr int HPER = (LN::HQ + TT::THREADS - 1) / TT::THREADS;
+  __shared__ double T0[TT::SIZE];
+  __shared__ double T1[TT::SIZE];
+  __shared__ double sm[72];
+  __shared__ bool last;
+  const int slot = list[blockIdx.x];
+  const int t = threadIdx.x;
+  const size_t base = (size_t)slot * G::NI;
+  double mx = 0, ss = 0, cnt = 0;
+  const bool leaf = L.leaf[slot] != 0;
+  if (leaf) {
+    int ns[HPER];
+#pragma unroll
+    for (int u = 0; u < HPER; ++u) {
+      const int q = t + u * TT::THREADS;
+      ns[u] = q < LN::HQ ? nbr_slot<D>(L, slot, q / LN::HT) : 0;  // -1: physical face
+    }
+#pragma unroll
+    for (int q = 0; q < O::PER; ++q) {
+      int j, k, B;
+      O::at(q, j, k, B);
+      const int e = t + q * O::THR;
+      const int o0 = (j + k) & 1;
+      cp_async8(&T0[B + o0], L.phi + base + e);
+      cp_async8(&T1[B + 1 - o0], L.phi + base + G::H + e);
+    }
+    double hv[2][HPER];
+    int hix[2][HPER];
+#pragma unroll
+    for (int X = 0; X < 2; ++X)
+#pragma unroll
+      for (int u = 0; u < HPER; ++u) {
+        const int q = t + u * TT::THREADS;
+        hix[X][u] = -1;
+        if (q >= LN::HQ) continue;
+        const int dir = q / LN::HT, r = q % LN::HT;
+        switch (dir) {
+          case 0: hv[X][u] = lean_halo<D, N, 0, 0>(L, ns[u], X, r, hix[X][u], slot); break;
+          case 1: hv[X][u] = lean_halo<D, N, 0, 1>(L, ns[u], X, r, hix[X][u], slot); break;
+          case 2: hv[X][u] = lean_halo<D, N, 1, 0>(L, ns[u], X, r, hix[X][u], slot); break;
+          case 3: hv[X][u] = lean_halo<D, N, 1, 1>(L, ns[u], X, r, hix[X][u], slot); break;
+          case 4: if (D == 3) hv[X][u] = lean_halo<D, N, 2 % D, 0>(L, ns[u], X, r, hix[X][u], slot); break;
+          default: if (D == 3) hv[X][u] = lean_halo<D, N, 2 % D, 1>(L, ns[u], X, r, hix[X][u], slot); break;
+        }
+      }
+#pragma unroll
+    for (int u = 0; u < HPER; ++u) {
+      if (hix[0][u] >= 0) T0[hix[0][u]] = hv[0][u];
+      if (hix[1][u] >= 0) T1[hix[1][u]] = hv[1][u];
+    }
   }
+  cp_async_wait_all();
   __syncthreads();
-  if (!last) return;
-  __threadfence();
-  mx = 0;
-  ss = 0;
-  double cc = 0;
-  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
-    const volatile Rec* p = partial + b;
-    mx = fmax(mx, p->max);
-    ss += p->sumsq;
-    cc += (double)p->count;
+  if (leaf) {
+    const double w = L.w;
+#pragma unroll
+    for (int q = 0; q < O::PER; ++q) {
+      int j, k, B;
+      O::at(q, j, k, B);
+      const int e = t + q * O::THR;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int o = (c + j + k) & 1;
+        const double* To = c ? T0 : T1;
+        const double self = (c ? T1 : T0)[B + o];
+        double s = -2.0 * D * self;
+        s += To[B];
+        s += To[B + 1];
+        s += To[B + o - TT::RW];
+        s += To[B + o + TT::RW];
+        if (D == 3) {
+          s += To[B + o - TT::RW * TT::P];
+          s += To[B + o + TT::RW * TT::P];
+        }
+        const double rv = L.rhs[base + (size_t)c * G::H + e] - s * w;
+        mx = fmax(mx, fabs(rv));
+        ss += rv * rv;
+        cnt += 1;
+      }
+    }
   }
-  mx = block_max(mx, sm);
-  ss = block_sum(ss, sm);
-  cc = block_sum(cc, sm);
-  if (threadIdx.x == 0) {
-    rec[L.level].max = mx;
-    rec[L.level].sumsq = ss;
-    rec[L.level].count = (long long)cc;
-    *counter = 0;
-  }
+  record_finish(L, partial, rec, counter, slot, mx, ss, cnt, sm, &last);
 }
 
 }  // namespace pmgdev
