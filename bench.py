@@ -64,54 +64,95 @@ def vcycle_bytes(mesh, N, dim, nu1=2, nu2=2):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region by an NVML
+    polling thread (every ~2 ms, so even a 50 ms region gets many samples);
+    falls back to `nvidia-smi -lms` when NVML is unavailable."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    BAD = (("hw_slowdown", "HwSlowdown"), ("hw_thermal_slowdown", "HwThermalSlowdown"),
+           ("sw_thermal_slowdown", "SwThermalSlowdown"), ("sw_power_cap", "SwPowerCap"),
+           ("hw_power_brake_slowdown", "HwPowerBrakeSlowdown"))
 
     def __init__(self, device):
         self.device = device
+        self.sm, self.max_mhz, self.reasons = [], None, set()
+        self._stop = None
         self.proc = None
 
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        idx = self.device
+        ids = [x for x in vis.split(",") if x.strip()]
+        if ids and all(x.strip().isdigit() for x in ids) and self.device < len(ids):
+            idx = int(ids[self.device])
+        return pynvml, pynvml.nvmlDeviceGetHandleByIndex(idx)
+
     def __enter__(self):
+        import threading
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            nv, h = self._nvml_handle()
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons",
+                            getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons", None))
+            bits = {name: getattr(nv, "nvmlClocksEventReason" + suf,
+                                  getattr(nv, "nvmlClocksThrottleReason" + suf, 0))
+                    for name, suf in self.BAD}
+            self._stop = threading.Event()
+
+            def poll():
+                while not self._stop.is_set():
+                    try:
+                        self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                        r = get_r(h)
+                        self.reasons.update(n for n, bit in bits.items() if bit and (r & bit))
+                    except Exception:
+                        pass
+                    self._stop.wait(0.002)
+
+            self._th = threading.Thread(target=poll, daemon=True)
+            self._th.start()
         except Exception:
-            self.proc = None
+            self._stop = None
+            try:
+                q = ("clocks.sm,clocks.max.sm,clocks_throttle_reasons.hw_slowdown,"
+                     "clocks_throttle_reasons.hw_thermal_slowdown,"
+                     "clocks_throttle_reasons.sw_thermal_slowdown,clocks_throttle_reasons.sw_power_cap")
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", f"--id={self.device}", f"--query-gpu={q}",
+                     "--format=csv,noheader,nounits", "-lms", "20"],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            except Exception:
+                self.proc = None
         return self
 
     def __exit__(self, *a):
-        self.out = ""
+        if self._stop is not None:
+            self._stop.set()
+            self._th.join(timeout=2)
         if self.proc:
             self.proc.terminate()
             try:
-                self.out, _ = self.proc.communicate(timeout=5)
+                out, _ = self.proc.communicate(timeout=5)
             except Exception:
                 self.proc.kill()
+                out = ""
+            for line in out.splitlines():
+                f = [x.strip() for x in line.split(",")]
+                try:
+                    self.sm.append(float(f[0]))
+                    self.max_mhz = float(f[1])
+                except (ValueError, IndexError):
+                    continue
+                for (name, _), v in zip(self.BAD, f[2:6]):
+                    if v.lower() == "active":
+                        self.reasons.add(name)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        for line in getattr(self, "out", "").splitlines():
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
-            except ValueError:
-                continue
-            for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
-                                "sw_power_cap"), f[5:9]):
-                if v.lower() == "active":
-                    reasons.add(name)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.sm)}
 
 
 def dist_env():

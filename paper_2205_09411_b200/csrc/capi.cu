@@ -173,12 +173,14 @@ static void upload_stencils(Ctx& c) {
           no_cf = no_cf && !(m.nbr[(size_t)id * 6 + f] < 0 && m.cnbr[(size_t)id * 6 + f] >= 0);
         (no_cf ? fast : slow).push_back(s);
         (no_cf && kind[(size_t)s] == pmgdev::KIND_UNIFORM ? ufast : uslow).push_back(s);
-        // special rows of lean interface blocks, per colour, for k_gs_fix
+        // cut (non-inside) rows of lean interface blocks, per colour, for k_gs_fix
         if (no_cf && kind[(size_t)s] == pmgdev::KIND_IFACE) {
           const int32_t* page = row_of.data() + (size_t)srow[(size_t)s] * NI;
           for (int cc = 0; cc < 2; ++cc)
-            for (int e = 0; e < H; ++e)
-              if (page[cc * H + e] >= 0) fix[cc].push_back(s), fix[cc].push_back(e);
+            for (int e = 0; e < H; ++e) {
+              const int32_t r = page[cc * H + e];
+              if (r >= 0 && mask[(size_t)r] != PMG_INSIDE) fix[cc].push_back(s), fix[cc].push_back(e);
+            }
         }
       }
       d.n_fast = (int)fast.size();

@@ -30,29 +30,26 @@ struct OpsImpl final : Ops {
 
   void gs(Ctx& c, int l, int parity) override {
     const LevelView& L = V(c, l);
-    if constexpr (TILE)
-    {
-      // persistent, software-pipelined sweep: fill every SM to its occupancy
-      static int occ = 0;
-      if (!occ) PMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gs_pers<D, N>, TT::THREADS, 0));
-      const int grid = std::min(L.nb, std::max(1, occ) * c.sms);
-      (void)grid;
+    if constexpr (TILE) {
       const LevelDev& d = *c.lev[(size_t)l];
-      // the latency-bound general blocks run on a forked branch concurrently
-      // with the bandwidth-bound lean blocks (both write disjoint cells)
-      const bool fork = d.n_fast > 0 && d.n_slow > 0;
+      // the latency-bound general blocks and the cut-row fix-up run on a
+      // forked branch concurrently with the bandwidth-bound lean blocks: all
+      // three write disjoint cells of colour `parity` and read only the other
+      // colour (plus, in k_gs_fix, the cut cell's own old value)
+      const bool side_work = d.n_slow > 0 || d.n_fix[parity] > 0;
+      const bool fork = d.n_fast > 0 && side_work;
       if (fork) {
         PMG_CUDA(cudaEventRecord(c.ev_fork, c.stream));
         PMG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
       }
+      cudaStream_t s2 = fork ? c.side : c.stream;
       if (d.n_slow > 0)
-        k_gs_tile<D, N><<<d.n_slow, TT::THREADS, 0, fork ? c.side : c.stream>>>(
-            L, Vc(c, l), c.phi_b.p, parity, d.slow_list.p);
+        k_gs_tile<D, N><<<d.n_slow, TT::THREADS, 0, s2>>>(L, Vc(c, l), c.phi_b.p, parity, d.slow_list.p);
+      if (d.n_fix[parity] > 0)
+        k_gs_fix<D, N><<<grid_for(d.n_fix[parity], 128), 128, 0, s2>>>(
+            L, Vc(c, l), c.phi_b.p, parity, (const int2*)d.fix_list[parity].p, d.n_fix[parity]);
       if (d.n_fast > 0)
         k_gs_lean<D, N><<<d.n_fast, Lean<D, N>::THR, 0, c.stream>>>(L, parity, d.fast_list.p);
-      if (d.n_fix[parity] > 0)
-        k_gs_fix<D, N><<<grid_for(d.n_fix[parity]), 256, 0, c.stream>>>(
-            L, Vc(c, l), c.phi_b.p, parity, (const int2*)d.fix_list[parity].p, d.n_fix[parity]);
       if (fork) {
         PMG_CUDA(cudaEventRecord(c.ev_join, c.side));
         PMG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));

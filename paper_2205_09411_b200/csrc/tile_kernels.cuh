@@ -342,10 +342,14 @@ __global__ void __launch_bounds__(Lean<D, N>::THR) k_gs_lean(LevelView L, int pa
     }
     return;
   }
-  // interface block: the uniform-row formula of multigrid.hpp:667-672 for every
-  // cell; its special (cut / inside) rows are redone by k_gs_fix afterwards
+  // interface block: the uniform-row formula of multigrid.hpp:667-672 for
+  // every uniform row; special rows are left alone (inside rows keep their
+  // pin, cut rows are updated by k_gs_fix, which still reads their old value
+  // for a physical-face ghost 2bc - f1)
+  const int32_t* __restrict__ rof = L.row_of + (size_t)L.srow[slot] * G::NI + (size_t)c * G::H;
 #pragma unroll
   for (int q = 0; q < LN::PER; ++q) {
+    if (rof[t + q * LN::THR] >= 0) continue;
     const int row = row0 + LN::RS * q;
     const int j = row % N, k = D == 3 ? row / N : 0;
     const int B = (D == 3 ? ((k + 1) * TT::P + (j + 1)) : (j + 1)) * TT::RW + m;
@@ -363,118 +367,18 @@ __global__ void __launch_bounds__(Lean<D, N>::THR) k_gs_lean(LevelView L, int pa
   }
 }
 
-// Special rows of interface blocks after k_gs_lean: cut rows get their
-// boundary-modified update (multigrid.hpp:674-684), inside rows their pinned
-// value back.  One thread per special cell of the active colour.
+// Cut rows of lean interface blocks (k_gs_lean skips every special row): the
+// boundary-modified update of multigrid.hpp:674-684.  One thread per cut cell
+// of the active colour; inside rows are never written, so they keep their pin.
 template <int D, int N>
-__global__ void __launch_bounds__(256) k_gs_fix(LevelView L, LevelView Lc,
+__global__ void __launch_bounds__(128) k_gs_fix(LevelView L, LevelView Lc,
                                                const double* __restrict__ phi_b, int parity,
                                                const int2* __restrict__ cells, int n) {
   using G = Geo<D, N>;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int2 se = cells[i];
-  const int r = L.row_of[(size_t)L.srow[se.x] * G::NI + parity * G::H + se.y];
-  if (L.r_mask[r] == 1) {
-    L.phi[(size_t)se.x * G::NI + (size_t)parity * G::H + se.y] = phi_b[L.r_pin[r]];
-    return;
-  }
   gs_cell<D, N>(L, Lc, phi_b, se.x, parity, se.y);
-}
-
-// ------------------------------------------------------------------ persistent GS-RB half-sweep
-// Software-pipelined version: a grid of ~2 CTAs per SM walks the blocks
-// b = blockIdx.x, +gridDim.x, ...  While a CTA runs the shared-memory stencil
-// of block b, the global loads of the next block (opposite colour, rhs, halo)
-// are already in flight in registers, and the neighbour slots of the block
-// after that are being fetched, so DRAM streaming and the smem-bound update
-// overlap instead of alternating.
-template <int D, int N>
-__global__ void __launch_bounds__(Tile<D, N>::THREADS, 2) k_gs_pers(LevelView L, LevelView Lc,
-                                                                    const double* __restrict__ phi_b,
-                                                                    int parity) {
-  using G = Geo<D, N>;
-  using TT = Tile<D, N>;
-  using O = Own<D, N>;
-  using HL = Halo<D, N>;
-  __shared__ double T[TT::SIZE];
-  const int c = parity, X = 1 - c;
-  const int step = gridDim.x;
-  int b = blockIdx.x;
-  if (b >= L.nb) return;
-  HL h;
-  int ns_n[HL::PER];
-  double ov[O::PER], gv[O::PER];
-  uint8_t kind = 0, kind_n = 0;
-  auto issue = [&](int blk) {
-    const size_t base = (size_t)blk * G::NI;
-#pragma unroll
-    for (int q = 0; q < O::PER; ++q) {
-      const int e = threadIdx.x + q * O::THR;
-      ov[q] = L.phi[base + (size_t)X * G::H + e];
-      gv[q] = L.rhs[base + (size_t)c * G::H + e];
-    }
-    h.issue(L, Lc, blk, X);
-  };
-  auto prefetch_nbr = [&](int blk) {
-#pragma unroll
-    for (int u = 0; u < HL::PER; ++u) {
-      const int q = threadIdx.x + u * TT::THREADS;
-      ns_n[u] = (blk < L.nb && q < HL::NQ) ? L.nbr[blk * G::F + q / HL::HT] : -2;
-    }
-    kind_n = blk < L.nb ? L.kind[blk] : 0;
-  };
-  // prologue: block b's loads, next block's neighbour slots
-  h.prefetch(L, b);
-  kind = L.kind[b];
-  prefetch_nbr(b + step);
-  issue(b);
-  for (;;) {
-    // stage block b into shared memory
-#pragma unroll
-    for (int q = 0; q < O::PER; ++q) {
-      int j, k, B;
-      O::at(q, j, k, B);
-      T[B + ((X + j + k) & 1)] = ov[q];
-    }
-    h.store(T);
-    __syncthreads();
-    double gc[O::PER];
-#pragma unroll
-    for (int q = 0; q < O::PER; ++q) gc[q] = gv[q];
-    const uint8_t kc = kind;
-    const int bc = b;
-    b += step;
-    if (b < L.nb) {  // next block's loads go in flight now
-#pragma unroll
-      for (int u = 0; u < HL::PER; ++u) h.ns[u] = ns_n[u];
-      kind = kind_n;
-      prefetch_nbr(b + step);
-      issue(b);
-    }
-    if (kc != KIND_ALL_INSIDE) {
-      const size_t base = (size_t)bc * G::NI;
-      double* __restrict__ dst = L.phi + base + (size_t)c * G::H;
-      const int32_t* rowp =
-          kc == KIND_UNIFORM ? nullptr : L.row_of + (size_t)L.srow[bc] * G::NI + c * G::H;
-#pragma unroll
-      for (int q = 0; q < O::PER; ++q) {
-        int j, k, B;
-        O::at(q, j, k, B);
-        const int e = threadIdx.x + q * O::THR;
-        int r = -1;
-        if (rowp) {
-          r = rowp[e];
-          if (r >= 0 && L.r_mask[r] == 1) continue;
-        }
-        double p[2 * D];
-        nbrs_at<D, N>(T, B, (c + j + k) & 1, p);
-        dst[e] = gs_value<D>(L, phi_b, kc, r, p, gc[q]);
-      }
-    }
-    if (bc + step >= L.nb) break;
-    __syncthreads();  // T is restaged next iteration
-  }
 }
 
 // Both colour tiles (interiors + optional halos), register-staged; the caller

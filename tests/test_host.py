@@ -116,3 +116,36 @@ def test_abi_argument_errors_without_gpu():
     h = lib.pmg_b200_create(3, 12, np.zeros(3), np.ones(3), 0)
     assert b"power of two" in lib.pmg_b200_last_error(h)
     lib.pmg_b200_destroy(h)
+
+
+def _cbrt_restated(x):
+    """numpy restatement of the device libm_cbrt (stencil_build.cuh): glibc's
+    dbl-64 s_cbrt algorithm, which the reference's std::cbrt runs."""
+    xm, xe = np.frexp(np.abs(x))
+    u = (0.354895765043919860 + ((1.50819193781584896 + ((-2.11499494167371287 + (
+        (2.44693122563534430 + ((-1.83469277483613086 + (0.784932344976639262
+                                                         - 0.145263899385486377 * xm) * xm) * xm))
+        * xm)) * xm)) * xm))
+    t2 = u * u * u
+    c2, s2 = 1.2599210498948731648, 1.5874010519681994748
+    fac = np.array([1.0 / s2, 1.0 / c2, 1.0, c2, s2])
+    idx = 2 + np.fmod(xe, 3)  # C's truncating %
+    ym = u * (t2 + 2.0 * xm) / (2.0 * t2 + xm) * fac[idx]
+    q = np.trunc(xe / 3).astype(np.int64)  # C's truncating /
+    out = np.ldexp(np.where(x > 0, ym, -ym), q)
+    return np.where(x == 0, x + x, out)
+
+
+def test_cbrt_restatement_matches_host_libm():
+    """The heart/astroid level sets call std::cbrt (levelset.hpp:114-120); the
+    GPU reproduces the host libm's (not correctly rounded) cbrt bit for bit."""
+    import ctypes
+    import ctypes.util
+    libm = ctypes.CDLL(ctypes.util.find_library("m"))
+    libm.cbrt.restype = ctypes.c_double
+    libm.cbrt.argtypes = [ctypes.c_double]
+    rng = np.random.default_rng(7)
+    x = np.concatenate([rng.uniform(0, 64, 40000) ** 2, rng.uniform(-1e-3, 1e3, 20000),
+                        np.exp(rng.uniform(-700, 700, 20000)), [0.0, 1.0, 8.0, 27.0, 5e-324]])
+    ref = np.array([libm.cbrt(float(v)) for v in x])
+    assert np.array_equal(_cbrt_restated(x).view(np.uint64), ref.view(np.uint64))
