@@ -146,7 +146,8 @@ int pmg_b200_coarse_info(pmg_b200_ctx* ctx, int32_t* iters, double* rel);
  *   op 3: leaf-residual record of `level`
  *   op 4: coarse solve
  *   op 5: one V-cycle (graph)        op 6: one FMG cycle (graph, with guess)
- * Ops 1-6 modify the solution exactly as the solver would. */
+ *   op 7: residual+restriction of `level` alone   op 8: FAS/OLD of `level`-1 alone
+ * Ops 1-8 modify the solution exactly as the solver would. */
 int pmg_b200_time_op(pmg_b200_ctx* ctx, int op, int level, int reps, double* ms_avg);
 
 #ifdef __cplusplus

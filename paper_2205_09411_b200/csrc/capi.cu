@@ -125,6 +125,7 @@ static void upload_stencils(Ctx& c) {
   const HostMesh& m = c.mesh;
   const HostStencils& st = c.st;
   const int NI = c.NI, H = NI / 2, F = c.F;
+  std::vector<std::vector<uint8_t>> kindv((size_t)m.L + 1);
   for (int l = 1; l <= m.L; ++l) {
     LevelDev& d = *c.lev[(size_t)l];
     std::vector<int32_t> srow((size_t)d.nb, -1), row_of;
@@ -163,15 +164,31 @@ static void upload_stencils(Ctx& c) {
     }
     d.srow.upload(srow, c.stream);
     d.kind.upload(kind, c.stream);
+    kindv[(size_t)l] = kind;
     // block classes for the specialised kernels
     {
-      std::vector<int32_t> fast, slow, ufast, uslow, fix[2];
+      std::vector<int32_t> fast, slow, ufast, uslow, fix[2], gsl, rsl;
       for (int s = 0; s < d.nb; ++s) {
         const int id = m.slots[(size_t)l][(size_t)s];
         bool no_cf = true;  // lean kernels handle same-level and physical faces
         for (int f = 0; f < F; ++f)
           no_cf = no_cf && !(m.nbr[(size_t)id * 6 + f] < 0 && m.cnbr[(size_t)id * 6 + f] >= 0);
         (no_cf ? fast : slow).push_back(s);
+        if (no_cf) {
+          // stream.cuh BlockPlan: slot, kind | phys << 8 | srow << 14, 6 neighbour slots
+          int pm = 0;
+          int32_t ns[6] = {-1, -1, -1, -1, -1, -1};
+          for (int f = 0; f < F; ++f) {
+            const int nid = m.nbr[(size_t)id * 6 + f];
+            if (nid < 0) pm |= 1 << f;
+            else ns[f] = m.slot_of[(size_t)nid];
+          }
+          const int sr = srow[(size_t)s] < 0 ? 0 : srow[(size_t)s];
+          require(sr < (1 << 17), "too many interface blocks on one level for the streaming plan");
+          const int32_t e[8] = {s, (int32_t)kind[(size_t)s] | (pm << 8) | (sr << 14), ns[0], ns[1], ns[2], ns[3], ns[4], ns[5]};
+          rsl.insert(rsl.end(), e, e + 8);
+          if (kind[(size_t)s] != pmgdev::KIND_ALL_INSIDE) gsl.insert(gsl.end(), e, e + 8);
+        }
         (no_cf && kind[(size_t)s] == pmgdev::KIND_UNIFORM ? ufast : uslow).push_back(s);
         // cut (non-inside) rows of lean interface blocks, per colour, for k_gs_fix
         if (no_cf && kind[(size_t)s] == pmgdev::KIND_IFACE) {
@@ -183,6 +200,10 @@ static void upload_stencils(Ctx& c) {
             }
         }
       }
+      d.n_gs = (int)gsl.size() / 8;
+      d.gs_plan.upload(gsl, c.stream);
+      d.n_rs = (int)rsl.size() / 8;
+      d.rs_plan.upload(rsl, c.stream);
       d.n_fast = (int)fast.size();
       d.n_slow = (int)slow.size();
       d.fast_list.upload(fast, c.stream);
@@ -203,6 +224,61 @@ static void upload_stencils(Ctx& c) {
     d.r_obj.upload(obj, c.stream);
     d.r_mask.upload(mask, c.stream);
     d.r_pin.upload(pin, c.stream);
+  }
+  // k_restrict_fix lists (3D): parents of level l-1 whose fused restriction
+  // needs the general path -- a child with a special row, or a pinned parent
+  if (c.dim == 3) {
+    const int N = c.N, HN = N / 2;
+    auto row_at = [&](int id, int i, int j, int k) -> int {
+      if (!st.valid || !st.boundary[(size_t)id]) return -1;
+      const int r = st.row_of[(size_t)id * NI + (size_t)(i + N * (j + N * k))];
+      return r < 0 ? -1 : st.row_start[(size_t)id] + r;
+    };
+    for (int l = 2; l <= m.L; ++l) {
+      LevelDev& d = *c.lev[(size_t)l];
+      std::vector<int32_t> fx;
+      for (int s = 0; s < d.nb; ++s) {
+        const int id = m.slots[(size_t)l][(size_t)s];
+        const int p = m.parent[(size_t)id];
+        const int cx = m.coords[(size_t)id * 3] & 1, cy = m.coords[(size_t)id * 3 + 1] & 1,
+                  cz = m.coords[(size_t)id * 3 + 2] & 1;
+        (void)p;
+        (void)cx;
+        (void)cy;
+        (void)cz;
+        // interface blocks only: all-inside blocks restrict exactly in the stream kernel
+        if (!(st.valid && st.boundary[(size_t)id]) || kindv[(size_t)l][(size_t)s] != pmgdev::KIND_IFACE) continue;
+        for (int t = 0; t < HN * HN * HN; ++t) {
+          const int ii = t % HN, jj = (t / HN) % HN, kk = t / (HN * HN);
+          bool need = false;
+          for (int ch = 0; ch < 8 && !need; ++ch)
+            need = row_at(id, 2 * ii + (ch & 1), 2 * jj + ((ch >> 1) & 1), 2 * kk + (ch >> 2)) >= 0;
+          if (need) fx.push_back(s), fx.push_back(t);
+        }
+      }
+      d.n_rfix = (int)fx.size() / 2;
+      d.rfix_list.upload(fx, c.stream);
+    }
+  }
+  // pin lists (every level): colour-split address and object of each inside row
+  for (int l = 1; l <= m.L; ++l) {
+    LevelDev& d = *c.lev[(size_t)l];
+    std::vector<int32_t> pl;
+    if (st.valid)
+      for (int s = 0; s < d.nb; ++s) {
+        const int id = m.slots[(size_t)l][(size_t)s];
+        if (!st.boundary[(size_t)id]) continue;
+        for (int ii = 0; ii < NI; ++ii) {
+          const int r = st.row_of[(size_t)id * NI + ii];
+          if (r < 0) continue;
+          const size_t q = (size_t)(st.row_start[(size_t)id] + r);
+          if (st.mask[q] != PMG_INSIDE) continue;
+          pl.push_back((int32_t)((size_t)s * NI + (size_t)cs_addr(ii, c.N, c.dim, H)));
+          pl.push_back(st.pin[q]);
+        }
+      }
+    d.n_pin = (int)pl.size() / 2;
+    d.pin_list.upload(pl, c.stream);
   }
   std::vector<double> pb = st.phi_b;
   if (pb.empty()) pb.push_back(0.0);
@@ -1136,8 +1212,8 @@ int pmg_b200_level_size(pmg_b200_ctx* h, int level) {
 int pmg_b200_time_op(pmg_b200_ctx* h, int op, int level, int reps, double* ms_avg) {
   return guard(h, [&](Ctx& c) {
     require(c.solver, "solver not created", PMG_ERR_STATE);
-    require(reps >= 1 && op >= 0 && op <= 6, "bad op/reps");
-    if (op <= 3) need_level(c, level, op == 0 || op == 3 ? 1 : 2);
+    require(reps >= 1 && op >= 0 && op <= 8, "bad op/reps");
+    if (op <= 3 || op >= 7) need_level(c, level, op == 0 || op == 3 ? 1 : 2);
     auto one = [&](int k) {
       switch (op) {
         case 0: c.ops->gs(c, level, k & 1); break;
@@ -1146,6 +1222,8 @@ int pmg_b200_time_op(pmg_b200_ctx* h, int op, int level, int reps, double* ms_av
         case 3: c.ops->record(c, level); break;
         case 4: enq_coarse(c); break;
         case 5: PMG_CUDA(cudaGraphLaunch(graph_for(c, CK_V).exec, c.stream)); break;
+        case 7: c.ops->restrict_(c, level, c.lev[(size_t)level]->has_cf ? pmgdev::RM_RES : pmgdev::RM_FUSED); break;
+        case 8: c.ops->fas(c, level - 1, true); break;
         default: PMG_CUDA(cudaGraphLaunch(graph_for(c, CK_FMG_GUESS).exec, c.stream)); break;
       }
     };

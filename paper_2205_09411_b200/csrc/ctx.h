@@ -92,6 +92,15 @@ struct LevelDev {
   // residual-family classes: lean = uniform stencil without coarse-fine faces
   DevBuf<int32_t> ufast_list, uslow_list;
   int n_ufast = 0, n_uslow = 0;
+  // streaming GS (stream.cuh): lean blocks that are not entirely inside
+  DevBuf<int32_t> gs_plan;  // 8 int32 per block (stream.cuh BlockPlan)
+  int n_gs = 0;
+  DevBuf<int32_t> rs_plan;  // every block without coarse-fine faces (incl. all-inside)
+  int n_rs = 0;
+  DevBuf<int32_t> rfix_list;  // (slot, parent-local index) pairs for k_restrict_fix
+  int n_rfix = 0;
+  DevBuf<int32_t> pin_list;   // (cell address, object) of this level's inside rows
+  int n_pin = 0;
   DevBuf<int32_t> fix_list[2];  // (slot, entry) pairs of special rows in lean interface blocks
   int n_fix[2] = {0, 0};
   bool has_cf = false;       // some block has a coarse-fine face

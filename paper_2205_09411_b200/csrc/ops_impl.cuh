@@ -7,10 +7,15 @@
 #include "tile_kernels.cuh"
 #include "coarse.cuh"
 #include "coarse_cluster.cuh"
+#include "stream.cuh"
 
 namespace pmghost {
 
 using namespace pmgdev;
+
+// streaming GS pipeline depth and residency (stream.cuh)
+constexpr int kStreamStages = 2;
+constexpr int kStreamCtasPerSm = 2;
 
 static inline unsigned grid_for(long long n, int threads = kThreads) {
   return (unsigned)((n + threads - 1) / threads);
@@ -48,8 +53,18 @@ struct OpsImpl final : Ops {
       if (d.n_fix[parity] > 0)
         k_gs_fix<D, N><<<grid_for(d.n_fix[parity], 128), 128, 0, s2>>>(
             L, Vc(c, l), c.phi_b.p, parity, (const int2*)d.fix_list[parity].p, d.n_fix[parity]);
-      if (d.n_fast > 0)
+      if constexpr (D == 3 && (N == 8 || N == 16)) {
+        if (d.n_gs > 0 && !(L.exp & 256)) {
+          if (L.exp & 4096)
+            launch_gs_stream<4, 1>(c, L, d, parity);
+          else
+            launch_gs_stream<kStreamStages, kStreamCtasPerSm>(c, L, d, parity);
+        } else if (d.n_fast > 0) {
+          k_gs_lean<D, N><<<d.n_fast, Lean<D, N>::THR, 0, c.stream>>>(L, parity, d.fast_list.p);
+        }
+      } else if (d.n_fast > 0) {
         k_gs_lean<D, N><<<d.n_fast, Lean<D, N>::THR, 0, c.stream>>>(L, parity, d.fast_list.p);
+      }
       if (fork) {
         PMG_CUDA(cudaEventRecord(c.ev_join, c.side));
         PMG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
@@ -60,6 +75,21 @@ struct OpsImpl final : Ops {
                                                                              c.phi_b.p, parity);
     check();
   }
+  template <int ST, int MINB>
+  void launch_gs_stream(Ctx& c, const LevelView& L, const LevelDev& d, int parity) {
+    if constexpr (D == 3 && (N == 8 || N == 16)) {
+      constexpr size_t smem = (size_t)ST * Stream3<N>::STAGE * sizeof(double);
+      static bool attr = false;
+      if (!attr) {
+        PMG_CUDA(cudaFuncSetAttribute(k_gs_stream<N, ST, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+        attr = true;
+      }
+      const int grid = std::min(d.n_gs, c.sms * MINB);
+      k_gs_stream<N, ST, MINB><<<grid, Stream3<N>::THR, smem, c.stream>>>(L, parity, (const int4*)d.gs_plan.p,
+                                                                           d.n_gs);
+    }
+  }
   void residual(Ctx& c, int l) override {
     const LevelView& L = V(c, l);
     k_residual<D, N><<<grid_for((long long)L.nb * G::NI), kThreads, 0, c.stream>>>(L, Vc(c, l),
@@ -69,6 +99,31 @@ struct OpsImpl final : Ops {
   void restrict_(Ctx& c, int l, int mode) override {
     const LevelView& Lf = V(c, l);
     const unsigned g = grid_for((long long)Lf.nb * (G::NI / G::NC));
+    if constexpr (D == 3 && N == 16) {
+      const LevelDev& d = *c.lev[(size_t)l];
+      if (mode == RM_FUSED && !d.has_cf && d.n_rs == Lf.nb && !(Lf.exp & 8192)) {
+        constexpr int ST = 2, MINB = 1;
+        constexpr size_t smem = (size_t)ST * RStream3<N>::STAGE * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+          PMG_CUDA(cudaFuncSetAttribute(k_restrict_stream<N, ST, MINB>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          attr = true;
+        }
+        const int grid = std::min(d.n_rs, c.sms * MINB);
+        k_restrict_stream<N, ST, MINB><<<grid, RStream3<N>::THR, smem, c.stream>>>(
+            Lf, V(c, l - 1), c.phi_b.p, (const int4*)d.rs_plan.p, d.n_rs);
+        if (d.n_rfix > 0)
+          k_restrict_fix<D, N><<<grid_for((long long)d.n_rfix * 8, 128), 128, 0, c.stream>>>(
+              Lf, Vc(c, l), V(c, l - 1), c.phi_b.p, (const int2*)d.rfix_list.p, d.n_rfix);
+        const LevelDev& dp = *c.lev[(size_t)(l - 1)];
+        if (dp.n_pin > 0)  // apply_pins(l-1)
+          k_pin_list<<<grid_for(dp.n_pin, 256), 256, 0, c.stream>>>(V(c, l - 1).phi, c.phi_b.p,
+                                                                    (const int2*)dp.pin_list.p, dp.n_pin);
+        check();
+        return;
+      }
+    }
     if constexpr (TILE) {
       if (mode == RM_RES)
         k_restrict_tile<D, N, RM_RES><<<Lf.nb, TT::THREADS, 0, c.stream>>>(Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);

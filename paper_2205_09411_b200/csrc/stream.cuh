@@ -1,0 +1,607 @@
+// stream.cuh -- persistent, TMA-pipelined streaming kernels for lean 3D blocks.
+//
+// The GS-RB half-sweep of a block needs its other-colour half of phi (N^3/2
+// doubles, contiguous in the colour-split layout), its own-colour half of g
+// (contiguous) and one face layer per side.  A CTA owns every G-th block of
+// the lean list (G = grid size, one or two CTAs per SM) and keeps S blocks in
+// flight: one elected warp issues 1D bulk copies (cp.async.bulk, the TMA
+// engine) of the two halves and of the z / y face layers into an S-stage
+// shared-memory ring, completing on a per-stage mbarrier; the strided x-face
+// values are gathered by the threads one block ahead.  The compute of block b
+// therefore overlaps the DRAM streaming of blocks b+1 .. b+S-1 without
+// holding any of it in registers.
+#pragma once
+#include "tiles.cuh"
+#include "cells.cuh"
+
+namespace pmgdev {
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred P1;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy (bytes % 16 == 0, both addresses 16-B aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int PENDING>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(PENDING) : "memory");
+}
+
+// ------------------------------------------------------------------ per-block plan
+// Host-built, one int4 pair per lean block of a level (capi.cu upload_stencils):
+// a = {slot, kind | physical-face mask << 8 | srow << 14, nbr(-x), nbr(+x)},
+// b = {nbr(-y), nbr(+y), nbr(-z), nbr(+z)}   (-1 = physical face).
+struct BlockPlan {
+  int4 a, b;
+  __device__ __forceinline__ int slot() const { return a.x; }
+  __device__ __forceinline__ int kind() const { return a.y & 0xff; }
+  __device__ __forceinline__ int phys() const { return (a.y >> 8) & 63; }
+  __device__ __forceinline__ int srow() const { return a.y >> 14; }
+  __device__ __forceinline__ int nbr(int d) const {
+    return d == 0 ? a.z : d == 1 ? a.w : d == 2 ? b.x : d == 3 ? b.y : d == 4 ? b.z : b.w;
+  }
+};
+__device__ __forceinline__ BlockPlan load_plan(const int4* plan, int p) {
+  BlockPlan P;
+  P.a = __ldg(plan + 2 * p);
+  P.b = __ldg(plan + 2 * p + 1);
+  return P;
+}
+
+// ------------------------------------------------------------------ stage layout
+template <int N>
+struct Stream3 {
+  static constexpr int HN = N / 2;
+  static constexpr int H = N * N * N / 2;
+  static constexpr int FH = N * HN;  // z / y face layer of one colour
+  static constexpr int THR = H < 512 ? H : 512;
+  static constexpr int PER = H / THR;
+  // doubles per stage: X half, g half, hz[2], hy[2], hx[2] (x rows indexed
+  // k*N+j), then H int32 row_of entries of an interface block
+  static constexpr int OX = 0, OG = H, OZ = 2 * H, OY = OZ + 2 * FH, OXF = OY + 2 * FH;
+  static constexpr int ORQ = OXF + 2 * N * N;  // in doubles; H int32 = H/2 doubles
+  static constexpr int STAGE = ORQ + H / 2;
+  static constexpr uint32_t TX_BYTES = (uint32_t)(2 * H + 2 * FH) * 8u;  // bulk part
+  static constexpr int YC = N * HN;  // 16-B chunks of the two y layers (2 sides x N rows x HN/2)
+  static constexpr int XT0 = 0, YT0 = THR - YC;  // thread ranges issuing x / y face copies
+};
+
+// Bulk copies of one block into a stage (one elected thread): the two
+// halves and the z layers (physical faces copy the block's own colour-c
+// layer; it becomes 2 bc - f1 / f1 after the wait).
+template <int N>
+__device__ __forceinline__ void gs_issue(const LevelView& L, const BlockPlan& P, int c, double* st,
+                                         uint64_t* bar) {
+  using S = Stream3<N>;
+  constexpr int NI = N * N * N;
+  const int X = 1 - c;
+  const int slot = P.slot();
+  const double* own = L.phi + (size_t)slot * NI + (size_t)c * S::H;
+  mbar_arrive_expect_tx(bar, S::TX_BYTES);
+  bulk_g2s(st + S::OX, L.phi + (size_t)slot * NI + (size_t)X * S::H, S::H * 8, bar);
+  bulk_g2s(st + S::OG, L.rhs + (size_t)slot * NI + (size_t)c * S::H, S::H * 8, bar);
+  const int zm = P.nbr(4), zp = P.nbr(5);
+  const double* s0 = zm >= 0 ? L.phi + (size_t)zm * NI + (size_t)X * S::H + (N - 1) * S::FH : own;
+  const double* s1 = zp >= 0 ? L.phi + (size_t)zp * NI + (size_t)X * S::H : own + (N - 1) * S::FH;
+  bulk_g2s(st + S::OZ, s0, S::FH * 8, bar);
+  bulk_g2s(st + S::OZ + S::FH, s1, S::FH * 8, bar);
+}
+
+// x-face row u (0 .. N*N-1): side = u / (N*N/2); the row (j,k) holds a
+// colour-c cell on that face.
+template <int N>
+__device__ __forceinline__ void xface_of(int c, int u, int& side, int& j, int& k) {
+  side = u / (N * N / 2);
+  const int r = u % (N * N / 2);
+  k = r / (N / 2);
+  j = 2 * (r % (N / 2)) + ((c + k + side) & 1);
+}
+
+// Thread-issued async copies of one block: the strided x-face values (the
+// neighbour's X value, or the own value on a physical face) and, for an
+// interface block, this thread's row_of entries.
+template <int N>
+__device__ __forceinline__ void gs_issue_async(const LevelView& L, const BlockPlan& P, int c, double* st) {
+  using S = Stream3<N>;
+  constexpr int NI = N * N * N;
+  const int t = threadIdx.x;
+  if (t < N * N) {
+    int side, j, k;
+    xface_of<N>(c, t, side, j, k);
+    const int ns = P.nbr(side);
+    const double* src;
+    if (ns >= 0)  // -x: neighbour cell (N-1,j,k); +x: (0,j,k); both colour X
+      src = L.phi + (size_t)ns * NI + (size_t)(1 - c) * S::H + (size_t)(side ? 0 : S::HN - 1) + S::HN * (j + N * k);
+    else
+      src = L.phi + (size_t)P.slot() * NI + (size_t)c * S::H + (size_t)(side ? S::HN - 1 : 0) + S::HN * (j + N * k);
+    cp_async8(st + S::OXF + side * N * N + k * N + j, src);
+  }
+  if (t >= S::YT0) {  // y layers: 16-B chunks of the x-rows j = N-1 / 0 (neighbour) or own row
+    const int u = t - S::YT0;
+    constexpr int CR = S::HN / 2;  // chunks per row
+    const int side = u / (N * CR), k = (u / CR) % N, ch = u % CR;
+    const int ns = P.nbr(2 + side);
+    const double* src;
+    if (ns >= 0)
+      src = L.phi + (size_t)ns * NI + (size_t)(1 - c) * S::H + (size_t)k * S::FH + (side ? 0 : (N - 1) * S::HN);
+    else
+      src = L.phi + (size_t)P.slot() * NI + (size_t)c * S::H + (size_t)k * S::FH + (side ? (N - 1) * S::HN : 0);
+    cp_async16(st + S::OY + side * S::FH + k * S::HN + 2 * ch, src + 2 * ch);
+  }
+  if (P.kind() == KIND_IFACE) {  // this block's row_of page (colour c), 16-B chunks
+    const int32_t* rof = L.row_of + (size_t)P.srow() * NI + (size_t)c * S::H;
+    int32_t* rq = reinterpret_cast<int32_t*>(st + S::ORQ);
+    for (int q = t; q < S::H / 4; q += S::THR) cp_async16(rq + 4 * q, rof + 4 * q);
+  }
+}
+
+// Physical faces: the staged own-colour values become ghosts 2 bc - f1
+// (Dirichlet) or stay f1 (Neumann), mesh.hpp:538-552.
+template <int N>
+__device__ __forceinline__ void gs_phys_faces(const LevelView& L, int slot, int pmask, int c, double* st) {
+  using S = Stream3<N>;
+  constexpr int NX = N * N;  // x rows (two sides)
+  for (int q = threadIdx.x; q < NX + 4 * S::FH; q += blockDim.x) {
+    int dir, i, tj;
+    double* h;
+    if (q < NX) {
+      int side, j, k;
+      xface_of<N>(c, q, side, j, k);
+      dir = side;
+      i = side ? N - 1 : 0;
+      tj = j + N * k;
+      h = st + S::OXF + side * N * N + k * N + j;
+    } else {
+      const int qq = q - NX;
+      const int f = qq / S::FH, r = qq % S::FH;  // f: 0 -y, 1 +y, 2 -z, 3 +z
+      dir = f < 2 ? 2 + f : 4 + (f - 2);
+      const int m = r % S::HN, a = r / S::HN;  // a = k on y faces, j on z faces
+      if (f < 2) {
+        const int j = f ? N - 1 : 0;
+        i = 2 * m + ((c + j + a) & 1);
+      } else {
+        const int k = f == 3 ? N - 1 : 0;
+        i = 2 * m + ((c + a + k) & 1);
+      }
+      tj = i + N * a;
+      h = st + (f < 2 ? S::OY + f * S::FH : S::OZ + (f - 2) * S::FH) + r;
+    }
+    if (!((pmask >> dir) & 1) || L.bctype[dir] == 1) continue;
+    double bcv = 0.0;
+    if (!L.bczero) {
+      const int bo = L.bcoff[slot * 6 + dir];
+      if (bo >= 0) bcv = L.bcval[bo + tj];
+    }
+    *h = 2.0 * bcv - *h;
+  }
+}
+
+// GS-RB half-sweep of the lean 3D blocks (UNIFORM / IFACE blocks without
+// coarse-fine faces, in plan order).  Special rows of IFACE blocks are
+// skipped (k_gs_fix updates the cut rows; inside rows keep their pin).
+template <int N, int S_STAGES, int MINB>
+__global__ void __launch_bounds__(Stream3<N>::THR, MINB) k_gs_stream(LevelView L, int parity,
+                                                                 const int4* __restrict__ plan, int n) {
+  using S = Stream3<N>;
+  constexpr int NI = N * N * N;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t full[S_STAGES];
+  __shared__ int meta[S_STAGES][2];
+  const int c = parity;
+  const int t = threadIdx.x;
+  const int G = gridDim.x;
+  const int nmine = (int)blockIdx.x < n ? (n - 1 - (int)blockIdx.x) / G + 1 : 0;
+  if (nmine == 0) return;
+  if (t == 0) {
+    for (int s = 0; s < S_STAGES; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  for (int s = 0; s < S_STAGES; ++s) {
+    if (s < nmine) {
+      const BlockPlan P = load_plan(plan, blockIdx.x + s * G);
+      if (t == 0) gs_issue<N>(L, P, c, sm + s * S::STAGE, &full[s]);
+      if (t == 0) meta[s][0] = P.slot(), meta[s][1] = P.a.y;
+      gs_issue_async<N>(L, P, c, sm + s * S::STAGE);
+    }
+    cp_async_commit();
+  }
+  BlockPlan pf;
+  if (S_STAGES < nmine) pf = load_plan(plan, blockIdx.x + S_STAGES * G);
+  const double h2 = L.h2;
+  for (int it = 0; it < nmine; ++it) {
+    const int s = it % S_STAGES;
+    double* st = sm + s * S::STAGE;
+    BlockPlan pf2;
+    if (it + S_STAGES + 1 < nmine) pf2 = load_plan(plan, blockIdx.x + (it + S_STAGES + 1) * G);
+    mbar_wait(&full[s], (uint32_t)((it / S_STAGES) & 1));
+    cp_async_wait<S_STAGES - 1>();
+    __syncthreads();
+    const int slot = meta[s][0], flags = meta[s][1];
+    const int kind = flags & 0xff, pmask = (flags >> 8) & 63;
+    if (pmask) {  // block-uniform branch
+      gs_phys_faces<N>(L, slot, pmask, c, st);
+      __syncthreads();
+    }
+    // Thread t owns entries e = t + q*THR: the same (m, j) and colour offset o
+    // for every q, z-plane k = k0 + q*KS.  Neighbour indices into the stage
+    // (own tile or halo layer) are chosen once per block; only the z layers at
+    // q = 0 / PER-1 are per-q choices.
+    constexpr int KS = S::THR / S::FH;
+    const int m = t % S::HN, j = (t / S::HN) % N, k0 = t / S::FH;
+    const int o = (c + j + k0) & 1;
+    const int rb = S::OX + (k0 * N + j) * S::HN + m;
+    constexpr int DT = KS * S::FH;  // tile step per q
+    int ixm = rb, dxm = DT, ixp = rb, dxp = DT, iym = rb - S::HN, dym = DT, iyp = rb + S::HN, dyp = DT;
+    if (!o) {
+      if (m > 0) ixm = rb - 1;
+      else ixm = S::OXF + k0 * N + j, dxm = KS * N;
+    } else {
+      if (m < S::HN - 1) ixp = rb + 1;
+      else ixp = S::OXF + N * N + k0 * N + j, dxp = KS * N;
+    }
+    if (j == 0) iym = S::OY + k0 * S::HN + m, dym = KS * S::HN;
+    if (j == N - 1) iyp = S::OY + S::FH + k0 * S::HN + m, dyp = KS * S::HN;
+    const int izm0 = k0 > 0 ? rb - S::FH : S::OZ + j * S::HN + m;
+    const int izpL = k0 < KS - 1 ? rb + (S::PER - 1) * DT + S::FH : S::OZ + S::FH + j * S::HN + m;
+    const int ig = S::OG + t;
+    double* __restrict__ dst = L.phi + (size_t)slot * NI + (size_t)c * S::H + t;
+    if (!(L.exp & 512)) {
+      if (kind == KIND_UNIFORM) {  // multigrid.hpp:651-653: (sum of 6 - h^2 g) / 6.0
+        double sv[S::PER], v[S::PER];
+        bool ok = true;
+#pragma unroll
+        for (int q = 0; q < S::PER; ++q) {
+          const double zm = st[q == 0 ? izm0 : rb + q * DT - S::FH];
+          const double zp = st[q == S::PER - 1 ? izpL : rb + q * DT + S::FH];
+          sv[q] = st[ixm + q * dxm] + st[ixp + q * dxp] + st[iym + q * dym] + st[iyp + q * dyp] + zm + zp -
+                  h2 * st[ig + q * S::THR];
+          v[q] = div6_fast(sv[q]);
+          ok = ok && div6_in_range(sv[q]);
+        }
+        if (!ok) {
+#pragma unroll
+          for (int q = 0; q < S::PER; ++q) v[q] = div6_slow(sv[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < S::PER; ++q) dst[q * S::THR] = v[q];
+      } else {  // interface block: uniform rows only (multigrid.hpp:667-672)
+        const int32_t* rq = reinterpret_cast<const int32_t*>(st + S::ORQ);
+#pragma unroll
+        for (int q = 0; q < S::PER; ++q) {
+          if (rq[t + q * S::THR] >= 0) continue;
+          double sv = -h2 * st[ig + q * S::THR];
+          sv += st[ixm + q * dxm];
+          sv += st[ixp + q * dxp];
+          sv += st[iym + q * dym];
+          sv += st[iyp + q * dyp];
+          sv += st[q == 0 ? izm0 : rb + q * DT - S::FH];
+          sv += st[q == S::PER - 1 ? izpL : rb + q * DT + S::FH];
+          dst[q * S::THR] = -sv * (-1.0 / 6.0);
+        }
+      }
+    }
+    __syncthreads();  // stage s consumed
+    if (it + S_STAGES < nmine) {
+      if (t == 0) gs_issue<N>(L, pf, c, st, &full[s]);
+      if (t == 0) meta[s][0] = pf.slot(), meta[s][1] = pf.a.y;
+      gs_issue_async<N>(L, pf, c, st);
+    }
+    cp_async_commit();
+    pf = pf2;
+  }
+}
+
+// ------------------------------------------------------------------ fused residual + restriction
+// residual_level(l) + restrict_level(l) (multigrid.hpp:374-398,510-517,
+// 697-722) for a level without coarse-fine faces: one stage holds both colour
+// halves of a block's phi and, indexed by the colour of the block's own
+// boundary cell, the neighbour (or physical-ghost) value next to every face
+// cell.  Thread t owns parent cell (ii,jj,kk) of the block's octant and its
+// 2x2x2 children; g comes straight from global memory (coalesced, issued
+// before the stage wait).
+template <int N>
+struct RStream3 {
+  static constexpr int HN = N / 2;
+  static constexpr int H = N * N * N / 2;
+  static constexpr int FH = N * HN;
+  static constexpr int THR = HN * HN * HN;  // parents per block
+  // doubles: P[2][H], g[2][H], hz[2 side][2 colour][FH], hy[2][2][FH], hx[2][N*N]
+  static constexpr int OP = 0, OG = 2 * H, OZ = 4 * H, OY = OZ + 4 * FH, OXF = OY + 4 * FH;
+  static constexpr int STAGE = OXF + 2 * N * N;
+  static constexpr uint32_t TX_BYTES = (uint32_t)(4 * H + 4 * FH) * 8u;
+  static constexpr int YC = 2 * 2 * N * (HN / 2);  // 16-B chunks of the y layers
+};
+
+template <int N>
+__device__ __forceinline__ void rs_issue(const LevelView& L, const BlockPlan& P, double* st, uint64_t* bar) {
+  using S = RStream3<N>;
+  constexpr int NI = N * N * N;
+  const int slot = P.slot();
+  const double* own = L.phi + (size_t)slot * NI;
+  mbar_arrive_expect_tx(bar, S::TX_BYTES);
+  bulk_g2s(st + S::OP, own, 2 * S::H * 8, bar);
+  bulk_g2s(st + S::OG, L.rhs + (size_t)slot * NI, 2 * S::H * 8, bar);
+  for (int side = 0; side < 2; ++side) {
+    const int ns = P.nbr(4 + side);
+    for (int cc = 0; cc < 2; ++cc) {
+      const double* src = ns >= 0 ? L.phi + (size_t)ns * NI + (size_t)(1 - cc) * S::H + (side ? 0 : (N - 1) * S::FH)
+                                  : own + (size_t)cc * S::H + (side ? (N - 1) * S::FH : 0);
+      bulk_g2s(st + S::OZ + (side * 2 + cc) * S::FH, src, S::FH * 8, bar);
+    }
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void rs_issue_async(const LevelView& L, const BlockPlan& P, double* st) {
+  using S = RStream3<N>;
+  constexpr int NI = N * N * N;
+  const int t = threadIdx.x;
+  const int slot = P.slot();
+  for (int u = t; u < 2 * N * N; u += S::THR) {  // x faces: one value per row (j,k)
+    const int side = u / (N * N), r = u % (N * N), k = r / N, j = r % N;
+    const int ib = side ? N - 1 : 0;
+    const int cb = (ib + j + k) & 1;  // colour of the block's own boundary cell
+    const int ns = P.nbr(side);
+    const double* src = ns >= 0
+                            ? L.phi + (size_t)ns * NI + (size_t)(1 - cb) * S::H + (side ? 0 : S::HN - 1) + S::HN * (j + N * k)
+                            : L.phi + (size_t)slot * NI + (size_t)cb * S::H + (ib >> 1) + S::HN * (j + N * k);
+    cp_async8(st + S::OXF + side * N * N + k * N + j, src);
+  }
+  for (int u = t; u < S::YC; u += S::THR) {  // y layers, 16-B chunks
+    constexpr int CR = S::HN / 2;
+    const int side = u / (2 * N * CR), cc = (u / (N * CR)) % 2, k = (u / CR) % N, ch = u % CR;
+    const int ns = P.nbr(2 + side);
+    const double* src = ns >= 0 ? L.phi + (size_t)ns * NI + (size_t)(1 - cc) * S::H + (size_t)k * S::FH +
+                                      (side ? 0 : (N - 1) * S::HN)
+                                : L.phi + (size_t)slot * NI + (size_t)cc * S::H + (size_t)k * S::FH +
+                                      (side ? (N - 1) * S::HN : 0);
+    cp_async16(st + S::OY + (side * 2 + cc) * S::FH + k * S::HN + 2 * ch, src + 2 * ch);
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void rs_phys_faces(const LevelView& L, int slot, int pmask, double* st) {
+  using S = RStream3<N>;
+  for (int q = threadIdx.x; q < 2 * N * N + 8 * S::FH; q += blockDim.x) {
+    int dir, tj;
+    double* h;
+    if (q < 2 * N * N) {
+      const int side = q / (N * N), r = q % (N * N);
+      dir = side;
+      tj = r % N + N * (r / N);  // j + N k
+      h = st + S::OXF + q;
+    } else {
+      const int qq = q - 2 * N * N;
+      const int f = qq / (2 * S::FH), cc = (qq / S::FH) % 2, r = qq % S::FH;  // f: -y +y -z +z
+      dir = 2 + f;
+      const int m = r % S::HN, a = r / S::HN;
+      const int side = f & 1;
+      if (f < 2) {  // y face: a = k
+        const int jb = side ? N - 1 : 0;
+        tj = 2 * m + ((cc + jb + a) & 1) + N * a;
+        h = st + S::OY + (side * 2 + cc) * S::FH + r;
+      } else {  // z face: a = j
+        const int kb = side ? N - 1 : 0;
+        tj = 2 * m + ((cc + a + kb) & 1) + N * a;
+        h = st + S::OZ + (side * 2 + cc) * S::FH + r;
+      }
+    }
+    if (!((pmask >> dir) & 1) || L.bctype[dir] == 1) continue;
+    double bcv = 0.0;
+    if (!L.bczero) {
+      const int bo = L.bcoff[slot * 6 + dir];
+      if (bo >= 0) bcv = L.bcval[bo + tj];
+    }
+    *h = 2.0 * bcv - *h;
+  }
+}
+
+template <int N, int S_STAGES, int MINB>
+__global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(LevelView Lf, LevelView Lp,
+                                                                           const double* __restrict__ phi_b,
+                                                                           const int4* __restrict__ plan, int n) {
+  using S = RStream3<N>;
+  constexpr int NI = N * N * N;
+  constexpr int HN = S::HN;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t full[S_STAGES];
+  __shared__ int meta[S_STAGES][2];
+  const int t = threadIdx.x;
+  const int G = gridDim.x;
+  const int nmine = (int)blockIdx.x < n ? (n - 1 - (int)blockIdx.x) / G + 1 : 0;
+  if (nmine == 0) return;
+  if (t == 0) {
+    for (int s = 0; s < S_STAGES; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  for (int s = 0; s < S_STAGES; ++s) {
+    if (s < nmine) {
+      const BlockPlan P = load_plan(plan, blockIdx.x + s * G);
+      if (t == 0) {
+        rs_issue<N>(Lf, P, sm + s * S::STAGE, &full[s]);
+        meta[s][0] = P.slot(), meta[s][1] = P.a.y;
+      }
+      rs_issue_async<N>(Lf, P, sm + s * S::STAGE);
+    }
+    cp_async_commit();
+  }
+  __syncthreads();  // meta of the first stages
+  BlockPlan pf;
+  if (S_STAGES < nmine) pf = load_plan(plan, blockIdx.x + S_STAGES * G);
+  const int ii = t % HN, jj = (t / HN) % HN, kk = t / (HN * HN);
+  const double w = Lf.w;
+  for (int it = 0; it < nmine; ++it) {
+    const int s = it % S_STAGES;
+    double* st = sm + s * S::STAGE;
+    BlockPlan pf2;
+    if (it + S_STAGES + 1 < nmine) pf2 = load_plan(plan, blockIdx.x + (it + S_STAGES + 1) * G);
+    const int slot = meta[s][0], flags = meta[s][1];
+    const int kind = flags & 0xff, pmask = (flags >> 8) & 63;
+    // parent slot / octant: loads in flight across the wait
+    const int Pp = Lf.parent[slot];
+    const int cx = Lf.coords[slot * 3] & 1, cy = Lf.coords[slot * 3 + 1] & 1, cz = Lf.coords[slot * 3 + 2] & 1;
+    mbar_wait(&full[s], (uint32_t)((it / S_STAGES) & 1));
+    cp_async_wait<S_STAGES - 1>();
+    __syncthreads();
+    if (pmask) {
+      rs_phys_faces<N>(Lf, slot, pmask, st);
+      __syncthreads();
+    }
+    const double* P0 = st + S::OP;
+    // own values of the 8 children
+    double f[8], g[8];
+#pragma unroll
+    for (int ch = 0; ch < 8; ++ch) {
+      const int dx = ch & 1, dy = (ch >> 1) & 1, dz = ch >> 2;
+      const int e = ii + HN * ((2 * jj + dy) + N * (2 * kk + dz));
+      f[ch] = P0[((dx + dy + dz) & 1) * S::H + e];
+      g[ch] = st[S::OG + ((dx + dy + dz) & 1) * S::H + e];
+    }
+    double res[8];
+#pragma unroll
+    for (int ch = 0; ch < 8; ++ch) {
+      const int dx = ch & 1, dy = (ch >> 1) & 1, dz = ch >> 2;
+      const int j = 2 * jj + dy, k = 2 * kk + dz;
+      const int cc = (dx + dy + dz) & 1;
+      const int e = ii + HN * (j + N * k);
+      const double* O = P0 + (1 - cc) * S::H;  // other colour
+      double p[6];
+      // x-, x+
+      if (dx) p[0] = f[ch - 1];
+      else p[0] = ii > 0 ? O[e - 1] : st[S::OXF + k * N + j];
+      if (!dx) p[1] = f[ch + 1];
+      else p[1] = ii < HN - 1 ? O[e + 1] : st[S::OXF + N * N + k * N + j];
+      // y-, y+
+      if (dy) p[2] = f[ch - 2];
+      else p[2] = jj > 0 ? O[e - HN] : st[S::OY + (0 * 2 + cc) * S::FH + k * HN + ii];
+      if (!dy) p[3] = f[ch + 2];
+      else p[3] = jj < HN - 1 ? O[e + HN] : st[S::OY + (1 * 2 + cc) * S::FH + k * HN + ii];
+      // z-, z+
+      if (dz) p[4] = f[ch - 4];
+      else p[4] = kk > 0 ? O[e - S::FH] : st[S::OZ + (0 * 2 + cc) * S::FH + j * HN + ii];
+      if (!dz) p[5] = f[ch + 4];
+      else p[5] = kk < HN - 1 ? O[e + S::FH] : st[S::OZ + (1 * 2 + cc) * S::FH + j * HN + ii];
+      // uniform row (stencil.hpp:300-322); all-inside blocks have residual 0;
+      // parents with a special child in an interface block are recomputed by
+      // k_restrict_fix
+      double sres = -2.0 * 3 * f[ch];
+#pragma unroll
+      for (int d = 0; d < 6; ++d) sres += p[d];
+      res[ch] = kind == KIND_ALL_INSIDE ? 0.0 : g[ch] - sres * w;
+    }
+    // sum of the children in x-fastest order (multigrid.hpp:706-721)
+    double sr = 0.0, sf = 0.0;
+#pragma unroll
+    for (int ch = 0; ch < 8; ++ch) {
+      sr += res[ch];
+      sf += f[ch];
+    }
+    const int pi = cx * HN + ii, pj = cy * HN + jj, pk = cz * HN + kk;
+    const int pc = (pi + pj + pk) & 1, pe = (pi + N * (pj + N * pk)) >> 1;
+    const size_t pa = (size_t)Pp * NI + (size_t)pc * S::H + pe;
+    Lp.phi[pa] = sf / 8.0;  // pinned parents: k_restrict_fix
+    Lp.rhs[pa] = sr / 8.0;
+    __syncthreads();  // stage s consumed
+    if (it + S_STAGES < nmine) {
+      if (t == 0) {
+        rs_issue<N>(Lf, pf, st, &full[s]);
+        meta[s][0] = pf.slot(), meta[s][1] = pf.a.y;
+      }
+      rs_issue_async<N>(Lf, pf, st);
+    }
+    cp_async_commit();
+    pf = pf2;
+  }
+}
+
+// Parents of the fused restriction that k_restrict_stream cannot finish: a
+// child with a special (cut / inside) row in an interface block.  Eight
+// threads per parent, one per child (residual stencil.hpp:325-359 from global
+// memory); lane 0 of the group sums them in the reference's x-fastest order
+// (multigrid.hpp:706-721).  Pinned parents are left to k_pin_list.
+template <int D, int N>
+__global__ void __launch_bounds__(128) k_restrict_fix(LevelView Lf, LevelView Lfc, LevelView Lp,
+                                                     const double* __restrict__ phi_b,
+                                                     const int2* __restrict__ list, int n) {
+  using G = Geo<D, N>;
+  constexpr int HN = N / 2, NC = 1 << D;
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int q = gid / NC, ch = gid % NC;
+  double r = 0.0, f = 0.0;
+  int slot = 0, t = 0;
+  if (q < n) {
+    slot = list[q].x;
+    t = list[q].y;
+    const int ii = t % HN, jj = (t / HN) % HN, kk = D == 3 ? t / (HN * HN) : 0;
+    const int i = 2 * ii + (ch & 1), j = 2 * jj + ((ch >> 1) & 1), k = D == 3 ? 2 * kk + (ch >> 2) : 0;
+    const int c = G::colour(i, j, k), e = G::entry(i, j, k);
+    bool inside;
+    r = resid_cell<D, N>(Lf, Lfc, phi_b, slot, c, e, &inside);
+    f = Lf.phi[(size_t)slot * G::NI + (size_t)c * G::H + e];
+  }
+  const int base = threadIdx.x & ~(NC - 1) & 31;
+  double sr = 0.0, sf = 0.0;
+#pragma unroll
+  for (int u = 0; u < NC; ++u) {
+    sr += __shfl_sync(0xffffffffu, r, base + u);
+    sf += __shfl_sync(0xffffffffu, f, base + u);
+  }
+  if (q >= n || ch != 0) return;
+  const int ii = t % HN, jj = (t / HN) % HN, kk = D == 3 ? t / (HN * HN) : 0;
+  const int P = Lf.parent[slot];
+  int cp[3] = {0, 0, 0};
+  for (int a = 0; a < D; ++a) cp[a] = (Lf.coords[slot * D + a] & 1) * HN;
+  const int pi = cp[0] + ii, pj = cp[1] + jj, pk = cp[2] + kk;
+  const size_t pa = (size_t)P * G::NI + (size_t)(G::colour(pi, pj, pk) * G::H + G::entry(pi, pj, pk));
+  Lp.phi[pa] = sf / (double)NC;
+  Lp.rhs[pa] = sr / (double)NC;
+}
+
+// apply_pins (stencil.hpp:225-237) over a list of (cell address, object) pairs
+static __global__ void __launch_bounds__(256) k_pin_list(double* __restrict__ phi, const double* __restrict__ phi_b,
+                                                 const int2* __restrict__ list, int n) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) phi[list[q].x] = phi_b[list[q].y];
+}
+
+}  // namespace pmgdev

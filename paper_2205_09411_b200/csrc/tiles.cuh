@@ -34,6 +34,19 @@ struct Tile {
 // subnormal range take the plain division, so the result is bit-identical to
 // the reference's `/ 6.0` for every input (multigrid.hpp:651-653).
 static __device__ __noinline__ double div6_slow(double x) { return x / 6.0; }
+// x / 6.0 in three unconditional ops, exact (correctly rounded) whenever
+// div6_in_range(x); callers batch the range test and redo the rare rest
+// with the IEEE division.
+__device__ __forceinline__ double div6_fast(double x) {
+  const double y = 0.16666666666666666;  // RN(1/6)
+  const double q = __dmul_rn(x, y);
+  const double r = __fma_rn(-q, 6.0, x);
+  return __fma_rn(r, y, q);
+}
+__device__ __forceinline__ bool div6_in_range(double x) {
+  const double ax = fabs(x);
+  return (ax > 1e-290 && ax < 1e300) || x == 0.0;
+}
 __device__ __forceinline__ double div6(double x) {
   const double y = 0.16666666666666666;  // RN(1/6)
   const double q = __dmul_rn(x, y);

@@ -11,10 +11,11 @@ import io
 import subprocess
 import sys
 
+# (metric, label, target unit); values are converted with the report's unit row
 METRICS = [
-    ("gpu__time_duration.sum", "duration", 1e-3, "us"),
-    ("dram__bytes_read.sum", "dram read", 1e-6, "MB"),
-    ("dram__bytes_write.sum", "dram write", 1e-6, "MB"),
+    ("gpu__time_duration.sum", "duration", 1, "us"),
+    ("dram__bytes_read.sum", "dram read", 1, "MB"),
+    ("dram__bytes_write.sum", "dram write", 1, "MB"),
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram throughput", 1, "% of peak"),
     ("gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed", "memory throughput", 1, "% of peak"),
     ("lts__t_sector_hit_rate.pct", "L2 hit rate", 1, "%"),
@@ -24,8 +25,19 @@ METRICS = [
     ("launch__grid_size", "grid", 1, "CTAs"),
     ("launch__block_size", "block", 1, "threads"),
     ("launch__shared_mem_per_block_dynamic", "dyn smem/CTA", 1e-3, "KB"),
-    ("sm__cycles_elapsed.avg.per_second", "SM clock", 1e-9, "GHz"),
+    ("sm__cycles_elapsed.avg.per_second", "SM clock", 1, "GHz"),
 ]
+
+_UNIT = {("nsecond", "us"): 1e-3, ("usecond", "us"): 1.0, ("msecond", "us"): 1e3,
+         ("ns", "us"): 1e-3, ("us", "us"): 1.0, ("ms", "us"): 1e3,
+         ("byte", "MB"): 1e-6, ("Kbyte", "MB"): 1e-3, ("Mbyte", "MB"): 1.0, ("Gbyte", "MB"): 1e3,
+         ("hz", "GHz"): 1e-9, ("Khz", "GHz"): 1e-6, ("Mhz", "GHz"): 1e-3, ("Ghz", "GHz"): 1.0,
+         ("cycle/nsecond", "GHz"): 1.0, ("cycle/usecond", "GHz"): 1e-3, ("cycle/second", "GHz"): 1e-9,
+         ("Kbyte", "KB"): 1.0, ("byte", "KB"): 1e-3}
+
+
+def _conv(v, unit, target):
+    return v * _UNIT.get((unit, target), 1.0)
 
 
 def _num(s):
@@ -68,22 +80,34 @@ def full_report(path, regex=None):
     rows = list(csv.reader(io.StringIO(out)))
     if len(rows) < 3:
         return "(no data)"
-    h = rows[0]
+    h, units = rows[0], rows[1]
     lines = []
     for r in rows[2:]:
         if len(r) != len(h):
             continue
         name = r[h.index("Kernel Name")].split("(")[0] if "Kernel Name" in h else "?"
-        lines.append(f"### `{name}`\n\n| metric | value |\n|---|---:|")
-        for key, label, scale, unit in METRICS:
+        val = {}
+        for key, label, _, unit in METRICS:
             if key in h:
                 v = _num(r[h.index(key)])
                 if v is not None:
-                    lines.append(f"| {label} | {v * scale:.4g} {unit} |")
-        if "dram__bytes_read.sum" in h and "gpu__time_duration.sum" in h:
-            b = (_num(r[h.index("dram__bytes_read.sum")]) or 0) + (_num(r[h.index("dram__bytes_write.sum")]) or 0)
-            t = _num(r[h.index("gpu__time_duration.sum")]) or 1
-            lines.append(f"| dram GB/s (read+write / duration) | {b / t:.1f} |")
+                    val[key] = _conv(v, units[h.index(key)], unit)
+        lines.append(f"### `{name}`\n\n| metric | value |\n|---|---:|")
+        for key, label, _, unit in METRICS:
+            if key in val:
+                lines.append(f"| {label} | {val[key]:.4g} {unit} |")
+        if "dram__bytes_read.sum" in val and "gpu__time_duration.sum" in val:
+            b = val["dram__bytes_read.sum"] + val.get("dram__bytes_write.sum", 0)
+            lines.append(f"| dram GB/s ((read+write) / duration) | {b / val['gpu__time_duration.sum'] * 1e3:.1f} |")
+        st = []
+        for k, v in zip(h, r):
+            if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
+                x = _num(v)
+                if x:
+                    st.append((x, k[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]))
+        st.sort(reverse=True)
+        if st:
+            lines.append("| top stalls (warps per issue) | " + ", ".join(f"{n} {x:.2f}" for x, n in st[:5]) + " |")
         lines.append("")
     return "\n".join(lines)
 
