@@ -167,7 +167,7 @@ static void upload_stencils(Ctx& c) {
     kindv[(size_t)l] = kind;
     // block classes for the specialised kernels
     {
-      std::vector<int32_t> fast, slow, ufast, uslow, fix[2], gsl, rsl;
+      std::vector<int32_t> fast, slow, ufast, uslow, fix[2], gsl, rsl, url;
       for (int s = 0; s < d.nb; ++s) {
         const int id = m.slots[(size_t)l][(size_t)s];
         bool no_cf = true;  // lean kernels handle same-level and physical faces
@@ -187,6 +187,7 @@ static void upload_stencils(Ctx& c) {
           require(sr < (1 << 17), "too many interface blocks on one level for the streaming plan");
           const int32_t e[8] = {s, (int32_t)kind[(size_t)s] | (pm << 8) | (sr << 14), ns[0], ns[1], ns[2], ns[3], ns[4], ns[5]};
           rsl.insert(rsl.end(), e, e + 8);
+          if (kind[(size_t)s] == pmgdev::KIND_UNIFORM) url.insert(url.end(), e, e + 8);
           if (kind[(size_t)s] != pmgdev::KIND_ALL_INSIDE) gsl.insert(gsl.end(), e, e + 8);
         }
         (no_cf && kind[(size_t)s] == pmgdev::KIND_UNIFORM ? ufast : uslow).push_back(s);
@@ -204,6 +205,8 @@ static void upload_stencils(Ctx& c) {
       d.gs_plan.upload(gsl, c.stream);
       d.n_rs = (int)rsl.size() / 8;
       d.rs_plan.upload(rsl, c.stream);
+      d.n_ur = (int)url.size() / 8;
+      d.ur_plan.upload(url, c.stream);
       d.n_fast = (int)fast.size();
       d.n_slow = (int)slow.size();
       d.fast_list.upload(fast, c.stream);
@@ -734,6 +737,8 @@ static void set_mesh(Ctx& c, int nb, const int32_t* level, const int32_t* coords
     d.parent.upload(par, c.stream);
     d.child.upload(chl, c.stream);
     d.leaf.upload(leaf, c.stream);
+    d.n_leaf = 0;
+    for (uint8_t f : leaf) d.n_leaf += f ? 1 : 0;
     d.slot_id.upload(sid, c.stream);
     d.ref_slot.upload(rpos, c.stream);
     const size_t cells = (size_t)d.nb * c.NI;

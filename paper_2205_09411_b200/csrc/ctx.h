@@ -80,6 +80,7 @@ struct HostCoarse {
 
 struct LevelDev {
   int nb = 0;
+  int n_leaf = 0;  // leaf blocks (levels without leaves keep a zero record)
   DevBuf<int32_t> nbr, cnbr, coords, parent, child, srow, bcoff, cfoff, row_of, slot_id;
   DevBuf<uint8_t> leaf, kind, r_mask;
   DevBuf<double> phi, rhs, old, res, bcval, cfold, r_center, r_nb, r_bc;
@@ -97,6 +98,8 @@ struct LevelDev {
   int n_gs = 0;
   DevBuf<int32_t> rs_plan;  // every block without coarse-fine faces (incl. all-inside)
   int n_rs = 0;
+  DevBuf<int32_t> ur_plan;  // uniform blocks without coarse-fine faces (= ufast_list)
+  int n_ur = 0;
   DevBuf<int32_t> rfix_list;  // (slot, parent-local index) pairs for k_restrict_fix
   int n_rfix = 0;
   DevBuf<int32_t> pin_list;   // (cell address, object) of this level's inside rows

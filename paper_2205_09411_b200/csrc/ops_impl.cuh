@@ -13,6 +13,10 @@ namespace pmghost {
 
 using namespace pmgdev;
 
+// levels with at most this many blocks run the one-thread-per-cell kernels:
+// they are latency-bound, and a cell per thread gives the most loads in flight
+constexpr int kSmallLevel = 64;
+
 // streaming GS pipeline depth and residency (stream.cuh)
 constexpr int kStreamStages = 2;
 constexpr int kStreamCtasPerSm = 2;
@@ -35,6 +39,11 @@ struct OpsImpl final : Ops {
 
   void gs(Ctx& c, int l, int parity) override {
     const LevelView& L = V(c, l);
+    if (L.nb <= kSmallLevel && !(L.exp & 32768)) {
+      k_gs<D, N><<<grid_for((long long)L.nb * G::H), kThreads, 0, c.stream>>>(L, Vc(c, l), c.phi_b.p, parity);
+      check();
+      return;
+    }
     if constexpr (TILE) {
       const LevelDev& d = *c.lev[(size_t)l];
       // the latency-bound general blocks and the cut-row fix-up run on a
@@ -99,6 +108,16 @@ struct OpsImpl final : Ops {
   void restrict_(Ctx& c, int l, int mode) override {
     const LevelView& Lf = V(c, l);
     const unsigned g = grid_for((long long)Lf.nb * (G::NI / G::NC));
+    if (Lf.nb <= kSmallLevel && !(Lf.exp & 32768)) {
+      if (mode == RM_RES)
+        k_restrict<D, N, RM_RES><<<g, kThreads, 0, c.stream>>>(Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
+      else if (mode == RM_RHS)
+        k_restrict<D, N, RM_RHS><<<g, kThreads, 0, c.stream>>>(Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
+      else
+        k_restrict<D, N, RM_FUSED><<<g, kThreads, 0, c.stream>>>(Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
+      check();
+      return;
+    }
     if constexpr (D == 3 && N == 16) {
       const LevelDev& d = *c.lev[(size_t)l];
       if (mode == RM_FUSED && !d.has_cf && d.n_rs == Lf.nb && !(Lf.exp & 8192)) {
@@ -106,13 +125,13 @@ struct OpsImpl final : Ops {
         constexpr size_t smem = (size_t)ST * RStream3<N>::STAGE * sizeof(double);
         static bool attr = false;
         if (!attr) {
-          PMG_CUDA(cudaFuncSetAttribute(k_restrict_stream<N, ST, MINB>,
+          PMG_CUDA(cudaFuncSetAttribute(k_restrict_stream<N, ST, MINB, false>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
           attr = true;
         }
         const int grid = std::min(d.n_rs, c.sms * MINB);
-        k_restrict_stream<N, ST, MINB><<<grid, RStream3<N>::THR, smem, c.stream>>>(
-            Lf, V(c, l - 1), c.phi_b.p, (const int4*)d.rs_plan.p, d.n_rs);
+        k_restrict_stream<N, ST, MINB, false><<<grid, RStream3<N>::THR, smem, c.stream>>>(
+            Lf, V(c, l - 1), c.phi_b.p, (const int4*)d.rs_plan.p, d.n_rs, nullptr, nullptr, nullptr);
         if (d.n_rfix > 0)
           k_restrict_fix<D, N><<<grid_for((long long)d.n_rfix * 8, 128), 128, 0, c.stream>>>(
               Lf, Vc(c, l), V(c, l - 1), c.phi_b.p, (const int2*)d.rfix_list.p, d.n_rfix);
@@ -147,12 +166,14 @@ struct OpsImpl final : Ops {
     const LevelView& L = V(c, lc);
     const unsigned g = grid_for((long long)L.nb * G::NI);
     if constexpr (TILE) {
-      if (f)
-        k_fas_tile<D, N, true><<<L.nb, TT::THREADS, 0, c.stream>>>(L, Vc(c, lc), c.phi_b.p);
-      else
-        k_fas_tile<D, N, false><<<L.nb, TT::THREADS, 0, c.stream>>>(L, Vc(c, lc), c.phi_b.p);
-      check();
-      return;
+      if (!(L.nb <= kSmallLevel && !(L.exp & 32768))) {
+        if (f)
+          k_fas_tile<D, N, true><<<L.nb, TT::THREADS, 0, c.stream>>>(L, Vc(c, lc), c.phi_b.p);
+        else
+          k_fas_tile<D, N, false><<<L.nb, TT::THREADS, 0, c.stream>>>(L, Vc(c, lc), c.phi_b.p);
+        check();
+        return;
+      }
     }
     if (f)
       k_fas<D, N, true><<<g, kThreads, 0, c.stream>>>(L, Vc(c, lc), c.phi_b.p);
@@ -171,12 +192,14 @@ struct OpsImpl final : Ops {
     const LevelView& Lpp = Vc(c, l - 1);
     const unsigned g = grid_for((long long)Lf.nb * G::NI);
     if constexpr (TILE) {
-      if (full)
-        k_prolong_tile<D, N, true><<<Lf.nb, TT::THREADS, 0, c.stream>>>(Lf, Lp, Lpp);
-      else
-        k_prolong_tile<D, N, false><<<Lf.nb, TT::THREADS, 0, c.stream>>>(Lf, Lp, Lpp);
-      check();
-      return;
+      if (!(Lf.nb <= kSmallLevel && !(Lf.exp & 32768))) {
+        if (full)
+          k_prolong_tile<D, N, true><<<Lf.nb, TT::THREADS, 0, c.stream>>>(Lf, Lp, Lpp);
+        else
+          k_prolong_tile<D, N, false><<<Lf.nb, TT::THREADS, 0, c.stream>>>(Lf, Lp, Lpp);
+        check();
+        return;
+      }
     }
     if (full)
       k_prolong<D, N, true><<<g, kThreads, 0, c.stream>>>(Lf, Lp, Lpp);
@@ -186,6 +209,8 @@ struct OpsImpl final : Ops {
   }
   void record(Ctx& c, int l) override {
     const LevelView& L = V(c, l);
+    // a level without leaves records zeros, which enq_reset_records left there
+    if (c.lev[(size_t)l]->n_leaf == 0) return;
     if constexpr (TILE) {
       const LevelDev& d = *c.lev[(size_t)l];
       const bool fork = d.n_ufast > 0 && d.n_uslow > 0;
@@ -196,7 +221,24 @@ struct OpsImpl final : Ops {
       if (d.n_uslow > 0)
         k_record_tile<D, N><<<d.n_uslow, TT::THREADS, 0, fork ? c.side : c.stream>>>(
             L, Vc(c, l), c.phi_b.p, c.partial.p, c.rec.p, c.counter.p, d.uslow_list.p);
-      if (d.n_ufast > 0)
+      bool streamed = false;
+      if constexpr (D == 3 && N == 16) {
+        if (d.n_ur > 0 && !(L.exp & 16384)) {
+          constexpr int ST = 2, MINB = 1;
+          constexpr size_t smem = (size_t)ST * RStream3<N>::STAGE * sizeof(double);
+          static bool attr = false;
+          if (!attr) {
+            PMG_CUDA(cudaFuncSetAttribute(k_restrict_stream<N, ST, MINB, true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = true;
+          }
+          const int grid = std::min(d.n_ur, c.sms * MINB);
+          k_restrict_stream<N, ST, MINB, true><<<grid, RStream3<N>::THR, smem, c.stream>>>(
+              L, L, c.phi_b.p, (const int4*)d.ur_plan.p, d.n_ur, c.partial.p, c.rec.p, c.counter.p);
+          streamed = true;
+        }
+      }
+      if (d.n_ufast > 0 && !streamed)
         k_record_lean<D, N><<<d.n_ufast, TT::THREADS, 0, c.stream>>>(L, c.partial.p, c.rec.p,
                                                                      c.counter.p, d.ufast_list.p);
       if (fork) {

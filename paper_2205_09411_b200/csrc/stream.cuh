@@ -435,16 +435,24 @@ __device__ __forceinline__ void rs_phys_faces(const LevelView& L, int slot, int 
   }
 }
 
-template <int N, int S_STAGES, int MINB>
+// RECORD = false: fused residual + restriction into level l-1.
+// RECORD = true: leaf-residual record of uniform blocks (record_leaf_residual,
+// multigrid.hpp:529-562): per-block max |r|, sum r^2, count into `partial`,
+// the last block folds them in slot order (record_finish).
+template <int N, int S_STAGES, int MINB, bool RECORD>
 __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(LevelView Lf, LevelView Lp,
                                                                            const double* __restrict__ phi_b,
-                                                                           const int4* __restrict__ plan, int n) {
+                                                                           const int4* __restrict__ plan, int n,
+                                                                           Rec* __restrict__ partial, Rec* rec,
+                                                                           unsigned int* counter) {
   using S = RStream3<N>;
   constexpr int NI = N * N * N;
   constexpr int HN = S::HN;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t full[S_STAGES];
   __shared__ int meta[S_STAGES][2];
+  __shared__ double red[72];
+  __shared__ bool last;
   const int t = threadIdx.x;
   const int G = gridDim.x;
   const int nmine = (int)blockIdx.x < n ? (n - 1 - (int)blockIdx.x) / G + 1 : 0;
@@ -470,6 +478,8 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
   if (S_STAGES < nmine) pf = load_plan(plan, blockIdx.x + S_STAGES * G);
   const int ii = t % HN, jj = (t / HN) % HN, kk = t / (HN * HN);
   const double w = Lf.w;
+  double rmx = 0.0, rss = 0.0, rcnt = 0.0;  // RECORD: this CTA's running totals
+  const int first_slot = meta[0][0];
   for (int it = 0; it < nmine; ++it) {
     const int s = it % S_STAGES;
     double* st = sm + s * S::STAGE;
@@ -477,9 +487,11 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
     if (it + S_STAGES + 1 < nmine) pf2 = load_plan(plan, blockIdx.x + (it + S_STAGES + 1) * G);
     const int slot = meta[s][0], flags = meta[s][1];
     const int kind = flags & 0xff, pmask = (flags >> 8) & 63;
-    // parent slot / octant: loads in flight across the wait
-    const int Pp = Lf.parent[slot];
-    const int cx = Lf.coords[slot * 3] & 1, cy = Lf.coords[slot * 3 + 1] & 1, cz = Lf.coords[slot * 3 + 2] & 1;
+    // parent slot / octant (or leaf flag): loads in flight across the wait
+    const int Pp = RECORD ? 0 : Lf.parent[slot];
+    const int cx = RECORD ? 0 : Lf.coords[slot * 3] & 1, cy = RECORD ? 0 : Lf.coords[slot * 3 + 1] & 1,
+              cz = RECORD ? 0 : Lf.coords[slot * 3 + 2] & 1;
+    const bool leaf = RECORD ? Lf.leaf[slot] != 0 : false;
     mbar_wait(&full[s], (uint32_t)((it / S_STAGES) & 1));
     cp_async_wait<S_STAGES - 1>();
     __syncthreads();
@@ -529,6 +541,16 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
       for (int d = 0; d < 6; ++d) sres += p[d];
       res[ch] = kind == KIND_ALL_INSIDE ? 0.0 : g[ch] - sres * w;
     }
+    if (RECORD) {
+      if (leaf) {
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          rmx = fmax(rmx, fabs(res[ch]));
+          rss += res[ch] * res[ch];
+        }
+        rcnt += 8.0;
+      }
+    } else {
     // sum of the children in x-fastest order (multigrid.hpp:706-721)
     double sr = 0.0, sf = 0.0;
 #pragma unroll
@@ -541,6 +563,7 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
     const size_t pa = (size_t)Pp * NI + (size_t)pc * S::H + pe;
     Lp.phi[pa] = sf / 8.0;  // pinned parents: k_restrict_fix
     Lp.rhs[pa] = sr / 8.0;
+    }
     __syncthreads();  // stage s consumed
     if (it + S_STAGES < nmine) {
       if (t == 0) {
@@ -551,6 +574,15 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
     }
     cp_async_commit();
     pf = pf2;
+  }
+  if (RECORD) {  // totals in the first block's entry, zeros in the CTA's others
+    for (int q = 1 + t; q < nmine; q += S::THR) {
+      const int sl = load_plan(plan, blockIdx.x + q * G).slot();
+      partial[sl].max = 0.0;
+      partial[sl].sumsq = 0.0;
+      partial[sl].count = 0;
+    }
+    record_finish(Lf, partial, rec, counter, first_slot, rmx, rss, rcnt, red, &last, (unsigned)nmine);
   }
 }
 

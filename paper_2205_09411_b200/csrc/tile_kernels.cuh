@@ -671,10 +671,13 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_prolong_tile(LevelView 
 // one or two kernels (lean + general block classes, possibly concurrent); the
 // CTA that completes the level's count reduces all partials in slot order
 // (deterministic, multigrid.hpp:555-561).
+// `arrivals` blocks of the level are accounted for by this CTA (1 for the
+// one-block-per-CTA kernels; a persistent CTA reports all its blocks at once,
+// its totals in partial[slot] and zeros in its other blocks' entries).
 __device__ __forceinline__ void record_finish(const LevelView& L, Rec* __restrict__ partial,
                                               Rec* rec, unsigned int* counter, int slot,
                                               double mx, double ss, double cnt, double* sm,
-                                              bool* last) {
+                                              bool* last, unsigned arrivals = 1u) {
   mx = block_max(mx, sm);
   ss = block_sum(ss, sm);
   cnt = block_sum(cnt, sm);
@@ -683,7 +686,7 @@ __device__ __forceinline__ void record_finish(const LevelView& L, Rec* __restric
     partial[slot].sumsq = ss;
     partial[slot].count = (long long)cnt;
     __threadfence();
-    *last = atomicAdd(counter, 1u) == (unsigned)L.nb - 1;
+    *last = atomicAdd(counter, arrivals) + arrivals == (unsigned)L.nb;
   }
   __syncthreads();
   if (!*last) return;
