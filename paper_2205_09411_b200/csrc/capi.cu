@@ -121,6 +121,75 @@ static void upload_bc(Ctx& c) {
   }
 }
 
+// k_gs_cut tables: every cut (non-inside special) row of a lean interface
+// block (no coarse-fine face), per level and colour, with its row index in
+// the level's row arrays and the addresses of its 2D neighbour values
+// (same block, same-level neighbour block, or a physical-face code).
+static void build_cut_tables(Ctx& c) {
+  const HostMesh& m = c.mesh;
+  const HostStencils& st = c.st;
+  const int N = c.N, D = c.dim, NI = c.NI, H = NI / 2, F = c.F;
+  for (int l = 1; l <= m.L; ++l) {
+    LevelDev& d = *c.lev[(size_t)l];
+    std::vector<int32_t> ent[2];
+    std::vector<double> gbc[2];
+    int base = 0;  // row offset of the block within the level's row arrays (upload_stencils order)
+    for (int s = 0; s < d.nb && st.valid; ++s) {
+      const int id = m.slots[(size_t)l][(size_t)s];
+      if (!st.boundary[(size_t)id]) continue;
+      const int rc = st.row_count[(size_t)id];
+      const int r0 = st.row_start[(size_t)id];
+      bool no_cf = true, all_inside = true;
+      for (int f = 0; f < F; ++f) no_cf = no_cf && !(m.nbr[(size_t)id * 6 + f] < 0 && m.cnbr[(size_t)id * 6 + f] >= 0);
+      for (int ii = 0; ii < NI; ++ii) {
+        const int r = st.row_of[(size_t)id * NI + ii];
+        if (r < 0 || st.mask[(size_t)(r0 + r)] != PMG_INSIDE) all_inside = false;
+      }
+      if (no_cf && !all_inside)
+        for (int ii = 0; ii < NI; ++ii) {
+          const int r = st.row_of[(size_t)id * NI + ii];
+          if (r < 0 || st.mask[(size_t)(r0 + r)] == PMG_INSIDE) continue;
+          const int i = ii % N, j = (ii / N) % N, k = D == 3 ? ii / (N * N) : 0;
+          const int cc = (i + j + k) & 1;
+          int32_t e[8] = {(int32_t)((size_t)s * NI + cs_addr(ii, N, D, H)), base + r, 0, 0, 0, 0, 0, 0};
+          double gb[6] = {0, 0, 0, 0, 0, 0};
+          for (int f = 0; f < F; ++f) {
+            const int ax = f / 2, sg = (f & 1) ? 1 : -1;
+            int q[3] = {i, j, k};
+            q[ax] += sg;
+            if (q[ax] >= 0 && q[ax] < N) {
+              e[2 + f] = (int32_t)((size_t)s * NI + cs_addr(q[0] + N * (q[1] + N * q[2]), N, D, H));
+              continue;
+            }
+            const int nid = m.nbr[(size_t)id * 6 + f];
+            if (nid >= 0) {
+              q[ax] = sg > 0 ? 0 : N - 1;
+              e[2 + f] = (int32_t)((size_t)m.slot_of[(size_t)nid] * NI + cs_addr(q[0] + N * (q[1] + N * q[2]), N, D, H));
+              continue;
+            }
+            if (c.bctype[f] == PMG_BC_NEUMANN_ZERO) {
+              e[2 + f] = -1;
+              continue;
+            }
+            e[2 + f] = -2;
+            if (!c.face_off[f].empty() && c.face_off[f][(size_t)id] >= 0) {
+              const int t = D == 2 ? (ax == 0 ? j : i) : (ax == 0 ? j + N * k : ax == 1 ? i + N * k : i + N * j);
+              gb[f] = c.face_vals[f][(size_t)c.face_off[f][(size_t)id] + t];
+            }
+          }
+          ent[cc].insert(ent[cc].end(), e, e + 8);
+          gbc[cc].insert(gbc[cc].end(), gb, gb + 6);
+        }
+      base += rc;
+    }
+    for (int cc = 0; cc < 2; ++cc) {
+      d.n_cut[cc] = (int)ent[cc].size() / 8;
+      d.cut_ent[cc].upload(ent[cc], c.stream);
+      d.cut_gbc[cc].upload(gbc[cc], c.stream);
+    }
+  }
+}
+
 static void upload_stencils(Ctx& c) {
   const HostMesh& m = c.mesh;
   const HostStencils& st = c.st;
@@ -286,6 +355,7 @@ static void upload_stencils(Ctx& c) {
   std::vector<double> pb = st.phi_b;
   if (pb.empty()) pb.push_back(0.0);
   c.phi_b.upload(pb, c.stream);
+  build_cut_tables(c);
 }
 
 static void default_stencils(Ctx& c) {
@@ -809,6 +879,7 @@ static void set_face_bc(Ctx& c, int dir, int type, const double* values) {
     }
   }
   upload_bc(c);
+  if (c.st.valid) build_cut_tables(c);
   set_views(c);
   invalidate_graphs(c);
   PMG_CUDA(cudaStreamSynchronize(c.stream));

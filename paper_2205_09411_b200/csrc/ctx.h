@@ -104,6 +104,10 @@ struct LevelDev {
   int n_rfix = 0;
   DevBuf<int32_t> pin_list;   // (cell address, object) of this level's inside rows
   int n_pin = 0;
+  // k_gs_cut tables per colour: 8 int32 (cell, row, 6 neighbour addresses) + 6 ghost bc values
+  DevBuf<int32_t> cut_ent[2];
+  DevBuf<double> cut_gbc[2];
+  int n_cut[2] = {0, 0};
   DevBuf<int32_t> fix_list[2];  // (slot, entry) pairs of special rows in lean interface blocks
   int n_fix[2] = {0, 0};
   bool has_cf = false;       // some block has a coarse-fine face

@@ -46,12 +46,17 @@ struct OpsImpl final : Ops {
     }
     if constexpr (TILE) {
       const LevelDev& d = *c.lev[(size_t)l];
-      // the latency-bound general blocks and the cut-row fix-up run on a
-      // forked branch concurrently with the bandwidth-bound lean blocks: all
-      // three write disjoint cells of colour `parity` and read only the other
-      // colour (plus, in k_gs_fix, the cut cell's own old value)
-      const bool side_work = d.n_slow > 0 || d.n_fix[parity] > 0;
-      const bool fork = d.n_fast > 0 && side_work;
+      // The streaming kernel (3D, N = 8/16) covers every lean block, cut rows
+      // included; otherwise k_gs_lean does the uniform rows and k_gs_fix the
+      // cut rows.  The general blocks (coarse-fine faces) run on a forked
+      // branch: all kernels write disjoint cells of colour `parity` and read
+      // only the other colour (plus, in k_gs_fix, the cut cell's own value).
+      bool stream = false;
+      if constexpr (D == 3 && (N == 8 || N == 16)) stream = d.n_gs > 0 && !(L.exp & 256);
+      const int nfix = stream ? 0 : d.n_fix[parity];
+      const bool lean_work = stream || d.n_fast > 0;
+      const int ncut = stream ? d.n_cut[parity] : 0;
+      const bool fork = lean_work && (d.n_slow > 0 || nfix > 0 || ncut > 0);
       if (fork) {
         PMG_CUDA(cudaEventRecord(c.ev_fork, c.stream));
         PMG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
@@ -59,18 +64,20 @@ struct OpsImpl final : Ops {
       cudaStream_t s2 = fork ? c.side : c.stream;
       if (d.n_slow > 0)
         k_gs_tile<D, N><<<d.n_slow, TT::THREADS, 0, s2>>>(L, Vc(c, l), c.phi_b.p, parity, d.slow_list.p);
-      if (d.n_fix[parity] > 0)
-        k_gs_fix<D, N><<<grid_for(d.n_fix[parity], 128), 128, 0, s2>>>(
-            L, Vc(c, l), c.phi_b.p, parity, (const int2*)d.fix_list[parity].p, d.n_fix[parity]);
-      if constexpr (D == 3 && (N == 8 || N == 16)) {
-        if (d.n_gs > 0 && !(L.exp & 256)) {
+      if (nfix > 0)
+        k_gs_fix<D, N><<<grid_for(nfix, 128), 128, 0, s2>>>(L, Vc(c, l), c.phi_b.p, parity,
+                                                           (const int2*)d.fix_list[parity].p, nfix);
+      if (ncut > 0)  // cut rows: disjoint from the streaming kernel's cells and inputs
+        k_gs_cut<D><<<grid_for(ncut, 128), 128, 0, s2>>>(L, c.phi_b.p, d.cut_ent[parity].p,
+                                                        d.cut_gbc[parity].p, ncut);
+      if (stream) {
+        if constexpr (D == 3 && (N == 8 || N == 16)) {
           if (L.exp & 4096)
             launch_gs_stream<4, 1>(c, L, d, parity);
           else
             launch_gs_stream<kStreamStages, kStreamCtasPerSm>(c, L, d, parity);
-        } else if (d.n_fast > 0) {
-          k_gs_lean<D, N><<<d.n_fast, Lean<D, N>::THR, 0, c.stream>>>(L, parity, d.fast_list.p);
         }
+
       } else if (d.n_fast > 0) {
         k_gs_lean<D, N><<<d.n_fast, Lean<D, N>::THR, 0, c.stream>>>(L, parity, d.fast_list.p);
       }
@@ -95,8 +102,8 @@ struct OpsImpl final : Ops {
         attr = true;
       }
       const int grid = std::min(d.n_gs, c.sms * MINB);
-      k_gs_stream<N, ST, MINB><<<grid, Stream3<N>::THR, smem, c.stream>>>(L, parity, (const int4*)d.gs_plan.p,
-                                                                           d.n_gs);
+      k_gs_stream<N, ST, MINB><<<grid, Stream3<N>::THR, smem, c.stream>>>(L, parity, c.phi_b.p,
+                                                                           (const int4*)d.gs_plan.p, d.n_gs);
     }
   }
   void residual(Ctx& c, int l) override {

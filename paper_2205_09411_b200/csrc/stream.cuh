@@ -215,11 +215,12 @@ __device__ __forceinline__ void gs_phys_faces(const LevelView& L, int slot, int 
 }
 
 // GS-RB half-sweep of the lean 3D blocks (UNIFORM / IFACE blocks without
-// coarse-fine faces, in plan order).  Special rows of IFACE blocks are
-// skipped (k_gs_fix updates the cut rows; inside rows keep their pin).
+// coarse-fine faces, in plan order).  Special rows are left alone: k_gs_cut
+// updates the cut rows afterwards, inside rows keep their pin.
 template <int N, int S_STAGES, int MINB>
 __global__ void __launch_bounds__(Stream3<N>::THR, MINB) k_gs_stream(LevelView L, int parity,
-                                                                 const int4* __restrict__ plan, int n) {
+                                                                    const double* __restrict__ phi_b,
+                                                                    const int4* __restrict__ plan, int n) {
   using S = Stream3<N>;
   constexpr int NI = N * N * N;
   extern __shared__ __align__(128) double sm[];
@@ -303,19 +304,25 @@ __global__ void __launch_bounds__(Stream3<N>::THR, MINB) k_gs_stream(LevelView L
         }
 #pragma unroll
         for (int q = 0; q < S::PER; ++q) dst[q * S::THR] = v[q];
-      } else {  // interface block: uniform rows only (multigrid.hpp:667-672)
+      } else {  // interface block (multigrid.hpp:665-684)
         const int32_t* rq = reinterpret_cast<const int32_t*>(st + S::ORQ);
 #pragma unroll
         for (int q = 0; q < S::PER; ++q) {
-          if (rq[t + q * S::THR] >= 0) continue;
-          double sv = -h2 * st[ig + q * S::THR];
-          sv += st[ixm + q * dxm];
-          sv += st[ixp + q * dxp];
-          sv += st[iym + q * dym];
-          sv += st[iyp + q * dyp];
-          sv += st[q == 0 ? izm0 : rb + q * DT - S::FH];
-          sv += st[q == S::PER - 1 ? izpL : rb + q * DT + S::FH];
-          dst[q * S::THR] = -sv * (-1.0 / 6.0);
+          const int r = rq[t + q * S::THR];
+          const double g = st[ig + q * S::THR];
+          const double p0 = st[ixm + q * dxm], p1 = st[ixp + q * dxp], p2 = st[iym + q * dym],
+                       p3 = st[iyp + q * dyp], p4 = st[q == 0 ? izm0 : rb + q * DT - S::FH],
+                       p5 = st[q == S::PER - 1 ? izpL : rb + q * DT + S::FH];
+          if (r < 0) {  // uniform row (:667-672)
+            double sv = -h2 * g;
+            sv += p0;
+            sv += p1;
+            sv += p2;
+            sv += p3;
+            sv += p4;
+            sv += p5;
+            dst[q * S::THR] = -sv * (-1.0 / 6.0);
+          }  // special rows: cut rows by k_gs_cut, inside rows keep their pin
         }
       }
     }
@@ -634,6 +641,36 @@ static __global__ void __launch_bounds__(256) k_pin_list(double* __restrict__ ph
                                                  const int2* __restrict__ list, int n) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q < n) phi[list[q].x] = phi_b[list[q].y];
+}
+
+// Cut rows of the lean interface blocks after the streaming sweep
+// (multigrid.hpp:674-684), from a host-built table: per row the cell address,
+// the row index and the six neighbour addresses (-1: Neumann ghost f1,
+// -2: Dirichlet ghost 2 bc - f1 with bc in gbc), so a thread needs two
+// dependent round trips.  One thread per cut row of the active colour.
+template <int D>
+__global__ void __launch_bounds__(128) k_gs_cut(LevelView L, const double* __restrict__ phi_b,
+                                               const int32_t* __restrict__ ent, const double* __restrict__ gbc,
+                                               int n) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const int4 e0 = reinterpret_cast<const int4*>(ent)[2 * q];
+  const int4 e1 = reinterpret_cast<const int4*>(ent)[2 * q + 1];
+  const int a = e0.x, r = e0.y;
+  const int na[6] = {e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
+  const double self = L.phi[a];
+  double num = L.rhs[a];
+  double p[2 * D];
+#pragma unroll
+  for (int d = 0; d < 2 * D; ++d)
+    p[d] = na[d] >= 0 ? L.phi[na[d]] : (na[d] == -1 ? self : 2.0 * gbc[(size_t)q * 6 + d] - self);
+#pragma unroll
+  for (int d = 0; d < 2 * D; ++d) {
+    num -= L.r_nb[r * 2 * D + d] * p[d];
+    const double b = L.r_bc[r * 2 * D + d];
+    if (b != 0) num -= b * phi_b[L.r_obj[r * 2 * D + d]];
+  }
+  L.phi[a] = num / L.r_center[r];
 }
 
 }  // namespace pmgdev
