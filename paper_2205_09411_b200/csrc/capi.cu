@@ -332,6 +332,35 @@ static void upload_stencils(Ctx& c) {
       d.rfix_list.upload(fx, c.stream);
     }
   }
+  // streaming prolongation plans (3D): fine blocks that are not entirely
+  // inside; eligible when no parent octant face is a coarse-fine face
+  if (c.dim == 3) {
+    for (int l = 2; l <= m.L; ++l) {
+      LevelDev& d = *c.lev[(size_t)l];
+      std::vector<int32_t> pp;
+      bool ok = true;
+      for (int s = 0; s < d.nb && ok; ++s) {
+        if (kindv[(size_t)l][(size_t)s] == pmgdev::KIND_ALL_INSIDE) continue;
+        const int id = m.slots[(size_t)l][(size_t)s];
+        const int pid = m.parent[(size_t)id];
+        int oct = 0, pn[3];
+        for (int ax = 0; ax < 3; ++ax) {
+          const int cb = m.coords[(size_t)id * 3 + ax] & 1;
+          oct |= cb << ax;
+          const int dir = 2 * ax + cb;
+          const int nid = m.nbr[(size_t)pid * 6 + dir];
+          if (nid >= 0) pn[ax] = m.slot_of[(size_t)nid];
+          else if (m.cnbr[(size_t)pid * 6 + dir] >= 0) ok = false;
+          else pn[ax] = -1;
+        }
+        const int32_t e[8] = {s, m.slot_of[(size_t)pid], oct, pn[0], pn[1], pn[2], kindv[(size_t)l][(size_t)s], 0};
+        pp.insert(pp.end(), e, e + 8);
+      }
+      d.n_pp = ok ? (int)pp.size() / 8 : -1;
+      if (!ok) pp.clear();
+      d.pp_plan.upload(pp, c.stream);
+    }
+  }
   // pin lists (every level): colour-split address and object of each inside row
   for (int l = 1; l <= m.L; ++l) {
     LevelDev& d = *c.lev[(size_t)l];
@@ -845,7 +874,7 @@ static void set_mesh(Ctx& c, int nb, const int32_t* level, const int32_t* coords
   }
   int maxnb = 0;
   for (int l = 1; l <= m.L; ++l) maxnb = std::max(maxnb, c.lev[(size_t)l]->nb);
-  c.partial.alloc((size_t)maxnb);
+  c.partial.alloc((size_t)maxnb + 8192);  // + per-CTA partials of k_record_cut
   c.rec.alloc(pmgdev::kMaxLevels + 1);
   c.counter.alloc(1);
   PMG_CUDA(cudaMemsetAsync(c.counter.p, 0, sizeof(unsigned), c.stream));

@@ -104,6 +104,8 @@ struct LevelDev {
   int n_rfix = 0;
   DevBuf<int32_t> pin_list;   // (cell address, object) of this level's inside rows
   int n_pin = 0;
+  DevBuf<int32_t> pp_plan;    // streaming prolongation plan (stream.cuh), -1: level not eligible
+  int n_pp = -1;
   // k_gs_cut tables per colour: 8 int32 (cell, row, 6 neighbour addresses) + 6 ghost bc values
   DevBuf<int32_t> cut_ent[2];
   DevBuf<double> cut_gbc[2];

@@ -52,7 +52,8 @@ struct OpsImpl final : Ops {
       // branch: all kernels write disjoint cells of colour `parity` and read
       // only the other colour (plus, in k_gs_fix, the cut cell's own value).
       bool stream = false;
-      if constexpr (D == 3 && (N == 8 || N == 16)) stream = d.n_gs > 0 && !(L.exp & 256);
+      if constexpr (D == 3 && (N == 8 || N == 16))
+        stream = d.n_gs > ((L.exp & 262144) ? 1024 : 0) && !(L.exp & 256);
       const int nfix = stream ? 0 : d.n_fix[parity];
       const bool lean_work = stream || d.n_fast > 0;
       const int ncut = stream ? d.n_cut[parity] : 0;
@@ -173,7 +174,7 @@ struct OpsImpl final : Ops {
     const LevelView& L = V(c, lc);
     const unsigned g = grid_for((long long)L.nb * G::NI);
     if constexpr (TILE) {
-      if (!(L.nb <= kSmallLevel && !(L.exp & 32768))) {
+      if (!(L.nb <= ((L.exp & 65536) ? 4096 : kSmallLevel) && !(L.exp & 32768))) {
         if (f)
           k_fas_tile<D, N, true><<<L.nb, TT::THREADS, 0, c.stream>>>(L, Vc(c, lc), c.phi_b.p);
         else
@@ -193,11 +194,40 @@ struct OpsImpl final : Ops {
     k_cfold<D, N><<<grid_for((long long)L.nb * G::F * G::NT), kThreads, 0, c.stream>>>(L, Vc(c, lc));
     check();
   }
+  template <bool FULL>
+  void launch_prolong_stream(Ctx& c, int l) {
+    if constexpr (D == 3 && N == 16) {
+      const LevelDev& d = *c.lev[(size_t)l];
+      constexpr int ST = 2, MINB = 2;
+      constexpr size_t smem = (size_t)ST * PStream3<N>::STAGE * sizeof(double);
+      static bool attr = false;
+      if (!attr) {
+        PMG_CUDA(cudaFuncSetAttribute(k_prolong_stream<N, ST, MINB, FULL>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+      }
+      const int grid = std::min(d.n_pp, c.sms * MINB);
+      k_prolong_stream<N, ST, MINB, FULL><<<grid, PStream3<N>::THR, smem, c.stream>>>(
+          V(c, l), V(c, l - 1), (const int4*)d.pp_plan.p, d.n_pp);
+      if (d.n_pin > 0)  // inside cells were interpolated too: restore their pins
+        k_pin_list<<<grid_for(d.n_pin, 256), 256, 0, c.stream>>>(V(c, l).phi, c.phi_b.p,
+                                                                  (const int2*)d.pin_list.p, d.n_pin);
+    }
+  }
   void prolong(Ctx& c, int l, bool full) override {
     const LevelView& Lf = V(c, l);
     const LevelView& Lp = V(c, l - 1);
     const LevelView& Lpp = Vc(c, l - 1);
     const unsigned g = grid_for((long long)Lf.nb * G::NI);
+    if constexpr (D == 3 && N == 16) {
+      const LevelDev& d = *c.lev[(size_t)l];
+      if (Lf.nb > kSmallLevel && d.n_pp > 0 && !(Lf.exp & 131072)) {
+        if (full) launch_prolong_stream<true>(c, l);
+        else launch_prolong_stream<false>(c, l);
+        check();
+        return;
+      }
+    }
     if constexpr (TILE) {
       if (!(Lf.nb <= kSmallLevel && !(Lf.exp & 32768))) {
         if (full)
@@ -218,6 +248,46 @@ struct OpsImpl final : Ops {
     const LevelView& L = V(c, l);
     // a level without leaves records zeros, which enq_reset_records left there
     if (c.lev[(size_t)l]->n_leaf == 0) return;
+    if constexpr (D == 3 && N == 16) {
+      const LevelDev& d = *c.lev[(size_t)l];
+      if (d.n_rs > 0 && L.nb > kSmallLevel && !(L.exp & 16384)) {
+        // streaming record of every block without coarse-fine faces (special
+        // rows excluded), the cut rows from their table and the remaining
+        // blocks by k_record_tile, each into its own partials; folded in order
+        const int ncut = d.n_cut[0] + d.n_cut[1];
+        const int gcut = ncut > 0 ? (int)grid_for(ncut, 256) : 0;
+        const bool fork = d.n_slow > 0 || ncut > 0;
+        if (fork) {
+          PMG_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+          PMG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+        }
+        if (d.n_slow > 0)
+          k_record_tile<D, N><<<d.n_slow, TT::THREADS, 0, c.side>>>(L, Vc(c, l), c.phi_b.p, c.partial.p, c.rec.p,
+                                                                   nullptr, d.slow_list.p);
+        if (ncut > 0)
+          k_record_cut<D><<<gcut, 256, 0, c.side>>>(L, c.phi_b.p, d.cut_ent[0].p, d.cut_gbc[0].p, d.n_cut[0],
+                                                     d.cut_ent[1].p, d.cut_gbc[1].p, d.n_cut[1], G::NI,
+                                                     c.partial.p + L.nb);
+        constexpr int ST = 2, MINB = 1;
+        constexpr size_t smem = (size_t)ST * RStream3<N>::STAGE * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+          PMG_CUDA(cudaFuncSetAttribute(k_restrict_stream<N, ST, MINB, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          attr = true;
+        }
+        const int grid = std::min(d.n_rs, c.sms * MINB);
+        k_restrict_stream<N, ST, MINB, true><<<grid, RStream3<N>::THR, smem, c.stream>>>(
+            L, L, c.phi_b.p, (const int4*)d.rs_plan.p, d.n_rs, c.partial.p, c.rec.p, nullptr);
+        if (fork) {
+          PMG_CUDA(cudaEventRecord(c.ev_join, c.side));
+          PMG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
+        }
+        k_record_fold<<<1, 256, 0, c.stream>>>(c.partial.p, L.nb + gcut, c.rec.p + L.level);
+        check();
+        return;
+      }
+    }
     if constexpr (TILE) {
       const LevelDev& d = *c.lev[(size_t)l];
       const bool fork = d.n_ufast > 0 && d.n_uslow > 0;
@@ -228,24 +298,7 @@ struct OpsImpl final : Ops {
       if (d.n_uslow > 0)
         k_record_tile<D, N><<<d.n_uslow, TT::THREADS, 0, fork ? c.side : c.stream>>>(
             L, Vc(c, l), c.phi_b.p, c.partial.p, c.rec.p, c.counter.p, d.uslow_list.p);
-      bool streamed = false;
-      if constexpr (D == 3 && N == 16) {
-        if (d.n_ur > 0 && !(L.exp & 16384)) {
-          constexpr int ST = 2, MINB = 1;
-          constexpr size_t smem = (size_t)ST * RStream3<N>::STAGE * sizeof(double);
-          static bool attr = false;
-          if (!attr) {
-            PMG_CUDA(cudaFuncSetAttribute(k_restrict_stream<N, ST, MINB, true>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = true;
-          }
-          const int grid = std::min(d.n_ur, c.sms * MINB);
-          k_restrict_stream<N, ST, MINB, true><<<grid, RStream3<N>::THR, smem, c.stream>>>(
-              L, L, c.phi_b.p, (const int4*)d.ur_plan.p, d.n_ur, c.partial.p, c.rec.p, c.counter.p);
-          streamed = true;
-        }
-      }
-      if (d.n_ufast > 0 && !streamed)
+      if (d.n_ufast > 0)
         k_record_lean<D, N><<<d.n_ufast, TT::THREADS, 0, c.stream>>>(L, c.partial.p, c.rec.p,
                                                                      c.counter.p, d.ufast_list.p);
       if (fork) {

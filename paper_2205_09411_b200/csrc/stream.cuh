@@ -494,7 +494,17 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
     if (it + S_STAGES + 1 < nmine) pf2 = load_plan(plan, blockIdx.x + (it + S_STAGES + 1) * G);
     const int slot = meta[s][0], flags = meta[s][1];
     const int kind = flags & 0xff, pmask = (flags >> 8) & 63;
-    // parent slot / octant (or leaf flag): loads in flight across the wait
+    // RECORD: rows of the 8 children of an interface block, leaf flag;
+    // otherwise parent slot / octant -- loads in flight across the wait
+    int rr[8];
+    if (RECORD && kind == KIND_IFACE) {
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        const int dx = ch & 1, dy = (ch >> 1) & 1, dz = ch >> 2;
+        const int e = ii + HN * ((2 * jj + dy) + N * (2 * kk + dz));
+        rr[ch] = Lf.row_of[(size_t)(flags >> 14) * NI + (size_t)((dx + dy + dz) & 1) * S::H + e];
+      }
+    }
     const int Pp = RECORD ? 0 : Lf.parent[slot];
     const int cx = RECORD ? 0 : Lf.coords[slot * 3] & 1, cy = RECORD ? 0 : Lf.coords[slot * 3 + 1] & 1,
               cz = RECORD ? 0 : Lf.coords[slot * 3 + 2] & 1;
@@ -549,13 +559,21 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
       res[ch] = kind == KIND_ALL_INSIDE ? 0.0 : g[ch] - sres * w;
     }
     if (RECORD) {
-      if (leaf) {
+      if (leaf && kind == KIND_UNIFORM) {
 #pragma unroll
         for (int ch = 0; ch < 8; ++ch) {
           rmx = fmax(rmx, fabs(res[ch]));
           rss += res[ch] * res[ch];
         }
         rcnt += 8.0;
+      } else if (leaf && kind == KIND_IFACE) {  // special rows: inside excluded, cut rows by k_record_cut
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          if (rr[ch] >= 0) continue;
+          rmx = fmax(rmx, fabs(res[ch]));
+          rss += res[ch] * res[ch];
+          rcnt += 1.0;
+        }
       }
     } else {
     // sum of the children in x-fastest order (multigrid.hpp:706-721)
@@ -671,6 +689,221 @@ __global__ void __launch_bounds__(128) k_gs_cut(LevelView L, const double* __res
     if (b != 0) num -= b * phi_b[L.r_obj[r * 2 * D + d]];
   }
   L.phi[a] = num / L.r_center[r];
+}
+
+// ------------------------------------------------------------------ prolongation
+// prolong_correction / prolong_full (multigrid.hpp:422-438, 724-783) for 3D
+// fine blocks whose parent octant neighbourhood has no coarse-fine face.  A
+// stage holds the fine block's phi (bulk copy; not needed for FULL) and the
+// parent's phi and old on the octant plus its face-adjacent one-cell halo in
+// natural 10^3 order (cp.async); a prep pass turns them into the delta tile
+// (physical-face ghosts 2 bc - f1 evaluated for phi and old separately, as the
+// reference's filled ghosts are).  Inside cells are interpolated too and
+// re-pinned by k_pin_list afterwards (they always hold their pin).
+template <int N>
+struct PStream3 {
+  static constexpr int HN = N / 2;
+  static constexpr int H = N * N * N / 2;
+  static constexpr int PE = HN + 2, PS = PE * PE * PE;
+  static constexpr int THR = H < 512 ? H : 512;
+  static constexpr int PER = H / THR;
+  static constexpr int OF = 0, ORP = 2 * H, ORO = ORP + PS;
+  static constexpr int STAGE = ORO + PS;
+};
+
+// plan entry: {fine slot, parent slot, octant bits, parent neighbour across the
+// octant's outer face per axis (-1 physical), kind, 0}
+template <int N, bool FULL>
+__device__ __forceinline__ void pr_issue_async(const LevelView& Lp, const int4& a, const int4& b, double* st) {
+  using S = PStream3<N>;
+  constexpr int NI = N * N * N, HN = S::HN, PE = S::PE;
+  const int P = a.y, oct = a.z;
+  const int pn[3] = {a.w, b.x, b.y};
+  for (int q = threadIdx.x; q < S::PS; q += S::THR) {
+    const int t3[3] = {q % PE - 1, (q / PE) % PE - 1, q / (PE * PE) - 1};
+    int out = 0, ax = -1;
+    int c3[3];
+    for (int d = 0; d < 3; ++d) {
+      c3[d] = ((oct >> d) & 1) * HN + t3[d];
+      if (t3[d] < 0 || t3[d] >= HN) ++out;
+      if (c3[d] < 0 || c3[d] >= N) ax = d;
+    }
+    if (out > 1) continue;  // edges / corners are never read
+    int blk = P;
+    if (ax >= 0) {
+      if (pn[ax] >= 0) {
+        blk = pn[ax];
+        c3[ax] = c3[ax] < 0 ? N - 1 : 0;
+      } else {  // physical face: the parent's own boundary cell, transformed in the prep pass
+        c3[ax] = c3[ax] < 0 ? 0 : N - 1;
+      }
+    }
+    const size_t ad = (size_t)blk * NI + (size_t)(((c3[0] + c3[1] + c3[2]) & 1) * S::H) +
+                      (size_t)((c3[0] + N * (c3[1] + N * c3[2])) >> 1);
+    cp_async8(st + S::ORP + q, Lp.phi + ad);
+    if (!FULL) cp_async8(st + S::ORO + q, Lp.old + ad);
+  }
+}
+
+template <int N, int S_STAGES, int MINB, bool FULL>
+__global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(LevelView Lf, LevelView Lp,
+                                                                          const int4* __restrict__ plan, int n) {
+  using S = PStream3<N>;
+  constexpr int NI = N * N * N, HN = S::HN, PE = S::PE;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t full[S_STAGES];
+  __shared__ int4 meta[S_STAGES][2];
+  const int t = threadIdx.x;
+  const int G = gridDim.x;
+  const int nmine = (int)blockIdx.x < n ? (n - 1 - (int)blockIdx.x) / G + 1 : 0;
+  if (nmine == 0) return;
+  if (t == 0) {
+    for (int s = 0; s < S_STAGES; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int p, int s) {
+    const int4 a = __ldg(plan + 2 * p), b = __ldg(plan + 2 * p + 1);
+    double* st = sm + s * S::STAGE;
+    if (t == 0) {
+      meta[s][0] = a;
+      meta[s][1] = b;
+      if (FULL) {
+        mbar_arrive_expect_tx(&full[s], 0);
+      } else {
+        mbar_arrive_expect_tx(&full[s], 2 * S::H * 8);
+        bulk_g2s(st + S::OF, Lf.phi + (size_t)a.x * NI, 2 * S::H * 8, &full[s]);
+      }
+    }
+    pr_issue_async<N, FULL>(Lp, a, b, st);
+  };
+  for (int s = 0; s < S_STAGES; ++s) {
+    if (s < nmine) issue(blockIdx.x + s * G, s);
+    cp_async_commit();
+  }
+  for (int it = 0; it < nmine; ++it) {
+    const int s = it % S_STAGES;
+    double* st = sm + s * S::STAGE;
+    mbar_wait(&full[s], (uint32_t)((it / S_STAGES) & 1));
+    cp_async_wait<S_STAGES - 1>();
+    __syncthreads();
+    const int4 a = meta[s][0], b = meta[s][1];
+    const int slot = a.x, P = a.y, oct = a.z;
+    const int pn[3] = {a.w, b.x, b.y};
+    // prep: delta (or phi for FULL) in place of the raw phi tile
+    for (int q = t; q < S::PS; q += S::THR) {
+      const int t3[3] = {q % PE - 1, (q / PE) % PE - 1, q / (PE * PE) - 1};
+      int out = 0, ax = -1;
+      int c3[3];
+      for (int d = 0; d < 3; ++d) {
+        c3[d] = ((oct >> d) & 1) * HN + t3[d];
+        if (t3[d] < 0 || t3[d] >= HN) ++out;
+        if (c3[d] < 0 || c3[d] >= N) ax = d;
+      }
+      if (out > 1) continue;
+      double vp = st[S::ORP + q], vo = FULL ? 0.0 : st[S::ORO + q];
+      if (ax >= 0 && pn[ax] < 0) {  // physical-face ghost of phi and old (mesh.hpp:538-552)
+        const int side = c3[ax] >= N, dir = 2 * ax + side;
+        if (Lp.bctype[dir] != 1) {
+          c3[ax] = side ? N - 1 : 0;
+          const int bo = Lp.bcoff[P * 6 + dir];
+          const int tj = ax == 0 ? c3[1] + N * c3[2] : ax == 1 ? c3[0] + N * c3[2] : c3[0] + N * c3[1];
+          const double bcv = bo < 0 ? 0.0 : Lp.bcval[bo + tj];
+          vp = 2.0 * bcv - vp;
+          vo = 2.0 * bcv - vo;
+        }
+      }
+      st[S::ORP + q] = FULL ? vp : vp - vo;
+    }
+    __syncthreads();
+    const double* Dt = st + S::ORP;
+    double* __restrict__ dst = Lf.phi + (size_t)slot * NI;
+    const int m = t % HN;
+#pragma unroll
+    for (int q = 0; q < S::PER; ++q) {
+      const int e = t + q * S::THR;
+      const int j = (e / HN) % N, k = e / (HN * N);
+      const int ctr = (((k >> 1) + 1) * PE + (j >> 1) + 1) * PE + m + 1;
+      const double dc = Dt[ctr], dxm = Dt[ctr - 1], dxp = Dt[ctr + 1];
+      const double dy = Dt[ctr + ((j & 1) ? PE : -PE)];
+      const double dz = Dt[ctr + ((k & 1) ? PE * PE : -PE * PE)];
+      const int c0 = (j + k) & 1;  // colour of i = 2m (x sign -1); i = 2m+1 has +1
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = h ? 1 - c0 : c0;
+        double v = (1.0 - 0.25 * 3) * dc;  // multigrid.hpp:742-752
+        v += 0.25 * (h ? dxp : dxm);
+        v += 0.25 * dy;
+        v += 0.25 * dz;
+        const size_t ad = (size_t)c * S::H + e;
+        dst[ad] = FULL ? v : st[S::OF + ad] + v;
+      }
+    }
+    __syncthreads();  // stage s consumed
+    if (it + S_STAGES < nmine) issue(blockIdx.x + (it + S_STAGES) * G, s);
+    cp_async_commit();
+  }
+}
+
+// Leaf-residual record of the cut rows (the k_gs_cut tables of both colours):
+// r = g - (center phi + sum nb p + sum bc phi_b) (stencil.hpp:344-358); one
+// partial (max, sum r^2, count) per CTA into `partial`.
+template <int D>
+__global__ void __launch_bounds__(256) k_record_cut(LevelView L, const double* __restrict__ phi_b,
+                                                   const int32_t* __restrict__ ent0, const double* __restrict__ gbc0,
+                                                   int n0, const int32_t* __restrict__ ent1,
+                                                   const double* __restrict__ gbc1, int n1, int ni,
+                                                   Rec* __restrict__ partial) {
+  __shared__ double red[72];
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  double mx = 0.0, ss = 0.0, cnt = 0.0;
+  if (q < n0 + n1) {
+    const int qq = q < n0 ? q : q - n0;
+    const int32_t* ent = q < n0 ? ent0 : ent1;
+    const double* gbc = q < n0 ? gbc0 : gbc1;
+    const int4 e0 = reinterpret_cast<const int4*>(ent)[2 * qq];
+    const int4 e1 = reinterpret_cast<const int4*>(ent)[2 * qq + 1];
+    const int a = e0.x, r = e0.y;
+    if (L.leaf[a / ni]) {
+      const int na[6] = {e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
+      const double self = L.phi[a];
+      double p[2 * D];
+#pragma unroll
+      for (int d = 0; d < 2 * D; ++d)
+        p[d] = na[d] >= 0 ? L.phi[na[d]] : (na[d] == -1 ? self : 2.0 * gbc[(size_t)qq * 6 + d] - self);
+      const double rv = resid_value<D>(L, phi_b, r, self, p, L.rhs[a]);
+      mx = fabs(rv);
+      ss = rv * rv;
+      cnt = 1.0;
+    }
+  }
+  mx = block_max(mx, red);
+  ss = block_sum(ss, red);
+  cnt = block_sum(cnt, red);
+  if (threadIdx.x == 0) {
+    partial[blockIdx.x].max = mx;
+    partial[blockIdx.x].sumsq = ss;
+    partial[blockIdx.x].count = (long long)cnt;
+  }
+}
+
+// rec = fold of partial[0 .. n) in index order (combine_records' per-level record)
+static __global__ void __launch_bounds__(256) k_record_fold(const Rec* __restrict__ partial, int n, Rec* out) {
+  __shared__ double red[72];
+  double mx = 0.0, ss = 0.0, cc = 0.0;
+  for (int b = threadIdx.x; b < n; b += blockDim.x) {
+    mx = fmax(mx, partial[b].max);
+    ss += partial[b].sumsq;
+    cc += (double)partial[b].count;
+  }
+  mx = block_max(mx, red);
+  ss = block_sum(ss, red);
+  cc = block_sum(cc, red);
+  if (threadIdx.x == 0) {
+    out->max = mx;
+    out->sumsq = ss;
+    out->count = (long long)cc;
+  }
 }
 
 }  // namespace pmgdev

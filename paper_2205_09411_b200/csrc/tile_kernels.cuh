@@ -685,8 +685,12 @@ __device__ __forceinline__ void record_finish(const LevelView& L, Rec* __restric
     partial[slot].max = mx;
     partial[slot].sumsq = ss;
     partial[slot].count = (long long)cnt;
-    __threadfence();
-    *last = atomicAdd(counter, arrivals) + arrivals == (unsigned)L.nb;
+    if (counter) {
+      __threadfence();
+      *last = atomicAdd(counter, arrivals) + arrivals == (unsigned)L.nb;
+    } else {
+      *last = false;  // folded by k_record_fold
+    }
   }
   __syncthreads();
   if (!*last) return;
