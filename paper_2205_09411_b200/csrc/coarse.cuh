@@ -36,9 +36,12 @@ struct CoarseFast {
   int max_iters;
   int fallback_ok;
   int n_unknowns;
+  const int2* pins;  // level-1 pin list (cell address, object)
+  int n_pins;
 };
 
-constexpr int kCoarseThreads = 1024;
+constexpr int kCoarseThreads = 512;  // 16 warps, CPT = 8 cells per thread in 3D N=16
+constexpr int kCoarseWarps = kCoarseThreads / 32;
 
 // deterministic CTA reduction of one / two values; `buf` must not be in use
 // by another reduction that some thread may still be reading.
@@ -47,7 +50,7 @@ __device__ __forceinline__ double cta_sum1(double v, double* buf) {
   v = warp_sum(v);
   if (lane == 0) buf[wid] = v;
   __syncthreads();
-  return warp_sum(buf[lane]);  // kCoarseThreads / 32 == 32 partials
+  return warp_sum(lane < kCoarseWarps ? buf[lane] : 0.0);
 }
 __device__ __forceinline__ void cta_sum2(double& a, double& b, double* buf) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -58,8 +61,8 @@ __device__ __forceinline__ void cta_sum2(double& a, double& b, double* buf) {
     buf[32 + wid] = b;
   }
   __syncthreads();
-  a = warp_sum(buf[lane]);
-  b = warp_sum(buf[32 + lane]);
+  a = warp_sum(lane < kCoarseWarps ? buf[lane] : 0.0);
+  b = warp_sum(lane < kCoarseWarps ? buf[32 + lane] : 0.0);
 }
 
 template <int D, int N>

@@ -1,9 +1,9 @@
 // coarse_cluster.cuh -- K6 on a thread-block cluster (3D levels with N <= 16).
 //
 // Same algorithm and row arithmetic as coarse.cuh (a replica of
-// detail::bicgstab, multigrid.hpp:208-280), distributed over a cluster of N
-// CTAs: CTA z owns plane z of the root block, one cell per thread, every
-// per-cell vector lives in registers.  The vectors the SpMV gathers (x, p^,
+// detail::bicgstab, multigrid.hpp:208-280), distributed over a cluster of
+// N/PPC CTAs: CTA r owns planes r*PPC .. r*PPC+PPC-1 of the root block, one
+// cell per thread, every per-cell vector lives in registers.  The vectors the SpMV gathers (x, p^,
 // s^) are kept as zero-padded planes in each CTA's shared memory; the z-1 and
 // z+1 values are read from the neighbouring CTAs through distributed shared
 // memory.  Each dot product is reduced inside the CTA, its partial broadcast
@@ -20,11 +20,12 @@ namespace pmgdev {
 
 namespace cg = cooperative_groups;
 
-template <int N>
+template <int N, int PPC = 1>
 struct CC {
   static constexpr int P = N + 2;           // padded plane extent
   static constexpr int PP = P * P;
-  static constexpr int THR = N * N;         // one thread per cell of the plane
+  static constexpr int NC = N / PPC;        // CTAs in the cluster (PPC planes each)
+  static constexpr int THR = PPC * N * N;   // one thread per cell of the CTA's planes
   static constexpr int NW = (THR + 31) / 32;
   static constexpr int NSTAGE = 6;          // reduction stages per iteration (+ setup)
 };
@@ -33,13 +34,13 @@ template <int N>
 __device__ __forceinline__ double cc_row(const CoarseFast& C, const double* __restrict__ G,
                                          const double* __restrict__ Gm,
                                          const double* __restrict__ Gp, uint8_t f, double dg,
-                                         int pi, int ii) {
+                                         int pi, const double* sc) {
   // sorted column order: z-, y-, x-, diag, x+, y+, z+ (coarse.cuh); absent
-  // terms are exact zeros (0*x with x finite) and change nothing
+  // terms are exact zeros (0*x with x finite) and change nothing.  `sc`: the
+  // special row's six off-diagonals, held in registers by the caller.
   constexpr int P = N + 2;
   double s = 0;
   if (f & 0x80) {
-    const double* sc = C.spec_c + (size_t)C.spec[ii] * 6;
     s += sc[4] * Gm[pi];
     s += sc[2] * G[pi - P];
     s += sc[0] * G[pi - 1];
@@ -60,33 +61,40 @@ __device__ __forceinline__ double cc_row(const CoarseFast& C, const double* __re
   return s;
 }
 
-template <int N>
-__global__ void __launch_bounds__(CC<N>::THR) k_coarse_cluster(LevelView L, CoarseFast C,
-                                                               const double* __restrict__ phi_b,
-                                                               Rec* rec, int* status,
-                                                               double* diag_out) {
+template <int N, int PPC>
+__global__ void __launch_bounds__(CC<N, PPC>::THR) k_coarse_cluster(LevelView L, CoarseFast C,
+                                                                    const double* __restrict__ phi_b,
+                                                                    Rec* rec, int* status,
+                                                                    double* diag_out) {
   using G = Geo<3, N>;
-  using K = CC<N>;
+  using K = CC<N, PPC>;
   cg::cluster_group cl = cg::this_cluster();
-  __shared__ double Gx[K::PP];                  // own plane of the gathered vector
-  __shared__ double part[K::NSTAGE][N][2];      // partials of every CTA, per stage
+  __shared__ double Gx[PPC][K::PP];             // own planes of the gathered vector
+  __shared__ double part[K::NSTAGE][K::NC][2];  // partials of every CTA, per stage
   __shared__ double wred[K::NW][2];
-  const int z = (int)cl.block_rank();
+  const int zr = (int)cl.block_rank();
   const int t = threadIdx.x;
   const int lane = t & 31, wid = t >> 5;
-  const int x = t % N, y = t / N;
+  const int x = t % N, y = (t / N) % N, lp = t / (N * N);
+  const int z = zr * PPC + lp;  // plane of this thread's cell
   const int ii = x + N * (y + N * z);
   const int pi = (x + 1) + (y + 1) * K::P;
-  // neighbour planes (z-1, z+1); out-of-block planes alias our own (coefficient 0)
-  const double* Gm = z > 0 ? cl.map_shared_rank(Gx, z - 1) : Gx;
-  const double* Gp = z < N - 1 ? cl.map_shared_rank(Gx, z + 1) : Gx;
-  for (int q = t; q < K::PP; q += K::THR) Gx[q] = 0.0;
+  // own plane and its z-1 / z+1 neighbours (in this CTA or, across the CTA's
+  // edge planes, in the neighbouring CTA); out-of-block planes alias our own
+  // (coefficient 0)
+  double* Gs = Gx[lp];
+  const double* Gm = lp > 0 ? Gx[lp - 1] : (zr > 0 ? cl.map_shared_rank(Gx[PPC - 1], zr - 1) : Gs);
+  const double* Gp = lp < PPC - 1 ? Gx[lp + 1] : (zr < K::NC - 1 ? cl.map_shared_rank(Gx[0], zr + 1) : Gs);
+  for (int q = t; q < PPC * K::PP; q += K::THR) (&Gx[0][0])[q] = 0.0;
   __syncthreads();
   // ---- per-cell data (multigrid.hpp:213-217, 445-453)
   const uint8_t f = C.flags[ii];
   const double dg = C.diag[ii];
   const double dinv = (dg != 0) ? 1.0 / dg : 1.0;
   const bool unk = (f & 0x40) != 0;
+  double sc[6] = {0, 0, 0, 0, 0, 0};  // special-row off-diagonals, loaded once
+  if (f & 0x80)
+    for (int d = 0; d < 6; ++d) sc[d] = C.spec_c[(size_t)C.spec[ii] * 6 + d];
   const size_t a = G::addr(0, x, y, z);
   double xv = unk ? L.phi[a] : 0.0;
   double bv = 0;
@@ -103,31 +111,29 @@ __global__ void __launch_bounds__(CC<N>::THR) k_coarse_cluster(LevelView L, Coar
       wred[wid][1] = vb;
     }
     __syncthreads();
-    if (t == 0) {
+    if (t < K::NC) {  // thread r broadcasts this CTA's partial to rank r
       double sa = 0, sb = 0;
       for (int w = 0; w < K::NW; ++w) {
         sa += wred[w][0];
         sb += wred[w][1];
       }
-      for (int r = 0; r < (int)cl.num_blocks(); ++r) {
-        double* dst = cl.map_shared_rank(&part[stage][z][0], r);
-        dst[0] = sa;
-        dst[1] = sb;
-      }
+      double* dst = cl.map_shared_rank(&part[stage][zr][0], t);
+      dst[0] = sa;
+      dst[1] = sb;
     }
     cl.sync();
     double sa = 0, sb = 0;
-    for (int r = 0; r < N; ++r) {
+    for (int r = 0; r < K::NC; ++r) {
       sa += part[stage][r][0];
       sb += part[stage][r][1];
     }
     va = sa;
     vb = sb;
   };
-  Gx[pi] = xv;
+  Gs[pi] = xv;
   cl.sync();  // every plane of x published
   double r = 0;
-  if (unk) r = bv - cc_row<N>(C, Gx, Gm, Gp, f, dg, pi, ii);
+  if (unk) r = bv - cc_row<N>(C, Gs, Gm, Gp, f, dg, pi, sc);
   const double r0 = r;
   double n2 = unk ? r * r : 0.0, rho1 = unk ? r0 * r : 0.0;
   csum(0, n2, rho1);
@@ -147,17 +153,17 @@ __global__ void __launch_bounds__(CC<N>::THR) k_coarse_cluster(LevelView L, Coar
       const double beta = it == 0 ? 0.0 : (rho1 / rho) * (alpha / omega);
       if (unk) p = it == 0 ? r : r + beta * (p - omega * v);
       const double ph = unk ? dinv * p : 0.0;
-      Gx[pi] = ph;
+      Gs[pi] = ph;
       cl.sync();  // B1: p^ planes visible
-      v = unk ? cc_row<N>(C, Gx, Gm, Gp, f, dg, pi, ii) : 0.0;
+      v = unk ? cc_row<N>(C, Gs, Gm, Gp, f, dg, pi, sc) : 0.0;
       double r0v = unk ? r0 * v : 0.0, dummy = 0;
       csum(1, r0v, dummy);  // B2
       if (r0v == 0) break;
       alpha = rho1 / r0v;
       s = unk ? r - alpha * v : 0.0;
       double ss = s * s;
-      Gx[pi] = unk ? dinv * s : 0.0;  // s^ (neighbours finished reading p^ before B2)
-      const double sh = Gx[pi];
+      Gs[pi] = unk ? dinv * s : 0.0;  // s^ (neighbours finished reading p^ before B2)
+      const double sh = Gs[pi];
       csum(2, ss, dummy);  // B3: also publishes s^
       const double ns = sqrt(ss);
       if (ns <= target) {
@@ -167,7 +173,7 @@ __global__ void __launch_bounds__(CC<N>::THR) k_coarse_cluster(LevelView L, Coar
         rel = ns / norm0;
         break;
       }
-      tv = unk ? cc_row<N>(C, Gx, Gm, Gp, f, dg, pi, ii) : 0.0;
+      tv = unk ? cc_row<N>(C, Gs, Gm, Gp, f, dg, pi, sc) : 0.0;
       double ts = tv * s, tt = tv * tv;
       csum(3, ts, tt);  // B4
       if (tt == 0) break;
@@ -191,8 +197,11 @@ __global__ void __launch_bounds__(CC<N>::THR) k_coarse_cluster(LevelView L, Coar
   }
   const bool wb = converged || C.fallback_ok;
   if (unk && wb) L.phi[a] = xv;
+  // apply_pins(1) (multigrid.hpp:469): inside cells are not unknowns, so the
+  // write-back never touched them; re-pinning is spread over the cluster
+  for (int q = zr * K::THR + t; q < C.n_pins; q += K::NC * K::THR) L.phi[C.pins[q].x] = phi_b[C.pins[q].y];
   cl.sync();  // write-back complete in every plane before the tail
-  if (z != 0) return;
+  if (zr != 0) return;
   // ---- tail on rank 0 (whole root block): fallback, pins, level-1 record
   __shared__ double sm[72];
   if (t == 0) {
@@ -224,14 +233,13 @@ __global__ void __launch_bounds__(CC<N>::THR) k_coarse_cluster(LevelView L, Coar
     if (!ok && t == 0) status[0] = 4;
     __syncthreads();
   }
-  if (L.srow[0] >= 0)
-    for (int ce = t; ce < G::NI; ce += blockDim.x) {
-      const int rr = L.row_of[(size_t)L.srow[0] * G::NI + ce];
-      if (rr >= 0 && L.r_mask[rr] == 1) L.phi[ce] = phi_b[L.r_pin[rr]];
-    }
-  __syncthreads();
+  if (!converged && C.fallback_ok && L.srow[0] >= 0) {  // the fallback sweeps skip inside cells; re-pin anyway
+    for (int q = t; q < C.n_pins; q += blockDim.x) L.phi[C.pins[q].x] = phi_b[C.pins[q].y];
+    __syncthreads();
+  }
+  if (!L.leaf[0]) return;  // level 1 has no leaves: its record stays zero
   double mx = 0, ss = 0, cnt = 0;
-  if (L.leaf[0]) {
+  {
     for (int ce = t; ce < G::NI; ce += blockDim.x) {
       bool ins;
       const double rr = resid_cell<3, N>(L, L, phi_b, 0, ce / G::H, ce % G::H, &ins);

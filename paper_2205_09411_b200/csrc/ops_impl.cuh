@@ -39,6 +39,8 @@ struct OpsImpl final : Ops {
 
   void gs(Ctx& c, int l, int parity) override {
     const LevelView& L = V(c, l);
+    if ((L.exp & (1 << 19)) && L.nb <= kSmallLevel) return;          // timing experiment only
+    if ((L.exp & (1 << 20)) && l < (int)c.mesh.L) return;            // timing experiment only
     if (L.nb <= kSmallLevel && !(L.exp & 32768)) {
       k_gs<D, N><<<grid_for((long long)L.nb * G::H), kThreads, 0, c.stream>>>(L, Vc(c, l), c.phi_b.p, parity);
       check();
@@ -317,7 +319,34 @@ struct OpsImpl final : Ops {
     k_pins<D, N><<<grid_for((long long)L.nb * G::NI), kThreads, 0, c.stream>>>(L, c.phi_b.p);
     check();
   }
+  template <int PPC>
+  void launch_coarse_cluster(Ctx& c, const CoarseFast& F) {
+    if constexpr (D == 3 && (N == 8 || N == 16)) {
+      using K = CC<N, PPC>;
+      static bool cattr = false;
+      if (!cattr) {
+        if (K::NC > 8)
+          PMG_CUDA(cudaFuncSetAttribute(k_coarse_cluster<N, PPC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cattr = true;
+      }
+      cudaLaunchConfig_t cfgl = {};
+      cfgl.gridDim = dim3(K::NC, 1, 1);
+      cfgl.blockDim = dim3(K::THR, 1, 1);
+      cfgl.dynamicSmemBytes = 0;
+      cfgl.stream = c.stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = K::NC;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfgl.attrs = at;
+      cfgl.numAttrs = 1;
+      PMG_CUDA(cudaLaunchKernelEx(&cfgl, k_coarse_cluster<N, PPC>, V(c, 1), F, (const double*)c.phi_b.p, c.rec.p,
+                                  c.status.p, c.diag.p));
+    }
+  }
   void coarse(Ctx& c) override {
+    if (V(c, 1).exp & (1 << 21)) return;  // timing experiment only
     if constexpr (FASTC) {
       CoarseFast F{};
       F.flags = c.cf_flags.p;
@@ -335,29 +364,14 @@ struct OpsImpl final : Ops {
       for (int k = 0; k < D; ++k) lim *= 8;
       F.fallback_ok = c.coarse.n <= lim + 1;
       F.n_unknowns = c.coarse.n;
+      F.pins = (const int2*)c.lev[1]->pin_list.p;
+      F.n_pins = c.lev[1]->n_pin;
       if constexpr (D == 3 && (N == 8 || N == 16)) {
         if (!(V(c, 1).exp & 32)) {
-          // one CTA per z-plane of the root block, as one thread-block cluster
-          static bool cattr = false;
-          if (!cattr) {
-            PMG_CUDA(cudaFuncSetAttribute(k_coarse_cluster<N>,
-                                          cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            cattr = true;
-          }
-          cudaLaunchConfig_t cfgl = {};
-          cfgl.gridDim = dim3(N, 1, 1);
-          cfgl.blockDim = dim3(CC<N>::THR, 1, 1);
-          cfgl.dynamicSmemBytes = 0;
-          cfgl.stream = c.stream;
-          cudaLaunchAttribute at[1];
-          at[0].id = cudaLaunchAttributeClusterDimension;
-          at[0].val.clusterDim.x = N;
-          at[0].val.clusterDim.y = 1;
-          at[0].val.clusterDim.z = 1;
-          cfgl.attrs = at;
-          cfgl.numAttrs = 1;
-          PMG_CUDA(cudaLaunchKernelEx(&cfgl, k_coarse_cluster<N>, V(c, 1), F, (const double*)c.phi_b.p,
-                                      c.rec.p, c.status.p, c.diag.p));
+          // planes of the root block spread over a thread-block cluster
+          if (V(c, 1).exp & (1 << 22)) launch_coarse_cluster<1>(c, F);
+          else if (V(c, 1).exp & (1 << 23)) launch_coarse_cluster<4>(c, F);
+          else launch_coarse_cluster<2>(c, F);
           check();
           return;
         }
