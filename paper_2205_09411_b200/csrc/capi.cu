@@ -624,7 +624,7 @@ static void enq_reset_records(Ctx& c) {
   PMG_CUDA(cudaMemsetAsync(c.rec.p, 0, c.rec.n * sizeof(pmgdev::Rec), c.stream));
 }
 static void enq_finish(Ctx& c) {
-  pmgdev::k_combine<<<1, 32, 0, c.stream>>>(c.rec.p, c.mesh.L, c.stats.p);
+  pdl_launch(pmgdev::k_combine, 1, 32, 0, c.stream, c.rec.p, c.mesh.L, c.stats.p);
   PMG_CUDA(cudaGetLastError());
   PMG_CUDA(cudaMemcpyAsync(c.h_out, c.stats.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
   PMG_CUDA(cudaMemcpyAsync(c.h_out + 2, c.diag.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c.stream));

@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(kCoarseThreads, 1) k_coarse_fast(LevelView L, 
                                                                    const double* __restrict__ phi_b,
                                                                    Rec* rec, int* status,
                                                                    double* diag_out) {
+  pdl_begin();
   using G = Geo<D, N>;
   using CG = CoarseGeo<D, N>;
   constexpr int NI = G::NI;

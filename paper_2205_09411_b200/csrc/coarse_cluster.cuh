@@ -66,6 +66,7 @@ __global__ void __launch_bounds__(CC<N, PPC>::THR) k_coarse_cluster(LevelView L,
                                                                     const double* __restrict__ phi_b,
                                                                     Rec* rec, int* status,
                                                                     double* diag_out) {
+  pdl_begin();
   using G = Geo<3, N>;
   using K = CC<N, PPC>;
   cg::cluster_group cl = cg::this_cluster();

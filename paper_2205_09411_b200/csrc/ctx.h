@@ -2,7 +2,9 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <memory>
+#include <utility>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -24,6 +26,34 @@ struct PmgError : std::runtime_error {
       throw ::pmghost::PmgError(PMG_ERR_CUDA, std::string("CUDA error: ") +            \
                                                   cudaGetErrorString(e_) + " at " #x); \
   } while (0)
+
+// Kernel launch with programmatic stream serialization (programmatic
+// dependent launch): the next kernel of the stream -- or of the captured
+// graph -- is scheduled while this one drains; every kernel starts with
+// pmgdev::pdl_begin() (griddepcontrol.wait), so correctness does not depend on
+// it.  Off by default (measured no gain inside the captured cycle graphs;
+// the streaming kernels occupy every SM); PMG_PDL=1 enables it.
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PMG_PDL");
+    return e && *e && *e != '0';
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline void pdl_launch(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  PMG_CUDA(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
+}
 
 template <typename T>
 struct DevBuf {

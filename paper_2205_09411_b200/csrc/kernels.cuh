@@ -97,6 +97,7 @@ __device__ __forceinline__ double block_max(double v, double* smem) {
 template <int D, int N>
 __global__ void __launch_bounds__(kThreads) k_gs(LevelView L, LevelView Lc,
                                                  const double* __restrict__ phi_b, int parity) {
+  pdl_begin();
   using G = Geo<D, N>;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long long)L.nb * G::H) return;
@@ -109,6 +110,7 @@ __global__ void __launch_bounds__(kThreads) k_gs(LevelView L, LevelView Lc,
 template <int D, int N>
 __global__ void __launch_bounds__(kThreads) k_residual(LevelView L, LevelView Lc,
                                                        const double* __restrict__ phi_b) {
+  pdl_begin();
   using G = Geo<D, N>;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long long)L.nb * G::NI) return;
@@ -131,6 +133,7 @@ template <int D, int N, int MODE>
 __global__ void __launch_bounds__(kThreads) k_restrict(LevelView Lf, LevelView Lfc,
                                                        LevelView Lp,
                                                        const double* __restrict__ phi_b) {
+  pdl_begin();
   using G = Geo<D, N>;
   constexpr int NQ = G::NI / G::NC;  // parent cells per fine block
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -172,6 +175,7 @@ __global__ void __launch_bounds__(kThreads) k_restrict(LevelView Lf, LevelView L
 template <int D, int N, bool FAS>
 __global__ void __launch_bounds__(kThreads) k_fas(LevelView L, LevelView Lc,
                                                   const double* __restrict__ phi_b) {
+  pdl_begin();
   using G = Geo<D, N>;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long long)L.nb * G::NI) return;
@@ -189,6 +193,7 @@ __global__ void __launch_bounds__(kThreads) k_fas(LevelView L, LevelView Lc,
 // precedes the snapshot.  One thread per (block, face, transverse cell).
 template <int D, int N>
 __global__ void __launch_bounds__(kThreads) k_cfold(LevelView L, LevelView Lc) {
+  pdl_begin();
   using G = Geo<D, N>;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long long)L.nb * G::F * G::NT) return;
@@ -213,6 +218,7 @@ __global__ void __launch_bounds__(kThreads) k_cfold(LevelView L, LevelView Lc) {
 // ---------------------------------------------------------------- prolongation
 template <int D, int N, bool FULL>
 __global__ void __launch_bounds__(kThreads) k_prolong(LevelView Lf, LevelView Lp, LevelView Lpp) {
+  pdl_begin();
   using G = Geo<D, N>;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long long)Lf.nb * G::NI) return;
@@ -257,6 +263,7 @@ __global__ void __launch_bounds__(kThreads) k_prolong(LevelView Lf, LevelView Lp
 // ---------------------------------------------------------------- pins
 template <int D, int N>
 __global__ void __launch_bounds__(kThreads) k_pins(LevelView L, const double* __restrict__ phi_b) {
+  pdl_begin();
   using G = Geo<D, N>;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long long)L.nb * G::NI) return;
@@ -276,6 +283,7 @@ __global__ void __launch_bounds__(kThreads) k_record(LevelView L, LevelView Lc,
                                                      const double* __restrict__ phi_b,
                                                      Rec* __restrict__ partial, Rec* rec,
                                                      unsigned int* counter) {
+  pdl_begin();
   using G = Geo<D, N>;
   __shared__ double sm[72];
   __shared__ bool last;
@@ -329,6 +337,7 @@ __global__ void __launch_bounds__(kThreads) k_record(LevelView L, LevelView Lc,
 
 // CycleStats from the level records (multigrid.hpp:564-575).
 static __global__ void k_combine(const Rec* __restrict__ rec, int nlev, double* out) {
+  pdl_begin();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double m = 0, s = 0;
   long long c = 0;
@@ -375,6 +384,7 @@ template <int D, int N>
 __global__ void __launch_bounds__(1024) k_coarse(LevelView L, CoarseDev C,
                                                  const double* __restrict__ phi_b, Rec* rec,
                                                  int* status, double* diag) {
+  pdl_begin();
   using G = Geo<D, N>;
   __shared__ double sm[72];
   const int n = C.n;
@@ -557,6 +567,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter(int nb, double* __restrict
                                                       const double* __restrict__ src,
                                                       const int32_t* __restrict__ slot_id,
                                                       int layout) {
+  pdl_begin();
   using G = Geo<D, N>;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long long)nb * G::NI) return;
@@ -581,6 +592,7 @@ __global__ void __launch_bounds__(kThreads) k_gather(LevelView L, LevelView Lc, 
                                                      double* __restrict__ dst,
                                                      const int32_t* __restrict__ slot_id,
                                                      int layout) {
+  pdl_begin();
   using G = Geo<D, N>;
   const int s1 = N + 2;
   const int S = D == 2 ? s1 * s1 : s1 * s1 * s1;

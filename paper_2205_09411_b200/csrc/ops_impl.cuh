@@ -42,7 +42,7 @@ struct OpsImpl final : Ops {
     if ((L.exp & (1 << 19)) && L.nb <= kSmallLevel) return;          // timing experiment only
     if ((L.exp & (1 << 20)) && l < (int)c.mesh.L) return;            // timing experiment only
     if (L.nb <= kSmallLevel && !(L.exp & 32768)) {
-      k_gs<D, N><<<grid_for((long long)L.nb * G::H), kThreads, 0, c.stream>>>(L, Vc(c, l), c.phi_b.p, parity);
+      pdl_launch(k_gs<D, N>, grid_for((long long)L.nb * G::H), kThreads, 0, c.stream, L, Vc(c, l), c.phi_b.p, parity);
       check();
       return;
     }
@@ -66,12 +66,12 @@ struct OpsImpl final : Ops {
       }
       cudaStream_t s2 = fork ? c.side : c.stream;
       if (d.n_slow > 0)
-        k_gs_tile<D, N><<<d.n_slow, TT::THREADS, 0, s2>>>(L, Vc(c, l), c.phi_b.p, parity, d.slow_list.p);
+        pdl_launch(k_gs_tile<D, N>, d.n_slow, TT::THREADS, 0, s2, L, Vc(c, l), c.phi_b.p, parity, d.slow_list.p);
       if (nfix > 0)
-        k_gs_fix<D, N><<<grid_for(nfix, 128), 128, 0, s2>>>(L, Vc(c, l), c.phi_b.p, parity,
+        pdl_launch(k_gs_fix<D, N>, grid_for(nfix, 128), 128, 0, s2, L, Vc(c, l), c.phi_b.p, parity,
                                                            (const int2*)d.fix_list[parity].p, nfix);
       if (ncut > 0)  // cut rows: disjoint from the streaming kernel's cells and inputs
-        k_gs_cut<D><<<grid_for(ncut, 128), 128, 0, s2>>>(L, c.phi_b.p, d.cut_ent[parity].p,
+        pdl_launch(k_gs_cut<D>, grid_for(ncut, 128), 128, 0, s2, L, c.phi_b.p, d.cut_ent[parity].p,
                                                         d.cut_gbc[parity].p, ncut);
       if (stream) {
         if constexpr (D == 3 && (N == 8 || N == 16)) {
@@ -82,7 +82,7 @@ struct OpsImpl final : Ops {
         }
 
       } else if (d.n_fast > 0) {
-        k_gs_lean<D, N><<<d.n_fast, Lean<D, N>::THR, 0, c.stream>>>(L, parity, d.fast_list.p);
+        pdl_launch(k_gs_lean<D, N>, d.n_fast, Lean<D, N>::THR, 0, c.stream, L, parity, d.fast_list.p);
       }
       if (fork) {
         PMG_CUDA(cudaEventRecord(c.ev_join, c.side));
@@ -90,7 +90,7 @@ struct OpsImpl final : Ops {
       }
     }
     else
-      k_gs<D, N><<<grid_for((long long)L.nb * G::H), kThreads, 0, c.stream>>>(L, Vc(c, l),
+      pdl_launch(k_gs<D, N>, grid_for((long long)L.nb * G::H), kThreads, 0, c.stream, L, Vc(c, l),
                                                                              c.phi_b.p, parity);
     check();
   }
@@ -105,13 +105,13 @@ struct OpsImpl final : Ops {
         attr = true;
       }
       const int grid = std::min(d.n_gs, c.sms * MINB);
-      k_gs_stream<N, ST, MINB><<<grid, Stream3<N>::THR, smem, c.stream>>>(L, parity, c.phi_b.p,
+      pdl_launch(k_gs_stream<N, ST, MINB>, grid, Stream3<N>::THR, smem, c.stream, L, parity, c.phi_b.p,
                                                                            (const int4*)d.gs_plan.p, d.n_gs);
     }
   }
   void residual(Ctx& c, int l) override {
     const LevelView& L = V(c, l);
-    k_residual<D, N><<<grid_for((long long)L.nb * G::NI), kThreads, 0, c.stream>>>(L, Vc(c, l),
+    pdl_launch(k_residual<D, N>, grid_for((long long)L.nb * G::NI), kThreads, 0, c.stream, L, Vc(c, l),
                                                                                   c.phi_b.p);
     check();
   }
@@ -120,11 +120,11 @@ struct OpsImpl final : Ops {
     const unsigned g = grid_for((long long)Lf.nb * (G::NI / G::NC));
     if (Lf.nb <= kSmallLevel && !(Lf.exp & 32768)) {
       if (mode == RM_RES)
-        k_restrict<D, N, RM_RES><<<g, kThreads, 0, c.stream>>>(Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
+        pdl_launch(k_restrict<D, N, RM_RES>, g, kThreads, 0, c.stream, Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
       else if (mode == RM_RHS)
-        k_restrict<D, N, RM_RHS><<<g, kThreads, 0, c.stream>>>(Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
+        pdl_launch(k_restrict<D, N, RM_RHS>, g, kThreads, 0, c.stream, Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
       else
-        k_restrict<D, N, RM_FUSED><<<g, kThreads, 0, c.stream>>>(Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
+        pdl_launch(k_restrict<D, N, RM_FUSED>, g, kThreads, 0, c.stream, Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
       check();
       return;
     }
@@ -140,14 +140,14 @@ struct OpsImpl final : Ops {
           attr = true;
         }
         const int grid = std::min(d.n_rs, c.sms * MINB);
-        k_restrict_stream<N, ST, MINB, false><<<grid, RStream3<N>::THR, smem, c.stream>>>(
+        pdl_launch(k_restrict_stream<N, ST, MINB, false>, grid, RStream3<N>::THR, smem, c.stream, 
             Lf, V(c, l - 1), c.phi_b.p, (const int4*)d.rs_plan.p, d.n_rs, nullptr, nullptr, nullptr);
         if (d.n_rfix > 0)
-          k_restrict_fix<D, N><<<grid_for((long long)d.n_rfix * 8, 128), 128, 0, c.stream>>>(
+          pdl_launch(k_restrict_fix<D, N>, grid_for((long long)d.n_rfix * 8, 128), 128, 0, c.stream, 
               Lf, Vc(c, l), V(c, l - 1), c.phi_b.p, (const int2*)d.rfix_list.p, d.n_rfix);
         const LevelDev& dp = *c.lev[(size_t)(l - 1)];
         if (dp.n_pin > 0)  // apply_pins(l-1)
-          k_pin_list<<<grid_for(dp.n_pin, 256), 256, 0, c.stream>>>(V(c, l - 1).phi, c.phi_b.p,
+          pdl_launch(k_pin_list, grid_for(dp.n_pin, 256), 256, 0, c.stream, V(c, l - 1).phi, c.phi_b.p,
                                                                     (const int2*)dp.pin_list.p, dp.n_pin);
         check();
         return;
@@ -155,20 +155,20 @@ struct OpsImpl final : Ops {
     }
     if constexpr (TILE) {
       if (mode == RM_RES)
-        k_restrict_tile<D, N, RM_RES><<<Lf.nb, TT::THREADS, 0, c.stream>>>(Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
+        pdl_launch(k_restrict_tile<D, N, RM_RES>, Lf.nb, TT::THREADS, 0, c.stream, Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
       else if (mode == RM_RHS)
-        k_restrict_tile<D, N, RM_RHS><<<Lf.nb, TT::THREADS, 0, c.stream>>>(Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
+        pdl_launch(k_restrict_tile<D, N, RM_RHS>, Lf.nb, TT::THREADS, 0, c.stream, Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
       else
-        k_restrict_tile<D, N, RM_FUSED><<<Lf.nb, TT::THREADS, 0, c.stream>>>(Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
+        pdl_launch(k_restrict_tile<D, N, RM_FUSED>, Lf.nb, TT::THREADS, 0, c.stream, Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
       check();
       return;
     }
     if (mode == RM_RES)
-      k_restrict<D, N, RM_RES><<<g, kThreads, 0, c.stream>>>(Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
+      pdl_launch(k_restrict<D, N, RM_RES>, g, kThreads, 0, c.stream, Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
     else if (mode == RM_RHS)
-      k_restrict<D, N, RM_RHS><<<g, kThreads, 0, c.stream>>>(Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
+      pdl_launch(k_restrict<D, N, RM_RHS>, g, kThreads, 0, c.stream, Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
     else
-      k_restrict<D, N, RM_FUSED><<<g, kThreads, 0, c.stream>>>(Lf, Vc(c, l), V(c, l - 1),
+      pdl_launch(k_restrict<D, N, RM_FUSED>, g, kThreads, 0, c.stream, Lf, Vc(c, l), V(c, l - 1),
                                                              c.phi_b.p);
     check();
   }
@@ -178,22 +178,22 @@ struct OpsImpl final : Ops {
     if constexpr (TILE) {
       if (!(L.nb <= ((L.exp & 65536) ? 4096 : kSmallLevel) && !(L.exp & 32768))) {
         if (f)
-          k_fas_tile<D, N, true><<<L.nb, TT::THREADS, 0, c.stream>>>(L, Vc(c, lc), c.phi_b.p);
+          pdl_launch(k_fas_tile<D, N, true>, L.nb, TT::THREADS, 0, c.stream, L, Vc(c, lc), c.phi_b.p);
         else
-          k_fas_tile<D, N, false><<<L.nb, TT::THREADS, 0, c.stream>>>(L, Vc(c, lc), c.phi_b.p);
+          pdl_launch(k_fas_tile<D, N, false>, L.nb, TT::THREADS, 0, c.stream, L, Vc(c, lc), c.phi_b.p);
         check();
         return;
       }
     }
     if (f)
-      k_fas<D, N, true><<<g, kThreads, 0, c.stream>>>(L, Vc(c, lc), c.phi_b.p);
+      pdl_launch(k_fas<D, N, true>, g, kThreads, 0, c.stream, L, Vc(c, lc), c.phi_b.p);
     else
-      k_fas<D, N, false><<<g, kThreads, 0, c.stream>>>(L, Vc(c, lc), c.phi_b.p);
+      pdl_launch(k_fas<D, N, false>, g, kThreads, 0, c.stream, L, Vc(c, lc), c.phi_b.p);
     check();
   }
   void cfold(Ctx& c, int lc) override {
     const LevelView& L = V(c, lc);
-    k_cfold<D, N><<<grid_for((long long)L.nb * G::F * G::NT), kThreads, 0, c.stream>>>(L, Vc(c, lc));
+    pdl_launch(k_cfold<D, N>, grid_for((long long)L.nb * G::F * G::NT), kThreads, 0, c.stream, L, Vc(c, lc));
     check();
   }
   template <bool FULL>
@@ -209,10 +209,10 @@ struct OpsImpl final : Ops {
         attr = true;
       }
       const int grid = std::min(d.n_pp, c.sms * MINB);
-      k_prolong_stream<N, ST, MINB, FULL><<<grid, PStream3<N>::THR, smem, c.stream>>>(
+      pdl_launch(k_prolong_stream<N, ST, MINB, FULL>, grid, PStream3<N>::THR, smem, c.stream, 
           V(c, l), V(c, l - 1), (const int4*)d.pp_plan.p, d.n_pp);
       if (d.n_pin > 0)  // inside cells were interpolated too: restore their pins
-        k_pin_list<<<grid_for(d.n_pin, 256), 256, 0, c.stream>>>(V(c, l).phi, c.phi_b.p,
+        pdl_launch(k_pin_list, grid_for(d.n_pin, 256), 256, 0, c.stream, V(c, l).phi, c.phi_b.p,
                                                                   (const int2*)d.pin_list.p, d.n_pin);
     }
   }
@@ -233,17 +233,17 @@ struct OpsImpl final : Ops {
     if constexpr (TILE) {
       if (!(Lf.nb <= kSmallLevel && !(Lf.exp & 32768))) {
         if (full)
-          k_prolong_tile<D, N, true><<<Lf.nb, TT::THREADS, 0, c.stream>>>(Lf, Lp, Lpp);
+          pdl_launch(k_prolong_tile<D, N, true>, Lf.nb, TT::THREADS, 0, c.stream, Lf, Lp, Lpp);
         else
-          k_prolong_tile<D, N, false><<<Lf.nb, TT::THREADS, 0, c.stream>>>(Lf, Lp, Lpp);
+          pdl_launch(k_prolong_tile<D, N, false>, Lf.nb, TT::THREADS, 0, c.stream, Lf, Lp, Lpp);
         check();
         return;
       }
     }
     if (full)
-      k_prolong<D, N, true><<<g, kThreads, 0, c.stream>>>(Lf, Lp, Lpp);
+      pdl_launch(k_prolong<D, N, true>, g, kThreads, 0, c.stream, Lf, Lp, Lpp);
     else
-      k_prolong<D, N, false><<<g, kThreads, 0, c.stream>>>(Lf, Lp, Lpp);
+      pdl_launch(k_prolong<D, N, false>, g, kThreads, 0, c.stream, Lf, Lp, Lpp);
     check();
   }
   void record(Ctx& c, int l) override {
@@ -264,10 +264,10 @@ struct OpsImpl final : Ops {
           PMG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
         }
         if (d.n_slow > 0)
-          k_record_tile<D, N><<<d.n_slow, TT::THREADS, 0, c.side>>>(L, Vc(c, l), c.phi_b.p, c.partial.p, c.rec.p,
+          pdl_launch(k_record_tile<D, N>, d.n_slow, TT::THREADS, 0, c.side, L, Vc(c, l), c.phi_b.p, c.partial.p, c.rec.p,
                                                                    nullptr, d.slow_list.p);
         if (ncut > 0)
-          k_record_cut<D><<<gcut, 256, 0, c.side>>>(L, c.phi_b.p, d.cut_ent[0].p, d.cut_gbc[0].p, d.n_cut[0],
+          pdl_launch(k_record_cut<D>, gcut, 256, 0, c.side, L, c.phi_b.p, d.cut_ent[0].p, d.cut_gbc[0].p, d.n_cut[0],
                                                      d.cut_ent[1].p, d.cut_gbc[1].p, d.n_cut[1], G::NI,
                                                      c.partial.p + L.nb);
         constexpr int ST = 2, MINB = 1;
@@ -279,13 +279,13 @@ struct OpsImpl final : Ops {
           attr = true;
         }
         const int grid = std::min(d.n_rs, c.sms * MINB);
-        k_restrict_stream<N, ST, MINB, true><<<grid, RStream3<N>::THR, smem, c.stream>>>(
+        pdl_launch(k_restrict_stream<N, ST, MINB, true>, grid, RStream3<N>::THR, smem, c.stream, 
             L, L, c.phi_b.p, (const int4*)d.rs_plan.p, d.n_rs, c.partial.p, c.rec.p, nullptr);
         if (fork) {
           PMG_CUDA(cudaEventRecord(c.ev_join, c.side));
           PMG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
         }
-        k_record_fold<<<1, 256, 0, c.stream>>>(c.partial.p, L.nb + gcut, c.rec.p + L.level);
+        pdl_launch(k_record_fold, 1, 256, 0, c.stream, c.partial.p, L.nb + gcut, c.rec.p + L.level);
         check();
         return;
       }
@@ -298,10 +298,10 @@ struct OpsImpl final : Ops {
         PMG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
       }
       if (d.n_uslow > 0)
-        k_record_tile<D, N><<<d.n_uslow, TT::THREADS, 0, fork ? c.side : c.stream>>>(
+        pdl_launch(k_record_tile<D, N>, d.n_uslow, TT::THREADS, 0, fork ? c.side : c.stream, 
             L, Vc(c, l), c.phi_b.p, c.partial.p, c.rec.p, c.counter.p, d.uslow_list.p);
       if (d.n_ufast > 0)
-        k_record_lean<D, N><<<d.n_ufast, TT::THREADS, 0, c.stream>>>(L, c.partial.p, c.rec.p,
+        pdl_launch(k_record_lean<D, N>, d.n_ufast, TT::THREADS, 0, c.stream, L, c.partial.p, c.rec.p,
                                                                      c.counter.p, d.ufast_list.p);
       if (fork) {
         PMG_CUDA(cudaEventRecord(c.ev_join, c.side));
@@ -310,13 +310,13 @@ struct OpsImpl final : Ops {
       check();
       return;
     }
-    k_record<D, N><<<L.nb, kThreads, 0, c.stream>>>(L, Vc(c, l), c.phi_b.p, c.partial.p, c.rec.p,
+    pdl_launch(k_record<D, N>, L.nb, kThreads, 0, c.stream, L, Vc(c, l), c.phi_b.p, c.partial.p, c.rec.p,
                                                     c.counter.p);
     check();
   }
   void pins(Ctx& c, int l) override {
     const LevelView& L = V(c, l);
-    k_pins<D, N><<<grid_for((long long)L.nb * G::NI), kThreads, 0, c.stream>>>(L, c.phi_b.p);
+    pdl_launch(k_pins<D, N>, grid_for((long long)L.nb * G::NI), kThreads, 0, c.stream, L, c.phi_b.p);
     check();
   }
   template <int PPC>
@@ -334,13 +334,15 @@ struct OpsImpl final : Ops {
       cfgl.blockDim = dim3(K::THR, 1, 1);
       cfgl.dynamicSmemBytes = 0;
       cfgl.stream = c.stream;
-      cudaLaunchAttribute at[1];
+      cudaLaunchAttribute at[2];
       at[0].id = cudaLaunchAttributeClusterDimension;
       at[0].val.clusterDim.x = K::NC;
       at[0].val.clusterDim.y = 1;
       at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[1].val.programmaticStreamSerializationAllowed = 1;
       cfgl.attrs = at;
-      cfgl.numAttrs = 1;
+      cfgl.numAttrs = pdl_enabled() ? 2 : 1;
       PMG_CUDA(cudaLaunchKernelEx(&cfgl, k_coarse_cluster<N, PPC>, V(c, 1), F, (const double*)c.phi_b.p, c.rec.p,
                                   c.status.p, c.diag.p));
     }
@@ -382,7 +384,7 @@ struct OpsImpl final : Ops {
         PMG_CUDA(cudaFuncSetAttribute(k_coarse_fast<D, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
       }
-      k_coarse_fast<D, N><<<1, kCoarseThreads, smem, c.stream>>>(V(c, 1), F, c.phi_b.p, c.rec.p,
+      pdl_launch(k_coarse_fast<D, N>, 1, kCoarseThreads, smem, c.stream, V(c, 1), F, c.phi_b.p, c.rec.p,
                                                                    c.status.p, c.diag.p);
       check();
       return;
@@ -404,13 +406,13 @@ struct OpsImpl final : Ops {
     int lim = 1;
     for (int k = 0; k < D; ++k) lim *= 8;
     C.fallback_ok = c.coarse.n <= lim + 1;
-    k_coarse<D, N><<<1, 1024, 0, c.stream>>>(V(c, 1), C, c.phi_b.p, c.rec.p, c.status.p, c.diag.p);
+    pdl_launch(k_coarse<D, N>, 1, 1024, 0, c.stream, V(c, 1), C, c.phi_b.p, c.rec.p, c.status.p, c.diag.p);
     check();
   }
   void scatter(Ctx& c, int l, double* dst, const double* staging, const int32_t* slot_id,
                int layout) override {
     const LevelView& L = V(c, l);
-    k_scatter<D, N><<<grid_for((long long)L.nb * G::NI), kThreads, 0, c.stream>>>(
+    pdl_launch(k_scatter<D, N>, grid_for((long long)L.nb * G::NI), kThreads, 0, c.stream, 
         L.nb, dst, staging, slot_id, layout);
     check();
   }
@@ -418,7 +420,7 @@ struct OpsImpl final : Ops {
               int layout) override {
     const LevelView& L = V(c, l);
     const long long per = layout == 0 ? c.S : G::NI;
-    k_gather<D, N><<<grid_for((long long)L.nb * per), kThreads, 0, c.stream>>>(
+    pdl_launch(k_gather<D, N>, grid_for((long long)L.nb * per), kThreads, 0, c.stream, 
         L, Vc(c, l), var, staging, slot_id, layout);
     check();
   }

@@ -28,6 +28,15 @@
 
 namespace pmgdev {
 
+// Programmatic dependent launch (every cycle kernel is launched with
+// programmatic stream serialization): let the next kernel in the stream be
+// scheduled now, then wait until the previous kernel has completed and its
+// writes are visible.  Nothing before pdl_begin() may read device data.
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 constexpr int kMaxLevels = 24;
 
 enum BlockKind : uint8_t { KIND_UNIFORM = 0, KIND_IFACE = 1, KIND_ALL_INSIDE = 2 };

@@ -267,6 +267,7 @@ template <int D, int N>
 __global__ void __launch_bounds__(256) k_block_flag(LsfDev L, const double* __restrict__ origin,
                                                     const double* __restrict__ dx, int nb,
                                                     double safety, uint8_t* flag) {
+  pdl_begin();
   __shared__ int any;
   const int b = blockIdx.x;
   if (b >= nb) return;
@@ -298,6 +299,7 @@ __global__ void __launch_bounds__(256) k_block_flag(LsfDev L, const double* __re
 
 template <int D, int N>
 __global__ void __launch_bounds__(128) k_cell_rows(LsfDev L, BuildArgs A, pmg_stencil_cfg_t cfg) {
+  pdl_begin();
   constexpr int NI = D == 2 ? N * N : N * N * N;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long long)A.nflag * NI) return;
@@ -423,6 +425,7 @@ __global__ void __launch_bounds__(1024) k_compact(BuildArgs A, const int32_t* __
                                                   int32_t* row_of, double* center, double* nbv,
                                                   double* bcv, double* dv, int8_t* objv,
                                                   uint8_t* maskv, int8_t* pinv, int32_t* linv) {
+  pdl_begin();
   constexpr int NI = D == 2 ? N * N : N * N * N;
   constexpr int F = 2 * D;
   constexpr int PER = (NI + 1023) / 1024;

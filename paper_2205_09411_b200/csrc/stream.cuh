@@ -221,6 +221,7 @@ template <int N, int S_STAGES, int MINB>
 __global__ void __launch_bounds__(Stream3<N>::THR, MINB) k_gs_stream(LevelView L, int parity,
                                                                     const double* __restrict__ phi_b,
                                                                     const int4* __restrict__ plan, int n) {
+  pdl_begin();
   using S = Stream3<N>;
   constexpr int NI = N * N * N;
   extern __shared__ __align__(128) double sm[];
@@ -452,6 +453,7 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
                                                                            const int4* __restrict__ plan, int n,
                                                                            Rec* __restrict__ partial, Rec* rec,
                                                                            unsigned int* counter) {
+  pdl_begin();
   using S = RStream3<N>;
   constexpr int NI = N * N * N;
   constexpr int HN = S::HN;
@@ -620,6 +622,7 @@ template <int D, int N>
 __global__ void __launch_bounds__(128) k_restrict_fix(LevelView Lf, LevelView Lfc, LevelView Lp,
                                                      const double* __restrict__ phi_b,
                                                      const int2* __restrict__ list, int n) {
+  pdl_begin();
   using G = Geo<D, N>;
   constexpr int HN = N / 2, NC = 1 << D;
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -657,6 +660,7 @@ __global__ void __launch_bounds__(128) k_restrict_fix(LevelView Lf, LevelView Lf
 // apply_pins (stencil.hpp:225-237) over a list of (cell address, object) pairs
 static __global__ void __launch_bounds__(256) k_pin_list(double* __restrict__ phi, const double* __restrict__ phi_b,
                                                  const int2* __restrict__ list, int n) {
+  pdl_begin();
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q < n) phi[list[q].x] = phi_b[list[q].y];
 }
@@ -670,6 +674,7 @@ template <int D>
 __global__ void __launch_bounds__(128) k_gs_cut(LevelView L, const double* __restrict__ phi_b,
                                                const int32_t* __restrict__ ent, const double* __restrict__ gbc,
                                                int n) {
+  pdl_begin();
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n) return;
   const int4 e0 = reinterpret_cast<const int4*>(ent)[2 * q];
@@ -748,6 +753,7 @@ __device__ __forceinline__ void pr_issue_async(const LevelView& Lp, const int4& 
 template <int N, int S_STAGES, int MINB, bool FULL>
 __global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(LevelView Lf, LevelView Lp,
                                                                           const int4* __restrict__ plan, int n) {
+  pdl_begin();
   using S = PStream3<N>;
   constexpr int NI = N * N * N, HN = S::HN, PE = S::PE;
   extern __shared__ __align__(128) double sm[];
@@ -854,6 +860,7 @@ __global__ void __launch_bounds__(256) k_record_cut(LevelView L, const double* _
                                                    int n0, const int32_t* __restrict__ ent1,
                                                    const double* __restrict__ gbc1, int n1, int ni,
                                                    Rec* __restrict__ partial) {
+  pdl_begin();
   __shared__ double red[72];
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   double mx = 0.0, ss = 0.0, cnt = 0.0;
@@ -889,6 +896,7 @@ __global__ void __launch_bounds__(256) k_record_cut(LevelView L, const double* _
 
 // rec = fold of partial[0 .. n) in index order (combine_records' per-level record)
 static __global__ void __launch_bounds__(256) k_record_fold(const Rec* __restrict__ partial, int n, Rec* out) {
+  pdl_begin();
   __shared__ double red[72];
   double mx = 0.0, ss = 0.0, cc = 0.0;
   for (int b = threadIdx.x; b < n; b += blockDim.x) {

@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_gs_tile(LevelView L, Le
                                                                  const double* __restrict__ phi_b,
                                                                  int parity,
                                                                  const int32_t* __restrict__ list) {
+  pdl_begin();
   using G = Geo<D, N>;
   using TT = Tile<D, N>;
   using O = Own<D, N>;
@@ -270,6 +271,7 @@ __device__ __forceinline__ double lean_halo(const LevelView& L, int ns, int X, i
 template <int D, int N>
 __global__ void __launch_bounds__(Lean<D, N>::THR) k_gs_lean(LevelView L, int parity,
                                                             const int32_t* __restrict__ list) {
+  pdl_begin();
   using G = Geo<D, N>;
   using TT = Tile<D, N>;
   using LN = Lean<D, N>;
@@ -374,6 +376,7 @@ template <int D, int N>
 __global__ void __launch_bounds__(128) k_gs_fix(LevelView L, LevelView Lc,
                                                const double* __restrict__ phi_b, int parity,
                                                const int2* __restrict__ cells, int n) {
+  pdl_begin();
   using G = Geo<D, N>;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -445,6 +448,7 @@ template <int D, int N, int MODE>
 __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_restrict_tile(LevelView Lf, LevelView Lfc,
                                                                        LevelView Lp,
                                                                        const double* __restrict__ phi_b) {
+  pdl_begin();
   using G = Geo<D, N>;
   using TT = Tile<D, N>;
   constexpr int HN = N / 2;
@@ -538,6 +542,7 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_restrict_tile(LevelView
 template <int D, int N, bool FAS>
 __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_fas_tile(LevelView L, LevelView Lc,
                                                                   const double* __restrict__ phi_b) {
+  pdl_begin();
   using G = Geo<D, N>;
   using TT = Tile<D, N>;
   using O = Own<D, N>;
@@ -596,6 +601,7 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_fas_tile(LevelView L, L
 template <int D, int N, bool FULL>
 __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_prolong_tile(LevelView Lf, LevelView Lp,
                                                                       LevelView Lpp) {
+  pdl_begin();
   using G = Geo<D, N>;
   using O = Own<D, N>;
   constexpr int HN = N / 2;
@@ -721,6 +727,7 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_record_tile(LevelView L
                                                                      Rec* __restrict__ partial,
                                                                      Rec* rec, unsigned int* counter,
                                                                      const int32_t* __restrict__ list) {
+  pdl_begin();
   using G = Geo<D, N>;
   using TT = Tile<D, N>;
   using O = Own<D, N>;
@@ -778,6 +785,7 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_record_lean(LevelView L
                                                                      Rec* __restrict__ partial,
                                                                      Rec* rec, unsigned int* counter,
                                                                      const int32_t* __restrict__ list) {
+  pdl_begin();
   using G = Geo<D, N>;
   using TT = Tile<D, N>;
   using O = Own<D, N>;
