@@ -134,40 +134,52 @@ __global__ void __launch_bounds__(kThreads) k_restrict(LevelView Lf, LevelView L
                                                        LevelView Lp,
                                                        const double* __restrict__ phi_b) {
   pdl_begin();
+  // 2^D threads per parent cell, one per child (its residual is a chain of
+  // dependent loads); the group's first lane sums them in x-fastest order
   using G = Geo<D, N>;
-  constexpr int NQ = G::NI / G::NC;  // parent cells per fine block
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long long)Lf.nb * NQ) return;
-  const int slot = (int)(t / NQ);
-  const int q = (int)(t % NQ);
+  constexpr int NC = G::NC;
+  constexpr int NQ = G::NI / NC;  // parent cells per fine block
   constexpr int HN = N / 2;
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long t = gid / NC;
+  const int d = (int)(gid % NC);
+  const bool live = t < (long long)Lf.nb * NQ;
+  const int slot = live ? (int)(t / NQ) : 0;
+  const int q = live ? (int)(t % NQ) : 0;
   const int qx = q % HN, qy = (q / HN) % HN, qz = D == 3 ? q / (HN * HN) : 0;
-  double sphi = 0, sq = 0;
-  for (int d = 0; d < G::NC; ++d) {
-    const int fi = 2 * qx + (d & 1), fj = 2 * qy + ((d >> 1) & 1),
-              fk = D == 3 ? 2 * qz + ((d >> 2) & 1) : 0;
+  double vphi = 0, vq = 0;
+  if (live) {
+    const int fi = 2 * qx + (d & 1), fj = 2 * qy + ((d >> 1) & 1), fk = D == 3 ? 2 * qz + ((d >> 2) & 1) : 0;
     const int c = G::colour(fi, fj, fk), e = G::entry(fi, fj, fk);
     const size_t a = (size_t)slot * G::NI + (size_t)(c * G::H + e);
-    sphi += Lf.phi[a];
+    vphi = Lf.phi[a];
     if (MODE == RM_RES) {
-      sq += Lf.res[a];
+      vq = Lf.res[a];
     } else if (MODE == RM_RHS) {
-      sq += Lf.rhs[a];
+      vq = Lf.rhs[a];
     } else {
       bool ins;
-      sq += resid_cell<D, N>(Lf, Lfc, phi_b, slot, c, e, &ins);
+      vq = resid_cell<D, N>(Lf, Lfc, phi_b, slot, c, e, &ins);
     }
   }
+  const int base = threadIdx.x & ~(NC - 1) & 31;
+  double sphi = 0, sq = 0;
+#pragma unroll
+  for (int u = 0; u < NC; ++u) {
+    sphi += __shfl_sync(0xffffffffu, vphi, base + u);
+    sq += __shfl_sync(0xffffffffu, vq, base + u);
+  }
+  if (!live || d != 0) return;
   const int P = Lf.parent[slot];
   int cp[3] = {0, 0, 0};
   for (int a = 0; a < D; ++a) cp[a] = (Lf.coords[slot * D + a] & 1) * HN;
   const int pi = cp[0] + qx, pj = cp[1] + qy, pk = D == 3 ? cp[2] + qz : 0;
   const int pc = G::colour(pi, pj, pk), pe = G::entry(pi, pj, pk);
   const size_t pa = (size_t)P * G::NI + (size_t)(pc * G::H + pe);
-  double vphi = sphi / (double)(1 << D);
+  double pv = sphi / (double)(1 << D);
   const int r = row_index<D, N>(Lp, P, pc, pe);
-  if (r >= 0 && Lp.r_mask[r] == 1) vphi = phi_b[Lp.r_pin[r]];
-  Lp.phi[pa] = vphi;
+  if (r >= 0 && Lp.r_mask[r] == 1) pv = phi_b[Lp.r_pin[r]];
+  Lp.phi[pa] = pv;
   Lp.rhs[pa] = sq / (double)(1 << D);
 }
 

@@ -117,7 +117,7 @@ struct OpsImpl final : Ops {
   }
   void restrict_(Ctx& c, int l, int mode) override {
     const LevelView& Lf = V(c, l);
-    const unsigned g = grid_for((long long)Lf.nb * (G::NI / G::NC));
+    const unsigned g = grid_for((long long)Lf.nb * G::NI);  // k_restrict: one thread per child cell
     if (Lf.nb <= kSmallLevel && !(Lf.exp & 32768)) {
       if (mode == RM_RES)
         pdl_launch(k_restrict<D, N, RM_RES>, g, kThreads, 0, c.stream, Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
