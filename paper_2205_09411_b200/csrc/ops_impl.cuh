@@ -75,10 +75,11 @@ struct OpsImpl final : Ops {
                                                         d.cut_gbc[parity].p, ncut);
       if (stream) {
         if constexpr (D == 3 && (N == 8 || N == 16)) {
-          if (L.exp & 4096)
-            launch_gs_stream<4, 1>(c, L, d, parity);
-          else
-            launch_gs_stream<kStreamStages, kStreamCtasPerSm>(c, L, d, parity);
+          constexpr int T256 = N == 16 ? 256 : 0;
+          if (L.exp & (1 << 28)) launch_gs_stream<2, 3, T256>(c, L, d, parity);
+          else if (L.exp & (1 << 29)) launch_gs_stream<2, 4, T256>(c, L, d, parity);
+          else if (L.exp & (1 << 30)) launch_gs_stream<3, 2, T256>(c, L, d, parity);
+          else launch_gs_stream<kStreamStages, kStreamCtasPerSm, 0>(c, L, d, parity);
         }
 
       } else if (d.n_fast > 0) {
@@ -94,19 +95,20 @@ struct OpsImpl final : Ops {
                                                                              c.phi_b.p, parity);
     check();
   }
-  template <int ST, int MINB>
+  template <int ST, int MINB, int TH>
   void launch_gs_stream(Ctx& c, const LevelView& L, const LevelDev& d, int parity) {
     if constexpr (D == 3 && (N == 8 || N == 16)) {
-      constexpr size_t smem = (size_t)ST * Stream3<N>::STAGE * sizeof(double);
+      using S = Stream3<N, TH>;
+      constexpr size_t smem = (size_t)ST * S::STAGE * sizeof(double);
       static bool attr = false;
       if (!attr) {
-        PMG_CUDA(cudaFuncSetAttribute(k_gs_stream<N, ST, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        PMG_CUDA(cudaFuncSetAttribute(k_gs_stream<N, ST, MINB, TH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
         attr = true;
       }
       const int grid = std::min(d.n_gs, c.sms * MINB);
-      pdl_launch(k_gs_stream<N, ST, MINB>, grid, Stream3<N>::THR, smem, c.stream, L, parity, c.phi_b.p,
-                                                                           (const int4*)d.gs_plan.p, d.n_gs);
+      pdl_launch(k_gs_stream<N, ST, MINB, TH>, grid, S::THR, smem, c.stream, L, parity, c.phi_b.p,
+                 (const int4*)d.gs_plan.p, d.n_gs);
     }
   }
   void residual(Ctx& c, int l) override {

@@ -87,21 +87,21 @@ __device__ __forceinline__ BlockPlan load_plan(const int4* plan, int p) {
 }
 
 // ------------------------------------------------------------------ stage layout
-template <int N>
+template <int N, int TH = 0>
 struct Stream3 {
   static constexpr int HN = N / 2;
   static constexpr int H = N * N * N / 2;
   static constexpr int FH = N * HN;  // z / y face layer of one colour
-  static constexpr int THR = H < 512 ? H : 512;
+  static constexpr int THR = TH ? TH : (H < 512 ? H : 512);
   static constexpr int PER = H / THR;
-  // doubles per stage: X half, g half, hz[2], hy[2], hx[2] (x rows indexed
-  // k*N+j), then H int32 row_of entries of an interface block
-  static constexpr int OX = 0, OG = H, OZ = 2 * H, OY = OZ + 2 * FH, OXF = OY + 2 * FH;
+  // doubles per stage: X half, hz[2], hy[2], hx[2] (x rows indexed k*N+j),
+  // then H int32 row_of entries of an interface block.  g is not staged: each
+  // thread loads its own g values into registers one block ahead.
+  static constexpr int OX = 0, OZ = H, OY = OZ + 2 * FH, OXF = OY + 2 * FH;
   static constexpr int ORQ = OXF + 2 * N * N;  // in doubles; H int32 = H/2 doubles
   static constexpr int STAGE = ORQ + H / 2;
-  static constexpr uint32_t TX_BYTES = (uint32_t)(2 * H + 2 * FH) * 8u;  // bulk part
+  static constexpr uint32_t TX_BYTES = (uint32_t)(H + 2 * FH) * 8u;  // bulk part
   static constexpr int YC = N * HN;  // 16-B chunks of the two y layers (2 sides x N rows x HN/2)
-  static constexpr int XT0 = 0, YT0 = THR - YC;  // thread ranges issuing x / y face copies
 };
 
 // Bulk copies of one block into a stage (one elected thread): the two
@@ -117,7 +117,6 @@ __device__ __forceinline__ void gs_issue(const LevelView& L, const BlockPlan& P,
   const double* own = L.phi + (size_t)slot * NI + (size_t)c * S::H;
   mbar_arrive_expect_tx(bar, S::TX_BYTES);
   bulk_g2s(st + S::OX, L.phi + (size_t)slot * NI + (size_t)X * S::H, S::H * 8, bar);
-  bulk_g2s(st + S::OG, L.rhs + (size_t)slot * NI + (size_t)c * S::H, S::H * 8, bar);
   const int zm = P.nbr(4), zp = P.nbr(5);
   const double* s0 = zm >= 0 ? L.phi + (size_t)zm * NI + (size_t)X * S::H + (N - 1) * S::FH : own;
   const double* s1 = zp >= 0 ? L.phi + (size_t)zp * NI + (size_t)X * S::H : own + (N - 1) * S::FH;
@@ -138,14 +137,14 @@ __device__ __forceinline__ void xface_of(int c, int u, int& side, int& j, int& k
 // Thread-issued async copies of one block: the strided x-face values (the
 // neighbour's X value, or the own value on a physical face) and, for an
 // interface block, this thread's row_of entries.
-template <int N>
+template <int N, int TH>
 __device__ __forceinline__ void gs_issue_async(const LevelView& L, const BlockPlan& P, int c, double* st) {
-  using S = Stream3<N>;
+  using S = Stream3<N, TH>;
   constexpr int NI = N * N * N;
   const int t = threadIdx.x;
-  if (t < N * N) {
+  for (int u = t; u < N * N; u += S::THR) {
     int side, j, k;
-    xface_of<N>(c, t, side, j, k);
+    xface_of<N>(c, u, side, j, k);
     const int ns = P.nbr(side);
     const double* src;
     if (ns >= 0)  // -x: neighbour cell (N-1,j,k); +x: (0,j,k); both colour X
@@ -154,8 +153,9 @@ __device__ __forceinline__ void gs_issue_async(const LevelView& L, const BlockPl
       src = L.phi + (size_t)P.slot() * NI + (size_t)c * S::H + (size_t)(side ? S::HN - 1 : 0) + S::HN * (j + N * k);
     cp_async8(st + S::OXF + side * N * N + k * N + j, src);
   }
-  if (t >= S::YT0) {  // y layers: 16-B chunks of the x-rows j = N-1 / 0 (neighbour) or own row
-    const int u = t - S::YT0;
+  // y layers: 16-B chunks of the x-rows j = N-1 / 0 (neighbour) or own row,
+  // issued by the last threads (the first ones carry the x faces)
+  for (int u = S::THR - 1 - t; u < S::YC; u += S::THR) {
     constexpr int CR = S::HN / 2;  // chunks per row
     const int side = u / (N * CR), k = (u / CR) % N, ch = u % CR;
     const int ns = P.nbr(2 + side);
@@ -217,12 +217,12 @@ __device__ __forceinline__ void gs_phys_faces(const LevelView& L, int slot, int 
 // GS-RB half-sweep of the lean 3D blocks (UNIFORM / IFACE blocks without
 // coarse-fine faces, in plan order).  Special rows are left alone: k_gs_cut
 // updates the cut rows afterwards, inside rows keep their pin.
-template <int N, int S_STAGES, int MINB>
-__global__ void __launch_bounds__(Stream3<N>::THR, MINB) k_gs_stream(LevelView L, int parity,
-                                                                    const double* __restrict__ phi_b,
-                                                                    const int4* __restrict__ plan, int n) {
+template <int N, int S_STAGES, int MINB, int TH>
+__global__ void __launch_bounds__(Stream3<N, TH>::THR, MINB) k_gs_stream(LevelView L, int parity,
+                                                                        const double* __restrict__ phi_b,
+                                                                        const int4* __restrict__ plan, int n) {
   pdl_begin();
-  using S = Stream3<N>;
+  using S = Stream3<N, TH>;
   constexpr int NI = N * N * N;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t full[S_STAGES];
@@ -242,13 +242,21 @@ __global__ void __launch_bounds__(Stream3<N>::THR, MINB) k_gs_stream(LevelView L
       const BlockPlan P = load_plan(plan, blockIdx.x + s * G);
       if (t == 0) gs_issue<N>(L, P, c, sm + s * S::STAGE, &full[s]);
       if (t == 0) meta[s][0] = P.slot(), meta[s][1] = P.a.y;
-      gs_issue_async<N>(L, P, c, sm + s * S::STAGE);
+      gs_issue_async<N, TH>(L, P, c, sm + s * S::STAGE);
     }
     cp_async_commit();
   }
   BlockPlan pf;
   if (S_STAGES < nmine) pf = load_plan(plan, blockIdx.x + S_STAGES * G);
   const double h2 = L.h2;
+  static_assert(S_STAGES >= 2, "g of block it+1 is read through meta[] one iteration ahead");
+  __syncthreads();  // meta of the first stages
+  double gcur[S::PER], gnext[S::PER];
+  {
+    const double* gsrc = L.rhs + (size_t)meta[0][0] * NI + (size_t)c * S::H + t;
+#pragma unroll
+    for (int q = 0; q < S::PER; ++q) gcur[q] = gsrc[q * S::THR];
+  }
   for (int it = 0; it < nmine; ++it) {
     const int s = it % S_STAGES;
     double* st = sm + s * S::STAGE;
@@ -259,6 +267,11 @@ __global__ void __launch_bounds__(Stream3<N>::THR, MINB) k_gs_stream(LevelView L
     __syncthreads();
     const int slot = meta[s][0], flags = meta[s][1];
     const int kind = flags & 0xff, pmask = (flags >> 8) & 63;
+    if (it + 1 < nmine) {  // this thread's g of the next block, in flight during this one
+      const double* gsrc = L.rhs + (size_t)meta[(it + 1) % S_STAGES][0] * NI + (size_t)c * S::H + t;
+#pragma unroll
+      for (int q = 0; q < S::PER; ++q) gnext[q] = gsrc[q * S::THR];
+    }
     if (pmask) {  // block-uniform branch
       gs_phys_faces<N>(L, slot, pmask, c, st);
       __syncthreads();
@@ -284,7 +297,6 @@ __global__ void __launch_bounds__(Stream3<N>::THR, MINB) k_gs_stream(LevelView L
     if (j == N - 1) iyp = S::OY + S::FH + k0 * S::HN + m, dyp = KS * S::HN;
     const int izm0 = k0 > 0 ? rb - S::FH : S::OZ + j * S::HN + m;
     const int izpL = k0 < KS - 1 ? rb + (S::PER - 1) * DT + S::FH : S::OZ + S::FH + j * S::HN + m;
-    const int ig = S::OG + t;
     double* __restrict__ dst = L.phi + (size_t)slot * NI + (size_t)c * S::H + t;
     if (!(L.exp & 512)) {
       if (kind == KIND_UNIFORM) {  // multigrid.hpp:651-653: (sum of 6 - h^2 g) / 6.0
@@ -295,7 +307,7 @@ __global__ void __launch_bounds__(Stream3<N>::THR, MINB) k_gs_stream(LevelView L
           const double zm = st[q == 0 ? izm0 : rb + q * DT - S::FH];
           const double zp = st[q == S::PER - 1 ? izpL : rb + q * DT + S::FH];
           sv[q] = st[ixm + q * dxm] + st[ixp + q * dxp] + st[iym + q * dym] + st[iyp + q * dyp] + zm + zp -
-                  h2 * st[ig + q * S::THR];
+                  h2 * gcur[q];
           v[q] = div6_fast(sv[q]);
           ok = ok && div6_in_range(sv[q]);
         }
@@ -310,7 +322,7 @@ __global__ void __launch_bounds__(Stream3<N>::THR, MINB) k_gs_stream(LevelView L
 #pragma unroll
         for (int q = 0; q < S::PER; ++q) {
           const int r = rq[t + q * S::THR];
-          const double g = st[ig + q * S::THR];
+          const double g = gcur[q];
           const double p0 = st[ixm + q * dxm], p1 = st[ixp + q * dxp], p2 = st[iym + q * dym],
                        p3 = st[iyp + q * dyp], p4 = st[q == 0 ? izm0 : rb + q * DT - S::FH],
                        p5 = st[q == S::PER - 1 ? izpL : rb + q * DT + S::FH];
@@ -331,10 +343,12 @@ __global__ void __launch_bounds__(Stream3<N>::THR, MINB) k_gs_stream(LevelView L
     if (it + S_STAGES < nmine) {
       if (t == 0) gs_issue<N>(L, pf, c, st, &full[s]);
       if (t == 0) meta[s][0] = pf.slot(), meta[s][1] = pf.a.y;
-      gs_issue_async<N>(L, pf, c, st);
+      gs_issue_async<N, TH>(L, pf, c, st);
     }
     cp_async_commit();
     pf = pf2;
+#pragma unroll
+    for (int q = 0; q < S::PER; ++q) gcur[q] = gnext[q];
   }
 }
 
