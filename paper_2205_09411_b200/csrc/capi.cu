@@ -190,6 +190,71 @@ static void build_cut_tables(Ctx& c) {
   }
 }
 
+// small.cuh tables for levels of at most kSmallLevel blocks without
+// coarse-fine faces: per cell (colour-split address) the row code, the 2D
+// neighbour addresses / physical-ghost codes, the Dirichlet values, the leaf flag.
+static void build_small_tables(Ctx& c) {
+  const HostMesh& m = c.mesh;
+  const HostStencils& st = c.st;
+  const int N = c.N, D = c.dim, NI = c.NI, H = NI / 2, F = c.F;
+  for (int l = 1; l <= m.L; ++l) {
+    LevelDev& d = *c.lev[(size_t)l];
+    d.has_tab = false;
+    if (d.nb > kSmallLevel || d.has_cf || !st.valid) continue;
+    std::vector<int32_t> tab((size_t)d.nb * NI * 8, 0);
+    std::vector<double> gbc((size_t)d.nb * NI * 6, 0.0);
+    int base = 0;
+    for (int s = 0; s < d.nb; ++s) {
+      const int id = m.slots[(size_t)l][(size_t)s];
+      const bool bnd = st.boundary[(size_t)id] != 0;
+      const int r0 = bnd ? st.row_start[(size_t)id] : 0;
+      const int leaf = m.children[(size_t)id * 8] < 0 ? 1 : 0;
+      for (int ii = 0; ii < NI; ++ii) {
+        const int i = ii % N, j = (ii / N) % N, k = D == 3 ? ii / (N * N) : 0;
+        const size_t a = (size_t)s * NI + (size_t)cs_addr(ii, N, D, H);
+        int32_t* e = tab.data() + a * 8;
+        int code = -1;
+        if (bnd) {
+          const int r = st.row_of[(size_t)id * NI + ii];
+          if (r < 0) code = -2;
+          else if (st.mask[(size_t)(r0 + r)] == PMG_INSIDE) code = -3 - (base + r);
+          else code = base + r;
+        }
+        e[0] = code;
+        e[7] = leaf;
+        for (int f = 0; f < F; ++f) {
+          const int ax = f / 2, sg = (f & 1) ? 1 : -1;
+          int q[3] = {i, j, k};
+          q[ax] += sg;
+          if (q[ax] >= 0 && q[ax] < N) {
+            e[1 + f] = (int32_t)((size_t)s * NI + cs_addr(q[0] + N * (q[1] + N * q[2]), N, D, H));
+            continue;
+          }
+          const int nid = m.nbr[(size_t)id * 6 + f];
+          if (nid >= 0) {
+            q[ax] = sg > 0 ? 0 : N - 1;
+            e[1 + f] = (int32_t)((size_t)m.slot_of[(size_t)nid] * NI + cs_addr(q[0] + N * (q[1] + N * q[2]), N, D, H));
+            continue;
+          }
+          if (c.bctype[f] == PMG_BC_NEUMANN_ZERO) {
+            e[1 + f] = -1;
+            continue;
+          }
+          e[1 + f] = -2;
+          if (!c.face_off[f].empty() && c.face_off[f][(size_t)id] >= 0) {
+            const int t = D == 2 ? (ax == 0 ? j : i) : (ax == 0 ? j + N * k : ax == 1 ? i + N * k : i + N * j);
+            gbc[a * 6 + f] = c.face_vals[f][(size_t)c.face_off[f][(size_t)id] + t];
+          }
+        }
+      }
+      if (bnd) base += st.row_count[(size_t)id];
+    }
+    d.tab.upload(tab, c.stream);
+    d.tgbc.upload(gbc, c.stream);
+    d.has_tab = true;
+  }
+}
+
 static void upload_stencils(Ctx& c) {
   const HostMesh& m = c.mesh;
   const HostStencils& st = c.st;
@@ -385,6 +450,7 @@ static void upload_stencils(Ctx& c) {
   if (pb.empty()) pb.push_back(0.0);
   c.phi_b.upload(pb, c.stream);
   build_cut_tables(c);
+  build_small_tables(c);
 }
 
 static void default_stencils(Ctx& c) {
@@ -908,7 +974,10 @@ static void set_face_bc(Ctx& c, int dir, int type, const double* values) {
     }
   }
   upload_bc(c);
-  if (c.st.valid) build_cut_tables(c);
+  if (c.st.valid) {
+    build_cut_tables(c);
+    build_small_tables(c);
+  }
   set_views(c);
   invalidate_graphs(c);
   PMG_CUDA(cudaStreamSynchronize(c.stream));

@@ -80,6 +80,10 @@ struct DevBuf {
   }
 };
 
+// levels with at most this many blocks run the per-cell (small-level) kernels:
+// they are latency-bound, and a cell per thread gives the most loads in flight
+constexpr int kSmallLevel = 64;
+
 struct HostMesh {
   int nb = 0;
   int L = 0;
@@ -136,6 +140,9 @@ struct LevelDev {
   int n_pin = 0;
   DevBuf<int32_t> pp_plan;    // streaming prolongation plan (stream.cuh), -1: level not eligible
   int n_pp = -1;
+  DevBuf<int32_t> tab;        // small levels: per-cell row code + neighbour addresses (small.cuh)
+  DevBuf<double> tgbc;
+  bool has_tab = false;
   // k_gs_cut tables per colour: 8 int32 (cell, row, 6 neighbour addresses) + 6 ghost bc values
   DevBuf<int32_t> cut_ent[2];
   DevBuf<double> cut_gbc[2];

@@ -8,14 +8,11 @@
 #include "coarse.cuh"
 #include "coarse_cluster.cuh"
 #include "stream.cuh"
+#include "small.cuh"
 
 namespace pmghost {
 
 using namespace pmgdev;
-
-// levels with at most this many blocks run the one-thread-per-cell kernels:
-// they are latency-bound, and a cell per thread gives the most loads in flight
-constexpr int kSmallLevel = 64;
 
 // streaming GS pipeline depth and residency (stream.cuh)
 constexpr int kStreamStages = 2;
@@ -42,7 +39,13 @@ struct OpsImpl final : Ops {
     if ((L.exp & (1 << 19)) && L.nb <= kSmallLevel) return;          // timing experiment only
     if ((L.exp & (1 << 20)) && l < (int)c.mesh.L) return;            // timing experiment only
     if (L.nb <= kSmallLevel && !(L.exp & 32768)) {
-      pdl_launch(k_gs<D, N>, grid_for((long long)L.nb * G::H), kThreads, 0, c.stream, L, Vc(c, l), c.phi_b.p, parity);
+      const LevelDev& d = *c.lev[(size_t)l];
+      if (d.has_tab && !(L.exp & 65536))
+        pdl_launch(k_gs_tab<D, N>, grid_for((long long)L.nb * G::H), 256, 0, c.stream, L, c.phi_b.p,
+                   (const int4*)d.tab.p, (const double*)d.tgbc.p, parity);
+      else
+        pdl_launch(k_gs<D, N>, grid_for((long long)L.nb * G::H), kThreads, 0, c.stream, L, Vc(c, l), c.phi_b.p,
+                   parity);
       check();
       return;
     }
@@ -121,6 +124,21 @@ struct OpsImpl final : Ops {
     const LevelView& Lf = V(c, l);
     const unsigned g = grid_for((long long)Lf.nb * G::NI);  // k_restrict: one thread per child cell
     if (Lf.nb <= kSmallLevel && !(Lf.exp & 32768)) {
+      const LevelDev& d = *c.lev[(size_t)l];
+      if (d.has_tab && !(Lf.exp & 65536)) {
+        const LevelView& Lp = V(c, l - 1);
+        if (mode == RM_RES)
+          pdl_launch(k_restrict_tab<D, N, RM_RES>, g, 256, 0, c.stream, Lf, Lp, c.phi_b.p, (const int4*)d.tab.p,
+                     (const double*)d.tgbc.p);
+        else if (mode == RM_RHS)
+          pdl_launch(k_restrict_tab<D, N, RM_RHS>, g, 256, 0, c.stream, Lf, Lp, c.phi_b.p, (const int4*)d.tab.p,
+                     (const double*)d.tgbc.p);
+        else
+          pdl_launch(k_restrict_tab<D, N, RM_FUSED>, g, 256, 0, c.stream, Lf, Lp, c.phi_b.p,
+                     (const int4*)d.tab.p, (const double*)d.tgbc.p);
+        check();
+        return;
+      }
       if (mode == RM_RES)
         pdl_launch(k_restrict<D, N, RM_RES>, g, kThreads, 0, c.stream, Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
       else if (mode == RM_RHS)
@@ -177,8 +195,21 @@ struct OpsImpl final : Ops {
   void fas(Ctx& c, int lc, bool f) override {
     const LevelView& L = V(c, lc);
     const unsigned g = grid_for((long long)L.nb * G::NI);
+    {
+      const LevelDev& d = *c.lev[(size_t)lc];
+      if (L.nb <= kSmallLevel && d.has_tab && !(L.exp & 98304)) {
+        if (f)
+          pdl_launch(k_fas_tab<D, N, true>, grid_for((long long)L.nb * G::NI, 256), 256, 0, c.stream, L, c.phi_b.p,
+                     (const int4*)d.tab.p, (const double*)d.tgbc.p);
+        else
+          pdl_launch(k_fas_tab<D, N, false>, grid_for((long long)L.nb * G::NI, 256), 256, 0, c.stream, L,
+                     c.phi_b.p, (const int4*)d.tab.p, (const double*)d.tgbc.p);
+        check();
+        return;
+      }
+    }
     if constexpr (TILE) {
-      if (!(L.nb <= ((L.exp & 65536) ? 4096 : kSmallLevel) && !(L.exp & 32768))) {
+      if (!(L.nb <= kSmallLevel && !(L.exp & 32768))) {
         if (f)
           pdl_launch(k_fas_tile<D, N, true>, L.nb, TT::THREADS, 0, c.stream, L, Vc(c, lc), c.phi_b.p);
         else
@@ -252,6 +283,17 @@ struct OpsImpl final : Ops {
     const LevelView& L = V(c, l);
     // a level without leaves records zeros, which enq_reset_records left there
     if (c.lev[(size_t)l]->n_leaf == 0) return;
+    {
+      const LevelDev& d = *c.lev[(size_t)l];
+      if (L.nb <= kSmallLevel && d.has_tab && !(L.exp & 98304)) {
+        const int gr = (int)grid_for((long long)L.nb * G::NI, 256);
+        pdl_launch(k_record_tab<D, N>, gr, 256, 0, c.stream, L, c.phi_b.p, (const int4*)d.tab.p,
+                   (const double*)d.tgbc.p, c.partial.p);
+        pdl_launch(k_record_fold, 1, 256, 0, c.stream, (const Rec*)c.partial.p, gr, c.rec.p + L.level);
+        check();
+        return;
+      }
+    }
     if constexpr (D == 3 && N == 16) {
       const LevelDev& d = *c.lev[(size_t)l];
       if (d.n_rs > 0 && L.nb > kSmallLevel && !(L.exp & 16384)) {

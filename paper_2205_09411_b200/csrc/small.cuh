@@ -1,0 +1,176 @@
+// small.cuh -- table-driven per-cell kernels for the small levels.
+//
+// On a level of at most kSmallLevel blocks the work is a few hundred thousand
+// cells that live in L2, and the generic per-cell path is bound by its chain
+// of dependent loads (block kind -> interface page -> row -> neighbour slot
+// -> value).  The host resolves all of that once (capi.cu build_small_tables):
+// per cell, indexed by its colour-split address a,
+//   e[0]    row code: r >= 0 cut row, -1 uniform row of a uniform block,
+//           -2 uniform row of an interface block, -3 - r inside row r
+//   e[1..6] the 2D neighbour addresses (same block or same-level neighbour),
+//           -1 Neumann ghost f1, -2 Dirichlet ghost 2 bc - f1 (bc in gbc[6a+d])
+//   e[7]    1 if the block is a leaf
+// so every operator needs two dependent round trips (entry, then values).
+// The arithmetic is the reference's, as in cells.cuh.
+#pragma once
+#include "kernels.cuh"
+#include "tiles.cuh"
+#include "cells.cuh"
+
+namespace pmgdev {
+
+template <int D>
+__device__ __forceinline__ void tab_load(const LevelView& L, const int4* __restrict__ T,
+                                         const double* __restrict__ gbc, int a, int& code, int& leaf,
+                                         double& self, double* p) {
+  const int4 e0 = T[2 * a], e1 = T[2 * a + 1];
+  code = e0.x;
+  leaf = e1.w;
+  const int na[6] = {e0.y, e0.z, e0.w, e1.x, e1.y, e1.z};
+  self = L.phi[a];
+#pragma unroll
+  for (int d = 0; d < 2 * D; ++d)
+    p[d] = na[d] >= 0 ? L.phi[na[d]] : (na[d] == -1 ? self : 2.0 * gbc[(size_t)a * 6 + d] - self);
+}
+
+// gsrb_block half-sweep (multigrid.hpp:621-695), one thread per cell of the colour
+template <int D, int N>
+__global__ void __launch_bounds__(256) k_gs_tab(LevelView L, const double* __restrict__ phi_b,
+                                               const int4* __restrict__ T, const double* __restrict__ gbc,
+                                               int parity) {
+  pdl_begin();
+  using G = Geo<D, N>;
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= L.nb * G::H) return;
+  const int a = (gid / G::H) * G::NI + parity * G::H + gid % G::H;
+  int code, leaf;
+  double self, p[2 * D];
+  tab_load<D>(L, T, gbc, a, code, leaf, self, p);
+  if (code <= -3) return;  // inside: pinned
+  const double g = L.rhs[a];
+  const double h2 = L.h2;
+  double nv;
+  if (code == -1) {
+    if (D == 3)
+      nv = div6(p[0] + p[1] + p[2] + p[3] + p[4] + p[5] - h2 * g);  // :651-653
+    else
+      nv = 0.25 * (p[0] + p[1] + p[2] + p[3] - h2 * g);  // :640-641
+  } else if (code == -2) {
+    double s = -h2 * g;  // :668-671
+    for (int d = 0; d < 2 * D; ++d) s += p[d];
+    nv = -s * (-1.0 / (2.0 * D));
+  } else {
+    double num = g;  // :677-683
+    for (int d = 0; d < 2 * D; ++d) {
+      num -= L.r_nb[code * 2 * D + d] * p[d];
+      const double b = L.r_bc[code * 2 * D + d];
+      if (b != 0) num -= b * phi_b[L.r_obj[code * 2 * D + d]];
+    }
+    nv = num / L.r_center[code];
+  }
+  L.phi[a] = nv;
+}
+
+// FAS right-hand side g = L(phi) + R(r) on non-leaf blocks, OLD <- PHI
+// (multigrid.hpp:380-397); one thread per cell
+template <int D, int N, bool FAS>
+__global__ void __launch_bounds__(256) k_fas_tab(LevelView L, const double* __restrict__ phi_b,
+                                                const int4* __restrict__ T, const double* __restrict__ gbc) {
+  pdl_begin();
+  using G = Geo<D, N>;
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= L.nb * G::NI) return;
+  if (FAS) {
+    int code, leaf;
+    double self, p[2 * D];
+    tab_load<D>(L, T, gbc, a, code, leaf, self, p);
+    if (!leaf) {
+      const double out = code <= -3 ? 0.0 : apply_value<D>(L, phi_b, code >= 0 ? code : -1, self, p);
+      L.rhs[a] = out + L.rhs[a];
+    }
+    L.old[a] = self;
+  } else {
+    L.old[a] = L.phi[a];
+  }
+}
+
+// residual + restriction of a small level (multigrid.hpp:374-418, 697-722):
+// one thread per child cell, the first lane of each 2^D group sums them in
+// x-fastest order, pins the parent (apply_pins(l-1)) and writes it
+template <int D, int N, int MODE>
+__global__ void __launch_bounds__(256) k_restrict_tab(LevelView Lf, LevelView Lp, const double* __restrict__ phi_b,
+                                                     const int4* __restrict__ T, const double* __restrict__ gbc) {
+  pdl_begin();
+  using G = Geo<D, N>;
+  constexpr int NC = G::NC, NQ = G::NI / NC, HN = N / 2;
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = gid / NC, d = gid % NC;
+  const bool live = t < Lf.nb * NQ;
+  const int slot = live ? t / NQ : 0, q = live ? t % NQ : 0;
+  const int qx = q % HN, qy = (q / HN) % HN, qz = D == 3 ? q / (HN * HN) : 0;
+  double vphi = 0, vq = 0;
+  if (live) {
+    const int fi = 2 * qx + (d & 1), fj = 2 * qy + ((d >> 1) & 1), fk = D == 3 ? 2 * qz + ((d >> 2) & 1) : 0;
+    const int a = slot * G::NI + G::colour(fi, fj, fk) * G::H + G::entry(fi, fj, fk);
+    if (MODE == RM_FUSED) {
+      int code, leaf;
+      double p[2 * D];
+      tab_load<D>(Lf, T, gbc, a, code, leaf, vphi, p);
+      vq = code <= -3 ? 0.0 : resid_value<D>(Lf, phi_b, code >= 0 ? code : -1, vphi, p, Lf.rhs[a]);
+    } else {
+      vphi = Lf.phi[a];
+      vq = MODE == RM_RES ? Lf.res[a] : Lf.rhs[a];
+    }
+  }
+  const int base = threadIdx.x & ~(NC - 1) & 31;
+  double sphi = 0, sq = 0;
+#pragma unroll
+  for (int u = 0; u < NC; ++u) {
+    sphi += __shfl_sync(0xffffffffu, vphi, base + u);
+    sq += __shfl_sync(0xffffffffu, vq, base + u);
+  }
+  if (!live || d != 0) return;
+  const int P = Lf.parent[slot];
+  int cp[3] = {0, 0, 0};
+  for (int a2 = 0; a2 < D; ++a2) cp[a2] = (Lf.coords[slot * D + a2] & 1) * HN;
+  const int pi = cp[0] + qx, pj = cp[1] + qy, pk = D == 3 ? cp[2] + qz : 0;
+  const size_t pa = (size_t)P * G::NI + (size_t)(G::colour(pi, pj, pk) * G::H + G::entry(pi, pj, pk));
+  double pv = sphi / (double)NC;
+  const int r = row_index<D, N>(Lp, P, G::colour(pi, pj, pk), G::entry(pi, pj, pk));
+  if (r >= 0 && Lp.r_mask[r] == 1) pv = phi_b[Lp.r_pin[r]];
+  Lp.phi[pa] = pv;
+  Lp.rhs[pa] = sq / (double)NC;
+}
+
+// leaf-residual record of a small level: per-CTA partials, folded by k_record_fold
+template <int D, int N>
+__global__ void __launch_bounds__(256) k_record_tab(LevelView L, const double* __restrict__ phi_b,
+                                                   const int4* __restrict__ T, const double* __restrict__ gbc,
+                                                   Rec* __restrict__ partial) {
+  pdl_begin();
+  using G = Geo<D, N>;
+  __shared__ double red[72];
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  double mx = 0, ss = 0, cnt = 0;
+  if (a < L.nb * G::NI) {
+    int code, leaf;
+    double self, p[2 * D];
+    tab_load<D>(L, T, gbc, a, code, leaf, self, p);
+    if (leaf && code > -3) {
+      const double r = resid_value<D>(L, phi_b, code >= 0 ? code : -1, self, p, L.rhs[a]);
+      mx = fabs(r);
+      ss = r * r;
+      cnt = 1;
+    }
+  }
+  mx = block_max(mx, red);
+  ss = block_sum(ss, red);
+  cnt = block_sum(cnt, red);
+  if (threadIdx.x == 0) {
+    partial[blockIdx.x].max = mx;
+    partial[blockIdx.x].sumsq = ss;
+    partial[blockIdx.x].count = (long long)cnt;
+  }
+}
+
+}  // namespace pmgdev
