@@ -299,7 +299,11 @@ struct OpsImpl final : Ops {
       if (d.n_rs > 0 && L.nb > kSmallLevel && !(L.exp & 16384)) {
         // streaming record of every block without coarse-fine faces (special
         // rows excluded), the cut rows from their table and the remaining
-        // blocks by k_record_tile, each into its own partials; folded in order
+        // blocks by k_record_tile, each into its own partials: [0, G) per
+        // streaming CTA, [G, G + gcut) per cut-row CTA, then one per slot of
+        // the remaining blocks; folded in that order
+        constexpr int ST = 2, MINB = 1;
+        const int grid = std::min(d.n_rs, c.sms * MINB);
         const int ncut = d.n_cut[0] + d.n_cut[1];
         const int gcut = ncut > 0 ? (int)grid_for(ncut, 256) : 0;
         const bool fork = d.n_slow > 0 || ncut > 0;
@@ -308,13 +312,11 @@ struct OpsImpl final : Ops {
           PMG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
         }
         if (d.n_slow > 0)
-          pdl_launch(k_record_tile<D, N>, d.n_slow, TT::THREADS, 0, c.side, L, Vc(c, l), c.phi_b.p, c.partial.p, c.rec.p,
-                                                                   nullptr, d.slow_list.p);
+          pdl_launch(k_record_tile<D, N>, d.n_slow, TT::THREADS, 0, c.side, L, Vc(c, l), c.phi_b.p,
+                     c.partial.p + grid + gcut, c.rec.p, (unsigned int*)nullptr, d.slow_list.p);
         if (ncut > 0)
-          pdl_launch(k_record_cut<D>, gcut, 256, 0, c.side, L, c.phi_b.p, d.cut_ent[0].p, d.cut_gbc[0].p, d.n_cut[0],
-                                                     d.cut_ent[1].p, d.cut_gbc[1].p, d.n_cut[1], G::NI,
-                                                     c.partial.p + L.nb);
-        constexpr int ST = 2, MINB = 1;
+          pdl_launch(k_record_cut<D>, gcut, 256, 0, c.side, L, c.phi_b.p, d.cut_ent[0].p, d.cut_gbc[0].p,
+                     d.n_cut[0], d.cut_ent[1].p, d.cut_gbc[1].p, d.n_cut[1], G::NI, c.partial.p + grid);
         constexpr size_t smem = (size_t)ST * RStream3<N>::STAGE * sizeof(double);
         static bool attr = false;
         if (!attr) {
@@ -322,14 +324,14 @@ struct OpsImpl final : Ops {
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
           attr = true;
         }
-        const int grid = std::min(d.n_rs, c.sms * MINB);
-        pdl_launch(k_restrict_stream<N, ST, MINB, true>, grid, RStream3<N>::THR, smem, c.stream, 
-            L, L, c.phi_b.p, (const int4*)d.rs_plan.p, d.n_rs, c.partial.p, c.rec.p, nullptr);
+        pdl_launch(k_restrict_stream<N, ST, MINB, true>, grid, RStream3<N>::THR, smem, c.stream, L, L, c.phi_b.p,
+                   (const int4*)d.rs_plan.p, d.n_rs, c.partial.p, c.rec.p, (unsigned int*)nullptr);
         if (fork) {
           PMG_CUDA(cudaEventRecord(c.ev_join, c.side));
           PMG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
         }
-        pdl_launch(k_record_fold, 1, 256, 0, c.stream, c.partial.p, L.nb + gcut, c.rec.p + L.level);
+        pdl_launch(k_record_fold, 1, 256, 0, c.stream, (const Rec*)c.partial.p,
+                   grid + gcut + (d.n_slow > 0 ? L.nb : 0), c.rec.p + L.level);
         check();
         return;
       }

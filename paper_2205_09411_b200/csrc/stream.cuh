@@ -502,7 +502,6 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
   const int ii = t % HN, jj = (t / HN) % HN, kk = t / (HN * HN);
   const double w = Lf.w;
   double rmx = 0.0, rss = 0.0, rcnt = 0.0;  // RECORD: this CTA's running totals
-  const int first_slot = meta[0][0];
   for (int it = 0; it < nmine; ++it) {
     const int s = it % S_STAGES;
     double* st = sm + s * S::STAGE;
@@ -616,15 +615,8 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
     cp_async_commit();
     pf = pf2;
   }
-  if (RECORD) {  // totals in the first block's entry, zeros in the CTA's others
-    for (int q = 1 + t; q < nmine; q += S::THR) {
-      const int sl = load_plan(plan, blockIdx.x + q * G).slot();
-      partial[sl].max = 0.0;
-      partial[sl].sumsq = 0.0;
-      partial[sl].count = 0;
-    }
-    record_finish(Lf, partial, rec, counter, first_slot, rmx, rss, rcnt, red, &last, (unsigned)nmine);
-  }
+  if (RECORD)  // this CTA's totals, folded with the other partials by k_record_fold
+    record_finish(Lf, partial, rec, nullptr, (int)blockIdx.x, rmx, rss, rcnt, red, &last);
 }
 
 // Parents of the fused restriction that k_restrict_stream cannot finish: a
