@@ -77,6 +77,11 @@ class ClockSampler:
         self.sm, self.max_mhz, self.reasons = [], None, set()
         self._stop = None
         self.proc = None
+        self._nv = None
+        try:  # NVML initialised before the timed region so the first sample is immediate
+            self._nv = self._nvml_handle()
+        except Exception:
+            self._nv = None
 
     def _nvml_handle(self):
         import pynvml
@@ -91,7 +96,9 @@ class ClockSampler:
     def __enter__(self):
         import threading
         try:
-            nv, h = self._nvml_handle()
+            if self._nv is None:
+                raise RuntimeError("no NVML")
+            nv, h = self._nv
             self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
             get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons",
                             getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons", None))
@@ -108,7 +115,7 @@ class ClockSampler:
                         self.reasons.update(n for n, bit in bits.items() if bit and (r & bit))
                     except Exception:
                         pass
-                    self._stop.wait(0.002)
+                    self._stop.wait(0.0005)
 
             self._th = threading.Thread(target=poll, daemon=True)
             self._th.start()
