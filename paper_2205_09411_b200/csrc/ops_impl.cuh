@@ -155,12 +155,12 @@ struct OpsImpl final : Ops {
         constexpr size_t smem = (size_t)ST * RStream3<N>::STAGE * sizeof(double);
         static bool attr = false;
         if (!attr) {
-          PMG_CUDA(cudaFuncSetAttribute(k_restrict_stream<N, ST, MINB, false>,
+          PMG_CUDA(cudaFuncSetAttribute(k_restrict_stream<N, ST, MINB, 0>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
           attr = true;
         }
         const int grid = std::min(d.n_rs, c.sms * MINB);
-        pdl_launch(k_restrict_stream<N, ST, MINB, false>, grid, RStream3<N>::THR, smem, c.stream, 
+        pdl_launch(k_restrict_stream<N, ST, MINB, 0>, grid, RStream3<N>::THR, smem, c.stream, 
             Lf, V(c, l - 1), c.phi_b.p, (const int4*)d.rs_plan.p, d.n_rs, nullptr, nullptr, nullptr);
         if (d.n_rfix > 0)
           pdl_launch(k_restrict_fix<D, N>, grid_for((long long)d.n_rfix * 8, 128), 128, 0, c.stream, 
@@ -195,6 +195,29 @@ struct OpsImpl final : Ops {
   void fas(Ctx& c, int lc, bool f) override {
     const LevelView& L = V(c, lc);
     const unsigned g = grid_for((long long)L.nb * G::NI);
+    if constexpr (D == 3 && N == 16) {
+      const LevelDev& d = *c.lev[(size_t)lc];
+      if (f && L.nb > kSmallLevel && !d.has_cf && d.n_rs == L.nb && !(L.exp & 8192)) {
+        // streaming FAS (the fused-restriction kernel in FAS mode), then the cut rows
+        constexpr int ST = 2, MINB = 1;
+        constexpr size_t smem = (size_t)ST * RStream3<N>::STAGE * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+          PMG_CUDA(cudaFuncSetAttribute(k_restrict_stream<N, ST, MINB, 2>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          attr = true;
+        }
+        const int grid = std::min(d.n_rs, c.sms * MINB);
+        pdl_launch(k_restrict_stream<N, ST, MINB, 2>, grid, RStream3<N>::THR, smem, c.stream, L, L, c.phi_b.p,
+                   (const int4*)d.rs_plan.p, d.n_rs, (Rec*)nullptr, (Rec*)nullptr, (unsigned int*)nullptr);
+        const int ncut = d.n_cut[0] + d.n_cut[1];
+        if (ncut > 0)
+          pdl_launch(k_fas_fix<D, N>, grid_for(ncut, 128), 128, 0, c.stream, L, Vc(c, lc), c.phi_b.p,
+                     (const int32_t*)d.cut_ent[0].p, d.n_cut[0], (const int32_t*)d.cut_ent[1].p, d.n_cut[1]);
+        check();
+        return;
+      }
+    }
     {
       const LevelDev& d = *c.lev[(size_t)lc];
       if (L.nb <= kSmallLevel && d.has_tab && !(L.exp & 98304)) {
@@ -320,11 +343,11 @@ struct OpsImpl final : Ops {
         constexpr size_t smem = (size_t)ST * RStream3<N>::STAGE * sizeof(double);
         static bool attr = false;
         if (!attr) {
-          PMG_CUDA(cudaFuncSetAttribute(k_restrict_stream<N, ST, MINB, true>,
+          PMG_CUDA(cudaFuncSetAttribute(k_restrict_stream<N, ST, MINB, 1>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
           attr = true;
         }
-        pdl_launch(k_restrict_stream<N, ST, MINB, true>, grid, RStream3<N>::THR, smem, c.stream, L, L, c.phi_b.p,
+        pdl_launch(k_restrict_stream<N, ST, MINB, 1>, grid, RStream3<N>::THR, smem, c.stream, L, L, c.phi_b.p,
                    (const int4*)d.rs_plan.p, d.n_rs, c.partial.p, c.rec.p, (unsigned int*)nullptr);
         if (fork) {
           PMG_CUDA(cudaEventRecord(c.ev_join, c.side));

@@ -461,13 +461,14 @@ __device__ __forceinline__ void rs_phys_faces(const LevelView& L, int slot, int 
 // RECORD = true: leaf-residual record of uniform blocks (record_leaf_residual,
 // multigrid.hpp:529-562): per-block max |r|, sum r^2, count into `partial`,
 // the last block folds them in slot order (record_finish).
-template <int N, int S_STAGES, int MINB, bool RECORD>
+template <int N, int S_STAGES, int MINB, int MODE>
 __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(LevelView Lf, LevelView Lp,
                                                                            const double* __restrict__ phi_b,
                                                                            const int4* __restrict__ plan, int n,
                                                                            Rec* __restrict__ partial, Rec* rec,
                                                                            unsigned int* counter) {
   pdl_begin();
+  constexpr bool RECORD = MODE == 1, FASM = MODE == 2;
   using S = RStream3<N>;
   constexpr int NI = N * N * N;
   constexpr int HN = S::HN;
@@ -512,7 +513,7 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
     // RECORD: rows of the 8 children of an interface block, leaf flag;
     // otherwise parent slot / octant -- loads in flight across the wait
     int rr[8];
-    if (RECORD && kind == KIND_IFACE) {
+    if ((RECORD || FASM) && kind == KIND_IFACE) {
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch) {
         const int dx = ch & 1, dy = (ch >> 1) & 1, dz = ch >> 2;
@@ -520,10 +521,10 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
         rr[ch] = Lf.row_of[(size_t)(flags >> 14) * NI + (size_t)((dx + dy + dz) & 1) * S::H + e];
       }
     }
-    const int Pp = RECORD ? 0 : Lf.parent[slot];
-    const int cx = RECORD ? 0 : Lf.coords[slot * 3] & 1, cy = RECORD ? 0 : Lf.coords[slot * 3 + 1] & 1,
-              cz = RECORD ? 0 : Lf.coords[slot * 3 + 2] & 1;
-    const bool leaf = RECORD ? Lf.leaf[slot] != 0 : false;
+    const int Pp = MODE == 0 ? Lf.parent[slot] : 0;
+    const int cx = MODE == 0 ? Lf.coords[slot * 3] & 1 : 0, cy = MODE == 0 ? Lf.coords[slot * 3 + 1] & 1 : 0,
+              cz = MODE == 0 ? Lf.coords[slot * 3 + 2] & 1 : 0;
+    const bool leaf = MODE != 0 ? Lf.leaf[slot] != 0 : false;
     mbar_wait(&full[s], (uint32_t)((it / S_STAGES) & 1));
     cp_async_wait<S_STAGES - 1>();
     __syncthreads();
@@ -541,7 +542,7 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
       f[ch] = P0[((dx + dy + dz) & 1) * S::H + e];
       g[ch] = st[S::OG + ((dx + dy + dz) & 1) * S::H + e];
     }
-    double res[8];
+    double res[8], ap[8];
 #pragma unroll
     for (int ch = 0; ch < 8; ++ch) {
       const int dx = ch & 1, dy = (ch >> 1) & 1, dz = ch >> 2;
@@ -571,9 +572,21 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
       double sres = -2.0 * 3 * f[ch];
 #pragma unroll
       for (int d = 0; d < 6; ++d) sres += p[d];
-      res[ch] = kind == KIND_ALL_INSIDE ? 0.0 : g[ch] - sres * w;
+      ap[ch] = kind == KIND_ALL_INSIDE ? 0.0 : sres * w;  // L(phi), apply_block (stencil.hpp:300-322)
+      res[ch] = kind == KIND_ALL_INSIDE ? 0.0 : g[ch] - ap[ch];
     }
-    if (RECORD) {
+    if (FASM) {  // g = L(phi) + R(r) on non-leaf blocks, OLD <- PHI (multigrid.hpp:380-397)
+      double* __restrict__ rhs = Lf.rhs + (size_t)slot * NI;
+      double* __restrict__ old = Lf.old + (size_t)slot * NI;
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        const int dx = ch & 1, dy = (ch >> 1) & 1, dz = ch >> 2;
+        const size_t a = (size_t)((dx + dy + dz) & 1) * S::H + ii + HN * ((2 * jj + dy) + N * (2 * kk + dz));
+        // special rows of interface blocks: inside rows keep r (0 + r), cut rows by k_fas_fix
+        if (!leaf && (kind != KIND_IFACE || rr[ch] < 0)) rhs[a] = ap[ch] + g[ch];
+        old[a] = f[ch];
+      }
+    } else if (RECORD) {
       if (leaf && kind == KIND_UNIFORM) {
 #pragma unroll
         for (int ch = 0; ch < 8; ++ch) {
@@ -918,6 +931,23 @@ static __global__ void __launch_bounds__(256) k_record_fold(const Rec* __restric
     out->sumsq = ss;
     out->count = (long long)cc;
   }
+}
+
+// FAS right-hand side of the cut rows of the streamed blocks (the k_gs_cut
+// tables of both colours): g = L(phi) + r on non-leaf blocks (multigrid.hpp:388-392)
+template <int D, int N>
+__global__ void __launch_bounds__(128) k_fas_fix(LevelView L, LevelView Lc, const double* __restrict__ phi_b,
+                                                const int32_t* __restrict__ ent0, int n0,
+                                                const int32_t* __restrict__ ent1, int n1) {
+  pdl_begin();
+  using G = Geo<D, N>;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n0 + n1) return;
+  const int a = q < n0 ? ent0[8 * q] : ent1[8 * (q - n0)];
+  const int slot = a / G::NI, ce = a % G::NI;
+  if (L.leaf[slot]) return;
+  const double out = apply_cell<D, N>(L, Lc, phi_b, slot, ce / G::H, ce % G::H);
+  L.rhs[a] = out + L.rhs[a];
 }
 
 }  // namespace pmgdev
