@@ -48,6 +48,18 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def gs_traffic(name):
+    """DRAM bytes per launch of the finest GS kernel from the committed ncu
+    capture (profiles/r01_gs_traffic.json), for the headline config only."""
+    if name != "cfg2":
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_gs_traffic.json")) as f:
+            return float(json.load(f)["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 def vcycle_bytes(mesh, N, dim, nu1=2, nu2=2):
     """Algorithmic bytes of one V-cycle:
     B_V = sum_{l=2..L} [(24(nu1+nu2)+32) n_l + 32 n_l/2^D + 32 n_{l-1}] + 16 sum_l leaf_l."""
@@ -363,9 +375,10 @@ def run_b200(args, case):
                        "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
                        "l2_flush": "none needed: finest phi+rhs = "
                                    f"{2 * 8 * n_fine / 1e6:.0f} MB > 126 MB L2"},
-            "roofline": {"bound": "hbm", "kernel": f"k_gs<{case.dim},{case.N}> finest half-sweep",
+            "roofline": {"bound": "hbm",
+                         "kernel": "finest GS-RB half-sweep (k_gs_stream + concurrent k_gs_cut)",
                          "achieved": gs_gbs, "peak": peak, "unit": "GB/s",
-                         "frac": gs_gbs / peak, "traffic": None,
+                         "frac": gs_gbs / peak, "traffic": gs_traffic(case.name),
                          "bytes_per_launch": gs_bytes, "peak_kind": peak_kind},
             "vcycle_roofline": {"algorithmic_bytes": BV, "achieved": vc_gbs, "peak": peak,
                                 "unit": "GB/s", "frac": vc_gbs / peak,
