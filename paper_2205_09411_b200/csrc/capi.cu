@@ -70,6 +70,7 @@ static void set_views(Ctx& c) {
     v.old = d.old.p;
     v.res = d.res.p;
     v.row_of = d.row_of.p;
+    v.skind = d.skind.p;
     v.r_center = d.r_center.p;
     v.r_nb = d.r_nb.p;
     v.r_bc = d.r_bc.p;
@@ -132,7 +133,7 @@ static void build_cut_tables(Ctx& c) {
   for (int l = 1; l <= m.L; ++l) {
     LevelDev& d = *c.lev[(size_t)l];
     std::vector<int32_t> ent[2];
-    std::vector<double> gbc[2];
+    std::vector<double> gbc[2], coef[2];
     int base = 0;  // row offset of the block within the level's row arrays (upload_stencils order)
     for (int s = 0; s < d.nb && st.valid; ++s) {
       const int id = m.slots[(size_t)l][(size_t)s];
@@ -179,6 +180,21 @@ static void build_cut_tables(Ctx& c) {
           }
           ent[cc].insert(ent[cc].end(), e, e + 8);
           gbc[cc].insert(gbc[cc].end(), gb, gb + 6);
+          // row coefficients, with each cut direction's bc * phi_b product formed
+          // here exactly as the reference forms it (stencil.hpp:344-358)
+          const size_t q = (size_t)(r0 + r);
+          double cf[16] = {st.center[q]};
+          int bm = 0;
+          for (int f = 0; f < F; ++f) {
+            cf[1 + f] = st.nb[q * F + f];
+            const double b = st.bc[q * F + f];
+            if (b != 0) {
+              bm |= 1 << f;
+              cf[7 + f] = b * st.phi_b[(size_t)st.obj[q * F + f]];
+            }
+          }
+          cf[13] = (double)bm;
+          coef[cc].insert(coef[cc].end(), cf, cf + 16);
         }
       base += rc;
     }
@@ -186,6 +202,7 @@ static void build_cut_tables(Ctx& c) {
       d.n_cut[cc] = (int)ent[cc].size() / 8;
       d.cut_ent[cc].upload(ent[cc], c.stream);
       d.cut_gbc[cc].upload(gbc[cc], c.stream);
+      d.cut_coef[cc].upload(coef[cc], c.stream);
     }
   }
 }
@@ -355,6 +372,12 @@ static void upload_stencils(Ctx& c) {
       }
     }
     d.row_of.upload(row_of, c.stream);
+    {  // special-row kind per entry (stream.cuh): 0 uniform, 1 inside, 2 cut
+      std::vector<int8_t> sk(row_of.size(), 0);
+      for (size_t q = 0; q < row_of.size(); ++q)
+        if (row_of[q] >= 0) sk[q] = mask[(size_t)row_of[q]] == PMG_INSIDE ? 1 : 2;
+      d.skind.upload(sk, c.stream);
+    }
     d.r_center.upload(center, c.stream);
     d.r_nb.upload(nbv, c.stream);
     d.r_bc.upload(bcv, c.stream);
@@ -388,8 +411,10 @@ static void upload_stencils(Ctx& c) {
         for (int t = 0; t < HN * HN * HN; ++t) {
           const int ii = t % HN, jj = (t / HN) % HN, kk = t / (HN * HN);
           bool need = false;
-          for (int ch = 0; ch < 8 && !need; ++ch)
-            need = row_at(id, 2 * ii + (ch & 1), 2 * jj + ((ch >> 1) & 1), 2 * kk + (ch >> 2)) >= 0;
+          for (int ch = 0; ch < 8 && !need; ++ch) {  // a cut child (inside children restrict exactly in-stream)
+            const int r = row_at(id, 2 * ii + (ch & 1), 2 * jj + ((ch >> 1) & 1), 2 * kk + (ch >> 2));
+            need = r >= 0 && st.mask[(size_t)r] != PMG_INSIDE;
+          }
           if (need) fx.push_back(s), fx.push_back(t);
         }
       }
@@ -1211,6 +1236,7 @@ int pmg_b200_set_boundary_value(pmg_b200_ctx* h, int obj, double value) {
     c.st.phi_b[(size_t)obj] = value;
     PMG_CUDA(cudaMemcpyAsync(c.phi_b.p + obj, &c.st.phi_b[(size_t)obj], sizeof(double),
                              cudaMemcpyHostToDevice, c.stream));
+    if (c.st.valid) build_cut_tables(c);  // their bc * phi_b products
     PMG_CUDA(cudaStreamSynchronize(c.stream));
   });
 }

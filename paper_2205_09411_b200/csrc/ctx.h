@@ -118,7 +118,7 @@ struct LevelDev {
   DevBuf<int32_t> nbr, cnbr, coords, parent, child, srow, bcoff, cfoff, row_of, slot_id;
   DevBuf<uint8_t> leaf, kind, r_mask;
   DevBuf<double> phi, rhs, old, res, bcval, cfold, r_center, r_nb, r_bc;
-  DevBuf<int8_t> r_obj, r_pin;
+  DevBuf<int8_t> r_obj, r_pin, skind;
   DevBuf<int32_t> ref_slot;  // level_blocks order position -> slot
   // block classes: "fast" = uniform stencil and all 2D faces same-level
   // (served by the lean kernels), "slow" = everything else
@@ -146,6 +146,7 @@ struct LevelDev {
   // k_gs_cut tables per colour: 8 int32 (cell, row, 6 neighbour addresses) + 6 ghost bc values
   DevBuf<int32_t> cut_ent[2];
   DevBuf<double> cut_gbc[2];
+  DevBuf<double> cut_coef[2];  // 16 per cut row: center, nb[6], bc*phi_b[6], bc mask
   int n_cut[2] = {0, 0};
   DevBuf<int32_t> fix_list[2];  // (slot, entry) pairs of special rows in lean interface blocks
   int n_fix[2] = {0, 0};

@@ -61,7 +61,7 @@ struct OpsImpl final : Ops {
         stream = d.n_gs > ((L.exp & 262144) ? 1024 : 0) && !(L.exp & 256);
       const int nfix = stream ? 0 : d.n_fix[parity];
       const bool lean_work = stream || d.n_fast > 0;
-      const int ncut = stream ? d.n_cut[parity] : 0;
+      const int ncut = stream && !(L.exp & (1 << 24)) ? d.n_cut[parity] : 0;  // bit 24: timing experiment
       const bool fork = lean_work && (d.n_slow > 0 || nfix > 0 || ncut > 0);
       if (fork) {
         PMG_CUDA(cudaEventRecord(c.ev_fork, c.stream));
@@ -74,8 +74,8 @@ struct OpsImpl final : Ops {
         pdl_launch(k_gs_fix<D, N>, grid_for(nfix, 128), 128, 0, s2, L, Vc(c, l), c.phi_b.p, parity,
                                                            (const int2*)d.fix_list[parity].p, nfix);
       if (ncut > 0)  // cut rows: disjoint from the streaming kernel's cells and inputs
-        pdl_launch(k_gs_cut<D>, grid_for(ncut, 128), 128, 0, s2, L, c.phi_b.p, d.cut_ent[parity].p,
-                                                        d.cut_gbc[parity].p, ncut);
+        pdl_launch(k_gs_cut<D>, grid_for(ncut, 128), 128, 0, s2, L, (const int32_t*)d.cut_ent[parity].p,
+                   (const double*)d.cut_gbc[parity].p, (const double*)d.cut_coef[parity].p, ncut);
       if (stream) {
         if constexpr (D == 3 && (N == 8 || N == 16)) {
           constexpr int T256 = N == 16 ? 256 : 0;
@@ -162,7 +162,7 @@ struct OpsImpl final : Ops {
         const int grid = std::min(d.n_rs, c.sms * MINB);
         pdl_launch(k_restrict_stream<N, ST, MINB, 0>, grid, RStream3<N>::THR, smem, c.stream, 
             Lf, V(c, l - 1), c.phi_b.p, (const int4*)d.rs_plan.p, d.n_rs, nullptr, nullptr, nullptr);
-        if (d.n_rfix > 0)
+        if (d.n_rfix > 0 && !(Lf.exp & (1 << 25)))
           pdl_launch(k_restrict_fix<D, N>, grid_for((long long)d.n_rfix * 8, 128), 128, 0, c.stream, 
               Lf, Vc(c, l), V(c, l - 1), c.phi_b.p, (const int2*)d.rfix_list.p, d.n_rfix);
         const LevelDev& dp = *c.lev[(size_t)(l - 1)];

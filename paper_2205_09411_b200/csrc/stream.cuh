@@ -510,15 +510,16 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
     if (it + S_STAGES + 1 < nmine) pf2 = load_plan(plan, blockIdx.x + (it + S_STAGES + 1) * G);
     const int slot = meta[s][0], flags = meta[s][1];
     const int kind = flags & 0xff, pmask = (flags >> 8) & 63;
-    // RECORD: rows of the 8 children of an interface block, leaf flag;
-    // otherwise parent slot / octant -- loads in flight across the wait
+    // special-row kinds of the 8 children of an interface block (0 uniform,
+    // 1 inside, 2 cut), leaf flag / parent slot and octant: loads in flight
+    // across the wait
     int rr[8];
-    if ((RECORD || FASM) && kind == KIND_IFACE) {
+    if (kind == KIND_IFACE) {
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch) {
         const int dx = ch & 1, dy = (ch >> 1) & 1, dz = ch >> 2;
         const int e = ii + HN * ((2 * jj + dy) + N * (2 * kk + dz));
-        rr[ch] = Lf.row_of[(size_t)(flags >> 14) * NI + (size_t)((dx + dy + dz) & 1) * S::H + e];
+        rr[ch] = Lf.skind[(size_t)(flags >> 14) * NI + (size_t)((dx + dy + dz) & 1) * S::H + e];
       }
     }
     const int Pp = MODE == 0 ? Lf.parent[slot] : 0;
@@ -573,7 +574,8 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
 #pragma unroll
       for (int d = 0; d < 6; ++d) sres += p[d];
       ap[ch] = kind == KIND_ALL_INSIDE ? 0.0 : sres * w;  // L(phi), apply_block (stencil.hpp:300-322)
-      res[ch] = kind == KIND_ALL_INSIDE ? 0.0 : g[ch] - ap[ch];
+      // inside rows: residual 0; cut rows: parent recomputed by k_restrict_fix
+      res[ch] = (kind == KIND_ALL_INSIDE || (kind == KIND_IFACE && rr[ch] == 1)) ? 0.0 : g[ch] - ap[ch];
     }
     if (FASM) {  // g = L(phi) + R(r) on non-leaf blocks, OLD <- PHI (multigrid.hpp:380-397)
       double* __restrict__ rhs = Lf.rhs + (size_t)slot * NI;
@@ -583,7 +585,7 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
         const int dx = ch & 1, dy = (ch >> 1) & 1, dz = ch >> 2;
         const size_t a = (size_t)((dx + dy + dz) & 1) * S::H + ii + HN * ((2 * jj + dy) + N * (2 * kk + dz));
         // special rows of interface blocks: inside rows keep r (0 + r), cut rows by k_fas_fix
-        if (!leaf && (kind != KIND_IFACE || rr[ch] < 0)) rhs[a] = ap[ch] + g[ch];
+        if (!leaf && (kind != KIND_IFACE || rr[ch] == 0)) rhs[a] = ap[ch] + g[ch];
         old[a] = f[ch];
       }
     } else if (RECORD) {
@@ -597,7 +599,7 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
       } else if (leaf && kind == KIND_IFACE) {  // special rows: inside excluded, cut rows by k_record_cut
 #pragma unroll
         for (int ch = 0; ch < 8; ++ch) {
-          if (rr[ch] >= 0) continue;
+          if (rr[ch] != 0) continue;
           rmx = fmax(rmx, fabs(res[ch]));
           rss += res[ch] * res[ch];
           rcnt += 1.0;
@@ -690,16 +692,25 @@ static __global__ void __launch_bounds__(256) k_pin_list(double* __restrict__ ph
 // -2: Dirichlet ghost 2 bc - f1 with bc in gbc), so a thread needs two
 // dependent round trips.  One thread per cut row of the active colour.
 template <int D>
-__global__ void __launch_bounds__(128) k_gs_cut(LevelView L, const double* __restrict__ phi_b,
-                                               const int32_t* __restrict__ ent, const double* __restrict__ gbc,
+__global__ void __launch_bounds__(128) k_gs_cut(LevelView L, const int32_t* __restrict__ ent,
+                                               const double* __restrict__ gbc, const double* __restrict__ coef,
                                                int n) {
   pdl_begin();
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n) return;
   const int4 e0 = reinterpret_cast<const int4*>(ent)[2 * q];
   const int4 e1 = reinterpret_cast<const int4*>(ent)[2 * q + 1];
-  const int a = e0.x, r = e0.y;
+  const double2* cf2 = reinterpret_cast<const double2*>(coef) + (size_t)q * 8;
+  double cf[14];
+#pragma unroll
+  for (int u = 0; u < 7; ++u) {
+    const double2 v = cf2[u];
+    cf[2 * u] = v.x;
+    cf[2 * u + 1] = v.y;
+  }
+  const int a = e0.x;
   const int na[6] = {e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
+  const int bm = (int)cf[13];
   const double self = L.phi[a];
   double num = L.rhs[a];
   double p[2 * D];
@@ -708,11 +719,10 @@ __global__ void __launch_bounds__(128) k_gs_cut(LevelView L, const double* __res
     p[d] = na[d] >= 0 ? L.phi[na[d]] : (na[d] == -1 ? self : 2.0 * gbc[(size_t)q * 6 + d] - self);
 #pragma unroll
   for (int d = 0; d < 2 * D; ++d) {
-    num -= L.r_nb[r * 2 * D + d] * p[d];
-    const double b = L.r_bc[r * 2 * D + d];
-    if (b != 0) num -= b * phi_b[L.r_obj[r * 2 * D + d]];
+    num -= cf[1 + d] * p[d];
+    if ((bm >> d) & 1) num -= cf[7 + d];
   }
-  L.phi[a] = num / L.r_center[r];
+  L.phi[a] = num / cf[0];
 }
 
 // ------------------------------------------------------------------ prolongation
