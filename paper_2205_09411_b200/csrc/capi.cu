@@ -71,6 +71,7 @@ static void set_views(Ctx& c) {
     v.res = d.res.p;
     v.row_of = d.row_of.p;
     v.skind = d.skind.p;
+    v.r_coef = d.r_coef.p;
     v.r_center = d.r_center.p;
     v.r_nb = d.r_nb.p;
     v.r_bc = d.r_bc.p;
@@ -272,6 +273,122 @@ static void build_small_tables(Ctx& c) {
   }
 }
 
+// One cell's gather entry (small.cuh / stream.cuh fix kernels): e[0] row code
+// (r >= 0 special row r in the level's row arrays, -1 uniform row of a
+// uniform block, -2 uniform row of an interface block, -3 - r inside row r),
+// e[1..2D] the neighbour value addresses (same block or same-level
+// neighbour), -1 Neumann ghost f1, -2 Dirichlet ghost 2 bc - f1 with bc in gb.
+// `base` is the block's first row in the level's row arrays.  Blocks with a
+// coarse-fine face are not supported (callers exclude them).
+static void cell_entry(const Ctx& c, int s, int id, int ii, int base, int32_t* e, double* gb) {
+  const HostMesh& m = c.mesh;
+  const HostStencils& st = c.st;
+  const int N = c.N, D = c.dim, NI = c.NI, H = NI / 2, F = c.F;
+  const int i = ii % N, j = (ii / N) % N, k = D == 3 ? ii / (N * N) : 0;
+  int code = -1;
+  if (st.valid && st.boundary[(size_t)id]) {
+    const int r = st.row_of[(size_t)id * NI + ii];
+    if (r < 0) code = -2;
+    else if (st.mask[(size_t)(st.row_start[(size_t)id] + r)] == PMG_INSIDE) code = -3 - (base + r);
+    else code = base + r;
+  }
+  e[0] = code;
+  for (int f = 0; f < 6; ++f) gb[f] = 0.0;
+  for (int f = 0; f < F; ++f) {
+    const int ax = f / 2, sg = (f & 1) ? 1 : -1;
+    int q[3] = {i, j, k};
+    q[ax] += sg;
+    if (q[ax] >= 0 && q[ax] < N) {
+      e[1 + f] = (int32_t)((size_t)s * NI + cs_addr(q[0] + N * (q[1] + N * q[2]), N, D, H));
+      continue;
+    }
+    const int nid = m.nbr[(size_t)id * 6 + f];
+    if (nid >= 0) {
+      q[ax] = sg > 0 ? 0 : N - 1;
+      e[1 + f] = (int32_t)((size_t)m.slot_of[(size_t)nid] * NI + cs_addr(q[0] + N * (q[1] + N * q[2]), N, D, H));
+      continue;
+    }
+    if (c.bctype[f] == PMG_BC_NEUMANN_ZERO) {
+      e[1 + f] = -1;
+      continue;
+    }
+    e[1 + f] = -2;
+    if (!c.face_off[f].empty() && c.face_off[f][(size_t)id] >= 0) {
+      const int t = D == 2 ? (ax == 0 ? j : i) : (ax == 0 ? j + N * k : ax == 1 ? i + N * k : i + N * j);
+      gb[f] = c.face_vals[f][(size_t)c.face_off[f][(size_t)id] + t];
+    }
+  }
+}
+
+// Per level, per stencil row: center, nb[2D], each cut direction's bc * phi_b
+// product (formed exactly as the reference forms it, stencil.hpp:344-358), the
+// cut-direction mask, an inside flag -- 16 doubles, one 128-B line.
+static void build_row_coef(Ctx& c) {
+  const HostMesh& m = c.mesh;
+  const HostStencils& st = c.st;
+  const int F = c.F;
+  for (int l = 1; l <= m.L; ++l) {
+    LevelDev& d = *c.lev[(size_t)l];
+    std::vector<double> cf;
+    for (int s = 0; s < d.nb && st.valid; ++s) {
+      const int id = m.slots[(size_t)l][(size_t)s];
+      if (!st.boundary[(size_t)id]) continue;
+      const int r0 = st.row_start[(size_t)id], rc = st.row_count[(size_t)id];
+      for (int r = 0; r < rc; ++r) {
+        const size_t q = (size_t)(r0 + r);
+        double e[16] = {st.center[q]};
+        int bm = 0;
+        for (int f = 0; f < F; ++f) {
+          e[1 + f] = st.nb[q * F + f];
+          const double b = st.bc[q * F + f];
+          if (b != 0) {
+            bm |= 1 << f;
+            e[7 + f] = b * st.phi_b[(size_t)st.obj[q * F + f]];
+          }
+        }
+        e[13] = (double)bm;
+        e[14] = st.mask[q] == PMG_INSIDE ? 1.0 : 0.0;
+        cf.insert(cf.end(), e, e + 16);
+      }
+    }
+    d.r_coef.upload(cf, c.stream);
+  }
+}
+
+// k_restrict_fix tables: per listed parent, the gather entries of its 2^D
+// children (e[7] = the child's address), in child order.
+static void build_rfix_tables(Ctx& c) {
+  const HostMesh& m = c.mesh;
+  const int N = c.N, NI = c.NI, H = NI / 2, HN = N / 2;
+  if (c.dim != 3) return;
+  for (int l = 2; l <= m.L; ++l) {
+    LevelDev& d = *c.lev[(size_t)l];
+    const std::vector<int32_t>& host_list = d.rfix_host;
+    std::vector<int32_t> tab((size_t)d.n_rfix * 8 * 8);
+    std::vector<double> gbc((size_t)d.n_rfix * 8 * 6);
+    std::vector<int> base((size_t)d.nb, 0);
+    int acc = 0;
+    for (int s = 0; s < d.nb; ++s) {
+      const int id = m.slots[(size_t)l][(size_t)s];
+      base[(size_t)s] = acc;
+      if (c.st.valid && c.st.boundary[(size_t)id]) acc += c.st.row_count[(size_t)id];
+    }
+    for (int q = 0; q < d.n_rfix; ++q) {
+      const int s = host_list[(size_t)2 * q], t = host_list[(size_t)2 * q + 1];
+      const int id = m.slots[(size_t)l][(size_t)s];
+      const int ii = t % HN, jj = (t / HN) % HN, kk = t / (HN * HN);
+      for (int ch = 0; ch < 8; ++ch) {
+        const int ci = (2 * ii + (ch & 1)) + N * ((2 * jj + ((ch >> 1) & 1)) + N * (2 * kk + (ch >> 2)));
+        int32_t* e = tab.data() + ((size_t)q * 8 + ch) * 8;
+        cell_entry(c, s, id, ci, base[(size_t)s], e, gbc.data() + ((size_t)q * 8 + ch) * 6);
+        e[7] = (int32_t)((size_t)s * NI + cs_addr(ci, N, c.dim, H));
+      }
+    }
+    d.rfix_tab.upload(tab, c.stream);
+    d.rfix_gbc.upload(gbc, c.stream);
+  }
+}
+
 static void upload_stencils(Ctx& c) {
   const HostMesh& m = c.mesh;
   const HostStencils& st = c.st;
@@ -420,6 +537,7 @@ static void upload_stencils(Ctx& c) {
       }
       d.n_rfix = (int)fx.size() / 2;
       d.rfix_list.upload(fx, c.stream);
+      d.rfix_host = fx;
     }
   }
   // streaming prolongation plans (3D): fine blocks that are not entirely
@@ -476,6 +594,8 @@ static void upload_stencils(Ctx& c) {
   c.phi_b.upload(pb, c.stream);
   build_cut_tables(c);
   build_small_tables(c);
+  build_row_coef(c);
+  build_rfix_tables(c);
 }
 
 static void default_stencils(Ctx& c) {
@@ -1002,6 +1122,7 @@ static void set_face_bc(Ctx& c, int dir, int type, const double* values) {
   if (c.st.valid) {
     build_cut_tables(c);
     build_small_tables(c);
+    build_rfix_tables(c);
   }
   set_views(c);
   invalidate_graphs(c);
@@ -1236,7 +1357,10 @@ int pmg_b200_set_boundary_value(pmg_b200_ctx* h, int obj, double value) {
     c.st.phi_b[(size_t)obj] = value;
     PMG_CUDA(cudaMemcpyAsync(c.phi_b.p + obj, &c.st.phi_b[(size_t)obj], sizeof(double),
                              cudaMemcpyHostToDevice, c.stream));
-    if (c.st.valid) build_cut_tables(c);  // their bc * phi_b products
+    if (c.st.valid) {  // their bc * phi_b products
+      build_cut_tables(c);
+      build_row_coef(c);
+    }
     PMG_CUDA(cudaStreamSynchronize(c.stream));
   });
 }

@@ -118,6 +118,7 @@ struct LevelDev {
   DevBuf<int32_t> nbr, cnbr, coords, parent, child, srow, bcoff, cfoff, row_of, slot_id;
   DevBuf<uint8_t> leaf, kind, r_mask;
   DevBuf<double> phi, rhs, old, res, bcval, cfold, r_center, r_nb, r_bc;
+  DevBuf<double> r_coef;  // 16 per row (capi.cu build_row_coef)
   DevBuf<int8_t> r_obj, r_pin, skind;
   DevBuf<int32_t> ref_slot;  // level_blocks order position -> slot
   // block classes: "fast" = uniform stencil and all 2D faces same-level
@@ -136,6 +137,9 @@ struct LevelDev {
   int n_ur = 0;
   DevBuf<int32_t> rfix_list;  // (slot, parent-local index) pairs for k_restrict_fix
   int n_rfix = 0;
+  std::vector<int32_t> rfix_host;
+  DevBuf<int32_t> rfix_tab;   // per listed parent: 2^D child gather entries (capi.cu cell_entry)
+  DevBuf<double> rfix_gbc;
   DevBuf<int32_t> pin_list;   // (cell address, object) of this level's inside rows
   int n_pin = 0;
   DevBuf<int32_t> pp_plan;    // streaming prolongation plan (stream.cuh), -1: level not eligible

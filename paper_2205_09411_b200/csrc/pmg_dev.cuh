@@ -61,6 +61,7 @@ struct LevelView {
   double* res;
   const int32_t* row_of;  // [n_iface * N^D], colour-split entry order; -1 = uniform row
   const int8_t* skind;    // same layout: 0 uniform row, 1 inside row, 2 cut row
+  const double* r_coef;   // [R*16] center, nb[2D], bc*phi_b[2D], cut mask, inside flag
   const double* r_center; // [R]
   const double* r_nb;     // [R*2D]
   const double* r_bc;     // [R*2D]

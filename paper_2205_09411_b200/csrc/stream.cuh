@@ -634,31 +634,67 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
     record_finish(Lf, partial, rec, nullptr, (int)blockIdx.x, rmx, rss, rcnt, red, &last);
 }
 
+// Gather-entry evaluation (capi.cu cell_entry): the cell's value, its 2D
+// neighbour values (physical ghosts 2 bc - f1 / f1) and L(phi) at the cell --
+// uniform row (-2D self + sum p) w, special row center self + sum (nb p [+ bc phi_b])
+// from the level's row-coefficient table, 0 for an inside row -- with the
+// reference's operation order (stencil.hpp:290-359).
+template <int D>
+__device__ __forceinline__ double entry_apply(const LevelView& L, const int4& e0, const int4& e1,
+                                              const double* __restrict__ gb, int a, double& self, bool& inside) {
+  const int code = e0.x;
+  const int na[6] = {e0.y, e0.z, e0.w, e1.x, e1.y, e1.z};
+  self = L.phi[a];
+  double p[2 * D];
+#pragma unroll
+  for (int d = 0; d < 2 * D; ++d) p[d] = na[d] >= 0 ? L.phi[na[d]] : (na[d] == -1 ? self : 2.0 * gb[d] - self);
+  inside = code <= -3;
+  if (inside) return 0.0;
+  if (code < 0) {
+    double s = -2.0 * D * self;
+    for (int d = 0; d < 2 * D; ++d) s += p[d];
+    return s * L.w;
+  }
+  const double2* c2 = reinterpret_cast<const double2*>(L.r_coef) + (size_t)code * 8;
+  double cf[14];
+#pragma unroll
+  for (int u = 0; u < 7; ++u) {
+    const double2 v = c2[u];
+    cf[2 * u] = v.x;
+    cf[2 * u + 1] = v.y;
+  }
+  const int bm = (int)cf[13];
+  double s = cf[0] * self;
+#pragma unroll
+  for (int d = 0; d < 2 * D; ++d) {
+    s += cf[1 + d] * p[d];
+    if ((bm >> d) & 1) s += cf[7 + d];
+  }
+  return s;
+}
+
 // Parents of the fused restriction that k_restrict_stream cannot finish: a
-// child with a special (cut / inside) row in an interface block.  Eight
-// threads per parent, one per child (residual stencil.hpp:325-359 from global
-// memory); lane 0 of the group sums them in the reference's x-fastest order
-// (multigrid.hpp:706-721).  Pinned parents are left to k_pin_list.
+// cut child in an interface block.  Eight threads per parent, one per child,
+// each from its gather entry (two dependent round trips); lane 0 of the group
+// sums them in the reference's x-fastest order (multigrid.hpp:706-721).
+// Pinned parents are left to k_pin_list.
 template <int D, int N>
-__global__ void __launch_bounds__(128) k_restrict_fix(LevelView Lf, LevelView Lfc, LevelView Lp,
-                                                     const double* __restrict__ phi_b,
-                                                     const int2* __restrict__ list, int n) {
+__global__ void __launch_bounds__(128) k_restrict_fix(LevelView Lf, LevelView Lp, const int2* __restrict__ list,
+                                                     const int32_t* __restrict__ tab,
+                                                     const double* __restrict__ gbc, int n) {
   pdl_begin();
   using G = Geo<D, N>;
   constexpr int HN = N / 2, NC = 1 << D;
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
-  const int q = gid / NC, ch = gid % NC;
+  const int q = gid / NC;
   double r = 0.0, f = 0.0;
-  int slot = 0, t = 0;
   if (q < n) {
-    slot = list[q].x;
-    t = list[q].y;
-    const int ii = t % HN, jj = (t / HN) % HN, kk = D == 3 ? t / (HN * HN) : 0;
-    const int i = 2 * ii + (ch & 1), j = 2 * jj + ((ch >> 1) & 1), k = D == 3 ? 2 * kk + (ch >> 2) : 0;
-    const int c = G::colour(i, j, k), e = G::entry(i, j, k);
+    const int4 e0 = reinterpret_cast<const int4*>(tab)[2 * gid];
+    const int4 e1 = reinterpret_cast<const int4*>(tab)[2 * gid + 1];
+    const int a = e1.w;
     bool inside;
-    r = resid_cell<D, N>(Lf, Lfc, phi_b, slot, c, e, &inside);
-    f = Lf.phi[(size_t)slot * G::NI + (size_t)c * G::H + e];
+    const double ap = entry_apply<D>(Lf, e0, e1, gbc + (size_t)gid * 6, a, f, inside);
+    r = inside ? 0.0 : Lf.rhs[a] - ap;
   }
   const int base = threadIdx.x & ~(NC - 1) & 31;
   double sr = 0.0, sf = 0.0;
@@ -667,11 +703,12 @@ __global__ void __launch_bounds__(128) k_restrict_fix(LevelView Lf, LevelView Lf
     sr += __shfl_sync(0xffffffffu, r, base + u);
     sf += __shfl_sync(0xffffffffu, f, base + u);
   }
-  if (q >= n || ch != 0) return;
+  if (q >= n || gid % NC != 0) return;
+  const int slot = list[q].x, t = list[q].y;
   const int ii = t % HN, jj = (t / HN) % HN, kk = D == 3 ? t / (HN * HN) : 0;
   const int P = Lf.parent[slot];
   int cp[3] = {0, 0, 0};
-  for (int a = 0; a < D; ++a) cp[a] = (Lf.coords[slot * D + a] & 1) * HN;
+  for (int a2 = 0; a2 < D; ++a2) cp[a2] = (Lf.coords[slot * D + a2] & 1) * HN;
   const int pi = cp[0] + ii, pj = cp[1] + jj, pk = cp[2] + kk;
   const size_t pa = (size_t)P * G::NI + (size_t)(G::colour(pi, pj, pk) * G::H + G::entry(pi, pj, pk));
   Lp.phi[pa] = sf / (double)NC;
@@ -901,13 +938,12 @@ __global__ void __launch_bounds__(256) k_record_cut(LevelView L, const double* _
     const int4 e1 = reinterpret_cast<const int4*>(ent)[2 * qq + 1];
     const int a = e0.x, r = e0.y;
     if (L.leaf[a / ni]) {
-      const int na[6] = {e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
-      const double self = L.phi[a];
-      double p[2 * D];
-#pragma unroll
-      for (int d = 0; d < 2 * D; ++d)
-        p[d] = na[d] >= 0 ? L.phi[na[d]] : (na[d] == -1 ? self : 2.0 * gbc[(size_t)qq * 6 + d] - self);
-      const double rv = resid_value<D>(L, phi_b, r, self, p, L.rhs[a]);
+      // gather-entry form of this cut row: code r, then its neighbour addresses
+      const int4 f0 = make_int4(r, e0.z, e0.w, e1.x), f1 = make_int4(e1.y, e1.z, e1.w, 0);
+      double self;
+      bool inside;
+      const double ap = entry_apply<D>(L, f0, f1, gbc + (size_t)qq * 6, a, self, inside);
+      const double rv = L.rhs[a] - ap;
       mx = fabs(rv);
       ss = rv * rv;
       cnt = 1.0;
@@ -946,17 +982,25 @@ static __global__ void __launch_bounds__(256) k_record_fold(const Rec* __restric
 // FAS right-hand side of the cut rows of the streamed blocks (the k_gs_cut
 // tables of both colours): g = L(phi) + r on non-leaf blocks (multigrid.hpp:388-392)
 template <int D, int N>
-__global__ void __launch_bounds__(128) k_fas_fix(LevelView L, LevelView Lc, const double* __restrict__ phi_b,
-                                                const int32_t* __restrict__ ent0, int n0,
-                                                const int32_t* __restrict__ ent1, int n1) {
+__global__ void __launch_bounds__(128) k_fas_fix(LevelView L, const int32_t* __restrict__ ent0,
+                                                const double* __restrict__ gbc0, int n0,
+                                                const int32_t* __restrict__ ent1,
+                                                const double* __restrict__ gbc1, int n1) {
   pdl_begin();
   using G = Geo<D, N>;
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n0 + n1) return;
-  const int a = q < n0 ? ent0[8 * q] : ent1[8 * (q - n0)];
-  const int slot = a / G::NI, ce = a % G::NI;
-  if (L.leaf[slot]) return;
-  const double out = apply_cell<D, N>(L, Lc, phi_b, slot, ce / G::H, ce % G::H);
+  const int qq = q < n0 ? q : q - n0;
+  const int32_t* ent = q < n0 ? ent0 : ent1;
+  const double* gbc = q < n0 ? gbc0 : gbc1;
+  const int4 e0 = reinterpret_cast<const int4*>(ent)[2 * qq];
+  const int4 e1 = reinterpret_cast<const int4*>(ent)[2 * qq + 1];
+  const int a = e0.x;
+  if (L.leaf[a / G::NI]) return;
+  const int4 f0 = make_int4(e0.y, e0.z, e0.w, e1.x), f1 = make_int4(e1.y, e1.z, e1.w, 0);
+  double self;
+  bool inside;
+  const double out = entry_apply<D>(L, f0, f1, gbc + (size_t)qq * 6, a, self, inside);
   L.rhs[a] = out + L.rhs[a];
 }
 
