@@ -138,6 +138,23 @@ int pmg_b200_synchronize(pmg_b200_ctx* ctx);
 /* BiCGStab iterations and final relative residual of the most recent coarse
  * solve (KrylovResult, multigrid.hpp:200-204; the reference discards it) */
 int pmg_b200_coarse_info(pmg_b200_ctx* ctx, int32_t* iters, double* rel);
+/* ---- multi-GPU hooks (driven by paper_2205_09411_b200/distributed.py) ----
+ * set_owned: the blocks of `level` this rank computes, one byte per block in
+ * device slot order (Morton order of the block coordinates; NULL = all).  Every
+ * kernel then skips the other blocks; their storage keeps whatever the halo
+ * exchange copies in.
+ * level_field_ptr: device pointer to the level's PHI / RHS / RES / OLD array
+ * (n_blocks * N^D doubles, colour-split block layout) for the exchange.
+ * restrict_only / fas_level: the two halves of restrict_level (multigrid.hpp:374-398)
+ * -- residual + restriction into level-1, then FAS g = L(phi) + r and OLD on `level`.
+ * level_record: record_leaf_residual(level) (:529-562) of the owned blocks:
+ * out3 = {max |r|, sum r^2, count}. */
+int pmg_b200_set_owned(pmg_b200_ctx* ctx, int level, const uint8_t* owned_by_slot);
+void* pmg_b200_level_field_ptr(pmg_b200_ctx* ctx, int var, int level);
+int pmg_b200_restrict_only(pmg_b200_ctx* ctx, int level);
+int pmg_b200_fas_level(pmg_b200_ctx* ctx, int level);
+int pmg_b200_level_record(pmg_b200_ctx* ctx, int level, double* out3);
+
 /* Average device time (CUDA events on pmg_b200_stream) of `reps` back-to-back
  * launches of one phase, after one untimed launch:
  *   op 0: GS-RB half-sweep on `level` (parities alternate)

@@ -68,6 +68,8 @@ EXPORTS = [
     "pmg_b200_set_have_guess", "pmg_b200_coarse_sizes", "pmg_b200_coarse_get",
     "pmg_b200_cycle_kernel_count", "pmg_b200_n_levels", "pmg_b200_level_size",
     "pmg_b200_synchronize", "pmg_b200_time_op", "pmg_b200_coarse_info",
+    "pmg_b200_set_owned", "pmg_b200_level_field_ptr", "pmg_b200_restrict_only", "pmg_b200_fas_level",
+    "pmg_b200_level_record",
 ]
 
 _lib = None
@@ -122,6 +124,12 @@ def load():
     lib.pmg_b200_coarse_get.argtypes = [vp, i32p, i32p, f64p, f64p, f64p, i32p, i32p]
     lib.pmg_b200_time_op.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
     lib.pmg_b200_coarse_info.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_double)]
+    lib.pmg_b200_set_owned.argtypes = [vp, C.c_int, C.c_void_p]
+    lib.pmg_b200_level_field_ptr.argtypes = [vp, C.c_int, C.c_int]
+    lib.pmg_b200_level_field_ptr.restype = C.c_void_p
+    for n in ("pmg_b200_restrict_only", "pmg_b200_fas_level"):
+        getattr(lib, n).argtypes = [vp, C.c_int]
+    lib.pmg_b200_level_record.argtypes = [vp, C.c_int, f64p]
     _lib = lib
     return lib
 

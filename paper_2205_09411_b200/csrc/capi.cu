@@ -71,6 +71,7 @@ static void set_views(Ctx& c) {
     v.res = d.res.p;
     v.row_of = d.row_of.p;
     v.skind = d.skind.p;
+    v.own = d.has_own ? d.own.p : nullptr;
     v.r_coef = d.r_coef.p;
     v.r_center = d.r_center.p;
     v.r_nb = d.r_nb.p;
@@ -100,6 +101,12 @@ static void invalidate_graphs(Ctx& c) {
 static inline int cs_addr(int ii, int N, int dim, int H) {
   const int i = ii % N, j = (ii / N) % N, k = dim == 3 ? ii / (N * N) : 0;
   return ((i + j + k) & 1) * H + (ii >> 1);
+}
+
+// multi-GPU ownership (pmg_b200_set_owned): blocks this rank computes
+static bool own_slot(const Ctx& c, int l, int s) {
+  const auto& o = c.owned;
+  return (size_t)l >= o.size() || o[(size_t)l].empty() || o[(size_t)l][(size_t)s] != 0;
 }
 
 static void upload_bc(Ctx& c) {
@@ -147,7 +154,7 @@ static void build_cut_tables(Ctx& c) {
         const int r = st.row_of[(size_t)id * NI + ii];
         if (r < 0 || st.mask[(size_t)(r0 + r)] != PMG_INSIDE) all_inside = false;
       }
-      if (no_cf && !all_inside)
+      if (no_cf && !all_inside && own_slot(c, l, s))
         for (int ii = 0; ii < NI; ++ii) {
           const int r = st.row_of[(size_t)id * NI + ii];
           if (r < 0 || st.mask[(size_t)(r0 + r)] == PMG_INSIDE) continue;
@@ -437,6 +444,7 @@ static void upload_stencils(Ctx& c) {
     {
       std::vector<int32_t> fast, slow, ufast, uslow, fix[2], gsl, rsl, url;
       for (int s = 0; s < d.nb; ++s) {
+        if (!own_slot(c, l, s)) continue;
         const int id = m.slots[(size_t)l][(size_t)s];
         bool no_cf = true;  // lean kernels handle same-level and physical faces
         for (int f = 0; f < F; ++f)
@@ -515,6 +523,7 @@ static void upload_stencils(Ctx& c) {
       LevelDev& d = *c.lev[(size_t)l];
       std::vector<int32_t> fx;
       for (int s = 0; s < d.nb; ++s) {
+        if (!own_slot(c, l, s)) continue;
         const int id = m.slots[(size_t)l][(size_t)s];
         const int p = m.parent[(size_t)id];
         const int cx = m.coords[(size_t)id * 3] & 1, cy = m.coords[(size_t)id * 3 + 1] & 1,
@@ -548,7 +557,7 @@ static void upload_stencils(Ctx& c) {
       std::vector<int32_t> pp;
       bool ok = true;
       for (int s = 0; s < d.nb && ok; ++s) {
-        if (kindv[(size_t)l][(size_t)s] == pmgdev::KIND_ALL_INSIDE) continue;
+        if (kindv[(size_t)l][(size_t)s] == pmgdev::KIND_ALL_INSIDE || !own_slot(c, l, s)) continue;
         const int id = m.slots[(size_t)l][(size_t)s];
         const int pid = m.parent[(size_t)id];
         int oct = 0, pn[3];
@@ -576,7 +585,7 @@ static void upload_stencils(Ctx& c) {
     if (st.valid)
       for (int s = 0; s < d.nb; ++s) {
         const int id = m.slots[(size_t)l][(size_t)s];
-        if (!st.boundary[(size_t)id]) continue;
+        if (!st.boundary[(size_t)id] || !own_slot(c, l, s)) continue;
         for (int ii = 0; ii < NI; ++ii) {
           const int r = st.row_of[(size_t)id * NI + ii];
           if (r < 0) continue;
@@ -1046,6 +1055,7 @@ static void set_mesh(Ctx& c, int nb, const int32_t* level, const int32_t* coords
     d.coords.upload(crd, c.stream);
     d.parent.upload(par, c.stream);
     d.child.upload(chl, c.stream);
+    d.n_own = d.nb;
     d.leaf.upload(leaf, c.stream);
     d.n_leaf = 0;
     for (uint8_t f : leaf) d.n_leaf += f ? 1 : 0;
@@ -1567,6 +1577,73 @@ int pmg_b200_time_op(pmg_b200_ctx* h, int op, int level, int reps, double* ms_av
     *ms_avg = (double)ms / reps;
   });
 }
+// ---- multi-GPU hooks (paper_2205_09411_b200/distributed.py) ---------------
+int pmg_b200_set_owned(pmg_b200_ctx* h, int level, const uint8_t* owned_by_slot) {
+  return guard(h, [&](Ctx& c) {
+    need_level(c, level, 1);
+    LevelDev& d = *c.lev[(size_t)level];
+    if (c.owned.size() < (size_t)c.mesh.L + 1) c.owned.resize((size_t)c.mesh.L + 1);
+    auto& o = c.owned[(size_t)level];
+    if (owned_by_slot) {
+      o.assign(owned_by_slot, owned_by_slot + d.nb);
+      d.own.upload(o, c.stream);
+      d.has_own = true;
+    } else {
+      o.clear();
+      d.has_own = false;
+    }
+    d.n_own = 0;
+    for (int s = 0; s < d.nb; ++s) d.n_own += own_slot(c, level, s) ? 1 : 0;
+    if (c.st.valid) upload_stencils(c);
+    set_views(c);
+    invalidate_graphs(c);
+    PMG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+void* pmg_b200_level_field_ptr(pmg_b200_ctx* h, int var, int level) {
+  void* out = nullptr;
+  guard(h, [&](Ctx& c) {
+    need_level(c, level, 1);
+    LevelDev& d = *c.lev[(size_t)level];
+    require(var >= 0 && var <= 3, "var must be PHI, RHS, RES or OLD");
+    out = var == 0 ? (void*)d.phi.p : var == 1 ? (void*)d.rhs.p : var == 2 ? (void*)d.res.p : (void*)d.old.p;
+  });
+  return out;
+}
+int pmg_b200_restrict_only(pmg_b200_ctx* h, int level) {
+  return guard(h, [&](Ctx& c) {
+    need_level(c, level, 2);
+    if (c.lev[(size_t)level]->has_cf) {
+      c.ops->residual(c, level);
+      c.ops->restrict_(c, level, pmgdev::RM_RES);
+    } else {
+      c.ops->restrict_(c, level, pmgdev::RM_FUSED);
+    }
+    PMG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+int pmg_b200_fas_level(pmg_b200_ctx* h, int level) {
+  return guard(h, [&](Ctx& c) {
+    need_level(c, level, 1);
+    c.ops->fas(c, level, true);
+    if (c.lev[(size_t)level]->has_cfold) c.ops->cfold(c, level);
+    PMG_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+int pmg_b200_level_record(pmg_b200_ctx* h, int level, double* out3) {
+  return guard(h, [&](Ctx& c) {
+    need_level(c, level, 1);
+    PMG_CUDA(cudaMemsetAsync(c.rec.p + level, 0, sizeof(pmgdev::Rec), c.stream));
+    c.ops->record(c, level);
+    pmgdev::Rec r;
+    PMG_CUDA(cudaMemcpyAsync(&r, c.rec.p + level, sizeof(r), cudaMemcpyDeviceToHost, c.stream));
+    PMG_CUDA(cudaStreamSynchronize(c.stream));
+    out3[0] = r.max;
+    out3[1] = r.sumsq;
+    out3[2] = (double)r.count;
+  });
+}
+
 int pmg_b200_coarse_info(pmg_b200_ctx* h, int32_t* iters, double* rel) {
   return guard(h, [&](Ctx& c) {
     PMG_CUDA(cudaStreamSynchronize(c.stream));

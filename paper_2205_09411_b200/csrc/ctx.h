@@ -115,6 +115,9 @@ struct HostCoarse {
 struct LevelDev {
   int nb = 0;
   int n_leaf = 0;  // leaf blocks (levels without leaves keep a zero record)
+  DevBuf<uint8_t> own;  // multi-GPU ownership mask by slot (pmg_b200_set_owned)
+  bool has_own = false;
+  int n_own = 0;        // blocks this rank computes (nb unless set_owned restricted them)
   DevBuf<int32_t> nbr, cnbr, coords, parent, child, srow, bcoff, cfoff, row_of, slot_id;
   DevBuf<uint8_t> leaf, kind, r_mask;
   DevBuf<double> phi, rhs, old, res, bcval, cfold, r_center, r_nb, r_bc;
@@ -199,6 +202,7 @@ struct Ctx {
   int dim = 3, N = 16, F = 6, NI = 0, S = 0, NT = 0;
   double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
   int device = 0;
+  std::vector<std::vector<uint8_t>> owned;  // per level, by slot (empty: every block)
   int sms = 148;  // multiprocessors of `device`
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // forked branch for concurrent block classes

@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(kThreads) k_gs(LevelView L, LevelView Lc,
   if (t >= (long long)L.nb * G::H) return;
   const int slot = (int)(t / G::H);
   const int e = (int)(t % G::H);
+  if (!owned(L, slot)) return;
   gs_cell<D, N>(L, Lc, phi_b, slot, parity, e);
 }
 
@@ -116,6 +117,7 @@ __global__ void __launch_bounds__(kThreads) k_residual(LevelView L, LevelView Lc
   if (t >= (long long)L.nb * G::NI) return;
   const int slot = (int)(t / G::NI);
   const int ce = (int)(t % G::NI);
+  if (!owned(L, slot)) return;
   bool ins;
   L.res[(size_t)slot * G::NI + ce] =
       resid_cell<D, N>(L, Lc, phi_b, slot, ce / G::H, ce % G::H, &ins);
@@ -143,8 +145,8 @@ __global__ void __launch_bounds__(kThreads) k_restrict(LevelView Lf, LevelView L
   const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long t = gid / NC;
   const int d = (int)(gid % NC);
-  const bool live = t < (long long)Lf.nb * NQ;
-  const int slot = live ? (int)(t / NQ) : 0;
+  const int slot = t < (long long)Lf.nb * NQ ? (int)(t / NQ) : 0;
+  const bool live = t < (long long)Lf.nb * NQ && owned(Lf, slot);
   const int q = live ? (int)(t % NQ) : 0;
   const int qx = q % HN, qy = (q / HN) % HN, qz = D == 3 ? q / (HN * HN) : 0;
   double vphi = 0, vq = 0;
@@ -193,6 +195,7 @@ __global__ void __launch_bounds__(kThreads) k_fas(LevelView L, LevelView Lc,
   if (t >= (long long)L.nb * G::NI) return;
   const int slot = (int)(t / G::NI);
   const int ce = (int)(t % G::NI);
+  if (!owned(L, slot)) return;
   const size_t a = (size_t)slot * G::NI + ce;
   if (FAS && !L.leaf[slot]) {
     const double out = apply_cell<D, N>(L, Lc, phi_b, slot, ce / G::H, ce % G::H);
@@ -213,7 +216,7 @@ __global__ void __launch_bounds__(kThreads) k_cfold(LevelView L, LevelView Lc) {
   const int dir = (int)((t / G::NT) % G::F);
   const int tt = (int)(t % G::NT);
   const int off = L.cfoff[slot * G::F + dir];
-  if (off < 0) return;
+  if (off < 0 || !owned(L, slot)) return;
   const int axis = dir >> 1, side = dir & 1;
   int c3[3] = {0, 0, 0};
   int u = tt;
@@ -237,6 +240,7 @@ __global__ void __launch_bounds__(kThreads) k_prolong(LevelView Lf, LevelView Lp
   const int slot = (int)(t / G::NI);
   const int ce = (int)(t % G::NI);
   const int c = ce / G::H, e = ce % G::H;
+  if (!owned(Lf, slot)) return;
   if (Lf.kind[slot] != KIND_UNIFORM) {
     const int r = Lf.row_of[(size_t)Lf.srow[slot] * G::NI + ce];
     if (r >= 0 && Lf.r_mask[r] == 1) return;  // inside cells are skipped
@@ -280,7 +284,7 @@ __global__ void __launch_bounds__(kThreads) k_pins(LevelView L, const double* __
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long long)L.nb * G::NI) return;
   const int slot = (int)(t / G::NI);
-  if (L.srow[slot] < 0) return;
+  if (L.srow[slot] < 0 || !owned(L, slot)) return;
   const int ce = (int)(t % G::NI);
   const int r = L.row_of[(size_t)L.srow[slot] * G::NI + ce];
   if (r >= 0 && L.r_mask[r] == 1) L.phi[(size_t)slot * G::NI + ce] = phi_b[L.r_pin[r]];
@@ -302,7 +306,7 @@ __global__ void __launch_bounds__(kThreads) k_record(LevelView L, LevelView Lc,
   const int slot = blockIdx.x;
   double mx = 0, ss = 0;
   long long cnt = 0;
-  if (L.leaf[slot]) {
+  if (L.leaf[slot] && owned(L, slot)) {
     for (int ce = threadIdx.x; ce < G::NI; ce += blockDim.x) {
       bool ins;
       const double r = resid_cell<D, N>(L, Lc, phi_b, slot, ce / G::H, ce % G::H, &ins);

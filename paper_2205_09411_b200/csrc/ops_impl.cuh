@@ -150,7 +150,7 @@ struct OpsImpl final : Ops {
     }
     if constexpr (D == 3 && N == 16) {
       const LevelDev& d = *c.lev[(size_t)l];
-      if (mode == RM_FUSED && !d.has_cf && d.n_rs == Lf.nb && !(Lf.exp & 8192)) {
+      if (mode == RM_FUSED && !d.has_cf && d.n_rs == d.n_own && !(Lf.exp & 8192)) {
         constexpr int ST = 2, MINB = 1;
         constexpr size_t smem = (size_t)ST * RStream3<N>::STAGE * sizeof(double);
         static bool attr = false;
@@ -198,7 +198,7 @@ struct OpsImpl final : Ops {
     const unsigned g = grid_for((long long)L.nb * G::NI);
     if constexpr (D == 3 && N == 16) {
       const LevelDev& d = *c.lev[(size_t)lc];
-      if (f && L.nb > kSmallLevel && !d.has_cf && d.n_rs == L.nb && !(L.exp & 8192)) {
+      if (f && L.nb > kSmallLevel && !d.has_cf && d.n_rs == d.n_own && !(L.exp & 8192)) {
         // streaming FAS (the fused-restriction kernel in FAS mode), then the cut rows
         constexpr int ST = 2, MINB = 1;
         constexpr size_t smem = (size_t)ST * RStream3<N>::STAGE * sizeof(double);

@@ -75,7 +75,10 @@ struct LevelView {
   int dense;              // 1: all (2^(l-1))^D blocks present and slot == Morton code
   int nside;              // blocks per axis on this level (dense levels)
   int bczero;             // 1: no Dirichlet face values on this level (all zero)
+  const uint8_t* own;     // multi-GPU: 1 for blocks this rank computes (nullptr: all)
 };
+
+__device__ __forceinline__ bool owned(const LevelView& L, int slot) { return !L.own || L.own[slot]; }
 
 // Morton (Z-order) helpers: on a dense level the slot of a block is the
 // interleave of its coordinates, so face neighbours need no table lookup.

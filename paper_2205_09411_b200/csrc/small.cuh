@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(256) k_gs_tab(LevelView L, const double* __res
   using G = Geo<D, N>;
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= L.nb * G::H) return;
+  if (!owned(L, gid / G::H)) return;
   const int a = (gid / G::H) * G::NI + parity * G::H + gid % G::H;
   int code, leaf;
   double self, p[2 * D];
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(256) k_fas_tab(LevelView L, const double* __re
   pdl_begin();
   using G = Geo<D, N>;
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a >= L.nb * G::NI) return;
+  if (a >= L.nb * G::NI || !owned(L, a / G::NI)) return;
   if (FAS) {
     int code, leaf;
     double self, p[2 * D];
@@ -105,8 +106,9 @@ __global__ void __launch_bounds__(256) k_restrict_tab(LevelView Lf, LevelView Lp
   constexpr int NC = G::NC, NQ = G::NI / NC, HN = N / 2;
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   const int t = gid / NC, d = gid % NC;
-  const bool live = t < Lf.nb * NQ;
-  const int slot = live ? t / NQ : 0, q = live ? t % NQ : 0;
+  const int slot = t < Lf.nb * NQ ? t / NQ : 0;
+  const bool live = t < Lf.nb * NQ && owned(Lf, slot);
+  const int q = live ? t % NQ : 0;
   const int qx = q % HN, qy = (q / HN) % HN, qz = D == 3 ? q / (HN * HN) : 0;
   double vphi = 0, vq = 0;
   if (live) {
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(256) k_record_tab(LevelView L, const double* _
   __shared__ double red[72];
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   double mx = 0, ss = 0, cnt = 0;
-  if (a < L.nb * G::NI) {
+  if (a < L.nb * G::NI && owned(L, a / G::NI)) {
     int code, leaf;
     double self, p[2 * D];
     tab_load<D>(L, T, gbc, a, code, leaf, self, p);

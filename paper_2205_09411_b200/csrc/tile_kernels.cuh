@@ -449,6 +449,7 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_restrict_tile(LevelView
                                                                        LevelView Lp,
                                                                        const double* __restrict__ phi_b) {
   pdl_begin();
+  if (!owned(Lf, blockIdx.x)) return;  // multi-GPU: another rank's block
   using G = Geo<D, N>;
   using TT = Tile<D, N>;
   constexpr int HN = N / 2;
@@ -543,6 +544,7 @@ template <int D, int N, bool FAS>
 __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_fas_tile(LevelView L, LevelView Lc,
                                                                   const double* __restrict__ phi_b) {
   pdl_begin();
+  if (!owned(L, blockIdx.x)) return;  // multi-GPU: another rank's block
   using G = Geo<D, N>;
   using TT = Tile<D, N>;
   using O = Own<D, N>;
@@ -602,6 +604,7 @@ template <int D, int N, bool FULL>
 __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_prolong_tile(LevelView Lf, LevelView Lp,
                                                                       LevelView Lpp) {
   pdl_begin();
+  if (!owned(Lf, blockIdx.x)) return;  // multi-GPU: another rank's block
   using G = Geo<D, N>;
   using O = Own<D, N>;
   constexpr int HN = N / 2;
