@@ -31,7 +31,7 @@ def interior(o, var, dim, N):
     return cfgs.interior_from_padded(o.get_field(var), dim, N)
 
 
-def setup_pair(case, which="ref", gpu_stencils=False, rhs=None, phi=None, mg=None):
+def setup_pair(case, which="ref", gpu_stencils=False, rhs=None, phi=None, mg=None, threads=1):
     """Returns (oracle, DeviceMesh, MgSolver, mesh, stencils) with identical inputs."""
     from paper_2205_09411_b200 import DeviceMesh, MgConfig, MgSolver, StencilBuildConfig
     from paper_2205_09411_b200 import build_stencils as gpu_build
@@ -54,7 +54,7 @@ def setup_pair(case, which="ref", gpu_stencils=False, rhs=None, phi=None, mg=Non
         dev.set_field(VAR_PHI, phi, layout=LAYOUT_INTERIOR)
         o.set_field(VAR_PHI, cfgs.padded_from_interior(phi, case.dim, case.N))
     mgc = mg or MgConfig()
-    o.solver_create(mgc.n_down, mgc.n_up, mgc.coarse_rel_tol, mgc.coarse_max_iters, 1)
+    o.solver_create(mgc.n_down, mgc.n_up, mgc.coarse_rel_tol, mgc.coarse_max_iters, threads)
     sol = MgSolver(dev, st, mgc)
     return o, dev, sol, mesh, st
 
