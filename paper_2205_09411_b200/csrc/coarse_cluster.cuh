@@ -15,6 +15,7 @@
 #include <cooperative_groups.h>
 
 #include "coarse.cuh"
+#include "stream.cuh"  // mbarrier helpers
 
 namespace pmgdev {
 
@@ -103,7 +104,13 @@ __global__ void __launch_bounds__(CC<N, PPC>::THR) k_coarse_cluster(LevelView L,
     bv = L.rhs[a] + C.c0[ii];
     for (int q = C.ob_start[ii]; q < C.ob_start[ii + 1]; ++q) bv += C.ob_val[q] * phi_b[C.ob_obj[q]];
   }
-  // cluster-wide deterministic sum of (a, b): CTA tree, DSMEM broadcast, rank-ordered sum
+  // cluster-wide deterministic sum of (a, b): CTA tree, then each CTA's partial
+  // pushed into every CTA's part[stage][rank] with st.async, completing on the
+  // receiver's per-stage mbarrier (no cluster barrier); rank-ordered sum.
+  // Buffer reuse is safe: a CTA pushes stage k of the next iteration only after
+  // it has received every CTA's later stages of this one.
+  __shared__ __align__(8) uint64_t sbar[K::NSTAGE];
+  unsigned uses = 0;  // bit k: parity of stage k's next phase
   auto csum = [&](int stage, double& va, double& vb) {
     va = warp_sum(va);
     vb = warp_sum(vb);
@@ -111,18 +118,23 @@ __global__ void __launch_bounds__(CC<N, PPC>::THR) k_coarse_cluster(LevelView L,
       wred[wid][0] = va;
       wred[wid][1] = vb;
     }
+    if (t == 0) mbar_arrive_expect_tx(&sbar[stage], K::NC * 16u);
     __syncthreads();
-    if (t < K::NC) {  // thread r broadcasts this CTA's partial to rank r
+    if (t < K::NC) {  // thread r pushes this CTA's partial to rank r
       double sa = 0, sb = 0;
       for (int w = 0; w < K::NW; ++w) {
         sa += wred[w][0];
         sb += wred[w][1];
       }
-      double* dst = cl.map_shared_rank(&part[stage][zr][0], t);
-      dst[0] = sa;
-      dst[1] = sb;
+      uint32_t ra, rb;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(&part[stage][zr][0])), "r"(t));
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(&sbar[stage])), "r"(t));
+      asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(ra),
+                   "d"(sa), "d"(sb), "r"(rb)
+                   : "memory");
     }
-    cl.sync();
+    mbar_wait(&sbar[stage], (uses >> stage) & 1u);
+    uses ^= 1u << stage;
     double sa = 0, sb = 0;
     for (int r = 0; r < K::NC; ++r) {
       sa += part[stage][r][0];
@@ -131,8 +143,12 @@ __global__ void __launch_bounds__(CC<N, PPC>::THR) k_coarse_cluster(LevelView L,
     va = sa;
     vb = sb;
   };
+  if (t == 0) {
+    for (int k = 0; k < K::NSTAGE; ++k) mbar_init(&sbar[k], 1);
+    fence_mbar_init();
+  }
   Gs[pi] = xv;
-  cl.sync();  // every plane of x published
+  cl.sync();  // every plane of x published (and every CTA's stage barriers initialised)
   double r = 0;
   if (unk) r = bv - cc_row<N>(C, Gs, Gm, Gp, f, dg, pi, sc);
   const double r0 = r;
