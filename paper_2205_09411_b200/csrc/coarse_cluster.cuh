@@ -85,8 +85,15 @@ __global__ void __launch_bounds__(CC<N, PPC>::THR) k_coarse_cluster(LevelView L,
   // edge planes, in the neighbouring CTA); out-of-block planes alias our own
   // (coefficient 0)
   double* Gs = Gx[lp];
-  const double* Gm = lp > 0 ? Gx[lp - 1] : (zr > 0 ? cl.map_shared_rank(Gx[PPC - 1], zr - 1) : Gs);
-  const double* Gp = lp < PPC - 1 ? Gx[lp + 1] : (zr < K::NC - 1 ? cl.map_shared_rank(Gx[0], zr + 1) : Gs);
+  // neighbour planes across the CTA's edge planes are pushed here by the
+  // neighbouring CTAs (st.async, completing on gbar): [0] x / p^, [1] s^
+  __shared__ double gh[2][2][K::PP];
+  __shared__ __align__(8) uint64_t gbar[2];
+  const double* Gm0 = lp > 0 ? Gx[lp - 1] : (zr > 0 ? gh[0][0] : Gs);
+  const double* Gp0 = lp < PPC - 1 ? Gx[lp + 1] : (zr < K::NC - 1 ? gh[0][1] : Gs);
+  const double* Gm1 = lp > 0 ? Gx[lp - 1] : (zr > 0 ? gh[1][0] : Gs);
+  const double* Gp1 = lp < PPC - 1 ? Gx[lp + 1] : (zr < K::NC - 1 ? gh[1][1] : Gs);
+  for (int q = t; q < 4 * K::PP; q += K::THR) (&gh[0][0][0])[q] = 0.0;
   for (int q = t; q < PPC * K::PP; q += K::THR) (&Gx[0][0])[q] = 0.0;
   __syncthreads();
   // ---- per-cell data (multigrid.hpp:213-217, 445-453)
@@ -145,12 +152,41 @@ __global__ void __launch_bounds__(CC<N, PPC>::THR) k_coarse_cluster(LevelView L,
   };
   if (t == 0) {
     for (int k = 0; k < K::NSTAGE; ++k) mbar_init(&sbar[k], 1);
+    mbar_init(&gbar[0], 1);
+    mbar_init(&gbar[1], 1);
     fence_mbar_init();
   }
-  Gs[pi] = xv;
-  cl.sync();  // every plane of x published (and every CTA's stage barriers initialised)
+  cl.sync();  // every CTA's barriers initialised, ghost planes zeroed
+  // publish a vector's plane values: own planes in shared memory, edge planes
+  // pushed into the neighbouring CTAs' ghost planes; then wait for ours
+  const uint32_t gbytes = (uint32_t)(((zr > 0) + (zr < K::NC - 1)) * N * N * 8);
+  unsigned guses = 0;
+  auto publish = [&](int k, double val) {
+    Gs[pi] = val;
+    if (t == 0) mbar_arrive_expect_tx(&gbar[k], gbytes);
+    if (lp == 0 && zr > 0) {
+      uint32_t ra, rb;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(&gh[k][1][pi])), "r"(zr - 1));
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(&gbar[k])), "r"(zr - 1));
+      asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(ra), "d"(val),
+                   "r"(rb)
+                   : "memory");
+    }
+    if (lp == PPC - 1 && zr < K::NC - 1) {
+      uint32_t ra, rb;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(&gh[k][0][pi])), "r"(zr + 1));
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(&gbar[k])), "r"(zr + 1));
+      asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(ra), "d"(val),
+                   "r"(rb)
+                   : "memory");
+    }
+    __syncthreads();
+    mbar_wait(&gbar[k], (guses >> k) & 1u);
+    guses ^= 1u << k;
+  };
+  publish(0, xv);  // x planes
   double r = 0;
-  if (unk) r = bv - cc_row<N>(C, Gs, Gm, Gp, f, dg, pi, sc);
+  if (unk) r = bv - cc_row<N>(C, Gs, Gm0, Gp0, f, dg, pi, sc);
   const double r0 = r;
   double n2 = unk ? r * r : 0.0, rho1 = unk ? r0 * r : 0.0;
   csum(0, n2, rho1);
@@ -170,17 +206,15 @@ __global__ void __launch_bounds__(CC<N, PPC>::THR) k_coarse_cluster(LevelView L,
       const double beta = it == 0 ? 0.0 : (rho1 / rho) * (alpha / omega);
       if (unk) p = it == 0 ? r : r + beta * (p - omega * v);
       const double ph = unk ? dinv * p : 0.0;
-      Gs[pi] = ph;
-      cl.sync();  // B1: p^ planes visible
-      v = unk ? cc_row<N>(C, Gs, Gm, Gp, f, dg, pi, sc) : 0.0;
+      publish(0, ph);  // B1: p^ planes
+      v = unk ? cc_row<N>(C, Gs, Gm0, Gp0, f, dg, pi, sc) : 0.0;
       double r0v = unk ? r0 * v : 0.0, dummy = 0;
       csum(1, r0v, dummy);  // B2
       if (r0v == 0) break;
       alpha = rho1 / r0v;
       s = unk ? r - alpha * v : 0.0;
       double ss = s * s;
-      Gs[pi] = unk ? dinv * s : 0.0;  // s^ (neighbours finished reading p^ before B2)
-      const double sh = Gs[pi];
+      const double sh = unk ? dinv * s : 0.0;  // s^
       csum(2, ss, dummy);  // B3: also publishes s^
       const double ns = sqrt(ss);
       if (ns <= target) {
@@ -190,7 +224,8 @@ __global__ void __launch_bounds__(CC<N, PPC>::THR) k_coarse_cluster(LevelView L,
         rel = ns / norm0;
         break;
       }
-      tv = unk ? cc_row<N>(C, Gs, Gm, Gp, f, dg, pi, sc) : 0.0;
+      publish(1, sh);  // s^ planes (everyone finished reading p^ before the last reduction)
+      tv = unk ? cc_row<N>(C, Gs, Gm1, Gp1, f, dg, pi, sc) : 0.0;
       double ts = tv * s, tt = tv * tv;
       csum(3, ts, tt);  // B4
       if (tt == 0) break;
