@@ -164,6 +164,8 @@ int pmg_b200_level_record(pmg_b200_ctx* ctx, int level, double* out3);
  *   op 4: coarse solve
  *   op 5: one V-cycle (graph)        op 6: one FMG cycle (graph, with guess)
  *   op 7: residual+restriction of `level` alone   op 8: FAS/OLD of `level`-1 alone
+ *   op + 100 (ops 0-4, 7, 8): the reps are captured into one CUDA graph and
+ *   replayed, so launch gaps are those inside the cycle graphs
  * Ops 1-8 modify the solution exactly as the solver would. */
 int pmg_b200_time_op(pmg_b200_ctx* ctx, int op, int level, int reps, double* ms_avg);
 

@@ -1546,7 +1546,11 @@ int pmg_b200_level_size(pmg_b200_ctx* h, int level) {
 int pmg_b200_time_op(pmg_b200_ctx* h, int op, int level, int reps, double* ms_avg) {
   return guard(h, [&](Ctx& c) {
     require(c.solver, "solver not created", PMG_ERR_STATE);
-    require(reps >= 1 && op >= 0 && op <= 8, "bad op/reps");
+    // op + 100: the reps are captured into one CUDA graph and replayed (the
+    // in-cycle cost of a small op, launch gaps as inside the cycle graphs)
+    const bool in_graph = op >= 100;
+    if (in_graph) op -= 100;
+    require(reps >= 1 && op >= 0 && op <= 8 && !(in_graph && (op == 5 || op == 6)), "bad op/reps");
     if (op <= 3 || op >= 7) need_level(c, level, op == 0 || op == 3 ? 1 : 2);
     auto one = [&](int k) {
       switch (op) {
@@ -1562,17 +1566,30 @@ int pmg_b200_time_op(pmg_b200_ctx* h, int op, int level, int reps, double* ms_av
       }
     };
     one(0);
+    cudaGraphExec_t gx = nullptr;
+    if (in_graph) {
+      cudaGraph_t gr;
+      PMG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+      for (int k = 0; k < reps; ++k) one(k + 1);
+      PMG_CUDA(cudaStreamEndCapture(c.stream, &gr));
+      PMG_CUDA(cudaGraphInstantiate(&gx, gr, 0));
+      cudaGraphDestroy(gr);
+      PMG_CUDA(cudaGraphLaunch(gx, c.stream));  // warm
+    }
     cudaEvent_t e0, e1;
     PMG_CUDA(cudaEventCreate(&e0));
     PMG_CUDA(cudaEventCreate(&e1));
     PMG_CUDA(cudaEventRecord(e0, c.stream));
-    for (int k = 0; k < reps; ++k) one(k + 1);
+    if (in_graph) PMG_CUDA(cudaGraphLaunch(gx, c.stream));
+    else
+      for (int k = 0; k < reps; ++k) one(k + 1);
     PMG_CUDA(cudaEventRecord(e1, c.stream));
     PMG_CUDA(cudaEventSynchronize(e1));
     float ms = 0;
     PMG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    if (gx) cudaGraphExecDestroy(gx);
     if (op >= 5) c.have_guess = true;
     *ms_avg = (double)ms / reps;
   });

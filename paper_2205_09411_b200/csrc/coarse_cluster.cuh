@@ -6,11 +6,11 @@
 // cell per thread, every per-cell vector lives in registers.  The vectors the SpMV gathers (x, p^,
 // s^) are kept as zero-padded planes in each CTA's shared memory; the z-1 and
 // z+1 values are read from the neighbouring CTAs through distributed shared
-// memory.  Each dot product is reduced inside the CTA, its partial broadcast
-// to every CTA of the cluster by DSMEM stores, and after one cluster barrier
-// every CTA sums the N partials in rank order -- deterministic, and identical
-// in every CTA, so all CTAs take the same branch at every breakdown/stopping
-// test.  Five cluster barriers per iteration.
+// memory.  Each dot product is reduced inside the CTA by one warp, its partial
+// pushed to every CTA of the cluster with st.async onto a per-stage mbarrier,
+// and every CTA sums the N partials in rank order -- deterministic, and
+// identical in every CTA, so all CTAs take the same branch at every
+// breakdown/stopping test.  No cluster barrier inside the iteration loop.
 #pragma once
 #include <cooperative_groups.h>
 
@@ -62,8 +62,12 @@ __device__ __forceinline__ double cc_row(const CoarseFast& C, const double* __re
   return s;
 }
 
+struct D3 {
+  double x, y, z;
+};
+
 template <int N, int PPC>
-__global__ void __launch_bounds__(CC<N, PPC>::THR) k_coarse_cluster(LevelView L, CoarseFast C,
+__global__ void __launch_bounds__(CC<N, PPC>::THR, 1) k_coarse_cluster(LevelView L, CoarseFast C,
                                                                     const double* __restrict__ phi_b,
                                                                     Rec* rec, int* status,
                                                                     double* diag_out) {
@@ -71,9 +75,10 @@ __global__ void __launch_bounds__(CC<N, PPC>::THR) k_coarse_cluster(LevelView L,
   using G = Geo<3, N>;
   using K = CC<N, PPC>;
   cg::cluster_group cl = cg::this_cluster();
-  __shared__ double Gx[PPC][K::PP];             // own planes of the gathered vector
-  __shared__ double part[K::NSTAGE][K::NC][2];  // partials of every CTA, per stage
-  __shared__ double wred[K::NW][2];
+  // own planes of the two gathered vectors: [0] x / p^, [1] s^
+  __shared__ double Gx[2][PPC][K::PP];
+  // partials of every warp of every CTA, per reduction stage
+  __shared__ double part[K::NSTAGE][K::NC * K::NW][2];
   const int zr = (int)cl.block_rank();
   const int t = threadIdx.x;
   const int lane = t & 31, wid = t >> 5;
@@ -81,20 +86,19 @@ __global__ void __launch_bounds__(CC<N, PPC>::THR) k_coarse_cluster(LevelView L,
   const int z = zr * PPC + lp;  // plane of this thread's cell
   const int ii = x + N * (y + N * z);
   const int pi = (x + 1) + (y + 1) * K::P;
-  // own plane and its z-1 / z+1 neighbours (in this CTA or, across the CTA's
-  // edge planes, in the neighbouring CTA); out-of-block planes alias our own
-  // (coefficient 0)
-  double* Gs = Gx[lp];
   // neighbour planes across the CTA's edge planes are pushed here by the
-  // neighbouring CTAs (st.async, completing on gbar): [0] x / p^, [1] s^
+  // neighbouring CTAs (st.async, completing on gbar[k]); out-of-block planes
+  // alias our own (coefficient 0)
   __shared__ double gh[2][2][K::PP];
   __shared__ __align__(8) uint64_t gbar[2];
-  const double* Gm0 = lp > 0 ? Gx[lp - 1] : (zr > 0 ? gh[0][0] : Gs);
-  const double* Gp0 = lp < PPC - 1 ? Gx[lp + 1] : (zr < K::NC - 1 ? gh[0][1] : Gs);
-  const double* Gm1 = lp > 0 ? Gx[lp - 1] : (zr > 0 ? gh[1][0] : Gs);
-  const double* Gp1 = lp < PPC - 1 ? Gx[lp + 1] : (zr < K::NC - 1 ? gh[1][1] : Gs);
+  double* Gs0 = Gx[0][lp];
+  double* Gs1 = Gx[1][lp];
+  const double* Gm0 = lp > 0 ? Gx[0][lp - 1] : (zr > 0 ? gh[0][0] : Gs0);
+  const double* Gp0 = lp < PPC - 1 ? Gx[0][lp + 1] : (zr < K::NC - 1 ? gh[0][1] : Gs0);
+  const double* Gm1 = lp > 0 ? Gx[1][lp - 1] : (zr > 0 ? gh[1][0] : Gs1);
+  const double* Gp1 = lp < PPC - 1 ? Gx[1][lp + 1] : (zr < K::NC - 1 ? gh[1][1] : Gs1);
   for (int q = t; q < 4 * K::PP; q += K::THR) (&gh[0][0][0])[q] = 0.0;
-  for (int q = t; q < PPC * K::PP; q += K::THR) (&Gx[0][0])[q] = 0.0;
+  for (int q = t; q < 2 * PPC * K::PP; q += K::THR) (&Gx[0][0][0])[q] = 0.0;
   __syncthreads();
   // ---- per-cell data (multigrid.hpp:213-217, 445-453)
   const uint8_t f = C.flags[ii];
@@ -111,45 +115,48 @@ __global__ void __launch_bounds__(CC<N, PPC>::THR) k_coarse_cluster(LevelView L,
     bv = L.rhs[a] + C.c0[ii];
     for (int q = C.ob_start[ii]; q < C.ob_start[ii + 1]; ++q) bv += C.ob_val[q] * phi_b[C.ob_obj[q]];
   }
-  // cluster-wide deterministic sum of (a, b): CTA tree, then each CTA's partial
-  // pushed into every CTA's part[stage][rank] with st.async, completing on the
-  // receiver's per-stage mbarrier (no cluster barrier); rank-ordered sum.
-  // Buffer reuse is safe: a CTA pushes stage k of the next iteration only after
-  // it has received every CTA's later stages of this one.
+  // Cluster-wide deterministic sum of (a, b) plus the scalar recurrence that
+  // consumes it, with no CTA or cluster barrier: every warp reduces its pair
+  // (xor butterfly), lane r pushes it into part[stage][rank * NW + warp] of
+  // CTA r with st.async, completing on that CTA's per-stage mbarrier; every
+  // warp of every CTA waits for the NC * NW partials, sums them in one fixed
+  // order (strided per lane, then the butterfly: every lane holds the same
+  // bits) and evaluates the stage's scalars itself.  Identical inputs and
+  // order everywhere, so every warp of every CTA takes the same branch.
+  // Buffer reuse: a CTA pushes stage k of the next iteration only after every
+  // warp of every CTA has pushed the later stages of this one, i.e. after
+  // every warp has read stage k.
   __shared__ __align__(8) uint64_t sbar[K::NSTAGE];
+  constexpr int NP = K::NC * K::NW;
+  static_assert(K::NC <= 32, "one lane per destination CTA");
   unsigned uses = 0;  // bit k: parity of stage k's next phase
-  auto csum = [&](int stage, double& va, double& vb) {
+  auto csum = [&](int stage, double va, double vb, auto&& fn) -> D3 {
     va = warp_sum(va);
     vb = warp_sum(vb);
-    if (lane == 0) {
-      wred[wid][0] = va;
-      wred[wid][1] = vb;
-    }
-    if (t == 0) mbar_arrive_expect_tx(&sbar[stage], K::NC * 16u);
-    __syncthreads();
-    if (t < K::NC) {  // thread r pushes this CTA's partial to rank r
-      double sa = 0, sb = 0;
-      for (int w = 0; w < K::NW; ++w) {
-        sa += wred[w][0];
-        sb += wred[w][1];
-      }
+    if (t == 0) mbar_arrive_expect_tx(&sbar[stage], NP * 16u);
+    if (lane < K::NC) {  // lane r pushes this warp's partial to rank r
       uint32_t ra, rb;
-      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(&part[stage][zr][0])), "r"(t));
-      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(&sbar[stage])), "r"(t));
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                   : "=r"(ra)
+                   : "r"(smem_u32(&part[stage][zr * K::NW + wid][0])), "r"(lane));
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(&sbar[stage])), "r"(lane));
       asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(ra),
-                   "d"(sa), "d"(sb), "r"(rb)
+                   "d"(va), "d"(vb), "r"(rb)
                    : "memory");
     }
     mbar_wait(&sbar[stage], (uses >> stage) & 1u);
     uses ^= 1u << stage;
-    double sa = 0, sb = 0;
-    for (int r = 0; r < K::NC; ++r) {
-      sa += part[stage][r][0];
-      sb += part[stage][r][1];
+    double ta = 0, tb = 0;
+#pragma unroll
+    for (int k = lane; k < NP; k += 32) {
+      ta += part[stage][k][0];
+      tb += part[stage][k][1];
     }
-    va = sa;
-    vb = sb;
+    ta = warp_sum(ta);
+    tb = warp_sum(tb);
+    return fn(ta, tb);
   };
+  static_assert(K::THR % 32 == 0, "whole warps");
   if (t == 0) {
     for (int k = 0; k < K::NSTAGE; ++k) mbar_init(&sbar[k], 1);
     mbar_init(&gbar[0], 1);
@@ -158,11 +165,11 @@ __global__ void __launch_bounds__(CC<N, PPC>::THR) k_coarse_cluster(LevelView L,
   }
   cl.sync();  // every CTA's barriers initialised, ghost planes zeroed
   // publish a vector's plane values: own planes in shared memory, edge planes
-  // pushed into the neighbouring CTAs' ghost planes; then wait for ours
+  // pushed into the neighbouring CTAs' ghost planes (k: which vector)
   const uint32_t gbytes = (uint32_t)(((zr > 0) + (zr < K::NC - 1)) * N * N * 8);
   unsigned guses = 0;
-  auto publish = [&](int k, double val) {
-    Gs[pi] = val;
+  auto push = [&](int k, double val) {
+    (k ? Gs1 : Gs0)[pi] = val;
     if (t == 0) mbar_arrive_expect_tx(&gbar[k], gbytes);
     if (lp == 0 && zr > 0) {
       uint32_t ra, rb;
@@ -180,17 +187,22 @@ __global__ void __launch_bounds__(CC<N, PPC>::THR) k_coarse_cluster(LevelView L,
                    "r"(rb)
                    : "memory");
     }
-    __syncthreads();
-    mbar_wait(&gbar[k], (guses >> k) & 1u);
-    guses ^= 1u << k;
   };
-  publish(0, xv);  // x planes
+  // wait for vector k's ghost planes, then a CTA barrier for the own planes
+  auto land = [&](int k) {
+    if (wid == 0) mbar_wait(&gbar[k], (guses >> k) & 1u);
+    guses ^= 1u << k;
+    __syncthreads();
+  };
+  push(0, xv);  // x planes
+  land(0);
   double r = 0;
-  if (unk) r = bv - cc_row<N>(C, Gs, Gm0, Gp0, f, dg, pi, sc);
+  if (unk) r = bv - cc_row<N>(C, Gs0, Gm0, Gp0, f, dg, pi, sc);
   const double r0 = r;
-  double n2 = unk ? r * r : 0.0, rho1 = unk ? r0 * r : 0.0;
-  csum(0, n2, rho1);
-  const double norm0 = sqrt(n2);
+  // setup: n2 = (r, r), rho1 = (r0, r); norm0 = sqrt(n2)
+  D3 o = csum(0, unk ? r * r : 0.0, unk ? r0 * r : 0.0, [](double a2, double b2) { return D3{a2, b2, sqrt(a2)}; });
+  double rho1 = o.y;
+  const double norm0 = o.z;
   bool converged = false;
   double rel = 1.0;
   int iters = 0;
@@ -200,23 +212,30 @@ __global__ void __launch_bounds__(CC<N, PPC>::THR) k_coarse_cluster(LevelView L,
     rel = 0;
   } else {
     const double target = C.rel_tol * norm0;
-    double rho = 1, alpha = 1, omega = 1;
+    const double rtol = C.rel_tol;
+    double alpha = 1, omega = 1, beta = 0;
     for (int it = 0; it < C.max_iters; ++it) {
       if (rho1 == 0) break;
-      const double beta = it == 0 ? 0.0 : (rho1 / rho) * (alpha / omega);
       if (unk) p = it == 0 ? r : r + beta * (p - omega * v);
       const double ph = unk ? dinv * p : 0.0;
-      publish(0, ph);  // B1: p^ planes
-      v = unk ? cc_row<N>(C, Gs, Gm0, Gp0, f, dg, pi, sc) : 0.0;
-      double r0v = unk ? r0 * v : 0.0, dummy = 0;
-      csum(1, r0v, dummy);  // B2
-      if (r0v == 0) break;
-      alpha = rho1 / r0v;
+      // p^ planes: every warp has passed the last reduction, so nobody in
+      // this CTA or the neighbours still reads the previous p^
+      push(0, ph);
+      land(0);
+      v = unk ? cc_row<N>(C, Gs0, Gm0, Gp0, f, dg, pi, sc) : 0.0;
+      // (r0, v); alpha = rho1 / (r0, v)
+      o = csum(1, unk ? r0 * v : 0.0, 0.0,
+               [rho1](double a2, double) { return D3{a2, a2 == 0 ? 0.0 : rho1 / a2, 0.0}; });
+      if (o.x == 0) break;
+      alpha = o.y;
       s = unk ? r - alpha * v : 0.0;
-      double ss = s * s;
       const double sh = unk ? dinv * s : 0.0;  // s^
-      csum(2, ss, dummy);  // B3: also publishes s^
-      const double ns = sqrt(ss);
+      // s^ planes pushed before ||s|| (s^ of the previous iteration was
+      // consumed before the (r0, v) reduction everyone has passed)
+      push(1, sh);
+      o = csum(2, s * s, 0.0, [](double a2, double) { return D3{sqrt(a2), 0.0, 0.0}; });
+      land(1);  // also before an early exit: no st.async into this CTA in flight
+      const double ns = o.x;
       if (ns <= target) {
         if (unk) xv += alpha * ph;
         converged = true;
@@ -224,27 +243,28 @@ __global__ void __launch_bounds__(CC<N, PPC>::THR) k_coarse_cluster(LevelView L,
         rel = ns / norm0;
         break;
       }
-      publish(1, sh);  // s^ planes (everyone finished reading p^ before the last reduction)
-      tv = unk ? cc_row<N>(C, Gs, Gm1, Gp1, f, dg, pi, sc) : 0.0;
-      double ts = tv * s, tt = tv * tv;
-      csum(3, ts, tt);  // B4
-      if (tt == 0) break;
-      omega = ts / tt;
+      tv = unk ? cc_row<N>(C, Gs1, Gm1, Gp1, f, dg, pi, sc) : 0.0;
+      // (t, s), (t, t); omega = (t, s) / (t, t)
+      o = csum(3, tv * s, tv * tv, [](double a2, double b2) { return D3{b2, b2 == 0 ? 0.0 : a2 / b2, 0.0}; });
+      if (o.x == 0) break;
+      omega = o.y;
       if (unk) {
         xv += alpha * ph + omega * sh;
         r = s - omega * tv;
       }
-      double rr = unk ? r * r : 0.0, r0r = unk ? r0 * r : 0.0;
-      csum(4, rr, r0r);  // B5
-      rho = rho1;
+      // (r, r), (r0, r); rel = ||r|| / ||r0||; the next beta
+      o = csum(4, unk ? r * r : 0.0, unk ? r0 * r : 0.0, [norm0, rho1, alpha, omega](double a2, double b2) {
+        return D3{sqrt(a2) / norm0, b2, (b2 / rho1) * (alpha / omega)};
+      });
       iters = it + 1;
-      rel = sqrt(rr) / norm0;
-      if (rel <= C.rel_tol) {
+      rel = o.x;
+      if (rel <= rtol) {
         converged = true;
         break;
       }
       if (omega == 0) break;
-      rho1 = r0r;
+      rho1 = o.y;
+      beta = o.z;  // (rho1 / rho) * (alpha / omega), multigrid.hpp:236
     }
   }
   const bool wb = converged || C.fallback_ok;

@@ -160,12 +160,22 @@ struct OpsImpl final : Ops {
           attr = true;
         }
         const int grid = std::min(d.n_rs, c.sms * MINB);
-        pdl_launch(k_restrict_stream<N, ST, MINB, 0>, grid, RStream3<N>::THR, smem, c.stream, 
-            Lf, V(c, l - 1), c.phi_b.p, (const int4*)d.rs_plan.p, d.n_rs, nullptr, nullptr, nullptr);
-        if (d.n_rfix > 0 && !(Lf.exp & (1 << 25)))
-          pdl_launch(k_restrict_fix<D, N>, grid_for((long long)d.n_rfix * 8, 128), 128, 0, c.stream, Lf, V(c, l - 1),
+        // parents with a cut child: k_restrict_fix on the forked stream (the
+        // streaming kernel leaves them alone; both only read level l)
+        const bool fix = d.n_rfix > 0 && !(Lf.exp & (1 << 25));
+        if (fix) {
+          PMG_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+          PMG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+          pdl_launch(k_restrict_fix<D, N>, grid_for((long long)d.n_rfix * 8, 128), 128, 0, c.side, Lf, V(c, l - 1),
                      (const int2*)d.rfix_list.p, (const int32_t*)d.rfix_tab.p, (const double*)d.rfix_gbc.p,
                      d.n_rfix);
+        }
+        pdl_launch(k_restrict_stream<N, ST, MINB, 0>, grid, RStream3<N>::THR, smem, c.stream, 
+            Lf, V(c, l - 1), c.phi_b.p, (const int4*)d.rs_plan.p, d.n_rs, nullptr, nullptr, nullptr);
+        if (fix) {
+          PMG_CUDA(cudaEventRecord(c.ev_join, c.side));
+          PMG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
+        }
         const LevelDev& dp = *c.lev[(size_t)(l - 1)];
         if (dp.n_pin > 0)  // apply_pins(l-1)
           pdl_launch(k_pin_list, grid_for(dp.n_pin, 256), 256, 0, c.stream, V(c, l - 1).phi, c.phi_b.p,
@@ -209,13 +219,23 @@ struct OpsImpl final : Ops {
           attr = true;
         }
         const int grid = std::min(d.n_rs, c.sms * MINB);
-        pdl_launch(k_restrict_stream<N, ST, MINB, 2>, grid, RStream3<N>::THR, smem, c.stream, L, L, c.phi_b.p,
-                   (const int4*)d.rs_plan.p, d.n_rs, (Rec*)nullptr, (Rec*)nullptr, (unsigned int*)nullptr);
+        // cut rows on the forked stream: the streaming kernel writes g only at
+        // the other rows (and OLD everywhere), k_fas_fix reads phi and g of
+        // the cut rows and writes g there
         const int ncut = d.n_cut[0] + d.n_cut[1];
-        if (ncut > 0)
-          pdl_launch(k_fas_fix<D, N>, grid_for(ncut, 128), 128, 0, c.stream, L, (const int32_t*)d.cut_ent[0].p,
+        if (ncut > 0) {
+          PMG_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+          PMG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+          pdl_launch(k_fas_fix<D, N>, grid_for(ncut, 128), 128, 0, c.side, L, (const int32_t*)d.cut_ent[0].p,
                      (const double*)d.cut_gbc[0].p, d.n_cut[0], (const int32_t*)d.cut_ent[1].p,
                      (const double*)d.cut_gbc[1].p, d.n_cut[1]);
+        }
+        pdl_launch(k_restrict_stream<N, ST, MINB, 2>, grid, RStream3<N>::THR, smem, c.stream, L, L, c.phi_b.p,
+                   (const int4*)d.rs_plan.p, d.n_rs, (Rec*)nullptr, (Rec*)nullptr, (unsigned int*)nullptr);
+        if (ncut > 0) {
+          PMG_CUDA(cudaEventRecord(c.ev_join, c.side));
+          PMG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
+        }
         check();
         return;
       }

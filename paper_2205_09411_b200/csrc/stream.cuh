@@ -616,8 +616,17 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
     const int pi = cx * HN + ii, pj = cy * HN + jj, pk = cz * HN + kk;
     const int pc = (pi + pj + pk) & 1, pe = (pi + N * (pj + N * pk)) >> 1;
     const size_t pa = (size_t)Pp * NI + (size_t)pc * S::H + pe;
-    Lp.phi[pa] = sf / 8.0;  // pinned parents: k_restrict_fix
-    Lp.rhs[pa] = sr / 8.0;
+    // parents with a cut child belong to k_restrict_fix (running concurrently);
+    // pinned parents are re-pinned by k_pin_list afterwards
+    bool cut = false;
+    if (kind == KIND_IFACE) {
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) cut = cut || rr[ch] == 2;
+    }
+    if (!cut) {
+      Lp.phi[pa] = sf / 8.0;
+      Lp.rhs[pa] = sr / 8.0;
+    }
     }
     __syncthreads();  // stage s consumed
     if (it + S_STAGES < nmine) {
