@@ -114,6 +114,54 @@ struct OpsImpl final : Ops {
                  (const int4*)d.gs_plan.p, d.n_gs);
     }
   }
+  // residual-streaming kernels: k_restrict_stream (one thread per parent) or
+  // k_resid_stream (GS mapping); PMG_EXP bit 26 swaps them (timing comparisons)
+  template <int MODE, int ST, int MINB>
+  void launch_resid_stream(Ctx& c, const LevelView& Lf, const LevelView& Lp, const LevelDev& d, Rec* partial,
+                           Rec* rec) {
+    if constexpr (D == 3 && N == 16) {
+      using Q = QStream3<N>;
+      constexpr size_t smem = ((size_t)ST * Q::STAGE + (MODE == 0 ? 16 * Q::RP : 0)) * sizeof(double);
+      static bool attr = false;
+      if (!attr) {
+        PMG_CUDA(cudaFuncSetAttribute(k_resid_stream<N, ST, MINB, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+        attr = true;
+      }
+      const int grid = std::min(d.n_rs, c.sms * MINB);
+      pdl_launch(k_resid_stream<N, ST, MINB, MODE>, grid, Q::THR, smem, c.stream, Lf, Lp, c.phi_b.p,
+                 (const int4*)d.rs_plan.p, d.n_rs, partial, rec, (unsigned int*)nullptr);
+    }
+  }
+  template <int MODE>
+  void launch_rstream(Ctx& c, const LevelView& Lf, const LevelView& Lp, const LevelDev& d, Rec* partial, Rec* rec) {
+    if constexpr (D == 3 && N == 16) {
+      // restriction (MODE 0): the one-thread-per-parent kernel measured faster
+      // (97 us vs 137 us at 256^3); record / FAS: the GS-mapped kernel
+      if (MODE == 0 ? !(Lf.exp & (1 << 26)) : (Lf.exp & (1 << 26)) != 0) {
+        constexpr int ST = 2, MINB = 1;
+        constexpr size_t smem = (size_t)ST * RStream3<N>::STAGE * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+          PMG_CUDA(cudaFuncSetAttribute(k_restrict_stream<N, ST, MINB, MODE>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          attr = true;
+        }
+        const int grid = std::min(d.n_rs, c.sms * MINB);
+        pdl_launch(k_restrict_stream<N, ST, MINB, MODE>, grid, RStream3<N>::THR, smem, c.stream, Lf, Lp, c.phi_b.p,
+                   (const int4*)d.rs_plan.p, d.n_rs, partial, rec, (unsigned int*)nullptr);
+      } else if (MODE != 0 && !(Lf.exp & (1 << 27))) {
+        launch_resid_stream<MODE, 2, 2>(c, Lf, Lp, d, partial, rec);
+      } else {
+        launch_resid_stream<MODE, 3, 1>(c, Lf, Lp, d, partial, rec);
+      }
+    }
+  }
+  // number of CTAs launch_rstream uses (record partials)
+  int rstream_grid(Ctx& c, const LevelView& Lf, const LevelDev& d) {
+    const int minb = (!(Lf.exp & (1 << 26)) && !(Lf.exp & (1 << 27))) ? 2 : 1;  // MODE 1
+    return std::min(d.n_rs, c.sms * minb);
+  }
   void residual(Ctx& c, int l) override {
     const LevelView& L = V(c, l);
     pdl_launch(k_residual<D, N>, grid_for((long long)L.nb * G::NI), kThreads, 0, c.stream, L, Vc(c, l),
@@ -151,15 +199,6 @@ struct OpsImpl final : Ops {
     if constexpr (D == 3 && N == 16) {
       const LevelDev& d = *c.lev[(size_t)l];
       if (mode == RM_FUSED && !d.has_cf && d.n_rs == d.n_own && !(Lf.exp & 8192)) {
-        constexpr int ST = 2, MINB = 1;
-        constexpr size_t smem = (size_t)ST * RStream3<N>::STAGE * sizeof(double);
-        static bool attr = false;
-        if (!attr) {
-          PMG_CUDA(cudaFuncSetAttribute(k_restrict_stream<N, ST, MINB, 0>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-          attr = true;
-        }
-        const int grid = std::min(d.n_rs, c.sms * MINB);
         // parents with a cut child: k_restrict_fix on the forked stream (the
         // streaming kernel leaves them alone; both only read level l)
         const bool fix = d.n_rfix > 0 && !(Lf.exp & (1 << 25));
@@ -170,8 +209,7 @@ struct OpsImpl final : Ops {
                      (const int2*)d.rfix_list.p, (const int32_t*)d.rfix_tab.p, (const double*)d.rfix_gbc.p,
                      d.n_rfix);
         }
-        pdl_launch(k_restrict_stream<N, ST, MINB, 0>, grid, RStream3<N>::THR, smem, c.stream, 
-            Lf, V(c, l - 1), c.phi_b.p, (const int4*)d.rs_plan.p, d.n_rs, nullptr, nullptr, nullptr);
+        launch_rstream<0>(c, Lf, V(c, l - 1), d, nullptr, nullptr);
         if (fix) {
           PMG_CUDA(cudaEventRecord(c.ev_join, c.side));
           PMG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
@@ -209,16 +247,7 @@ struct OpsImpl final : Ops {
     if constexpr (D == 3 && N == 16) {
       const LevelDev& d = *c.lev[(size_t)lc];
       if (f && L.nb > kSmallLevel && !d.has_cf && d.n_rs == d.n_own && !(L.exp & 8192)) {
-        // streaming FAS (the fused-restriction kernel in FAS mode), then the cut rows
-        constexpr int ST = 2, MINB = 1;
-        constexpr size_t smem = (size_t)ST * RStream3<N>::STAGE * sizeof(double);
-        static bool attr = false;
-        if (!attr) {
-          PMG_CUDA(cudaFuncSetAttribute(k_restrict_stream<N, ST, MINB, 2>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-          attr = true;
-        }
-        const int grid = std::min(d.n_rs, c.sms * MINB);
+        // streaming FAS (the residual kernel in FAS mode) and the cut rows
         // cut rows on the forked stream: the streaming kernel writes g only at
         // the other rows (and OLD everywhere), k_fas_fix reads phi and g of
         // the cut rows and writes g there
@@ -230,8 +259,7 @@ struct OpsImpl final : Ops {
                      (const double*)d.cut_gbc[0].p, d.n_cut[0], (const int32_t*)d.cut_ent[1].p,
                      (const double*)d.cut_gbc[1].p, d.n_cut[1]);
         }
-        pdl_launch(k_restrict_stream<N, ST, MINB, 2>, grid, RStream3<N>::THR, smem, c.stream, L, L, c.phi_b.p,
-                   (const int4*)d.rs_plan.p, d.n_rs, (Rec*)nullptr, (Rec*)nullptr, (unsigned int*)nullptr);
+        launch_rstream<2>(c, L, L, d, nullptr, nullptr);
         if (ncut > 0) {
           PMG_CUDA(cudaEventRecord(c.ev_join, c.side));
           PMG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
@@ -347,8 +375,7 @@ struct OpsImpl final : Ops {
         // blocks by k_record_tile, each into its own partials: [0, G) per
         // streaming CTA, [G, G + gcut) per cut-row CTA, then one per slot of
         // the remaining blocks; folded in that order
-        constexpr int ST = 2, MINB = 1;
-        const int grid = std::min(d.n_rs, c.sms * MINB);
+        const int grid = rstream_grid(c, L, d);
         const int ncut = d.n_cut[0] + d.n_cut[1];
         const int gcut = ncut > 0 ? (int)grid_for(ncut, 256) : 0;
         const bool fork = d.n_slow > 0 || ncut > 0;
@@ -362,15 +389,7 @@ struct OpsImpl final : Ops {
         if (ncut > 0)
           pdl_launch(k_record_cut<D>, gcut, 256, 0, c.side, L, c.phi_b.p, d.cut_ent[0].p, d.cut_gbc[0].p,
                      d.n_cut[0], d.cut_ent[1].p, d.cut_gbc[1].p, d.n_cut[1], G::NI, c.partial.p + grid);
-        constexpr size_t smem = (size_t)ST * RStream3<N>::STAGE * sizeof(double);
-        static bool attr = false;
-        if (!attr) {
-          PMG_CUDA(cudaFuncSetAttribute(k_restrict_stream<N, ST, MINB, 1>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-          attr = true;
-        }
-        pdl_launch(k_restrict_stream<N, ST, MINB, 1>, grid, RStream3<N>::THR, smem, c.stream, L, L, c.phi_b.p,
-                   (const int4*)d.rs_plan.p, d.n_rs, c.partial.p, c.rec.p, (unsigned int*)nullptr);
+        launch_rstream<1>(c, L, L, d, c.partial.p, c.rec.p);
         if (fork) {
           PMG_CUDA(cudaEventRecord(c.ev_join, c.side));
           PMG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));

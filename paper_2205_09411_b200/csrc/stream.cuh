@@ -392,9 +392,8 @@ __device__ __forceinline__ void rs_issue(const LevelView& L, const BlockPlan& P,
   }
 }
 
-template <int N>
+template <int N, class S = RStream3<N>>
 __device__ __forceinline__ void rs_issue_async(const LevelView& L, const BlockPlan& P, double* st) {
-  using S = RStream3<N>;
   constexpr int NI = N * N * N;
   const int t = threadIdx.x;
   const int slot = P.slot();
@@ -420,9 +419,8 @@ __device__ __forceinline__ void rs_issue_async(const LevelView& L, const BlockPl
   }
 }
 
-template <int N>
+template <int N, class S = RStream3<N>>
 __device__ __forceinline__ void rs_phys_faces(const LevelView& L, int slot, int pmask, double* st) {
-  using S = RStream3<N>;
   for (int q = threadIdx.x; q < 2 * N * N + 8 * S::FH; q += blockDim.x) {
     int dir, tj;
     double* h;
@@ -640,6 +638,246 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
     pf = pf2;
   }
   if (RECORD)  // this CTA's totals, folded with the other partials by k_record_fold
+    record_finish(Lf, partial, rec, nullptr, (int)blockIdx.x, rmx, rss, rcnt, red, &last);
+}
+
+// ------------------------------------------------------------------ residual streaming (GS mapping)
+// residual_level + restrict_level, the FAS right-hand side and the leaf
+// record of lean 3D blocks, with the GS kernel's thread mapping: thread t owns
+// the colour-split entries e = t + q*THR of BOTH colours, so every
+// shared-memory access of a warp is a run of consecutive doubles and the
+// neighbour offsets are chosen once per block.  The stage holds both phi
+// halves (one bulk copy) and the face layers of both colours (the RStream3
+// layout without g); g goes straight from global memory into registers, one
+// block ahead.  Per cell r = g - L(phi) with the reference's operation order
+// (stencil.hpp:300-322, 336-358).
+//   MODE 0: residual + restriction (multigrid.hpp:374-398, 697-722): phase 1
+//           stores r and phi child-major (R2[child][parent]) in shared memory,
+//           phase 2 (one thread per parent) folds the 8 children in x-fastest
+//           order.  Parents with a cut child belong to k_restrict_fix.
+//   MODE 1: leaf-residual record (multigrid.hpp:529-562), per-CTA partials.
+//   MODE 2: FAS g = L(phi) + r on non-leaf blocks, OLD <- PHI (:380-397).
+template <int N>
+struct QStream3 {
+  static constexpr int HN = N / 2;
+  static constexpr int H = N * N * N / 2;
+  static constexpr int FH = N * HN;
+  static constexpr int THR = H < 512 ? H : 512;
+  static constexpr int PER = H / THR;
+  static constexpr int KS = THR / FH;     // z-plane step per q
+  static constexpr int NP = HN * HN * HN;  // parents per block
+  // child-major r / phi tiles of MODE 0: the children of a half-warp's
+  // parents differ in the child's x parity, so an odd child's row sits 8
+  // doubles (half a bank sweep) further: conflict-free stores and loads
+  static constexpr int RP = NP + 8;
+  // doubles: P[2][H], hz[2 side][2 colour][FH], hy[2][2][FH], hx[2][N*N]
+  static constexpr int OP = 0, OZ = 2 * H, OY = OZ + 4 * FH, OXF = OY + 4 * FH;
+  static constexpr int STAGE = OXF + 2 * N * N;
+  static constexpr uint32_t TX_BYTES = (uint32_t)(2 * H + 4 * FH) * 8u;
+  static constexpr int YC = 2 * 2 * N * (HN / 2);  // 16-B chunks of the y layers
+};
+
+template <int N>
+__device__ __forceinline__ void qs_issue(const LevelView& L, const BlockPlan& P, double* st, uint64_t* bar) {
+  using S = QStream3<N>;
+  constexpr int NI = N * N * N;
+  const double* own = L.phi + (size_t)P.slot() * NI;
+  mbar_arrive_expect_tx(bar, S::TX_BYTES);
+  bulk_g2s(st + S::OP, own, 2 * S::H * 8, bar);
+  for (int side = 0; side < 2; ++side) {
+    const int ns = P.nbr(4 + side);
+    for (int cc = 0; cc < 2; ++cc) {
+      const double* src = ns >= 0 ? L.phi + (size_t)ns * NI + (size_t)(1 - cc) * S::H + (side ? 0 : (N - 1) * S::FH)
+                                  : own + (size_t)cc * S::H + (side ? (N - 1) * S::FH : 0);
+      bulk_g2s(st + S::OZ + (side * 2 + cc) * S::FH, src, S::FH * 8, bar);
+    }
+  }
+}
+
+template <int N, int S_STAGES, int MINB, int MODE>
+__global__ void __launch_bounds__(QStream3<N>::THR, MINB) k_resid_stream(LevelView Lf, LevelView Lp,
+                                                                        const double* __restrict__ phi_b,
+                                                                        const int4* __restrict__ plan, int n,
+                                                                        Rec* __restrict__ partial, Rec* rec,
+                                                                        unsigned int* counter) {
+  pdl_begin();
+  using S = QStream3<N>;
+  constexpr int NI = N * N * N, HN = S::HN, H = S::H, FH = S::FH, PER = S::PER, KS = S::KS, THR = S::THR;
+  constexpr int NP = S::NP;
+  static_assert(S_STAGES >= 2, "g of block it+1 is read through meta[] one iteration ahead");
+  static_assert(MODE != 0 || NP == THR, "phase 2: one thread per parent");
+  extern __shared__ __align__(128) double sm[];
+  double* const R2 = sm + S_STAGES * S::STAGE;  // MODE 0: r [8][RP], then phi [8][RP]
+  constexpr int RP = S::RP;
+  __shared__ __align__(8) uint64_t full[S_STAGES];
+  __shared__ int meta[S_STAGES][2];
+  __shared__ double red[72];
+  __shared__ bool last;
+  __shared__ int cutp[MODE == 0 ? NP : 1];
+  const int t = threadIdx.x;
+  const int G = gridDim.x;
+  const int nmine = (int)blockIdx.x < n ? (n - 1 - (int)blockIdx.x) / G + 1 : 0;
+  if (nmine == 0) return;
+  if (t == 0) {
+    for (int s = 0; s < S_STAGES; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  if (MODE == 0) cutp[t] = 0;
+  __syncthreads();
+  for (int s = 0; s < S_STAGES; ++s) {
+    if (s < nmine) {
+      const BlockPlan P = load_plan(plan, blockIdx.x + s * G);
+      if (t == 0) {
+        qs_issue<N>(Lf, P, sm + s * S::STAGE, &full[s]);
+        meta[s][0] = P.slot(), meta[s][1] = P.a.y;
+      }
+      rs_issue_async<N, S>(Lf, P, sm + s * S::STAGE);
+    }
+    cp_async_commit();
+  }
+  __syncthreads();  // meta of the first stages
+  BlockPlan pf;
+  if (S_STAGES < nmine) pf = load_plan(plan, blockIdx.x + S_STAGES * G);
+  const int m = t % HN, j = (t / HN) % N, k0 = t / FH;
+  const double w = Lf.w;
+  double gcur[2][PER], gnext[2][PER];
+  {
+    const double* gsrc = Lf.rhs + (size_t)meta[0][0] * NI + t;
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int q = 0; q < PER; ++q) gcur[c][q] = gsrc[c * H + q * THR];
+  }
+  double rmx = 0.0, rss = 0.0, rcnt = 0.0;  // MODE 1: this CTA's running totals
+  for (int it = 0; it < nmine; ++it) {
+    const int s = it % S_STAGES;
+    double* st = sm + s * S::STAGE;
+    BlockPlan pf2;
+    if (it + S_STAGES + 1 < nmine) pf2 = load_plan(plan, blockIdx.x + (it + S_STAGES + 1) * G);
+    const int slot = meta[s][0], flags = meta[s][1];
+    const int kind = flags & 0xff, pmask = (flags >> 8) & 63;
+    // per-block scalars and the special-row kinds, in flight across the wait
+    int rr[2][PER];
+    if (kind == KIND_IFACE) {
+      const int8_t* sk = Lf.skind + (size_t)(flags >> 14) * NI + t;
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int q = 0; q < PER; ++q) rr[c][q] = sk[c * H + q * THR];
+    } else {
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int q = 0; q < PER; ++q) rr[c][q] = 0;
+    }
+    const int Pp = MODE == 0 ? Lf.parent[slot] : 0;
+    const int cx = MODE == 0 ? Lf.coords[slot * 3] & 1 : 0, cy = MODE == 0 ? Lf.coords[slot * 3 + 1] & 1 : 0,
+              cz = MODE == 0 ? Lf.coords[slot * 3 + 2] & 1 : 0;
+    const bool leaf = MODE != 0 ? Lf.leaf[slot] != 0 : false;
+    mbar_wait(&full[s], (uint32_t)((it / S_STAGES) & 1));
+    cp_async_wait<S_STAGES - 1>();
+    __syncthreads();
+    if (it + 1 < nmine) {  // this thread's g of the next block, in flight during this one
+      const double* gsrc = Lf.rhs + (size_t)meta[(it + 1) % S_STAGES][0] * NI + t;
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int q = 0; q < PER; ++q) gnext[c][q] = gsrc[c * H + q * THR];
+    }
+    if (pmask) {  // block-uniform branch
+      rs_phys_faces<N, S>(Lf, slot, pmask, st);
+      __syncthreads();
+    }
+    // ---- phase 1: r at every cell of the block
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int o = (c + j + k0) & 1;  // i = 2m + o (k = k0 + q KS keeps k0's parity)
+      const int OWN = S::OP + c * H, XO = S::OP + (1 - c) * H;
+      const int rb = XO + t;
+      constexpr int DT = THR;  // tile step per q
+      int ixm = rb, dxm = DT, ixp = rb, dxp = DT, iym = rb - HN, dym = DT, iyp = rb + HN, dyp = DT;
+      if (!o) {
+        if (m > 0) ixm = rb - 1;
+        else ixm = S::OXF + k0 * N + j, dxm = KS * N;
+      } else {
+        if (m < HN - 1) ixp = rb + 1;
+        else ixp = S::OXF + N * N + k0 * N + j, dxp = KS * N;
+      }
+      if (j == 0) iym = S::OY + (0 * 2 + c) * FH + k0 * HN + m, dym = KS * HN;
+      if (j == N - 1) iyp = S::OY + (1 * 2 + c) * FH + k0 * HN + m, dyp = KS * HN;
+      const int izm0 = k0 > 0 ? rb - FH : S::OZ + (0 * 2 + c) * FH + j * HN + m;
+      const int izpL = k0 < KS - 1 ? rb + (PER - 1) * DT + FH : S::OZ + (1 * 2 + c) * FH + j * HN + m;
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int k = k0 + q * KS;
+        const double f = st[OWN + t + q * DT];
+        const double p0 = st[ixm + q * dxm], p1 = st[ixp + q * dxp], p2 = st[iym + q * dym],
+                     p3 = st[iyp + q * dyp], p4 = st[q == 0 ? izm0 : rb + q * DT - FH],
+                     p5 = st[q == PER - 1 ? izpL : rb + q * DT + FH];
+        double sres = -2.0 * 3 * f;  // stencil.hpp:300-322, direction order
+        sres += p0;
+        sres += p1;
+        sres += p2;
+        sres += p3;
+        sres += p4;
+        sres += p5;
+        const double ap = kind == KIND_ALL_INSIDE ? 0.0 : sres * w;
+        const double g = gcur[c][q];
+        const int r8 = rr[c][q];
+        const double res = (kind == KIND_ALL_INSIDE || r8 == 1) ? 0.0 : g - ap;
+        if (MODE == 0) {
+          const int ch = o + 2 * (j & 1) + 4 * (k & 1);
+          const int p = m + HN * ((j >> 1) + HN * (k >> 1));
+          R2[ch * RP + p] = res;
+          R2[(8 + ch) * RP + p] = f;
+          if (r8 == 2) cutp[p] = 1;
+        } else if (MODE == 1) {
+          if (leaf && (kind == KIND_UNIFORM || (kind == KIND_IFACE && r8 == 0))) {
+            rmx = fmax(rmx, fabs(res));
+            rss += res * res;
+            rcnt += 1.0;
+          }
+        } else {
+          const size_t a = (size_t)slot * NI + (size_t)c * H + t + q * DT;
+          // special rows of interface blocks: inside rows keep r (0 + r), cut rows by k_fas_fix
+          if (!leaf && (kind != KIND_IFACE || r8 == 0)) Lf.rhs[a] = ap + g;
+          Lf.old[a] = f;
+        }
+      }
+    }
+    __syncthreads();  // stage s consumed
+    if (it + S_STAGES < nmine) {
+      if (t == 0) {
+        qs_issue<N>(Lf, pf, st, &full[s]);
+        meta[s][0] = pf.slot(), meta[s][1] = pf.a.y;
+      }
+      rs_issue_async<N, S>(Lf, pf, st);
+    }
+    cp_async_commit();
+    if (MODE == 0) {  // ---- phase 2: parent t folds its children (multigrid.hpp:706-721)
+      double sr = 0.0, sf = 0.0;
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        sr += R2[ch * RP + t];
+        sf += R2[(8 + ch) * RP + t];
+      }
+      const int cut = cutp[t];
+      cutp[t] = 0;
+      if (!cut) {  // pinned parents: re-pinned by k_pin_list afterwards
+        const int pi = cx * HN + t % HN, pj = cy * HN + (t / HN) % HN, pk = cz * HN + t / (HN * HN);
+        const int pc = (pi + pj + pk) & 1, pe = (pi + N * (pj + N * pk)) >> 1;
+        const size_t pa = (size_t)Pp * NI + (size_t)pc * H + pe;
+        Lp.phi[pa] = sf / 8.0;
+        Lp.rhs[pa] = sr / 8.0;
+      }
+    }
+    pf = pf2;
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int q = 0; q < PER; ++q) gcur[c][q] = gnext[c][q];
+  }
+  if (MODE == 1)  // this CTA's totals, folded with the other partials by k_record_fold
     record_finish(Lf, partial, rec, nullptr, (int)blockIdx.x, rmx, rss, rcnt, red, &last);
 }
 
