@@ -231,12 +231,11 @@ __global__ void __launch_bounds__(kThreads) k_cfold(LevelView L, LevelView Lc) {
 }
 
 // ---------------------------------------------------------------- prolongation
+// fine cell t (t < nb * NI); the body of k_prolong and of the cluster tail (tail.cuh)
 template <int D, int N, bool FULL>
-__global__ void __launch_bounds__(kThreads) k_prolong(LevelView Lf, LevelView Lp, LevelView Lpp) {
-  pdl_begin();
+__device__ __forceinline__ void prolong_cell(const LevelView& Lf, const LevelView& Lp, const LevelView& Lpp,
+                                             long long t) {
   using G = Geo<D, N>;
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long long)Lf.nb * G::NI) return;
   const int slot = (int)(t / G::NI);
   const int ce = (int)(t % G::NI);
   const int c = ce / G::H, e = ce % G::H;
@@ -274,6 +273,15 @@ __global__ void __launch_bounds__(kThreads) k_prolong(LevelView Lf, LevelView Lp
     }
     Lf.phi[fa] += corr;
   }
+}
+
+template <int D, int N, bool FULL>
+__global__ void __launch_bounds__(kThreads) k_prolong(LevelView Lf, LevelView Lp, LevelView Lpp) {
+  pdl_begin();
+  using G = Geo<D, N>;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)Lf.nb * G::NI) return;
+  prolong_cell<D, N, FULL>(Lf, Lp, Lpp, t);
 }
 
 // ---------------------------------------------------------------- pins

@@ -33,15 +33,13 @@ __device__ __forceinline__ void tab_load(const LevelView& L, const int4* __restr
     p[d] = na[d] >= 0 ? L.phi[na[d]] : (na[d] == -1 ? self : 2.0 * gbc[(size_t)a * 6 + d] - self);
 }
 
-// gsrb_block half-sweep (multigrid.hpp:621-695), one thread per cell of the colour
+// gsrb_block half-sweep (multigrid.hpp:621-695) of cell gid of the colour
+// (gid < nb * H): the body of k_gs_tab and of the cluster tail (tail.cuh)
 template <int D, int N>
-__global__ void __launch_bounds__(256) k_gs_tab(LevelView L, const double* __restrict__ phi_b,
-                                               const int4* __restrict__ T, const double* __restrict__ gbc,
-                                               int parity) {
-  pdl_begin();
+__device__ __forceinline__ void gs_tab_cell(const LevelView& L, const double* __restrict__ phi_b,
+                                            const int4* __restrict__ T, const double* __restrict__ gbc, int parity,
+                                            int gid) {
   using G = Geo<D, N>;
-  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= L.nb * G::H) return;
   if (!owned(L, gid / G::H)) return;
   const int a = (gid / G::H) * G::NI + parity * G::H + gid % G::H;
   int code, leaf;
@@ -72,15 +70,24 @@ __global__ void __launch_bounds__(256) k_gs_tab(LevelView L, const double* __res
   L.phi[a] = nv;
 }
 
-// FAS right-hand side g = L(phi) + R(r) on non-leaf blocks, OLD <- PHI
-// (multigrid.hpp:380-397); one thread per cell
-template <int D, int N, bool FAS>
-__global__ void __launch_bounds__(256) k_fas_tab(LevelView L, const double* __restrict__ phi_b,
-                                                const int4* __restrict__ T, const double* __restrict__ gbc) {
+template <int D, int N>
+__global__ void __launch_bounds__(256) k_gs_tab(LevelView L, const double* __restrict__ phi_b,
+                                               const int4* __restrict__ T, const double* __restrict__ gbc,
+                                               int parity) {
   pdl_begin();
   using G = Geo<D, N>;
-  const int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a >= L.nb * G::NI || !owned(L, a / G::NI)) return;
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= L.nb * G::H) return;
+  gs_tab_cell<D, N>(L, phi_b, T, gbc, parity, gid);
+}
+
+// FAS right-hand side g = L(phi) + R(r) on non-leaf blocks, OLD <- PHI
+// (multigrid.hpp:380-397) of cell a (a < nb * NI)
+template <int D, int N, bool FAS>
+__device__ __forceinline__ void fas_tab_cell(const LevelView& L, const double* __restrict__ phi_b,
+                                             const int4* __restrict__ T, const double* __restrict__ gbc, int a) {
+  using G = Geo<D, N>;
+  if (!owned(L, a / G::NI)) return;
   if (FAS) {
     int code, leaf;
     double self, p[2 * D];
@@ -95,16 +102,27 @@ __global__ void __launch_bounds__(256) k_fas_tab(LevelView L, const double* __re
   }
 }
 
-// residual + restriction of a small level (multigrid.hpp:374-418, 697-722):
-// one thread per child cell, the first lane of each 2^D group sums them in
-// x-fastest order, pins the parent (apply_pins(l-1)) and writes it
-template <int D, int N, int MODE>
-__global__ void __launch_bounds__(256) k_restrict_tab(LevelView Lf, LevelView Lp, const double* __restrict__ phi_b,
-                                                     const int4* __restrict__ T, const double* __restrict__ gbc) {
+template <int D, int N, bool FAS>
+__global__ void __launch_bounds__(256) k_fas_tab(LevelView L, const double* __restrict__ phi_b,
+                                                const int4* __restrict__ T, const double* __restrict__ gbc) {
   pdl_begin();
   using G = Geo<D, N>;
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= L.nb * G::NI) return;
+  fas_tab_cell<D, N, FAS>(L, phi_b, T, gbc, a);
+}
+
+// residual + restriction of a small level (multigrid.hpp:374-418, 697-722):
+// one thread per child cell, the first lane of each 2^D group sums them in
+// x-fastest order, pins the parent (apply_pins(l-1)) and writes it.  gid is
+// the child item; every lane of the warp must call it (the group sum is a
+// shuffle), items past the level are idle lanes.
+template <int D, int N, int MODE>
+__device__ __forceinline__ void restrict_tab_item(const LevelView& Lf, const LevelView& Lp,
+                                                  const double* __restrict__ phi_b, const int4* __restrict__ T,
+                                                  const double* __restrict__ gbc, int gid) {
+  using G = Geo<D, N>;
   constexpr int NC = G::NC, NQ = G::NI / NC, HN = N / 2;
-  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   const int t = gid / NC, d = gid % NC;
   const int slot = t < Lf.nb * NQ ? t / NQ : 0;
   const bool live = t < Lf.nb * NQ && owned(Lf, slot);
@@ -144,6 +162,31 @@ __global__ void __launch_bounds__(256) k_restrict_tab(LevelView Lf, LevelView Lp
   Lp.rhs[pa] = sq / (double)NC;
 }
 
+template <int D, int N, int MODE>
+__global__ void __launch_bounds__(256) k_restrict_tab(LevelView Lf, LevelView Lp, const double* __restrict__ phi_b,
+                                                     const int4* __restrict__ T, const double* __restrict__ gbc) {
+  pdl_begin();
+  restrict_tab_item<D, N, MODE>(Lf, Lp, phi_b, T, gbc, blockIdx.x * blockDim.x + threadIdx.x);
+}
+
+// leaf-residual record of cell a of a small level: accumulates into (mx, ss, cnt)
+template <int D, int N>
+__device__ __forceinline__ void record_tab_cell(const LevelView& L, const double* __restrict__ phi_b,
+                                                const int4* __restrict__ T, const double* __restrict__ gbc, int a,
+                                                double& mx, double& ss, double& cnt) {
+  using G = Geo<D, N>;
+  if (!owned(L, a / G::NI)) return;
+  int code, leaf;
+  double self, p[2 * D];
+  tab_load<D>(L, T, gbc, a, code, leaf, self, p);
+  if (leaf && code > -3) {
+    const double r = resid_value<D>(L, phi_b, code >= 0 ? code : -1, self, p, L.rhs[a]);
+    mx = fmax(mx, fabs(r));
+    ss += r * r;
+    cnt += 1;
+  }
+}
+
 // leaf-residual record of a small level: per-CTA partials, folded by k_record_fold
 template <int D, int N>
 __global__ void __launch_bounds__(256) k_record_tab(LevelView L, const double* __restrict__ phi_b,
@@ -154,17 +197,7 @@ __global__ void __launch_bounds__(256) k_record_tab(LevelView L, const double* _
   __shared__ double red[72];
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   double mx = 0, ss = 0, cnt = 0;
-  if (a < L.nb * G::NI && owned(L, a / G::NI)) {
-    int code, leaf;
-    double self, p[2 * D];
-    tab_load<D>(L, T, gbc, a, code, leaf, self, p);
-    if (leaf && code > -3) {
-      const double r = resid_value<D>(L, phi_b, code >= 0 ? code : -1, self, p, L.rhs[a]);
-      mx = fabs(r);
-      ss = r * r;
-      cnt = 1;
-    }
-  }
+  if (a < L.nb * G::NI) record_tab_cell<D, N>(L, phi_b, T, gbc, a, mx, ss, cnt);
   mx = block_max(mx, red);
   ss = block_sum(ss, red);
   cnt = block_sum(cnt, red);

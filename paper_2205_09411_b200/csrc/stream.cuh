@@ -86,6 +86,36 @@ __device__ __forceinline__ BlockPlan load_plan(const int4* plan, int p) {
   return P;
 }
 
+// Plan entries of a persistent streaming kernel, staged through a small
+// shared-memory ring: threads 0-1 load the entry of local block it + PK into
+// registers at iteration it and store it into the ring one iteration later,
+// so no warp ever waits on a plan load (it was the top stall of the
+// streaming loops).  The entry of block b is read at the end of iteration
+// b - S (issue time), after at least one barrier since its store (PK > S).
+template <int S>
+struct PlanRing {
+  static constexpr int PK = S + 2, PR = PK + 1;
+  int4* ring;  // [PR][2] in shared memory
+  int4 held;
+  __device__ __forceinline__ void init(const int4* __restrict__ plan, int nmine, int G) {  // caller syncs
+    const int nb = nmine < PK ? nmine : PK;
+    for (int q = threadIdx.x; q < 2 * nb; q += blockDim.x)
+      ring[((q >> 1) % PR) * 2 + (q & 1)] = __ldg(plan + 2 * ((int)blockIdx.x + (q >> 1) * G) + (q & 1));
+  }
+  __device__ __forceinline__ void advance(const int4* __restrict__ plan, int it, int nmine, int G) {
+    if (threadIdx.x < 2) {
+      if (it >= 1 && it - 1 + PK < nmine) ring[((it - 1 + PK) % PR) * 2 + threadIdx.x] = held;
+      if (it + PK < nmine) held = __ldg(plan + 2 * ((int)blockIdx.x + (it + PK) * G) + threadIdx.x);
+    }
+  }
+  __device__ __forceinline__ BlockPlan get(int b) const {
+    BlockPlan P;
+    P.a = ring[(b % PR) * 2];
+    P.b = ring[(b % PR) * 2 + 1];
+    return P;
+  }
+};
+
 // ------------------------------------------------------------------ stage layout
 template <int N, int TH = 0>
 struct Stream3 {
@@ -232,22 +262,23 @@ __global__ void __launch_bounds__(Stream3<N, TH>::THR, MINB) k_gs_stream(LevelVi
   const int G = gridDim.x;
   const int nmine = (int)blockIdx.x < n ? (n - 1 - (int)blockIdx.x) / G + 1 : 0;
   if (nmine == 0) return;
+  __shared__ int4 pring[PlanRing<S_STAGES>::PR * 2];
+  PlanRing<S_STAGES> R{pring};
   if (t == 0) {
     for (int s = 0; s < S_STAGES; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
+  R.init(plan, nmine, G);
   __syncthreads();
   for (int s = 0; s < S_STAGES; ++s) {
     if (s < nmine) {
-      const BlockPlan P = load_plan(plan, blockIdx.x + s * G);
+      const BlockPlan P = R.get(s);
       if (t == 0) gs_issue<N>(L, P, c, sm + s * S::STAGE, &full[s]);
       if (t == 0) meta[s][0] = P.slot(), meta[s][1] = P.a.y;
       gs_issue_async<N, TH>(L, P, c, sm + s * S::STAGE);
     }
     cp_async_commit();
   }
-  BlockPlan pf;
-  if (S_STAGES < nmine) pf = load_plan(plan, blockIdx.x + S_STAGES * G);
   const double h2 = L.h2;
   static_assert(S_STAGES >= 2, "g of block it+1 is read through meta[] one iteration ahead");
   __syncthreads();  // meta of the first stages
@@ -260,8 +291,7 @@ __global__ void __launch_bounds__(Stream3<N, TH>::THR, MINB) k_gs_stream(LevelVi
   for (int it = 0; it < nmine; ++it) {
     const int s = it % S_STAGES;
     double* st = sm + s * S::STAGE;
-    BlockPlan pf2;
-    if (it + S_STAGES + 1 < nmine) pf2 = load_plan(plan, blockIdx.x + (it + S_STAGES + 1) * G);
+    R.advance(plan, it, nmine, G);
     mbar_wait(&full[s], (uint32_t)((it / S_STAGES) & 1));
     cp_async_wait<S_STAGES - 1>();
     __syncthreads();
@@ -341,12 +371,12 @@ __global__ void __launch_bounds__(Stream3<N, TH>::THR, MINB) k_gs_stream(LevelVi
     }
     __syncthreads();  // stage s consumed
     if (it + S_STAGES < nmine) {
+      const BlockPlan pf = R.get(it + S_STAGES);
       if (t == 0) gs_issue<N>(L, pf, c, st, &full[s]);
       if (t == 0) meta[s][0] = pf.slot(), meta[s][1] = pf.a.y;
       gs_issue_async<N, TH>(L, pf, c, st);
     }
     cp_async_commit();
-    pf = pf2;
 #pragma unroll
     for (int q = 0; q < S::PER; ++q) gcur[q] = gnext[q];
   }
@@ -479,14 +509,17 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
   const int G = gridDim.x;
   const int nmine = (int)blockIdx.x < n ? (n - 1 - (int)blockIdx.x) / G + 1 : 0;
   if (nmine == 0) return;
+  __shared__ int4 pring[PlanRing<S_STAGES>::PR * 2];
+  PlanRing<S_STAGES> R{pring};
   if (t == 0) {
     for (int s = 0; s < S_STAGES; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
+  R.init(plan, nmine, G);
   __syncthreads();
   for (int s = 0; s < S_STAGES; ++s) {
     if (s < nmine) {
-      const BlockPlan P = load_plan(plan, blockIdx.x + s * G);
+      const BlockPlan P = R.get(s);
       if (t == 0) {
         rs_issue<N>(Lf, P, sm + s * S::STAGE, &full[s]);
         meta[s][0] = P.slot(), meta[s][1] = P.a.y;
@@ -496,16 +529,13 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
     cp_async_commit();
   }
   __syncthreads();  // meta of the first stages
-  BlockPlan pf;
-  if (S_STAGES < nmine) pf = load_plan(plan, blockIdx.x + S_STAGES * G);
   const int ii = t % HN, jj = (t / HN) % HN, kk = t / (HN * HN);
   const double w = Lf.w;
   double rmx = 0.0, rss = 0.0, rcnt = 0.0;  // RECORD: this CTA's running totals
   for (int it = 0; it < nmine; ++it) {
     const int s = it % S_STAGES;
     double* st = sm + s * S::STAGE;
-    BlockPlan pf2;
-    if (it + S_STAGES + 1 < nmine) pf2 = load_plan(plan, blockIdx.x + (it + S_STAGES + 1) * G);
+    R.advance(plan, it, nmine, G);
     const int slot = meta[s][0], flags = meta[s][1];
     const int kind = flags & 0xff, pmask = (flags >> 8) & 63;
     // special-row kinds of the 8 children of an interface block (0 uniform,
@@ -628,6 +658,7 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
     }
     __syncthreads();  // stage s consumed
     if (it + S_STAGES < nmine) {
+      const BlockPlan pf = R.get(it + S_STAGES);
       if (t == 0) {
         rs_issue<N>(Lf, pf, st, &full[s]);
         meta[s][0] = pf.slot(), meta[s][1] = pf.a.y;
@@ -635,7 +666,6 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
       rs_issue_async<N>(Lf, pf, st);
     }
     cp_async_commit();
-    pf = pf2;
   }
   if (RECORD)  // this CTA's totals, folded with the other partials by k_record_fold
     record_finish(Lf, partial, rec, nullptr, (int)blockIdx.x, rmx, rss, rcnt, red, &last);
@@ -718,15 +748,18 @@ __global__ void __launch_bounds__(QStream3<N>::THR, MINB) k_resid_stream(LevelVi
   const int G = gridDim.x;
   const int nmine = (int)blockIdx.x < n ? (n - 1 - (int)blockIdx.x) / G + 1 : 0;
   if (nmine == 0) return;
+  __shared__ int4 pring[PlanRing<S_STAGES>::PR * 2];
+  PlanRing<S_STAGES> R{pring};
   if (t == 0) {
     for (int s = 0; s < S_STAGES; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
+  R.init(plan, nmine, G);
   if (MODE == 0) cutp[t] = 0;
   __syncthreads();
   for (int s = 0; s < S_STAGES; ++s) {
     if (s < nmine) {
-      const BlockPlan P = load_plan(plan, blockIdx.x + s * G);
+      const BlockPlan P = R.get(s);
       if (t == 0) {
         qs_issue<N>(Lf, P, sm + s * S::STAGE, &full[s]);
         meta[s][0] = P.slot(), meta[s][1] = P.a.y;
@@ -736,8 +769,6 @@ __global__ void __launch_bounds__(QStream3<N>::THR, MINB) k_resid_stream(LevelVi
     cp_async_commit();
   }
   __syncthreads();  // meta of the first stages
-  BlockPlan pf;
-  if (S_STAGES < nmine) pf = load_plan(plan, blockIdx.x + S_STAGES * G);
   const int m = t % HN, j = (t / HN) % N, k0 = t / FH;
   const double w = Lf.w;
   double gcur[2][PER], gnext[2][PER];
@@ -752,8 +783,7 @@ __global__ void __launch_bounds__(QStream3<N>::THR, MINB) k_resid_stream(LevelVi
   for (int it = 0; it < nmine; ++it) {
     const int s = it % S_STAGES;
     double* st = sm + s * S::STAGE;
-    BlockPlan pf2;
-    if (it + S_STAGES + 1 < nmine) pf2 = load_plan(plan, blockIdx.x + (it + S_STAGES + 1) * G);
+    R.advance(plan, it, nmine, G);
     const int slot = meta[s][0], flags = meta[s][1];
     const int kind = flags & 0xff, pmask = (flags >> 8) & 63;
     // per-block scalars and the special-row kinds, in flight across the wait
@@ -847,6 +877,7 @@ __global__ void __launch_bounds__(QStream3<N>::THR, MINB) k_resid_stream(LevelVi
     }
     __syncthreads();  // stage s consumed
     if (it + S_STAGES < nmine) {
+      const BlockPlan pf = R.get(it + S_STAGES);
       if (t == 0) {
         qs_issue<N>(Lf, pf, st, &full[s]);
         meta[s][0] = pf.slot(), meta[s][1] = pf.a.y;
@@ -871,7 +902,6 @@ __global__ void __launch_bounds__(QStream3<N>::THR, MINB) k_resid_stream(LevelVi
         Lp.rhs[pa] = sr / 8.0;
       }
     }
-    pf = pf2;
 #pragma unroll
     for (int c = 0; c < 2; ++c)
 #pragma unroll
