@@ -244,6 +244,85 @@ __device__ __forceinline__ void gs_phys_faces(const LevelView& L, int slot, int 
   }
 }
 
+// Column mapping of the GS half-sweep: thread t owns the PER consecutive
+// z-planes k = kq*PER + q of entry column (m, j), so the other-colour values at
+// its own entries (the same-entry x neighbour and, one plane up / down, the z
+// neighbours) are loaded once as a column of PER + 2 values: 4.5 shared-memory
+// loads per cell instead of 6.  Warps still read runs of consecutive doubles.
+template <int N, int TH>
+__device__ __forceinline__ int gs_column_base(int t) {
+  using S = Stream3<N, TH>;
+  const int m = t % S::HN, j = (t / S::HN) % N, kq = t / S::FH;
+  return m + S::HN * j + S::FH * S::PER * kq;
+}
+template <int N, int TH>
+__device__ __forceinline__ void gs_stream_column(const LevelView& L, const double* __restrict__ st, int c, int kind,
+                                                 double h2, int slot, const double* gcur) {
+  using S = Stream3<N, TH>;
+  constexpr int NI = N * N * N, HN = S::HN, FH = S::FH, PER = S::PER, KS = S::THR / S::FH;
+  static_assert(PER * KS == N, "columns cover the block");
+  const int t = threadIdx.x;
+  const int m = t % HN, j = (t / HN) % N, kq = t / FH;
+  const int eb = m + HN * j + FH * PER * kq;  // entry of q = 0
+  const int o0 = (c + j + kq * PER) & 1;       // x offset of q = 0; flips with q
+  const int XB = S::OX + eb;
+  // the other x neighbour for o = 0 (x-: e - 1 or the -x face) and o = 1 (x+)
+  const int bx0 = m > 0 ? XB - 1 : S::OXF + kq * PER * N + j, sx0 = m > 0 ? FH : N;
+  const int bx1 = m < HN - 1 ? XB + 1 : S::OXF + N * N + kq * PER * N + j, sx1 = m < HN - 1 ? FH : N;
+  const int bym = j > 0 ? XB - HN : S::OY + kq * PER * HN + m, sym = j > 0 ? FH : HN;
+  const int byp = j < N - 1 ? XB + HN : S::OY + FH + kq * PER * HN + m, syp = j < N - 1 ? FH : HN;
+  double xc[PER + 2];
+  xc[0] = st[kq > 0 ? XB - FH : S::OZ + j * HN + m];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) xc[q + 1] = st[XB + q * FH];
+  xc[PER + 1] = st[kq < KS - 1 ? XB + PER * FH : S::OZ + FH + j * HN + m];
+  double* __restrict__ dst = L.phi + (size_t)slot * NI + (size_t)c * S::H + eb;
+  auto nbrs = [&](int q, double& xm, double& xp, double& ym, double& yp) {
+    const int o = o0 ^ (q & 1);
+    const double xo = st[o ? bx1 + q * sx1 : bx0 + q * sx0];
+    xm = o ? xc[q + 1] : xo;
+    xp = o ? xo : xc[q + 1];
+    ym = st[bym + q * sym];
+    yp = st[byp + q * syp];
+  };
+  if (kind == KIND_UNIFORM) {  // multigrid.hpp:651-653: (sum of 6 - h^2 g) / 6.0
+    double sv[PER], v[PER];
+    bool ok = true;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      double xm, xp, ym, yp;
+      nbrs(q, xm, xp, ym, yp);
+      sv[q] = xm + xp + ym + yp + xc[q] + xc[q + 2] - h2 * gcur[q];
+      v[q] = div6_fast(sv[q]);
+      ok = ok && div6_in_range(sv[q]);
+    }
+    if (!ok) {
+#pragma unroll
+      for (int q = 0; q < PER; ++q) v[q] = div6_slow(sv[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) dst[q * FH] = v[q];
+  } else {  // interface block (multigrid.hpp:665-684)
+    const int32_t* rq = reinterpret_cast<const int32_t*>(st + S::ORQ);
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int r = rq[eb + q * FH];
+      double xm, xp, ym, yp;
+      nbrs(q, xm, xp, ym, yp);
+      if (r < 0) {  // uniform row (:667-672)
+        double sv = -h2 * gcur[q];
+        sv += xm;
+        sv += xp;
+        sv += ym;
+        sv += yp;
+        sv += xc[q];
+        sv += xc[q + 2];
+        dst[q * FH] = -sv * (-1.0 / 6.0);
+      }  // special rows: cut rows by k_gs_cut, inside rows keep their pin
+    }
+  }
+}
+
 // GS-RB half-sweep of the lean 3D blocks (UNIFORM / IFACE blocks without
 // coarse-fine faces, in plan order).  Special rows are left alone: k_gs_cut
 // updates the cut rows afterwards, inside rows keep their pin.
@@ -283,10 +362,13 @@ __global__ void __launch_bounds__(Stream3<N, TH>::THR, MINB) k_gs_stream(LevelVi
   static_assert(S_STAGES >= 2, "g of block it+1 is read through meta[] one iteration ahead");
   __syncthreads();  // meta of the first stages
   double gcur[S::PER], gnext[S::PER];
+  // this thread's entries: e(q) = gbase + q * gstep (column order, or t + q * THR)
+  const int gbase = (L.exp & 4096) ? t : gs_column_base<N, TH>(t);
+  const int gstep = (L.exp & 4096) ? S::THR : S::FH;
   {
-    const double* gsrc = L.rhs + (size_t)meta[0][0] * NI + (size_t)c * S::H + t;
+    const double* gsrc = L.rhs + (size_t)meta[0][0] * NI + (size_t)c * S::H + gbase;
 #pragma unroll
-    for (int q = 0; q < S::PER; ++q) gcur[q] = gsrc[q * S::THR];
+    for (int q = 0; q < S::PER; ++q) gcur[q] = gsrc[q * gstep];
   }
   for (int it = 0; it < nmine; ++it) {
     const int s = it % S_STAGES;
@@ -298,74 +380,78 @@ __global__ void __launch_bounds__(Stream3<N, TH>::THR, MINB) k_gs_stream(LevelVi
     const int slot = meta[s][0], flags = meta[s][1];
     const int kind = flags & 0xff, pmask = (flags >> 8) & 63;
     if (it + 1 < nmine) {  // this thread's g of the next block, in flight during this one
-      const double* gsrc = L.rhs + (size_t)meta[(it + 1) % S_STAGES][0] * NI + (size_t)c * S::H + t;
+      const double* gsrc = L.rhs + (size_t)meta[(it + 1) % S_STAGES][0] * NI + (size_t)c * S::H + gbase;
 #pragma unroll
-      for (int q = 0; q < S::PER; ++q) gnext[q] = gsrc[q * S::THR];
+      for (int q = 0; q < S::PER; ++q) gnext[q] = gsrc[q * gstep];
     }
     if (pmask) {  // block-uniform branch
       gs_phys_faces<N>(L, slot, pmask, c, st);
       __syncthreads();
     }
-    // Thread t owns entries e = t + q*THR: the same (m, j) and colour offset o
-    // for every q, z-plane k = k0 + q*KS.  Neighbour indices into the stage
-    // (own tile or halo layer) are chosen once per block; only the z layers at
-    // q = 0 / PER-1 are per-q choices.
-    constexpr int KS = S::THR / S::FH;
-    const int m = t % S::HN, j = (t / S::HN) % N, k0 = t / S::FH;
-    const int o = (c + j + k0) & 1;
-    const int rb = S::OX + (k0 * N + j) * S::HN + m;
-    constexpr int DT = KS * S::FH;  // tile step per q
-    int ixm = rb, dxm = DT, ixp = rb, dxp = DT, iym = rb - S::HN, dym = DT, iyp = rb + S::HN, dyp = DT;
-    if (!o) {
-      if (m > 0) ixm = rb - 1;
-      else ixm = S::OXF + k0 * N + j, dxm = KS * N;
+    if (!(L.exp & 4096)) {
+      gs_stream_column<N, TH>(L, st, c, kind, h2, slot, gcur);
     } else {
-      if (m < S::HN - 1) ixp = rb + 1;
-      else ixp = S::OXF + N * N + k0 * N + j, dxp = KS * N;
-    }
-    if (j == 0) iym = S::OY + k0 * S::HN + m, dym = KS * S::HN;
-    if (j == N - 1) iyp = S::OY + S::FH + k0 * S::HN + m, dyp = KS * S::HN;
-    const int izm0 = k0 > 0 ? rb - S::FH : S::OZ + j * S::HN + m;
-    const int izpL = k0 < KS - 1 ? rb + (S::PER - 1) * DT + S::FH : S::OZ + S::FH + j * S::HN + m;
-    double* __restrict__ dst = L.phi + (size_t)slot * NI + (size_t)c * S::H + t;
-    if (!(L.exp & 512)) {
-      if (kind == KIND_UNIFORM) {  // multigrid.hpp:651-653: (sum of 6 - h^2 g) / 6.0
-        double sv[S::PER], v[S::PER];
-        bool ok = true;
-#pragma unroll
-        for (int q = 0; q < S::PER; ++q) {
-          const double zm = st[q == 0 ? izm0 : rb + q * DT - S::FH];
-          const double zp = st[q == S::PER - 1 ? izpL : rb + q * DT + S::FH];
-          sv[q] = st[ixm + q * dxm] + st[ixp + q * dxp] + st[iym + q * dym] + st[iyp + q * dyp] + zm + zp -
-                  h2 * gcur[q];
-          v[q] = div6_fast(sv[q]);
-          ok = ok && div6_in_range(sv[q]);
-        }
-        if (!ok) {
-#pragma unroll
-          for (int q = 0; q < S::PER; ++q) v[q] = div6_slow(sv[q]);
-        }
-#pragma unroll
-        for (int q = 0; q < S::PER; ++q) dst[q * S::THR] = v[q];
-      } else {  // interface block (multigrid.hpp:665-684)
-        const int32_t* rq = reinterpret_cast<const int32_t*>(st + S::ORQ);
-#pragma unroll
-        for (int q = 0; q < S::PER; ++q) {
-          const int r = rq[t + q * S::THR];
-          const double g = gcur[q];
-          const double p0 = st[ixm + q * dxm], p1 = st[ixp + q * dxp], p2 = st[iym + q * dym],
-                       p3 = st[iyp + q * dyp], p4 = st[q == 0 ? izm0 : rb + q * DT - S::FH],
-                       p5 = st[q == S::PER - 1 ? izpL : rb + q * DT + S::FH];
-          if (r < 0) {  // uniform row (:667-672)
-            double sv = -h2 * g;
-            sv += p0;
-            sv += p1;
-            sv += p2;
-            sv += p3;
-            sv += p4;
-            sv += p5;
-            dst[q * S::THR] = -sv * (-1.0 / 6.0);
-          }  // special rows: cut rows by k_gs_cut, inside rows keep their pin
+      // Thread t owns entries e = t + q*THR: the same (m, j) and colour offset o
+      // for every q, z-plane k = k0 + q*KS.  Neighbour indices into the stage
+      // (own tile or halo layer) are chosen once per block; only the z layers at
+      // q = 0 / PER-1 are per-q choices.
+      constexpr int KS = S::THR / S::FH;
+      const int m = t % S::HN, j = (t / S::HN) % N, k0 = t / S::FH;
+      const int o = (c + j + k0) & 1;
+      const int rb = S::OX + (k0 * N + j) * S::HN + m;
+      constexpr int DT = KS * S::FH;  // tile step per q
+      int ixm = rb, dxm = DT, ixp = rb, dxp = DT, iym = rb - S::HN, dym = DT, iyp = rb + S::HN, dyp = DT;
+      if (!o) {
+        if (m > 0) ixm = rb - 1;
+        else ixm = S::OXF + k0 * N + j, dxm = KS * N;
+      } else {
+        if (m < S::HN - 1) ixp = rb + 1;
+        else ixp = S::OXF + N * N + k0 * N + j, dxp = KS * N;
+      }
+      if (j == 0) iym = S::OY + k0 * S::HN + m, dym = KS * S::HN;
+      if (j == N - 1) iyp = S::OY + S::FH + k0 * S::HN + m, dyp = KS * S::HN;
+      const int izm0 = k0 > 0 ? rb - S::FH : S::OZ + j * S::HN + m;
+      const int izpL = k0 < KS - 1 ? rb + (S::PER - 1) * DT + S::FH : S::OZ + S::FH + j * S::HN + m;
+      double* __restrict__ dst = L.phi + (size_t)slot * NI + (size_t)c * S::H + t;
+      if (!(L.exp & 512)) {
+        if (kind == KIND_UNIFORM) {  // multigrid.hpp:651-653: (sum of 6 - h^2 g) / 6.0
+          double sv[S::PER], v[S::PER];
+          bool ok = true;
+  #pragma unroll
+          for (int q = 0; q < S::PER; ++q) {
+            const double zm = st[q == 0 ? izm0 : rb + q * DT - S::FH];
+            const double zp = st[q == S::PER - 1 ? izpL : rb + q * DT + S::FH];
+            sv[q] = st[ixm + q * dxm] + st[ixp + q * dxp] + st[iym + q * dym] + st[iyp + q * dyp] + zm + zp -
+                    h2 * gcur[q];
+            v[q] = div6_fast(sv[q]);
+            ok = ok && div6_in_range(sv[q]);
+          }
+          if (!ok) {
+  #pragma unroll
+            for (int q = 0; q < S::PER; ++q) v[q] = div6_slow(sv[q]);
+          }
+  #pragma unroll
+          for (int q = 0; q < S::PER; ++q) dst[q * S::THR] = v[q];
+        } else {  // interface block (multigrid.hpp:665-684)
+          const int32_t* rq = reinterpret_cast<const int32_t*>(st + S::ORQ);
+  #pragma unroll
+          for (int q = 0; q < S::PER; ++q) {
+            const int r = rq[t + q * S::THR];
+            const double g = gcur[q];
+            const double p0 = st[ixm + q * dxm], p1 = st[ixp + q * dxp], p2 = st[iym + q * dym],
+                         p3 = st[iyp + q * dyp], p4 = st[q == 0 ? izm0 : rb + q * DT - S::FH],
+                         p5 = st[q == S::PER - 1 ? izpL : rb + q * DT + S::FH];
+            if (r < 0) {  // uniform row (:667-672)
+              double sv = -h2 * g;
+              sv += p0;
+              sv += p1;
+              sv += p2;
+              sv += p3;
+              sv += p4;
+              sv += p5;
+              dst[q * S::THR] = -sv * (-1.0 / 6.0);
+            }  // special rows: cut rows by k_gs_cut, inside rows keep their pin
+          }
         }
       }
     }
