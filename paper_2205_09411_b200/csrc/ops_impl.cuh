@@ -116,29 +116,30 @@ struct OpsImpl final : Ops {
   }
   // residual-streaming kernels: k_restrict_stream (one thread per parent) or
   // k_resid_stream (GS mapping); PMG_EXP bit 26 swaps them (timing comparisons)
-  template <int MODE, int ST, int MINB>
+  template <int MODE, int ST, int MINB, int TT>
   void launch_resid_stream(Ctx& c, const LevelView& Lf, const LevelView& Lp, const LevelDev& d, Rec* partial,
                            Rec* rec) {
     if constexpr (D == 3 && N == 16) {
-      using Q = QStream3<N>;
-      constexpr size_t smem = ((size_t)ST * Q::STAGE + (MODE == 0 ? 16 * Q::RP : 0)) * sizeof(double);
+      using Q = QStream3<N, TT>;
+      constexpr size_t smem = (size_t)ST * Q::STAGE * sizeof(double);
       static bool attr = false;
       if (!attr) {
-        PMG_CUDA(cudaFuncSetAttribute(k_resid_stream<N, ST, MINB, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
+        PMG_CUDA(cudaFuncSetAttribute(k_resid_stream<N, ST, MINB, MODE, TT>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
       }
       const int grid = std::min(d.n_rs, c.sms * MINB);
-      pdl_launch(k_resid_stream<N, ST, MINB, MODE>, grid, Q::THR, smem, c.stream, Lf, Lp, c.phi_b.p,
+      pdl_launch(k_resid_stream<N, ST, MINB, MODE, TT>, grid, Q::THR, smem, c.stream, Lf, Lp, c.phi_b.p,
                  (const int4*)d.rs_plan.p, d.n_rs, partial, rec, (unsigned int*)nullptr);
     }
   }
   template <int MODE>
   void launch_rstream(Ctx& c, const LevelView& Lf, const LevelView& Lp, const LevelDev& d, Rec* partial, Rec* rec) {
     if constexpr (D == 3 && N == 16) {
-      // restriction (MODE 0): the one-thread-per-parent kernel measured faster
-      // (97 us vs 137 us at 256^3); record / FAS: the GS-mapped kernel
-      if (MODE == 0 ? !(Lf.exp & (1 << 26)) : (Lf.exp & (1 << 26)) != 0) {
+      // restriction: the one-thread-per-parent kernel (85 us at 256^3 vs 93 us
+      // for the column kernel); record / FAS: the column kernel
+      const bool old_kernel = MODE == 0 ? !(Lf.exp & (1 << 26)) : (Lf.exp & (1 << 26)) != 0;
+      if (old_kernel) {
         constexpr int ST = 2, MINB = 1;
         constexpr size_t smem = (size_t)ST * RStream3<N>::STAGE * sizeof(double);
         static bool attr = false;
@@ -150,16 +151,16 @@ struct OpsImpl final : Ops {
         const int grid = std::min(d.n_rs, c.sms * MINB);
         pdl_launch(k_restrict_stream<N, ST, MINB, MODE>, grid, RStream3<N>::THR, smem, c.stream, Lf, Lp, c.phi_b.p,
                    (const int4*)d.rs_plan.p, d.n_rs, partial, rec, (unsigned int*)nullptr);
-      } else if (MODE != 0 && !(Lf.exp & (1 << 27))) {
-        launch_resid_stream<MODE, 2, 2>(c, Lf, Lp, d, partial, rec);
+      } else if (Lf.exp & (1 << 27)) {
+        launch_resid_stream<MODE, 3, 1, 1024>(c, Lf, Lp, d, partial, rec);
       } else {
-        launch_resid_stream<MODE, 3, 1>(c, Lf, Lp, d, partial, rec);
+        launch_resid_stream<MODE, 3, 1, 512>(c, Lf, Lp, d, partial, rec);
       }
     }
   }
   // number of CTAs launch_rstream uses (record partials)
   int rstream_grid(Ctx& c, const LevelView& Lf, const LevelDev& d) {
-    const int minb = (!(Lf.exp & (1 << 26)) && !(Lf.exp & (1 << 27))) ? 2 : 1;  // MODE 1
+    const int minb = 1;  // MODE 1: every variant runs one CTA per SM
     return std::min(d.n_rs, c.sms * minb);
   }
   void residual(Ctx& c, int l) override {

@@ -757,35 +757,33 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
     record_finish(Lf, partial, rec, nullptr, (int)blockIdx.x, rmx, rss, rcnt, red, &last);
 }
 
-// ------------------------------------------------------------------ residual streaming (GS mapping)
+// ------------------------------------------------------------------ residual streaming (column mapping)
 // residual_level + restrict_level, the FAS right-hand side and the leaf
-// record of lean 3D blocks, with the GS kernel's thread mapping: thread t owns
-// the colour-split entries e = t + q*THR of BOTH colours, so every
-// shared-memory access of a warp is a run of consecutive doubles and the
-// neighbour offsets are chosen once per block.  The stage holds both phi
-// halves (one bulk copy) and the face layers of both colours (the RStream3
-// layout without g); g goes straight from global memory into registers, one
-// block ahead.  Per cell r = g - L(phi) with the reference's operation order
-// (stencil.hpp:300-322, 336-358).
-//   MODE 0: residual + restriction (multigrid.hpp:374-398, 697-722): phase 1
-//           stores r and phi child-major (R2[child][parent]) in shared memory,
-//           phase 2 (one thread per parent) folds the 8 children in x-fastest
-//           order.  Parents with a cut child belong to k_restrict_fix.
+// record of lean 3D blocks.  Thread t owns the entry column (m, j) on the PER
+// consecutive z-planes k = kq*PER + q, in BOTH colours: the cells (2m, j, k)
+// and (2m+1, j, k).  The own values of both colours are loaded once as two
+// columns, which also hold each cell's same-entry x neighbour and its z
+// neighbours, so a cell costs 3 more shared loads (the other x neighbour and
+// y-, y+) -- all runs of consecutive doubles across a warp.  The stage holds
+// both phi halves (one bulk copy) and the face layers of both colours (the
+// RStream3 layout without g); g goes straight from global memory into
+// registers, one block ahead.  Per cell r = g - L(phi) with the reference's
+// operation order (stencil.hpp:300-322, 336-358).
+//   MODE 0: residual + restriction (multigrid.hpp:374-398, 697-722).  A
+//           parent's 2x2x2 children are the x pair of two consecutive planes
+//           of this thread and of the thread with j + 1 (lane + 8): one
+//           shuffle exchange, then the fold in x-fastest order.  Parents with a
+//           cut child belong to k_restrict_fix.
 //   MODE 1: leaf-residual record (multigrid.hpp:529-562), per-CTA partials.
 //   MODE 2: FAS g = L(phi) + r on non-leaf blocks, OLD <- PHI (:380-397).
-template <int N>
+template <int N, int TT = 512>
 struct QStream3 {
   static constexpr int HN = N / 2;
   static constexpr int H = N * N * N / 2;
   static constexpr int FH = N * HN;
-  static constexpr int THR = H < 512 ? H : 512;
+  static constexpr int THR = H < TT ? H : TT;
   static constexpr int PER = H / THR;
-  static constexpr int KS = THR / FH;     // z-plane step per q
-  static constexpr int NP = HN * HN * HN;  // parents per block
-  // child-major r / phi tiles of MODE 0: the children of a half-warp's
-  // parents differ in the child's x parity, so an odd child's row sits 8
-  // doubles (half a bank sweep) further: conflict-free stores and loads
-  static constexpr int RP = NP + 8;
+  static constexpr int KS = THR / FH;  // columns per (m, j): z-plane groups
   // doubles: P[2][H], hz[2 side][2 colour][FH], hy[2][2][FH], hx[2][N*N]
   static constexpr int OP = 0, OZ = 2 * H, OY = OZ + 4 * FH, OXF = OY + 4 * FH;
   static constexpr int STAGE = OXF + 2 * N * N;
@@ -793,9 +791,9 @@ struct QStream3 {
   static constexpr int YC = 2 * 2 * N * (HN / 2);  // 16-B chunks of the y layers
 };
 
-template <int N>
+template <int N, int TT>
 __device__ __forceinline__ void qs_issue(const LevelView& L, const BlockPlan& P, double* st, uint64_t* bar) {
-  using S = QStream3<N>;
+  using S = QStream3<N, TT>;
   constexpr int NI = N * N * N;
   const double* own = L.phi + (size_t)P.slot() * NI;
   mbar_arrive_expect_tx(bar, S::TX_BYTES);
@@ -810,44 +808,39 @@ __device__ __forceinline__ void qs_issue(const LevelView& L, const BlockPlan& P,
   }
 }
 
-template <int N, int S_STAGES, int MINB, int MODE>
-__global__ void __launch_bounds__(QStream3<N>::THR, MINB) k_resid_stream(LevelView Lf, LevelView Lp,
+template <int N, int S_STAGES, int MINB, int MODE, int TT>
+__global__ void __launch_bounds__(QStream3<N, TT>::THR, MINB) k_resid_stream(LevelView Lf, LevelView Lp,
                                                                         const double* __restrict__ phi_b,
                                                                         const int4* __restrict__ plan, int n,
                                                                         Rec* __restrict__ partial, Rec* rec,
                                                                         unsigned int* counter) {
   pdl_begin();
-  using S = QStream3<N>;
-  constexpr int NI = N * N * N, HN = S::HN, H = S::H, FH = S::FH, PER = S::PER, KS = S::KS, THR = S::THR;
-  constexpr int NP = S::NP;
+  using S = QStream3<N, TT>;
+  constexpr int NI = N * N * N, HN = S::HN, H = S::H, FH = S::FH, PER = S::PER, KS = S::KS;
   static_assert(S_STAGES >= 2, "g of block it+1 is read through meta[] one iteration ahead");
-  static_assert(MODE != 0 || NP == THR, "phase 2: one thread per parent");
+  static_assert(PER * KS == N && PER % 2 == 0 && HN == 8, "columns of whole z pairs; j + 1 is lane + 8");
   extern __shared__ __align__(128) double sm[];
-  double* const R2 = sm + S_STAGES * S::STAGE;  // MODE 0: r [8][RP], then phi [8][RP]
-  constexpr int RP = S::RP;
   __shared__ __align__(8) uint64_t full[S_STAGES];
   __shared__ int meta[S_STAGES][2];
   __shared__ double red[72];
   __shared__ bool last;
-  __shared__ int cutp[MODE == 0 ? NP : 1];
+  __shared__ int4 pring[PlanRing<S_STAGES>::PR * 2];
+  PlanRing<S_STAGES> R{pring};
   const int t = threadIdx.x;
   const int G = gridDim.x;
   const int nmine = (int)blockIdx.x < n ? (n - 1 - (int)blockIdx.x) / G + 1 : 0;
   if (nmine == 0) return;
-  __shared__ int4 pring[PlanRing<S_STAGES>::PR * 2];
-  PlanRing<S_STAGES> R{pring};
   if (t == 0) {
     for (int s = 0; s < S_STAGES; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
   R.init(plan, nmine, G);
-  if (MODE == 0) cutp[t] = 0;
   __syncthreads();
   for (int s = 0; s < S_STAGES; ++s) {
     if (s < nmine) {
       const BlockPlan P = R.get(s);
       if (t == 0) {
-        qs_issue<N>(Lf, P, sm + s * S::STAGE, &full[s]);
+        qs_issue<N, TT>(Lf, P, sm + s * S::STAGE, &full[s]);
         meta[s][0] = P.slot(), meta[s][1] = P.a.y;
       }
       rs_issue_async<N, S>(Lf, P, sm + s * S::STAGE);
@@ -855,15 +848,17 @@ __global__ void __launch_bounds__(QStream3<N>::THR, MINB) k_resid_stream(LevelVi
     cp_async_commit();
   }
   __syncthreads();  // meta of the first stages
-  const int m = t % HN, j = (t / HN) % N, k0 = t / FH;
+  const int m = t % HN, j = (t / HN) % N, kq = t / FH;
+  const int eb = m + HN * j + FH * PER * kq;  // entry of q = 0
+  const int jo = (j + kq * PER) & 1;          // o of colour 0 at q = 0; o_c(q) = jo ^ c ^ (q & 1)
   const double w = Lf.w;
   double gcur[2][PER], gnext[2][PER];
   {
-    const double* gsrc = Lf.rhs + (size_t)meta[0][0] * NI + t;
+    const double* gsrc = Lf.rhs + (size_t)meta[0][0] * NI + eb;
 #pragma unroll
     for (int c = 0; c < 2; ++c)
 #pragma unroll
-      for (int q = 0; q < PER; ++q) gcur[c][q] = gsrc[c * H + q * THR];
+      for (int q = 0; q < PER; ++q) gcur[c][q] = gsrc[c * H + q * FH];
   }
   double rmx = 0.0, rss = 0.0, rcnt = 0.0;  // MODE 1: this CTA's running totals
   for (int it = 0; it < nmine; ++it) {
@@ -875,11 +870,11 @@ __global__ void __launch_bounds__(QStream3<N>::THR, MINB) k_resid_stream(LevelVi
     // per-block scalars and the special-row kinds, in flight across the wait
     int rr[2][PER];
     if (kind == KIND_IFACE) {
-      const int8_t* sk = Lf.skind + (size_t)(flags >> 14) * NI + t;
+      const int8_t* sk = Lf.skind + (size_t)(flags >> 14) * NI + eb;
 #pragma unroll
       for (int c = 0; c < 2; ++c)
 #pragma unroll
-        for (int q = 0; q < PER; ++q) rr[c][q] = sk[c * H + q * THR];
+        for (int q = 0; q < PER; ++q) rr[c][q] = sk[c * H + q * FH];
     } else {
 #pragma unroll
       for (int c = 0; c < 2; ++c)
@@ -894,98 +889,135 @@ __global__ void __launch_bounds__(QStream3<N>::THR, MINB) k_resid_stream(LevelVi
     cp_async_wait<S_STAGES - 1>();
     __syncthreads();
     if (it + 1 < nmine) {  // this thread's g of the next block, in flight during this one
-      const double* gsrc = Lf.rhs + (size_t)meta[(it + 1) % S_STAGES][0] * NI + t;
+      const double* gsrc = Lf.rhs + (size_t)meta[(it + 1) % S_STAGES][0] * NI + eb;
 #pragma unroll
       for (int c = 0; c < 2; ++c)
 #pragma unroll
-        for (int q = 0; q < PER; ++q) gnext[c][q] = gsrc[c * H + q * THR];
+        for (int q = 0; q < PER; ++q) gnext[c][q] = gsrc[c * H + q * FH];
     }
     if (pmask) {  // block-uniform branch
       rs_phys_faces<N, S>(Lf, slot, pmask, st);
       __syncthreads();
     }
-    // ---- phase 1: r at every cell of the block
+    // the two columns, then every cell
+    double col[2][PER];
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int q = 0; q < PER; ++q) col[c][q] = st[S::OP + c * H + eb + q * FH];
+    double res[2][PER], ap[2][PER];
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
-      const int o = (c + j + k0) & 1;  // i = 2m + o (k = k0 + q KS keeps k0's parity)
-      const int OWN = S::OP + c * H, XO = S::OP + (1 - c) * H;
-      const int rb = XO + t;
-      constexpr int DT = THR;  // tile step per q
-      int ixm = rb, dxm = DT, ixp = rb, dxp = DT, iym = rb - HN, dym = DT, iyp = rb + HN, dyp = DT;
-      if (!o) {
-        if (m > 0) ixm = rb - 1;
-        else ixm = S::OXF + k0 * N + j, dxm = KS * N;
-      } else {
-        if (m < HN - 1) ixp = rb + 1;
-        else ixp = S::OXF + N * N + k0 * N + j, dxp = KS * N;
-      }
-      if (j == 0) iym = S::OY + (0 * 2 + c) * FH + k0 * HN + m, dym = KS * HN;
-      if (j == N - 1) iyp = S::OY + (1 * 2 + c) * FH + k0 * HN + m, dyp = KS * HN;
-      const int izm0 = k0 > 0 ? rb - FH : S::OZ + (0 * 2 + c) * FH + j * HN + m;
-      const int izpL = k0 < KS - 1 ? rb + (PER - 1) * DT + FH : S::OZ + (1 * 2 + c) * FH + j * HN + m;
+      const int X = 1 - c;
+      const int XB = S::OP + X * H + eb;
+      // neighbour bases (index of q = 0) and per-q steps: the other x
+      // neighbour for o = 0 (e - 1 or the -x face) and o = 1 (e + 1 or +x),
+      // y- / y+ (e -+ HN or the y face of colour c), z halo of colour c
+      const int bx0 = m > 0 ? XB - 1 : S::OXF + kq * PER * N + j, sx0 = m > 0 ? FH : N;
+      const int bx1 = m < HN - 1 ? XB + 1 : S::OXF + N * N + kq * PER * N + j, sx1 = m < HN - 1 ? FH : N;
+      const int bym = j > 0 ? XB - HN : S::OY + (0 * 2 + c) * FH + kq * PER * HN + m, sym = j > 0 ? FH : HN;
+      const int byp = j < N - 1 ? XB + HN : S::OY + (1 * 2 + c) * FH + kq * PER * HN + m, syp = j < N - 1 ? FH : HN;
+      const double zlo = st[kq > 0 ? XB - FH : S::OZ + (0 * 2 + c) * FH + j * HN + m];
+      const double zhi = st[kq < KS - 1 ? XB + PER * FH : S::OZ + (1 * 2 + c) * FH + j * HN + m];
 #pragma unroll
       for (int q = 0; q < PER; ++q) {
-        const int k = k0 + q * KS;
-        const double f = st[OWN + t + q * DT];
-        const double p0 = st[ixm + q * dxm], p1 = st[ixp + q * dxp], p2 = st[iym + q * dym],
-                     p3 = st[iyp + q * dyp], p4 = st[q == 0 ? izm0 : rb + q * DT - FH],
-                     p5 = st[q == PER - 1 ? izpL : rb + q * DT + FH];
+        const int o = jo ^ c ^ (q & 1);
+        const double f = col[c][q];
+        const double xo = st[o ? bx1 + q * sx1 : bx0 + q * sx0];
+        const double xm = o ? col[X][q] : xo, xp = o ? xo : col[X][q];
+        const double ym = st[bym + q * sym], yp = st[byp + q * syp];
+        const double zm = q > 0 ? col[X][q - 1] : zlo, zp = q < PER - 1 ? col[X][q + 1] : zhi;
         double sres = -2.0 * 3 * f;  // stencil.hpp:300-322, direction order
-        sres += p0;
-        sres += p1;
-        sres += p2;
-        sres += p3;
-        sres += p4;
-        sres += p5;
-        const double ap = kind == KIND_ALL_INSIDE ? 0.0 : sres * w;
-        const double g = gcur[c][q];
+        sres += xm;
+        sres += xp;
+        sres += ym;
+        sres += yp;
+        sres += zm;
+        sres += zp;
+        ap[c][q] = kind == KIND_ALL_INSIDE ? 0.0 : sres * w;
         const int r8 = rr[c][q];
-        const double res = (kind == KIND_ALL_INSIDE || r8 == 1) ? 0.0 : g - ap;
-        if (MODE == 0) {
-          const int ch = o + 2 * (j & 1) + 4 * (k & 1);
-          const int p = m + HN * ((j >> 1) + HN * (k >> 1));
-          R2[ch * RP + p] = res;
-          R2[(8 + ch) * RP + p] = f;
-          if (r8 == 2) cutp[p] = 1;
-        } else if (MODE == 1) {
-          if (leaf && (kind == KIND_UNIFORM || (kind == KIND_IFACE && r8 == 0))) {
-            rmx = fmax(rmx, fabs(res));
-            rss += res * res;
+        res[c][q] = (kind == KIND_ALL_INSIDE || r8 == 1) ? 0.0 : gcur[c][q] - ap[c][q];
+      }
+    }
+    if (MODE == 1) {
+      if (leaf && kind != KIND_ALL_INSIDE) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int q = 0; q < PER; ++q) {
+            if (rr[c][q] != 0) continue;  // inside rows excluded, cut rows by k_record_cut
+            rmx = fmax(rmx, fabs(res[c][q]));
+            rss += res[c][q] * res[c][q];
             rcnt += 1.0;
           }
-        } else {
-          const size_t a = (size_t)slot * NI + (size_t)c * H + t + q * DT;
-          // special rows of interface blocks: inside rows keep r (0 + r), cut rows by k_fas_fix
-          if (!leaf && (kind != KIND_IFACE || r8 == 0)) Lf.rhs[a] = ap + g;
-          Lf.old[a] = f;
-        }
       }
+    } else if (MODE == 2) {
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+          const size_t a = (size_t)slot * NI + (size_t)c * H + eb + q * FH;
+          // special rows of interface blocks: inside rows keep r (0 + r), cut rows by k_fas_fix
+          if (!leaf && (kind != KIND_IFACE || rr[c][q] == 0)) Lf.rhs[a] = ap[c][q] + gcur[c][q];
+          Lf.old[a] = col[c][q];
+        }
     }
     __syncthreads();  // stage s consumed
     if (it + S_STAGES < nmine) {
       const BlockPlan pf = R.get(it + S_STAGES);
       if (t == 0) {
-        qs_issue<N>(Lf, pf, st, &full[s]);
+        qs_issue<N, TT>(Lf, pf, st, &full[s]);
         meta[s][0] = pf.slot(), meta[s][1] = pf.a.y;
       }
       rs_issue_async<N, S>(Lf, pf, st);
     }
     cp_async_commit();
-    if (MODE == 0) {  // ---- phase 2: parent t folds its children (multigrid.hpp:706-721)
-      double sr = 0.0, sf = 0.0;
+    if (MODE == 0) {
+      // children of parent (m, j/2, kq*PER/2 + p2): x pair (dx = o of the
+      // colour) of planes 2 p2 (dz 0) and 2 p2 + 1 (dz 1), this thread (dy = j & 1)
+      // and the thread of j + 1 (lane + 8)
 #pragma unroll
-      for (int ch = 0; ch < 8; ++ch) {
-        sr += R2[ch * RP + t];
-        sf += R2[(8 + ch) * RP + t];
-      }
-      const int cut = cutp[t];
-      cutp[t] = 0;
-      if (!cut) {  // pinned parents: re-pinned by k_pin_list afterwards
-        const int pi = cx * HN + t % HN, pj = cy * HN + (t / HN) % HN, pk = cz * HN + t / (HN * HN);
-        const int pc = (pi + pj + pk) & 1, pe = (pi + N * (pj + N * pk)) >> 1;
-        const size_t pa = (size_t)Pp * NI + (size_t)pc * H + pe;
-        Lp.phi[pa] = sf / 8.0;
-        Lp.rhs[pa] = sr / 8.0;
+      for (int p2 = 0; p2 < PER / 2; ++p2) {
+        double rv[2][2], fv[2][2];  // [dz][dx]
+        int cut = 0;
+#pragma unroll
+        for (int dz = 0; dz < 2; ++dz) {
+          const int q = 2 * p2 + dz;
+          const int c0 = jo ^ (q & 1);  // colour of the dx = 0 cell (o_c = 0)
+#pragma unroll
+          for (int dx = 0; dx < 2; ++dx) {
+            const int c = c0 ^ dx;
+            rv[dz][dx] = c ? res[1][q] : res[0][q];
+            fv[dz][dx] = c ? col[1][q] : col[0][q];
+            cut |= (c ? rr[1][q] : rr[0][q]) == 2;
+          }
+        }
+        double rn[2][2], fn[2][2];
+#pragma unroll
+        for (int dz = 0; dz < 2; ++dz)
+#pragma unroll
+          for (int dx = 0; dx < 2; ++dx) {
+            rn[dz][dx] = __shfl_down_sync(0xffffffffu, rv[dz][dx], HN);
+            fn[dz][dx] = __shfl_down_sync(0xffffffffu, fv[dz][dx], HN);
+          }
+        cut |= __shfl_down_sync(0xffffffffu, cut, HN);
+        if (!(j & 1) && !cut) {  // multigrid.hpp:706-721: x-fastest order
+          double sr = 0.0, sf = 0.0;
+          sr += rv[0][0], sf += fv[0][0];
+          sr += rv[0][1], sf += fv[0][1];
+          sr += rn[0][0], sf += fn[0][0];
+          sr += rn[0][1], sf += fn[0][1];
+          sr += rv[1][0], sf += fv[1][0];
+          sr += rv[1][1], sf += fv[1][1];
+          sr += rn[1][0], sf += fn[1][0];
+          sr += rn[1][1], sf += fn[1][1];
+          // pinned parents: re-pinned by k_pin_list afterwards
+          const int pi = cx * HN + m, pj = cy * HN + (j >> 1), pk = cz * HN + kq * (PER / 2) + p2;
+          const int pc = (pi + pj + pk) & 1, pe = (pi + N * (pj + N * pk)) >> 1;
+          const size_t pa = (size_t)Pp * NI + (size_t)pc * H + pe;
+          Lp.phi[pa] = sf / 8.0;
+          Lp.rhs[pa] = sr / 8.0;
+        }
       }
     }
 #pragma unroll
