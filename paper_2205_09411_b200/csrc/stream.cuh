@@ -1179,35 +1179,69 @@ struct PStream3 {
 
 // plan entry: {fine slot, parent slot, octant bits, parent neighbour across the
 // octant's outer face per axis (-1 physical), kind, 0}
-template <int N, bool FULL>
-__device__ __forceinline__ void pr_issue_async(const LevelView& Lp, const int4& a, const int4& b, double* st) {
+//
+// Tile element q (natural 10^3 order over the octant and its one-cell halo)
+// of this thread, decoded once per kernel: the thread owns q = t + e*THR.
+// `ax`/`side`: the axis on which the element leaves the octant (-1: inside;
+// edges and corners are never read and are skipped).  Whether it also
+// leaves the parent block depends only on the octant bit of that axis.
+struct PElem {
+  int q;          // tile index, -1: none
+  int t3[3];      // octant-relative coordinates, -1 .. HN
+  int ax, side;   // halo axis / side (0: -1, 1: HN), ax -1 inside
+};
+template <int N>
+__device__ __forceinline__ PElem pr_elem(int q) {
+  constexpr int HN = N / 2, PE = HN + 2, PS = PE * PE * PE;
+  PElem E;
+  E.q = -1;
+  E.ax = -1;
+  E.side = 0;
+  E.t3[0] = E.t3[1] = E.t3[2] = 0;
+  if (q >= PS) return E;
+  const int t3[3] = {q % PE - 1, (q / PE) % PE - 1, q / (PE * PE) - 1};
+  int out = 0;
+  for (int d = 0; d < 3; ++d) {
+    E.t3[d] = t3[d];
+    if (t3[d] < 0 || t3[d] >= HN) ++out, E.ax = d, E.side = t3[d] >= HN;
+  }
+  if (out > 1) return E;  // edges / corners are never read
+  E.q = q;
+  return E;
+}
+// parent-block cell of element E for octant `oct`: block (P or the
+// neighbour across the parent face, -1 physical) and colour-split address
+template <int N>
+__device__ __forceinline__ size_t pr_addr(const PElem& E, int oct, int P, const int* pn, int& phys, int c3[3]) {
+  constexpr int NI = N * N * N, HN = N / 2, H = NI / 2;
+  for (int d = 0; d < 3; ++d) c3[d] = ((oct >> d) & 1) * HN + E.t3[d];
+  int blk = P;
+  phys = 0;
+  if (E.ax >= 0 && ((oct >> E.ax) & 1) == E.side) {  // leaves the parent block
+    const int nb = E.ax == 0 ? pn[0] : E.ax == 1 ? pn[1] : pn[2];
+    if (nb >= 0) {
+      blk = nb;
+      c3[E.ax] = E.side ? 0 : N - 1;
+    } else {  // physical face: the parent's own boundary cell, made a ghost after the wait
+      c3[E.ax] = E.side ? N - 1 : 0;
+      phys = 1;
+    }
+  }
+  return (size_t)blk * NI + (size_t)(((c3[0] + c3[1] + c3[2]) & 1) * H) + (size_t)((c3[0] + N * (c3[1] + N * c3[2])) >> 1);
+}
+
+template <int N, bool FULL, int NE>
+__device__ __forceinline__ void pr_issue_async(const LevelView& Lp, const int4& a, const int4& b, double* st,
+                                               const PElem* E) {
   using S = PStream3<N>;
-  constexpr int NI = N * N * N, HN = S::HN, PE = S::PE;
-  const int P = a.y, oct = a.z;
   const int pn[3] = {a.w, b.x, b.y};
-  for (int q = threadIdx.x; q < S::PS; q += S::THR) {
-    const int t3[3] = {q % PE - 1, (q / PE) % PE - 1, q / (PE * PE) - 1};
-    int out = 0, ax = -1;
-    int c3[3];
-    for (int d = 0; d < 3; ++d) {
-      c3[d] = ((oct >> d) & 1) * HN + t3[d];
-      if (t3[d] < 0 || t3[d] >= HN) ++out;
-      if (c3[d] < 0 || c3[d] >= N) ax = d;
-    }
-    if (out > 1) continue;  // edges / corners are never read
-    int blk = P;
-    if (ax >= 0) {
-      if (pn[ax] >= 0) {
-        blk = pn[ax];
-        c3[ax] = c3[ax] < 0 ? N - 1 : 0;
-      } else {  // physical face: the parent's own boundary cell, transformed in the prep pass
-        c3[ax] = c3[ax] < 0 ? 0 : N - 1;
-      }
-    }
-    const size_t ad = (size_t)blk * NI + (size_t)(((c3[0] + c3[1] + c3[2]) & 1) * S::H) +
-                      (size_t)((c3[0] + N * (c3[1] + N * c3[2])) >> 1);
-    cp_async8(st + S::ORP + q, Lp.phi + ad);
-    if (!FULL) cp_async8(st + S::ORO + q, Lp.old + ad);
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    if (E[e].q < 0) continue;
+    int phys, c3[3];
+    const size_t ad = pr_addr<N>(E[e], a.z, a.y, pn, phys, c3);
+    cp_async8(st + S::ORP + E[e].q, Lp.phi + ad);
+    if (!FULL) cp_async8(st + S::ORO + E[e].q, Lp.old + ad);
   }
 }
 
@@ -1217,6 +1251,7 @@ __global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(Level
   pdl_begin();
   using S = PStream3<N>;
   constexpr int NI = N * N * N, HN = S::HN, PE = S::PE;
+  constexpr int NE = (S::PS + S::THR - 1) / S::THR;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t full[S_STAGES];
   __shared__ int4 meta[S_STAGES][2];
@@ -1224,6 +1259,9 @@ __global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(Level
   const int G = gridDim.x;
   const int nmine = (int)blockIdx.x < n ? (n - 1 - (int)blockIdx.x) / G + 1 : 0;
   if (nmine == 0) return;
+  PElem E[NE];
+#pragma unroll
+  for (int e = 0; e < NE; ++e) E[e] = pr_elem<N>(t + e * S::THR);
   if (t == 0) {
     for (int s = 0; s < S_STAGES; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
@@ -1242,12 +1280,20 @@ __global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(Level
         bulk_g2s(st + S::OF, Lf.phi + (size_t)a.x * NI, 2 * S::H * 8, &full[s]);
       }
     }
-    pr_issue_async<N, FULL>(Lp, a, b, st);
+    pr_issue_async<N, FULL, NE>(Lp, a, b, st, E);
   };
   for (int s = 0; s < S_STAGES; ++s) {
     if (s < nmine) issue(blockIdx.x + s * G, s);
     cp_async_commit();
   }
+  // fine-cell geometry of this thread: entries e = t + q*THR, both colours;
+  // j and the parity of k are fixed, the parent z row advances 2 planes per q
+  const int m = t % HN, j = (t / HN) % N, k0 = t / (HN * N);
+  constexpr int KS = S::THR / (HN * N);  // planes per q
+  static_assert(KS % 2 == 0, "the parent row advances by whole planes");
+  const int c0 = (j + k0) & 1;  // colour of i = 2m (x sign -1); i = 2m+1 has +1
+  const int ctr0 = (((k0 >> 1) + 1) * PE + (j >> 1) + 1) * PE + m + 1;
+  const int dyo = (j & 1) ? PE : -PE, dzo = (k0 & 1) ? PE * PE : -PE * PE;
   for (int it = 0; it < nmine; ++it) {
     const int s = it % S_STAGES;
     double* st = sm + s * S::STAGE;
@@ -1257,27 +1303,26 @@ __global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(Level
     const int4 a = meta[s][0], b = meta[s][1];
     const int slot = a.x, P = a.y, oct = a.z;
     const int pn[3] = {a.w, b.x, b.y};
-    // prep: delta (or phi for FULL) in place of the raw phi tile
-    for (int q = t; q < S::PS; q += S::THR) {
-      const int t3[3] = {q % PE - 1, (q / PE) % PE - 1, q / (PE * PE) - 1};
-      int out = 0, ax = -1;
-      int c3[3];
-      for (int d = 0; d < 3; ++d) {
-        c3[d] = ((oct >> d) & 1) * HN + t3[d];
-        if (t3[d] < 0 || t3[d] >= HN) ++out;
-        if (c3[d] < 0 || c3[d] >= N) ax = d;
-      }
-      if (out > 1) continue;
+    // prep: delta (or phi for FULL) in place of the raw phi tile; physical-face
+    // ghosts of phi and old evaluated separately (mesh.hpp:538-552)
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      if (E[e].q < 0) continue;
+      const int q = E[e].q;
       double vp = st[S::ORP + q], vo = FULL ? 0.0 : st[S::ORO + q];
-      if (ax >= 0 && pn[ax] < 0) {  // physical-face ghost of phi and old (mesh.hpp:538-552)
-        const int side = c3[ax] >= N, dir = 2 * ax + side;
-        if (Lp.bctype[dir] != 1) {
-          c3[ax] = side ? N - 1 : 0;
-          const int bo = Lp.bcoff[P * 6 + dir];
-          const int tj = ax == 0 ? c3[1] + N * c3[2] : ax == 1 ? c3[0] + N * c3[2] : c3[0] + N * c3[1];
-          const double bcv = bo < 0 ? 0.0 : Lp.bcval[bo + tj];
-          vp = 2.0 * bcv - vp;
-          vo = 2.0 * bcv - vo;
+      if (E[e].ax >= 0 && ((oct >> E[e].ax) & 1) == E[e].side) {
+        const int ax = E[e].ax;
+        if ((ax == 0 ? pn[0] : ax == 1 ? pn[1] : pn[2]) < 0) {
+          const int dir = 2 * ax + E[e].side;
+          if (Lp.bctype[dir] != 1) {
+            int phys, c3[3];
+            (void)pr_addr<N>(E[e], oct, P, pn, phys, c3);
+            const int bo = Lp.bcoff[P * 6 + dir];
+            const int tj = ax == 0 ? c3[1] + N * c3[2] : ax == 1 ? c3[0] + N * c3[2] : c3[0] + N * c3[1];
+            const double bcv = bo < 0 ? 0.0 : Lp.bcval[bo + tj];
+            vp = 2.0 * bcv - vp;
+            vo = 2.0 * bcv - vo;
+          }
         }
       }
       st[S::ORP + q] = FULL ? vp : vp - vo;
@@ -1285,16 +1330,13 @@ __global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(Level
     __syncthreads();
     const double* Dt = st + S::ORP;
     double* __restrict__ dst = Lf.phi + (size_t)slot * NI;
-    const int m = t % HN;
 #pragma unroll
     for (int q = 0; q < S::PER; ++q) {
-      const int e = t + q * S::THR;
-      const int j = (e / HN) % N, k = e / (HN * N);
-      const int ctr = (((k >> 1) + 1) * PE + (j >> 1) + 1) * PE + m + 1;
+      const int ctr = ctr0 + q * (KS / 2) * PE * PE;
       const double dc = Dt[ctr], dxm = Dt[ctr - 1], dxp = Dt[ctr + 1];
-      const double dy = Dt[ctr + ((j & 1) ? PE : -PE)];
-      const double dz = Dt[ctr + ((k & 1) ? PE * PE : -PE * PE)];
-      const int c0 = (j + k) & 1;  // colour of i = 2m (x sign -1); i = 2m+1 has +1
+      const double dy = Dt[ctr + dyo];
+      const double dz = Dt[ctr + dzo];
+      const int e = t + q * S::THR;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int c = h ? 1 - c0 : c0;
