@@ -1370,6 +1370,8 @@ int pmg_b200_set_boundary_value(pmg_b200_ctx* h, int obj, double value) {
     if (c.st.valid) {  // their bc * phi_b products
       build_cut_tables(c);
       build_row_coef(c);
+      set_views(c);          // the tables were reallocated: views and graphs
+      invalidate_graphs(c);  // hold their device pointers
     }
     PMG_CUDA(cudaStreamSynchronize(c.stream));
   });

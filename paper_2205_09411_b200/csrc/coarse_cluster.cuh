@@ -28,7 +28,7 @@ struct CC {
   static constexpr int NC = N / PPC;        // CTAs in the cluster (PPC planes each)
   static constexpr int THR = PPC * N * N;   // one thread per cell of the CTA's planes
   static constexpr int NW = (THR + 31) / 32;
-  static constexpr int NSTAGE = 6;          // reduction stages per iteration (+ setup)
+  static constexpr int NSTAGE = 6;          // reduction stages (0 setup; 1, 2, 4 per iteration)
 };
 
 template <int N>
@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(CC<N, PPC>::THR, 1) k_coarse_cluster(LevelView
   __shared__ double Gx[2][PPC][K::PP];
   // partials of every warp of every CTA, per reduction stage
   __shared__ double part[K::NSTAGE][K::NC * K::NW][2];
+  __shared__ double part3[K::NC * K::NW];  // third value of the (s, s) / (t, s) / (t, t) stage
   const int zr = (int)cl.block_rank();
   const int t = threadIdx.x;
   const int lane = t & 31, wid = t >> 5;
@@ -130,10 +131,11 @@ __global__ void __launch_bounds__(CC<N, PPC>::THR, 1) k_coarse_cluster(LevelView
   constexpr int NP = K::NC * K::NW;
   static_assert(K::NC <= 32, "one lane per destination CTA");
   unsigned uses = 0;  // bit k: parity of stage k's next phase
-  auto csum = [&](int stage, double va, double vb, auto&& fn) -> D3 {
+  auto csum3 = [&](int stage, double va, double vb, double vc, bool three, auto&& fn) -> D3 {
     va = warp_sum(va);
     vb = warp_sum(vb);
-    if (t == 0) mbar_arrive_expect_tx(&sbar[stage], NP * 16u);
+    if (three) vc = warp_sum(vc);
+    if (t == 0) mbar_arrive_expect_tx(&sbar[stage], NP * (three ? 24u : 16u));
     if (lane < K::NC) {  // lane r pushes this warp's partial to rank r
       uint32_t ra, rb;
       asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
@@ -143,18 +145,30 @@ __global__ void __launch_bounds__(CC<N, PPC>::THR, 1) k_coarse_cluster(LevelView
       asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(ra),
                    "d"(va), "d"(vb), "r"(rb)
                    : "memory");
+      if (three) {
+        uint32_t rc;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rc) : "r"(smem_u32(&part3[zr * K::NW + wid])), "r"(lane));
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(rc), "d"(vc),
+                     "r"(rb)
+                     : "memory");
+      }
     }
     mbar_wait(&sbar[stage], (uses >> stage) & 1u);
     uses ^= 1u << stage;
-    double ta = 0, tb = 0;
+    double ta = 0, tb = 0, tc = 0;
 #pragma unroll
     for (int k = lane; k < NP; k += 32) {
       ta += part[stage][k][0];
       tb += part[stage][k][1];
+      if (three) tc += part3[k];
     }
     ta = warp_sum(ta);
     tb = warp_sum(tb);
-    return fn(ta, tb);
+    if (three) tc = warp_sum(tc);
+    return fn(ta, tb, tc);
+  };
+  auto csum = [&](int stage, double va, double vb, auto&& fn) -> D3 {
+    return csum3(stage, va, vb, 0.0, false, [&](double a2, double b2, double) { return fn(a2, b2); });
   };
   static_assert(K::THR % 32 == 0, "whole warps");
   if (t == 0) {
@@ -230,11 +244,15 @@ __global__ void __launch_bounds__(CC<N, PPC>::THR, 1) k_coarse_cluster(LevelView
       alpha = o.y;
       s = unk ? r - alpha * v : 0.0;
       const double sh = unk ? dinv * s : 0.0;  // s^
-      // s^ planes pushed before ||s|| (s^ of the previous iteration was
-      // consumed before the (r0, v) reduction everyone has passed)
+      // s^ planes (s^ of the previous iteration was consumed before the
+      // (r0, v) reduction everyone has passed); t = A s^ is formed before
+      // ||s|| is known, so (s, s), (t, s) and (t, t) share one reduction --
+      // on the early exit (||s|| <= tol ||r0||) t is simply not used
       push(1, sh);
-      o = csum(2, s * s, 0.0, [](double a2, double) { return D3{sqrt(a2), 0.0, 0.0}; });
-      land(1);  // also before an early exit: no st.async into this CTA in flight
+      land(1);
+      tv = unk ? cc_row<N>(C, Gs1, Gm1, Gp1, f, dg, pi, sc) : 0.0;
+      o = csum3(2, s * s, tv * s, tv * tv, true,
+                [](double a2, double b2, double c2) { return D3{sqrt(a2), c2, c2 == 0 ? 0.0 : b2 / c2}; });
       const double ns = o.x;
       if (ns <= target) {
         if (unk) xv += alpha * ph;
@@ -243,11 +261,8 @@ __global__ void __launch_bounds__(CC<N, PPC>::THR, 1) k_coarse_cluster(LevelView
         rel = ns / norm0;
         break;
       }
-      tv = unk ? cc_row<N>(C, Gs1, Gm1, Gp1, f, dg, pi, sc) : 0.0;
-      // (t, s), (t, t); omega = (t, s) / (t, t)
-      o = csum(3, tv * s, tv * tv, [](double a2, double b2) { return D3{b2, b2 == 0 ? 0.0 : a2 / b2, 0.0}; });
-      if (o.x == 0) break;
-      omega = o.y;
+      if (o.y == 0) break;  // (t, t) = 0
+      omega = o.z;  // (t, s) / (t, t)
       if (unk) {
         xv += alpha * ph + omega * sh;
         r = s - omega * tv;

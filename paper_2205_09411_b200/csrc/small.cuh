@@ -58,14 +58,23 @@ __device__ __forceinline__ void gs_tab_cell(const LevelView& L, const double* __
     double s = -h2 * g;  // :668-671
     for (int d = 0; d < 2 * D; ++d) s += p[d];
     nv = -s * (-1.0 / (2.0 * D));
-  } else {
-    double num = g;  // :677-683
-    for (int d = 0; d < 2 * D; ++d) {
-      num -= L.r_nb[code * 2 * D + d] * p[d];
-      const double b = L.r_bc[code * 2 * D + d];
-      if (b != 0) num -= b * phi_b[L.r_obj[code * 2 * D + d]];
+  } else {  // :677-683, from the row-coefficient table (bc * phi_b folded: one round trip)
+    const double2* c2 = reinterpret_cast<const double2*>(L.r_coef) + (size_t)code * 8;
+    double cf[14];
+#pragma unroll
+    for (int u = 0; u < 7; ++u) {
+      const double2 v = c2[u];
+      cf[2 * u] = v.x;
+      cf[2 * u + 1] = v.y;
     }
-    nv = num / L.r_center[code];
+    const int bm = (int)cf[13];
+    double num = g;
+#pragma unroll
+    for (int d = 0; d < 2 * D; ++d) {
+      num -= cf[1 + d] * p[d];
+      if ((bm >> d) & 1) num -= cf[7 + d];
+    }
+    nv = num / cf[0];
   }
   L.phi[a] = nv;
 }

@@ -232,11 +232,25 @@ __device__ __forceinline__ double apply_value(const LevelView& L,
     for (int d = 0; d < 2 * D; ++d) s += p[d];
     return s * L.w;
   }
-  double s = L.r_center[r] * self;
+  // special row from the level's row-coefficient table (capi.cu
+  // build_row_coef: center, nb[6], bc * phi_b[obj] per cut side, side mask),
+  // so the row costs one round trip after its code: the same products and
+  // order as center*self + sum(nb p + bc phi_b) (stencil.hpp:273-284)
+  (void)phi_b;
+  const double2* c2 = reinterpret_cast<const double2*>(L.r_coef) + (size_t)r * 8;
+  double cf[14];
+#pragma unroll
+  for (int u = 0; u < 7; ++u) {
+    const double2 v = c2[u];
+    cf[2 * u] = v.x;
+    cf[2 * u + 1] = v.y;
+  }
+  const int bm = (int)cf[13];
+  double s = cf[0] * self;
+#pragma unroll
   for (int d = 0; d < 2 * D; ++d) {
-    s += L.r_nb[r * 2 * D + d] * p[d];
-    const double b = L.r_bc[r * 2 * D + d];
-    if (b != 0) s += b * phi_b[L.r_obj[r * 2 * D + d]];
+    s += cf[1 + d] * p[d];
+    if ((bm >> d) & 1) s += cf[7 + d];
   }
   return s;
 }
@@ -249,13 +263,7 @@ __device__ __forceinline__ double resid_value(const LevelView& L,
     for (int d = 0; d < 2 * D; ++d) s += p[d];
     return g - s * L.w;
   }
-  double s = L.r_center[r] * self;
-  for (int d = 0; d < 2 * D; ++d) {
-    s += L.r_nb[r * 2 * D + d] * p[d];
-    const double b = L.r_bc[r * 2 * D + d];
-    if (b != 0) s += b * phi_b[L.r_obj[r * 2 * D + d]];
-  }
-  return g - s;
+  return g - apply_value<D>(L, phi_b, r, self, p);
 }
 
 }  // namespace pmgdev
