@@ -570,7 +570,9 @@ static void upload_stencils(Ctx& c) {
           else if (m.cnbr[(size_t)pid * 6 + dir] >= 0) ok = false;
           else pn[ax] = -1;
         }
-        const int32_t e[8] = {s, m.slot_of[(size_t)pid], oct, pn[0], pn[1], pn[2], kindv[(size_t)l][(size_t)s], 0};
+        int edge = 0;  // a face of the fine block without a same-level neighbour
+        for (int dir = 0; dir < 6; ++dir) edge |= m.nbr[(size_t)id * 6 + dir] < 0;
+        const int32_t e[8] = {s, m.slot_of[(size_t)pid], oct, pn[0], pn[1], pn[2], kindv[(size_t)l][(size_t)s], edge};
         pp.insert(pp.end(), e, e + 8);
       }
       d.n_pp = ok ? (int)pp.size() / 8 : -1;
@@ -835,7 +837,12 @@ static void enq_v_span(Ctx& c, int top) {
   }
   enq_coarse(c);
   for (int l = 2; l <= top; ++l) {
+    // the red half-sweep that follows overwrites every red cell the
+    // prolongation would write, except where a physical-face ghost reads it
+    const char* ex = getenv("PMG_EXP");
+    c.prolong_dead = c.cfg.n_up > 0 && !(ex && (atoi(ex) & 2)) ? 0 : -1;
     c.ops->prolong(c, l, false);
+    c.prolong_dead = -1;
     enq_smooth(c, l, c.cfg.n_up);
     c.ops->record(c, l);
   }

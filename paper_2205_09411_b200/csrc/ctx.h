@@ -242,6 +242,9 @@ struct Ctx {
   pmg_mg_cfg_t cfg{2, 2, 1e-6, 2000, 1};
   bool solver = false;
   bool have_guess = false;
+  // colour whose prolonged values the caller overwrites next (the V-cycle's
+  // first post-smoothing half-sweep), -1: every cell (the op-level API)
+  int prolong_dead = -1;
   std::unique_ptr<Ops> ops;
   Graph g_v, g_fmg[2], g_measure;
   bool graphs_dirty = true;

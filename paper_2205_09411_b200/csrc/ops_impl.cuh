@@ -317,7 +317,7 @@ struct OpsImpl final : Ops {
       }
       const int grid = std::min(d.n_pp, c.sms * MINB);
       pdl_launch(k_prolong_stream<N, ST, MINB, FULL>, grid, PStream3<N>::THR, smem, c.stream, 
-          V(c, l), V(c, l - 1), (const int4*)d.pp_plan.p, d.n_pp);
+          V(c, l), V(c, l - 1), (const int4*)d.pp_plan.p, d.n_pp, FULL ? -1 : c.prolong_dead);
       if (d.n_pin > 0)  // inside cells were interpolated too: restore their pins
         pdl_launch(k_pin_list, grid_for(d.n_pin, 256), 256, 0, c.stream, V(c, l).phi, c.phi_b.p,
                                                                   (const int2*)d.pin_list.p, d.n_pin);

@@ -1245,9 +1245,14 @@ __device__ __forceinline__ void pr_issue_async(const LevelView& Lp, const int4& 
   }
 }
 
+// dead >= 0: the caller overwrites every cell of that colour next (the
+// V-cycle's first post-smoothing half-sweep, multigrid.hpp:491-498), so in
+// blocks without a physical / coarse-fine face -- where no ghost reads a cell
+// of that colour -- those cells are neither read nor written.
 template <int N, int S_STAGES, int MINB, bool FULL>
 __global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(LevelView Lf, LevelView Lp,
-                                                                          const int4* __restrict__ plan, int n) {
+                                                                          const int4* __restrict__ plan, int n,
+                                                                          int dead) {
   pdl_begin();
   using S = PStream3<N>;
   constexpr int NI = N * N * N, HN = S::HN, PE = S::PE;
@@ -1275,6 +1280,10 @@ __global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(Level
       meta[s][1] = b;
       if (FULL) {
         mbar_arrive_expect_tx(&full[s], 0);
+      } else if (dead >= 0 && !b.w) {  // the live colour only
+        const int lc = 1 - dead;
+        mbar_arrive_expect_tx(&full[s], S::H * 8);
+        bulk_g2s(st + S::OF + lc * S::H, Lf.phi + (size_t)a.x * NI + (size_t)lc * S::H, S::H * 8, &full[s]);
       } else {
         mbar_arrive_expect_tx(&full[s], 2 * S::H * 8);
         bulk_g2s(st + S::OF, Lf.phi + (size_t)a.x * NI, 2 * S::H * 8, &full[s]);
@@ -1330,6 +1339,7 @@ __global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(Level
     __syncthreads();
     const double* Dt = st + S::ORP;
     double* __restrict__ dst = Lf.phi + (size_t)slot * NI;
+    const int skipc = (!FULL && dead >= 0 && !b.w) ? dead : -1;
 #pragma unroll
     for (int q = 0; q < S::PER; ++q) {
       const int ctr = ctr0 + q * (KS / 2) * PE * PE;
@@ -1340,6 +1350,7 @@ __global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(Level
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int c = h ? 1 - c0 : c0;
+        if (c == skipc) continue;
         double v = (1.0 - 0.25 * 3) * dc;  // multigrid.hpp:742-752
         v += 0.25 * (h ? dxp : dxm);
         v += 0.25 * dy;
