@@ -155,6 +155,20 @@ int pmg_b200_restrict_only(pmg_b200_ctx* ctx, int level);
 int pmg_b200_fas_level(pmg_b200_ctx* ctx, int level);
 int pmg_b200_level_record(pmg_b200_ctx* ctx, int level, double* out3);
 
+/* ---- post-solve fields -------------------------
+ * pmg::face_gradient (proj/include/pmg/fields.hpp:149-232): the staggered
+ * gradient of PHI on the faces of every leaf cell -- centred difference on
+ * regular faces, (phi_b - phi)/(d dx) from the solved side on faces cut by a
+ * boundary, 0 inside objects -- with ghosts filled as the reference's
+ * fill_ghosts would.  Leaves in dump order (level-major, x-major inside a
+ * level; mesh.hpp:229-235).  faces: n_leaves x dim x (N+1) N^(dim-1) doubles,
+ * per axis in FaceField::face_index order (fields.hpp:80-89).  magnitude
+ * (optional): the cell-centred |grad| the reference writes to var_out,
+ * n_leaves x N^dim, x-fastest.  leaf_ids (optional): the leaves' block ids.
+ * var must be 0 (VAR_PHI). */
+int pmg_b200_n_leaves(pmg_b200_ctx* ctx);
+int pmg_b200_face_gradient(pmg_b200_ctx* ctx, int var, double* faces, double* magnitude, int32_t* leaf_ids);
+
 /* Average device time (CUDA events on pmg_b200_stream) of `reps` back-to-back
  * launches of one phase, after one untimed launch:
  *   op 0: GS-RB half-sweep on `level` (parities alternate)

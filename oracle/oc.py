@@ -214,6 +214,23 @@ class Oracle:
         assert buf.size == self.n_blocks * self.S
         self._check(self.lib.oc_set_field(self.h, var, buf))
 
+    def face_gradient(self, var=0, var_out=4):
+        """pmg::face_gradient on the reference build (fields.hpp:149-232): (leaf_ids,
+        faces[leaf, axis, face_index]); the magnitude lands in field var_out."""
+        fn = getattr(self.lib, "oc_face_gradient", None)
+        if fn is None:
+            raise NotImplementedError("face_gradient: reference build only")
+        fn.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+        nl = fn(self.h, var, var_out, None, None)
+        if nl < 0:
+            self._check(-1)
+        pa = (self.N + 1) * self.N ** (self.dim - 1)
+        faces = np.zeros((nl, self.dim, pa))
+        ids = np.zeros(nl, np.int32)
+        if fn(self.h, var, var_out, faces.ctypes.data, ids.ctypes.data) != nl:
+            self._check(-1)
+        return ids, faces
+
     def get_field(self, var):
         buf = np.zeros(self.n_blocks * self.S)
         self._check(self.lib.oc_get_field(self.h, var, buf))

@@ -95,6 +95,12 @@ int oc_coarse_get(oc_ctx* h, int32_t* rp, int32_t* ci, double* val, double* c0,
  * state (b and x0 assembled as in multigrid.hpp:443-453), without changing it */
 int oc_bicgstab_probe(oc_ctx* h, int32_t* converged, int32_t* iters, double* rel);
 
+/* post-solve fields, REFERENCE BUILD ONLY (libpmgref.so): pmg::face_gradient
+ * (fields.hpp:149-232) with var_out; faces[n_leaves][dim][(N+1) N^(dim-1)] in
+ * FaceField order, leaf_ids[n_leaves]; either may be NULL.  Returns the
+ * number of leaves, or < 0 on error. */
+int oc_face_gradient(oc_ctx* h, int var, int var_out, double* faces, int32_t* leaf_ids);
+
 #ifdef __cplusplus
 }
 #endif

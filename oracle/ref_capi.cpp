@@ -15,6 +15,7 @@
 //   oc_residual_level      -> pmg::residual_block per block  stencil.hpp:325-359
 //   oc_solver_create/...   -> pmg::MgSolver<D>               multigrid.hpp:292-792
 //   oc_coarse_*            -> MgSolver::coarse_system        multigrid.hpp:474
+//   oc_face_gradient       -> pmg::face_gradient             fields.hpp:149-232
 #include <limits>  // levelset.hpp uses numeric_limits without including it
 #include <memory>
 #include <string>
@@ -54,6 +55,7 @@ struct Base {
   virtual int coarse_sizes(int32_t*, int32_t*, int32_t*) = 0;
   virtual int coarse_get(int32_t*, int32_t*, double*, double*, double*, int32_t*, int32_t*) = 0;
   virtual int probe(int32_t*, int32_t*, double*) = 0;
+  virtual int face_grad(int var, int var_out, double* faces, int32_t* ids) = 0;
 };
 
 enum Op {
@@ -351,7 +353,21 @@ struct Impl final : Base {
     *iters = res.iters;
     *rel = res.rel;
     return 0;
+  }  // pmg::face_gradient (fields.hpp:149-232): faces flattened per leaf, axis
+  int face_grad(int var, int var_out, double* faces, int32_t* ids) override {
+    const FaceField<D> ff = pmg::face_gradient<D>(mesh, set, var, var_out);
+    size_t k = 0;
+    for (size_t b = 0; b < ff.block_ids.size(); ++b) {
+      if (ids) ids[b] = ff.block_ids[b];
+      for (int a = 0; a < D; ++a)
+        for (double v : ff.faces[b][static_cast<size_t>(a)]) {
+          if (faces) faces[k] = v;
+          ++k;
+        }
+    }
+    return static_cast<int>(ff.block_ids.size());
   }
+
   double tol = 1e-6;
   int max_iters = 2000;
 };
@@ -495,4 +511,15 @@ int oc_bicgstab_probe(oc_ctx* h, int32_t* conv, int32_t* iters, double* rel) {
   return guard(h, [&](Base& b) { return b.probe(conv, iters, rel); });
 }
 
+/* reference build only: pmg::face_gradient; returns the number of leaves (or < 0) */
+int oc_face_gradient(oc_ctx* h, int var, int var_out, double* faces, int32_t* leaf_ids) {
+  if (!h || !h->impl) return -1;
+  try {
+    h->err.clear();
+    return h->impl->face_grad(var, var_out, faces, leaf_ids);
+  } catch (const std::exception& e) {
+    h->err = e.what();
+    return -1;
+  }
+}
 }  // extern "C"

@@ -75,6 +75,7 @@ static void set_views(Ctx& c) {
     v.r_coef = d.r_coef.p;
     v.r_center = d.r_center.p;
     v.r_nb = d.r_nb.p;
+    v.r_d = d.r_d.p;
     v.r_bc = d.r_bc.p;
     v.r_obj = d.r_obj.p;
     v.r_mask = d.r_mask.p;
@@ -405,7 +406,7 @@ static void upload_stencils(Ctx& c) {
     LevelDev& d = *c.lev[(size_t)l];
     std::vector<int32_t> srow((size_t)d.nb, -1), row_of;
     std::vector<uint8_t> kind((size_t)d.nb, pmgdev::KIND_UNIFORM), mask;
-    std::vector<double> center, nbv, bcv;
+    std::vector<double> center, nbv, bcv, dv;
     std::vector<int8_t> obj, pin;
     int n_if = 0;
     for (int s = 0; s < d.nb; ++s) {
@@ -432,6 +433,7 @@ static void upload_stencils(Ctx& c) {
         for (int f = 0; f < F; ++f) {
           nbv.push_back(st.nb[q * F + f]);
           bcv.push_back(st.bc[q * F + f]);
+          dv.push_back(st.d.empty() ? 1.0 : st.d[q * F + f]);
           obj.push_back(st.obj[q * F + f]);
         }
       }
@@ -505,6 +507,7 @@ static void upload_stencils(Ctx& c) {
     }
     d.r_center.upload(center, c.stream);
     d.r_nb.upload(nbv, c.stream);
+    d.r_d.upload(dv, c.stream);
     d.r_bc.upload(bcv, c.stream);
     d.r_obj.upload(obj, c.stream);
     d.r_mask.upload(mask, c.stream);
@@ -1548,6 +1551,41 @@ int pmg_b200_cycle_kernel_count(pmg_b200_ctx* h, int kind) {
   return rc == 0 ? k : -rc;
 }
 int pmg_b200_n_levels(pmg_b200_ctx* h) { return h && h->c.have_mesh ? h->c.mesh.L : 0; }
+int pmg_b200_n_leaves(pmg_b200_ctx* h) {
+  if (!h || !h->c.have_mesh) return 0;
+  int n = 0;
+  for (int id = 0; id < h->c.mesh.nb; ++id) n += h->c.mesh.children[(size_t)id * 8] < 0 ? 1 : 0;
+  return n;
+}
+int pmg_b200_face_gradient(pmg_b200_ctx* h, int var, double* faces, double* magnitude, int32_t* leaf_ids) {
+  return guard(h, [&](Ctx& c) {
+    need_mesh(c);
+    require(var == 0, "face_gradient: only VAR_PHI lives on the device");
+    require(faces != nullptr, "face_gradient: faces buffer required");
+    const HostMesh& m = c.mesh;
+    // leaves in dump order: level-major, x-major within a level (mesh.hpp:229-235, io.hpp:17-21)
+    std::vector<int2> tab;
+    std::vector<int32_t> ids;
+    for (int l = 1; l <= m.L; ++l)
+      for (int id : m.ref_order[(size_t)l])
+        if (m.children[(size_t)id * 8] < 0) {
+          tab.push_back(make_int2(l, m.slot_of[(size_t)id]));
+          ids.push_back(id);
+        }
+    const int nl = (int)tab.size();
+    int pa = c.N + 1;
+    for (int k = 1; k < c.dim; ++k) pa *= c.N;
+    const size_t nf = (size_t)nl * c.dim * pa, nm = (size_t)nl * c.NI;
+    c.leaf_tab.upload(tab, c.stream);
+    if (c.ff_faces.n < nf) c.ff_faces.alloc(nf);
+    if (magnitude && c.ff_mag.n < nm) c.ff_mag.alloc(nm);
+    c.ops->face_gradient(c, nl, c.ff_faces.p, magnitude ? c.ff_mag.p : nullptr);
+    PMG_CUDA(cudaMemcpyAsync(faces, c.ff_faces.p, nf * 8, cudaMemcpyDeviceToHost, c.stream));
+    if (magnitude) PMG_CUDA(cudaMemcpyAsync(magnitude, c.ff_mag.p, nm * 8, cudaMemcpyDeviceToHost, c.stream));
+    PMG_CUDA(cudaStreamSynchronize(c.stream));
+    if (leaf_ids) std::copy(ids.begin(), ids.end(), leaf_ids);
+  });
+}
 int pmg_b200_level_size(pmg_b200_ctx* h, int level) {
   if (!h || !h->c.have_mesh || level < 1 || level > h->c.mesh.L) return 0;
   return h->c.lev[(size_t)level]->nb;

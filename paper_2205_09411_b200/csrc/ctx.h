@@ -120,7 +120,7 @@ struct LevelDev {
   int n_own = 0;        // blocks this rank computes (nb unless set_owned restricted them)
   DevBuf<int32_t> nbr, cnbr, coords, parent, child, srow, bcoff, cfoff, row_of, slot_id;
   DevBuf<uint8_t> leaf, kind, r_mask;
-  DevBuf<double> phi, rhs, old, res, bcval, cfold, r_center, r_nb, r_bc;
+  DevBuf<double> phi, rhs, old, res, bcval, cfold, r_center, r_nb, r_bc, r_d;
   DevBuf<double> r_coef;  // 16 per row (capi.cu build_row_coef)
   DevBuf<int8_t> r_obj, r_pin, skind;
   DevBuf<int32_t> ref_slot;  // level_blocks order position -> slot
@@ -178,6 +178,9 @@ struct Ops {
   virtual void record(Ctx& c, int l) = 0;
   virtual void pins(Ctx& c, int l) = 0;
   virtual void coarse(Ctx& c) = 0;
+  // face_gradient (fields.hpp:149-232) of PHI over the leaves: faces[n_leaves][D][(N+1) N^(D-1)],
+  // optionally the cell-centred magnitude mag[n_leaves][N^D]
+  virtual void face_gradient(Ctx& c, int n_leaves, double* faces, double* mag) = 0;
   virtual void scatter(Ctx& c, int l, double* dst, const double* staging, const int32_t* slot_id,
                        int layout) = 0;
   virtual void gather(Ctx& c, int l, int var, double* staging, const int32_t* slot_id,
@@ -220,6 +223,8 @@ struct Ctx {
   std::vector<std::unique_ptr<LevelDev>> lev;  // index 0 unused
   DevBuf<double> phi_b;
   DevBuf<pmgdev::Rec> rec, partial;
+  DevBuf<int2> leaf_tab;            // (level, slot) of every leaf in dump order (io.hpp:17-21)
+  DevBuf<double> ff_faces, ff_mag;  // face_gradient scratch
   DevBuf<unsigned int> counter;
   DevBuf<double> stats;
   DevBuf<int> status;

@@ -9,6 +9,7 @@
 #include "coarse_cluster.cuh"
 #include "stream.cuh"
 #include "small.cuh"
+#include "fields.cuh"
 
 namespace pmghost {
 
@@ -521,6 +522,27 @@ struct OpsImpl final : Ops {
     for (int k = 0; k < D; ++k) lim *= 8;
     C.fallback_ok = c.coarse.n <= lim + 1;
     pdl_launch(k_coarse<D, N>, 1, 1024, 0, c.stream, V(c, 1), C, c.phi_b.p, c.rec.p, c.status.p, c.diag.p);
+    check();
+  }
+  void face_gradient(Ctx& c, int n_leaves, double* faces, double* mag) override {
+    constexpr long long PA = (N + 1) * (D == 3 ? N * N : N);
+    // the leaf table is level-major: one launch per level over its range
+    std::vector<int2> tab((size_t)n_leaves);
+    if (n_leaves > 0)
+      PMG_CUDA(cudaMemcpy(tab.data(), c.leaf_tab.p, (size_t)n_leaves * sizeof(int2), cudaMemcpyDeviceToHost));
+    for (int q0 = 0; q0 < n_leaves;) {
+      const int l = tab[(size_t)q0].x;
+      int q1 = q0;
+      while (q1 < n_leaves && tab[(size_t)q1].x == l) ++q1;
+      const int n = q1 - q0;
+      const int2* lv = (const int2*)c.leaf_tab.p + q0;
+      pdl_launch(k_face_gradient<D, N>, grid_for((long long)n * D * PA, 256), 256, 0, c.stream, V(c, l), Vc(c, l),
+                 lv, n, (const double*)c.phi_b.p, faces + (size_t)q0 * D * PA);
+      if (mag)
+        pdl_launch(k_face_magnitude<D, N>, grid_for((long long)n * G::NI, 256), 256, 0, c.stream, V(c, l), lv, n,
+                   (const double*)faces + (size_t)q0 * D * PA, mag + (size_t)q0 * G::NI);
+      q0 = q1;
+    }
     check();
   }
   void scatter(Ctx& c, int l, double* dst, const double* staging, const int32_t* slot_id,

@@ -64,6 +64,7 @@ struct LevelView {
   const double* r_coef;   // [R*16] center, nb[2D], bc*phi_b[2D], cut mask, inside flag
   const double* r_center; // [R]
   const double* r_nb;     // [R*2D]
+  const double* r_d;      // [R*2D] cut distances (face_gradient, fields.hpp:96-139)
   const double* r_bc;     // [R*2D]
   const int8_t* r_obj;    // [R*2D]
   const uint8_t* r_mask;  // [R]

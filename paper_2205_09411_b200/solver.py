@@ -30,6 +30,25 @@ class CycleStats:
     l2_resid: float = 0.0
 
 
+def face_gradient(dev: "DeviceMesh", var: int = 0, magnitude: bool = True):
+    """pmg::face_gradient (fields.hpp:149-232) on the device: the staggered
+    gradient of PHI on the faces of every leaf cell, leaves in dump order.
+
+    Returns (leaf_ids, faces, mag): faces[leaf, axis, FaceField::face_index]
+    with (N+1) N^(dim-1) faces per axis; mag[leaf, i + N (j + N k)] the
+    cell-centred magnitude the reference writes to var_out (None if not asked).
+    """
+    lib, h = dev.lib, dev.h
+    nl = lib.pmg_b200_n_leaves(h)
+    pa = (dev.N + 1) * dev.N ** (dev.dim - 1)
+    faces = np.zeros((nl, dev.dim, pa))
+    mag = np.zeros((nl, dev.NI)) if magnitude else None
+    ids = np.zeros(nl, np.int32)
+    dev._check(lib.pmg_b200_face_gradient(h, var, faces.reshape(-1),
+                                          mag.ctypes.data if magnitude else None, ids.ctypes.data))
+    return ids, faces, mag
+
+
 @dataclass
 class MgConfig:
     """pmg::MgConfig (multigrid.hpp:12-28); threads is accepted and ignored."""
