@@ -167,6 +167,13 @@ int pmg_b200_level_record(pmg_b200_ctx* ctx, int level, double* out3);
  * n_leaves x N^dim, x-fastest.  leaf_ids (optional): the leaves' block ids.
  * var must be 0 (VAR_PHI). */
 int pmg_b200_n_leaves(pmg_b200_ctx* ctx);
+/* pmg::error_norms with an AnalyticSolution (fields.hpp:9-69): PHI on every
+ * solved leaf cell against phi_b + a log(r/R) (tag 0, sphere2d) or
+ * phi_b + a (1 - R/r) (tag 1, sphere3d), r = |cell centre|; linf = max |d|,
+ * l2 = RMS (cells weighted by dx^dim when volume_weighted).  A solved cell
+ * with r < R fails with the reference's "analytic solution undefined inside". */
+int pmg_b200_error_norms(pmg_b200_ctx* ctx, int var, int tag, double phi_b, double a, double R,
+                         int volume_weighted, double* linf, double* l2);
 int pmg_b200_face_gradient(pmg_b200_ctx* ctx, int var, double* faces, double* magnitude, int32_t* leaf_ids);
 
 /* Average device time (CUDA events on pmg_b200_stream) of `reps` back-to-back

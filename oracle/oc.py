@@ -231,6 +231,17 @@ class Oracle:
             self._check(-1)
         return ids, faces
 
+    def error_norms(self, phi_b, a=1.0, R=0.25, sphere3d=True, volume_weighted=False, var=0):
+        """pmg::error_norms against pmg::AnalyticSolution on the reference build."""
+        fn = getattr(self.lib, "oc_error_norms", None)
+        if fn is None:
+            raise NotImplementedError("error_norms: reference build only")
+        fn.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int, C.c_void_p]
+        out = np.zeros(2)
+        if fn(self.h, var, 1 if sphere3d else 0, phi_b, a, R, int(volume_weighted), out.ctypes.data) != 0:
+            self._check(-1)
+        return float(out[0]), float(out[1])
+
     def get_field(self, var):
         buf = np.zeros(self.n_blocks * self.S)
         self._check(self.lib.oc_get_field(self.h, var, buf))

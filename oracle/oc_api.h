@@ -100,6 +100,9 @@ int oc_bicgstab_probe(oc_ctx* h, int32_t* converged, int32_t* iters, double* rel
  * FaceField order, leaf_ids[n_leaves]; either may be NULL.  Returns the
  * number of leaves, or < 0 on error. */
 int oc_face_gradient(oc_ctx* h, int var, int var_out, double* faces, int32_t* leaf_ids);
+/* REFERENCE BUILD ONLY: pmg::error_norms with AnalyticSolution{tag (0 sphere2d,
+ * 1 sphere3d), phi_b, a, R} (fields.hpp:9-69); out = {linf, l2} */
+int oc_error_norms(oc_ctx* h, int var, int tag, double phi_b, double a, double R, int vw, double* out);
 
 #ifdef __cplusplus
 }

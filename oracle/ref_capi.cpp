@@ -16,6 +16,7 @@
 //   oc_solver_create/...   -> pmg::MgSolver<D>               multigrid.hpp:292-792
 //   oc_coarse_*            -> MgSolver::coarse_system        multigrid.hpp:474
 //   oc_face_gradient       -> pmg::face_gradient             fields.hpp:149-232
+//   oc_error_norms         -> pmg::error_norms               fields.hpp:35-69
 #include <limits>  // levelset.hpp uses numeric_limits without including it
 #include <memory>
 #include <string>
@@ -56,6 +57,7 @@ struct Base {
   virtual int coarse_get(int32_t*, int32_t*, double*, double*, double*, int32_t*, int32_t*) = 0;
   virtual int probe(int32_t*, int32_t*, double*) = 0;
   virtual int face_grad(int var, int var_out, double* faces, int32_t* ids) = 0;
+  virtual int err_norms(int var, int tag, double phi_b, double a, double R, int vw, double* out) = 0;
 };
 
 enum Op {
@@ -353,7 +355,19 @@ struct Impl final : Base {
     *iters = res.iters;
     *rel = res.rel;
     return 0;
-  }  // pmg::face_gradient (fields.hpp:149-232): faces flattened per leaf, axis
+  }  // pmg::error_norms with pmg::AnalyticSolution (fields.hpp:35-69)
+  int err_norms(int var, int tag, double phi_b, double a, double R, int vw, double* out) override {
+    AnalyticSolution sol;
+    sol.tag = tag == 0 ? AnalyticSolution::Case::sphere2d : AnalyticSolution::Case::sphere3d;
+    sol.phi_b = phi_b;
+    sol.a = a;
+    sol.R = R;
+    const ErrorNorms e = pmg::error_norms<D>(mesh, set, var, sol, vw != 0);
+    out[0] = e.linf;
+    out[1] = e.l2;
+    return 0;
+  }
+  // pmg::face_gradient (fields.hpp:149-232): faces flattened per leaf, axis
   int face_grad(int var, int var_out, double* faces, int32_t* ids) override {
     const FaceField<D> ff = pmg::face_gradient<D>(mesh, set, var, var_out);
     size_t k = 0;
@@ -511,6 +525,17 @@ int oc_bicgstab_probe(oc_ctx* h, int32_t* conv, int32_t* iters, double* rel) {
   return guard(h, [&](Base& b) { return b.probe(conv, iters, rel); });
 }
 
+/* reference build only: pmg::error_norms(AnalyticSolution); out = {linf, l2} */
+int oc_error_norms(oc_ctx* h, int var, int tag, double phi_b, double a, double R, int vw, double* out) {
+  if (!h || !h->impl) return -1;
+  try {
+    h->err.clear();
+    return h->impl->err_norms(var, tag, phi_b, a, R, vw, out);
+  } catch (const std::exception& e) {
+    h->err = e.what();
+    return -1;
+  }
+}
 /* reference build only: pmg::face_gradient; returns the number of leaves (or < 0) */
 int oc_face_gradient(oc_ctx* h, int var, int var_out, double* faces, int32_t* leaf_ids) {
   if (!h || !h->impl) return -1;

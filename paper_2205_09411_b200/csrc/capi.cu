@@ -1557,26 +1557,66 @@ int pmg_b200_n_leaves(pmg_b200_ctx* h) {
   for (int id = 0; id < h->c.mesh.nb; ++id) n += h->c.mesh.children[(size_t)id * 8] < 0 ? 1 : 0;
   return n;
 }
+// leaves in dump order: level-major, x-major within a level (mesh.hpp:229-235,
+// io.hpp:17-21); uploads (level, slot) per leaf, returns the block ids
+static std::vector<int32_t> upload_leaf_tab(Ctx& c) {
+  const HostMesh& m = c.mesh;
+  std::vector<int2> tab;
+  std::vector<int32_t> ids;
+  for (int l = 1; l <= m.L; ++l)
+    for (int id : m.ref_order[(size_t)l])
+      if (m.children[(size_t)id * 8] < 0) {
+        tab.push_back(make_int2(l, m.slot_of[(size_t)id]));
+        ids.push_back(id);
+      }
+  c.leaf_tab.upload(tab, c.stream);
+  return ids;
+}
+int pmg_b200_error_norms(pmg_b200_ctx* h, int var, int tag, double phi_b, double a, double R,
+                         int volume_weighted, double* linf, double* l2) {
+  return guard(h, [&](Ctx& c) {
+    need_mesh(c);
+    require(var == 0, "error_norms: only VAR_PHI lives on the device");
+    require(tag == 0 || tag == 1, "error_norms: tag 0 (sphere2d) or 1 (sphere3d)");
+    require(linf && l2, "error_norms: output pointers required");
+    const std::vector<int32_t> ids = upload_leaf_tab(c);
+    const int nl = (int)ids.size();
+    std::vector<double> org((size_t)nl * 3);
+    for (int q = 0; q < nl; ++q)
+      for (int k = 0; k < 3; ++k) org[(size_t)q * 3 + k] = c.mesh.origin[(size_t)ids[(size_t)q] * 3 + k];
+    DevBuf<double> dorg, part;
+    DevBuf<int> err;
+    dorg.upload(org, c.stream);
+    part.alloc((size_t)nl * c.NI / 256 * 3 + 3 * (c.mesh.L + 2) + 3);
+    err.alloc(1);
+    PMG_CUDA(cudaMemsetAsync(err.p, 0, sizeof(int), c.stream));
+    const int nb = c.ops->error_norms(c, nl, dorg.p, tag, phi_b, a, R, volume_weighted, part.p, err.p);
+    std::vector<double> hp((size_t)nb * 3);
+    int herr = 0;
+    if (nb > 0) PMG_CUDA(cudaMemcpyAsync(hp.data(), part.p, hp.size() * 8, cudaMemcpyDeviceToHost, c.stream));
+    PMG_CUDA(cudaMemcpyAsync(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    PMG_CUDA(cudaStreamSynchronize(c.stream));
+    if (herr) throw std::domain_error("analytic solution undefined inside");
+    double mx = 0, ss = 0, ws = 0;  // fixed order: the CTAs of each level in dump order
+    for (int b = 0; b < nb; ++b) {
+      mx = std::max(mx, hp[(size_t)b * 3]);
+      ss += hp[(size_t)b * 3 + 1];
+      ws += hp[(size_t)b * 3 + 2];
+    }
+    *linf = mx;
+    *l2 = ws > 0 ? std::sqrt(ss / ws) : 0;
+  });
+}
 int pmg_b200_face_gradient(pmg_b200_ctx* h, int var, double* faces, double* magnitude, int32_t* leaf_ids) {
   return guard(h, [&](Ctx& c) {
     need_mesh(c);
     require(var == 0, "face_gradient: only VAR_PHI lives on the device");
     require(faces != nullptr, "face_gradient: faces buffer required");
-    const HostMesh& m = c.mesh;
-    // leaves in dump order: level-major, x-major within a level (mesh.hpp:229-235, io.hpp:17-21)
-    std::vector<int2> tab;
-    std::vector<int32_t> ids;
-    for (int l = 1; l <= m.L; ++l)
-      for (int id : m.ref_order[(size_t)l])
-        if (m.children[(size_t)id * 8] < 0) {
-          tab.push_back(make_int2(l, m.slot_of[(size_t)id]));
-          ids.push_back(id);
-        }
-    const int nl = (int)tab.size();
+    const std::vector<int32_t> ids = upload_leaf_tab(c);
+    const int nl = (int)ids.size();
     int pa = c.N + 1;
     for (int k = 1; k < c.dim; ++k) pa *= c.N;
     const size_t nf = (size_t)nl * c.dim * pa, nm = (size_t)nl * c.NI;
-    c.leaf_tab.upload(tab, c.stream);
     if (c.ff_faces.n < nf) c.ff_faces.alloc(nf);
     if (magnitude && c.ff_mag.n < nm) c.ff_mag.alloc(nm);
     c.ops->face_gradient(c, nl, c.ff_faces.p, magnitude ? c.ff_mag.p : nullptr);

@@ -181,6 +181,10 @@ struct Ops {
   // face_gradient (fields.hpp:149-232) of PHI over the leaves: faces[n_leaves][D][(N+1) N^(D-1)],
   // optionally the cell-centred magnitude mag[n_leaves][N^D]
   virtual void face_gradient(Ctx& c, int n_leaves, double* faces, double* mag) = 0;
+  // error_norms against the analytic sphere solution (fields.hpp:35-69): fills
+  // `part` with 3 doubles per CTA (max |d|, sum w d^2, sum w), returns the CTA count
+  virtual int error_norms(Ctx& c, int n_leaves, const double* origin, int tag, double phi_b, double a,
+                          double R, int vw, double* part, int* err) = 0;
   virtual void scatter(Ctx& c, int l, double* dst, const double* staging, const int32_t* slot_id,
                        int layout) = 0;
   virtual void gather(Ctx& c, int l, int var, double* staging, const int32_t* slot_id,

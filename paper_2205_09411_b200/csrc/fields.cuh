@@ -141,3 +141,57 @@ __global__ void __launch_bounds__(256) k_face_magnitude(LevelView L, const int2*
 }
 
 }  // namespace pmgdev
+
+namespace pmgdev {
+
+// error_norms against the analytic sphere solution (fields.hpp:9-58): per
+// leaf solved cell d = phi - exact(cell centre) with exact = phi_b + a log(r/R)
+// (2D) or phi_b + a (1 - R/r) (3D), r = |x| (core.hpp:58-67); per CTA
+// {max |d|, sum w d^2, sum w} into part[blockIdx.x]; *err = 1 when a solved
+// cell lies inside r < R (the reference throws std::domain_error)
+template <int D, int N>
+__global__ void __launch_bounds__(256) k_error_norms(LevelView L, const int2* __restrict__ leaves,
+                                                    const double* __restrict__ origin, int n_leaves, int tag,
+                                                    double phi_b, double a, double R, int vw,
+                                                    double* __restrict__ part, int* err) {
+  pdl_begin();
+  using G = Geo<D, N>;
+  __shared__ double red[72];
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  double mx = 0, ss = 0, ws = 0;
+  if (gid < (long long)n_leaves * G::NI) {
+    const int q = (int)(gid / G::NI), ii = (int)(gid % G::NI);
+    const int2 lv = leaves[q];
+    const int i3[3] = {ii % N, (ii / N) % N, D == 3 ? ii / (N * N) : 0};
+    const int r = row_index<D, N>(L, lv.y, G::colour(i3[0], i3[1], i3[2]), G::entry(i3[0], i3[1], i3[2]));
+    if (!(r >= 0 && L.r_mask[r] == 1)) {  // pinned cells are excluded
+      double s = 0;
+      for (int k = 0; k < D; ++k) {
+        const double x = origin[(size_t)q * 3 + k] + ((double)i3[k] + 0.5) * L.dx;
+        s += x * x;
+      }
+      const double rr = sqrt(s);
+      if (rr < R) *err = 1;
+      const double ex = tag == 0 ? phi_b + a * log(rr / R) : phi_b + a * (1.0 - R / rr);
+      const double diff = L.phi[G::addr(lv.y, i3[0], i3[1], i3[2])] - ex;
+      double w = 1.0;
+      if (vw) {
+        w = L.dx;
+        for (int k = 1; k < D; ++k) w *= L.dx;
+      }
+      mx = fabs(diff);
+      ss = w * diff * diff;
+      ws = w;
+    }
+  }
+  mx = block_max(mx, red);
+  ss = block_sum(ss, red);
+  ws = block_sum(ws, red);
+  if (threadIdx.x == 0) {
+    part[3 * blockIdx.x] = mx;
+    part[3 * blockIdx.x + 1] = ss;
+    part[3 * blockIdx.x + 2] = ws;
+  }
+}
+
+}  // namespace pmgdev

@@ -545,6 +545,26 @@ struct OpsImpl final : Ops {
     }
     check();
   }
+  int error_norms(Ctx& c, int n_leaves, const double* origin, int tag, double phi_b, double a, double R, int vw,
+                  double* part, int* err) override {
+    std::vector<int2> tab((size_t)n_leaves);
+    if (n_leaves > 0)
+      PMG_CUDA(cudaMemcpy(tab.data(), c.leaf_tab.p, (size_t)n_leaves * sizeof(int2), cudaMemcpyDeviceToHost));
+    int nb = 0;
+    for (int q0 = 0; q0 < n_leaves;) {
+      const int l = tab[(size_t)q0].x;
+      int q1 = q0;
+      while (q1 < n_leaves && tab[(size_t)q1].x == l) ++q1;
+      const int n = q1 - q0;
+      const unsigned g = grid_for((long long)n * G::NI, 256);
+      pdl_launch(k_error_norms<D, N>, g, 256, 0, c.stream, V(c, l), (const int2*)c.leaf_tab.p + q0,
+                 origin + (size_t)q0 * 3, n, tag, phi_b, a, R, vw, part + (size_t)nb * 3, err);
+      nb += (int)g;
+      q0 = q1;
+    }
+    check();
+    return nb;
+  }
   void scatter(Ctx& c, int l, double* dst, const double* staging, const int32_t* slot_id,
                int layout) override {
     const LevelView& L = V(c, l);

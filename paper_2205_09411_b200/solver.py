@@ -49,6 +49,17 @@ def face_gradient(dev: "DeviceMesh", var: int = 0, magnitude: bool = True):
     return ids, faces, mag
 
 
+def error_norms(dev: "DeviceMesh", phi_b: float, a: float = 1.0, R: float = 0.25, sphere3d: bool = True,
+                volume_weighted: bool = False, var: int = 0):
+    """pmg::error_norms against pmg::AnalyticSolution (fields.hpp:9-69) on the
+    device: (linf, l2) of PHI minus phi_b + a (1 - R/r) (3D) or
+    phi_b + a log(r/R) (2D) over the solved leaf cells."""
+    linf, l2 = C.c_double(), C.c_double()
+    dev._check(dev.lib.pmg_b200_error_norms(dev.h, var, 1 if sphere3d else 0, phi_b, a, R, int(volume_weighted),
+                                            C.byref(linf), C.byref(l2)))
+    return linf.value, l2.value
+
+
 @dataclass
 class MgConfig:
     """pmg::MgConfig (multigrid.hpp:12-28); threads is accepted and ignored."""

@@ -45,3 +45,44 @@ def test_face_gradient_bit_exact(name):
     assert np.count_nonzero(ref_faces) > 0
     ref_mag = interior(o, VAR_AUX, case.dim, case.N)[ref_ids]
     assert np.array_equal(mag, ref_mag.reshape(mag.shape))
+
+
+@pytest.mark.skipif(not os.path.exists(REF_SO), reason="reference build missing (make -C oracle ref)")
+@pytest.mark.parametrize("name", ["cfg1@4", "cfg2@3", "cfg3@5"])
+@pytest.mark.parametrize("vw", [False, True])
+def test_error_norms_match_reference(name, vw):
+    """pmg::error_norms against AnalyticSolution (fields.hpp:35-69).  The
+    analytic sphere sits at the origin, a corner of these domains: R is small
+    enough that no solved cell lies inside it.  3D evaluates sqrt and / only
+    (correctly rounded on both sides: linf bit-exact); 2D adds log (CUDA's log
+    vs glibc's: within an ulp); l2 sums in a different order."""
+    from paper_2205_09411_b200 import error_norms
+
+    case = cfgs.get_case(name)
+    o, dev, sol, mesh, st = setup_pair(case)
+    o.fmg_cycle()
+    o.v_cycle()
+    dev.set_field(VAR_PHI, interior(o, VAR_PHI, case.dim, case.N), layout=LAYOUT_INTERIOR)
+    s3 = case.dim == 3
+    ref = o.error_norms(1.0, 0.7, 1e-3, sphere3d=s3, volume_weighted=vw)
+    got = error_norms(dev, 1.0, 0.7, 1e-3, sphere3d=s3, volume_weighted=vw)
+    if s3:
+        assert got[0] == ref[0]
+    else:
+        assert abs(got[0] - ref[0]) <= 4e-16 * abs(ref[0]) + 1e-300
+    assert abs(got[1] - ref[1]) <= 1e-13 * abs(ref[1])
+
+
+@pytest.mark.skipif(not os.path.exists(REF_SO), reason="reference build missing (make -C oracle ref)")
+def test_error_norms_inside_raises_like_reference():
+    from paper_2205_09411_b200 import error_norms
+    from paper_2205_09411_b200._lib import PmgError
+    from oracle.oc import OracleError
+
+    case = cfgs.get_case("cfg2@3")
+    o, dev, sol, mesh, st = setup_pair(case)
+    with pytest.raises(OracleError) as e_ref:
+        o.error_norms(1.0, 1.0, 0.3)
+    with pytest.raises(PmgError) as e_gpu:
+        error_norms(dev, 1.0, 1.0, 0.3)
+    assert str(e_gpu.value) == str(e_ref.value) == "analytic solution undefined inside"
