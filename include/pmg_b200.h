@@ -167,6 +167,10 @@ int pmg_b200_level_record(pmg_b200_ctx* ctx, int level, double* out3);
  * n_leaves x N^dim, x-fastest.  leaf_ids (optional): the leaves' block ids.
  * var must be 0 (VAR_PHI). */
 int pmg_b200_n_leaves(pmg_b200_ctx* ctx);
+/* pmg::write_dump (proj/include/pmg/io.hpp:23-71): the "pmg dump 1" file of
+ * field `var` over the leaf blocks, byte-identical to the reference's; the
+ * field streams from the device one level at a time. */
+int pmg_b200_write_dump(pmg_b200_ctx* ctx, int var, const char* path, const char* field_name);
 /* pmg::error_norms with an AnalyticSolution (fields.hpp:9-69): PHI on every
  * solved leaf cell against phi_b + a log(r/R) (tag 0, sphere2d) or
  * phi_b + a (1 - R/r) (tag 1, sphere3d), r = |cell centre|; linf = max |d|,

@@ -15,9 +15,12 @@
 // run on the GPU box by tests/test_gpu_cpp_dropin.py.
 #include <cmath>
 #include <cstdio>
+#include <fstream>
+#include <iterator>
 #include <string>
 
 #include "pmg/harness.hpp"
+#include "pmg/io.hpp"
 #include "pmg_b200/solver.hpp"
 
 using namespace pmg;
@@ -220,6 +223,22 @@ void run(CaseConfig cfg) {
   if (dmax > 1e-10 * maxphi) {
     fail(name, "phi differs by " + std::to_string(dmax));
     return diagnose<Dim>(name, mesh0, set0);
+  }
+  // device-side dump (pmg_b200_write_dump) against the reference's write_dump
+  // (io.hpp:23-71) of the same field: mesh_b holds the GPU's PHI after the sync
+  {
+    std::string tag = name;
+    for (char& ch : tag)
+      if (ch == '/' || ch == ' ') ch = '_';
+    const std::string pa = "/tmp/pmg_dropin_ref_" + tag + ".dump", pb = "/tmp/pmg_dropin_gpu_" + tag + ".dump";
+    write_dump<Dim>(mesh_b, VAR_PHI, pa, "phi");
+    b200::detail::check(b.context(), pmg_b200_write_dump(b.context(), VAR_PHI, pb.c_str(), "phi"));
+    std::ifstream fa(pa, std::ios::binary), fb(pb, std::ios::binary);
+    const std::string da((std::istreambuf_iterator<char>(fa)), std::istreambuf_iterator<char>());
+    const std::string db((std::istreambuf_iterator<char>(fb)), std::istreambuf_iterator<char>());
+    std::remove(pa.c_str());
+    std::remove(pb.c_str());
+    if (da.empty() || da != db) return fail(name, "device dump differs from the reference's write_dump");
   }
   std::printf("ok   %-28s blocks %6d  resid %.3e -> %.3e (gpu %.3e)  max|dphi| %.2e\n", name.c_str(),
               mesh.n_blocks(), ha[0].max_resid, ha.back().max_resid, hb.back().max_resid, dmax);

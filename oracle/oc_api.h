@@ -104,6 +104,7 @@ int oc_face_gradient(oc_ctx* h, int var, int var_out, double* faces, int32_t* le
  * 1 sphere3d), phi_b, a, R} (fields.hpp:9-69); out = {linf, l2} */
 int oc_error_norms(oc_ctx* h, int var, int tag, double phi_b, double a, double R, int vw, double* out);
 
+
 #ifdef __cplusplus
 }
 #endif

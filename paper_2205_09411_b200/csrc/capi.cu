@@ -5,6 +5,7 @@
 // reference phase maps to one or more kernels (see kernels.cuh) and every
 // cycle type is captured once into a CUDA graph and replayed.
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -1571,6 +1572,59 @@ static std::vector<int32_t> upload_leaf_tab(Ctx& c) {
       }
   c.leaf_tab.upload(tab, c.stream);
   return ids;
+}
+// pmg::write_dump (io.hpp:23-71): "pmg dump 1" text header of the leaf blocks
+// (level-major, x-major inside a level), then every leaf interior as raw
+// little-endian float64, x fastest.  The field streams from the device one
+// level at a time (host memory bounded by the largest level).
+int pmg_b200_write_dump(pmg_b200_ctx* h, int var, const char* path, const char* field_name) {
+  return guard(h, [&](Ctx& c) {
+    need_mesh(c);
+    require(var >= 0 && var <= 3, "unsupported field variable");
+    require(path && field_name, "write_dump: path and field name required");
+    const HostMesh& m = c.mesh;
+    FILE* out = std::fopen(path, "wb");
+    require(out != nullptr, std::string("cannot open dump file: ") + path);
+    struct Closer {
+      FILE* f;
+      ~Closer() {
+        if (f) std::fclose(f);
+      }
+    } closer{out};
+    const int N = c.N, D = c.dim;
+    size_t nleaf = 0;
+    for (int id = 0; id < m.nb; ++id) nleaf += m.children[(size_t)id * 8] < 0 ? 1 : 0;
+    std::fprintf(out, "pmg dump 1\nfield %s\ndim %d\n", field_name, D);
+    for (int v = 0; v < 2; ++v) {
+      std::fprintf(out, v ? "domain_hi" : "domain_lo");
+      for (int k = 0; k < D; ++k) std::fprintf(out, " %.17g", v ? c.hi[k] : c.lo[k]);
+      std::fprintf(out, "\n");
+    }
+    std::fprintf(out, "block_size %d\nblocks %zu\n", N, nleaf);
+    size_t offset = 0;
+    for (int l = 1; l <= m.L; ++l)
+      for (int id : m.ref_order[(size_t)l]) {
+        if (m.children[(size_t)id * 8] >= 0) continue;
+        std::fprintf(out, "block %d", l);
+        for (int k = 0; k < D; ++k) std::fprintf(out, " %d", m.coords[(size_t)id * 3 + k] * N);
+        std::fprintf(out, " %zu\n", offset);
+        offset += (size_t)c.NI;
+      }
+    std::fprintf(out, "data_doubles %zu\nDATA\n", offset);
+    std::vector<double> lvl;
+    for (int l = 1; l <= m.L; ++l) {
+      const LevelDev& d = *c.lev[(size_t)l];
+      if (d.n_leaf == 0) continue;
+      lvl.resize((size_t)d.nb * c.NI);
+      download_field(c, var, l, lvl.data(), PMG_LAYOUT_INTERIOR);  // reference (x-major) order
+      const auto& ro = m.ref_order[(size_t)l];
+      for (size_t q = 0; q < ro.size(); ++q)
+        if (m.children[(size_t)ro[q] * 8] < 0)
+          require(std::fwrite(lvl.data() + q * c.NI, sizeof(double), (size_t)c.NI, out) == (size_t)c.NI,
+                  std::string("failed writing dump file: ") + path);
+    }
+    require(std::fflush(out) == 0, std::string("failed writing dump file: ") + path);
+  });
 }
 int pmg_b200_error_norms(pmg_b200_ctx* h, int var, int tag, double phi_b, double a, double R,
                          int volume_weighted, double* linf, double* l2) {

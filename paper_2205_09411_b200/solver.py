@@ -14,6 +14,7 @@ Names, argument meaning and error behaviour follow pmg::MgSolver
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -47,6 +48,12 @@ def face_gradient(dev: "DeviceMesh", var: int = 0, magnitude: bool = True):
     dev._check(lib.pmg_b200_face_gradient(h, var, faces.reshape(-1),
                                           mag.ctypes.data if magnitude else None, ids.ctypes.data))
     return ids, faces, mag
+
+
+def write_dump(dev: "DeviceMesh", path: str, field_name: str = "phi", var: int = 0):
+    """pmg::write_dump (io.hpp:23-71) straight from the device: the "pmg dump 1"
+    file of the leaf blocks, byte-identical to the reference's."""
+    dev._check(dev.lib.pmg_b200_write_dump(dev.h, var, os.fsencode(path), field_name.encode()))
 
 
 def error_norms(dev: "DeviceMesh", phi_b: float, a: float = 1.0, R: float = 0.25, sphere3d: bool = True,

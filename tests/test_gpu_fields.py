@@ -86,3 +86,38 @@ def test_error_norms_inside_raises_like_reference():
     with pytest.raises(PmgError) as e_gpu:
         error_norms(dev, 1.0, 1.0, 0.3)
     assert str(e_gpu.value) == str(e_ref.value) == "analytic solution undefined inside"
+
+
+@pytest.mark.skipif(not os.path.exists(REF_SO), reason="reference build missing (make -C oracle ref)")
+@pytest.mark.parametrize("name", ["cfg1@4", "cfg3@5"])
+def test_write_dump_layout(name, tmp_path):
+    """pmg_b200_write_dump (io.hpp:23-71) parsed back the way pmg::read_dump
+    does (io.hpp:87-140): header fields, leaves level-major / x-major with their
+    cell origins and offsets, and the raw data equal to the reference's PHI of
+    those leaves.  Byte identity with the reference's own write_dump of the
+    same field is checked by the C++ drop-in driver (tests/test_gpu_cpp_dropin.py)."""
+    from paper_2205_09411_b200 import write_dump
+
+    case = cfgs.get_case(name)
+    o, dev, sol, mesh, st = setup_pair(case)
+    o.fmg_cycle()
+    o.v_cycle()
+    phi = interior(o, VAR_PHI, case.dim, case.N)
+    dev.set_field(VAR_PHI, phi, layout=LAYOUT_INTERIOR)
+    path = tmp_path / "gpu.dump"
+    write_dump(dev, str(path), "phi")
+    raw = path.read_bytes()
+    head, data = raw.split(b"DATA\n", 1)
+    lines = head.decode().splitlines()
+    assert lines[0] == "pmg dump 1" and lines[1] == "field phi" and lines[2] == f"dim {case.dim}"
+    assert lines[5] == f"block_size {case.N}"
+    blocks = [ln.split() for ln in lines if ln.startswith("block ")]
+    leaves = [b for lvl in range(1, mesh.n_levels + 1) for b in mesh.level_blocks(lvl) if mesh.is_leaf(b)]
+    assert lines[6] == f"blocks {len(leaves)}" and len(blocks) == len(leaves)
+    vals = np.frombuffer(data, dtype="<f8")
+    assert vals.size == len(leaves) * case.N ** case.dim
+    for q, b in enumerate(leaves):
+        rec = blocks[q]
+        assert int(rec[1]) == mesh.level[b] and int(rec[-1]) == q * case.N ** case.dim
+        assert [int(x) for x in rec[2:-1]] == [c * case.N for c in mesh.coords[b][:case.dim]]
+        assert np.array_equal(vals[q * case.N ** case.dim:(q + 1) * case.N ** case.dim], phi[b])
