@@ -83,6 +83,7 @@ struct OpsImpl final : Ops {
           if (L.exp & (1 << 28)) launch_gs_stream<2, 3, T256>(c, L, d, parity);
           else if (L.exp & (1 << 29)) launch_gs_stream<2, 4, T256>(c, L, d, parity);
           else if (L.exp & (1 << 30)) launch_gs_stream<3, 2, T256>(c, L, d, parity);
+          else if (d.n_gs <= 1024) launch_gs_stream<2, 3, T256>(c, L, d, parity);  // 7.7 vs 8.0 us at 512 blocks
           else launch_gs_stream<kStreamStages, kStreamCtasPerSm, 0>(c, L, d, parity);
         }
 
@@ -112,7 +113,7 @@ struct OpsImpl final : Ops {
       }
       const int grid = std::min(d.n_gs, c.sms * MINB);
       pdl_launch(k_gs_stream<N, ST, MINB, TH>, grid, S::THR, smem, c.stream, L, parity, c.phi_b.p,
-                 (const int4*)d.gs_plan.p, d.n_gs);
+                 (const int4*)d.gs_plan.p, d.n_gs, (L.exp & 8) ? 0 : parity);
     }
   }
   // residual-streaming kernels: k_restrict_stream (one thread per parent) or
@@ -318,7 +319,8 @@ struct OpsImpl final : Ops {
       }
       const int grid = std::min(d.n_pp, c.sms * MINB);
       pdl_launch(k_prolong_stream<N, ST, MINB, FULL>, grid, PStream3<N>::THR, smem, c.stream, 
-          V(c, l), V(c, l - 1), (const int4*)d.pp_plan.p, d.n_pp, FULL ? -1 : c.prolong_dead);
+          V(c, l), V(c, l - 1), (const int4*)d.pp_plan.p, d.n_pp, FULL ? -1 : c.prolong_dead,
+          (V(c, l).exp & 8) ? 0 : 1);
       if (d.n_pin > 0)  // inside cells were interpolated too: restore their pins
         pdl_launch(k_pin_list, grid_for(d.n_pin, 256), 256, 0, c.stream, V(c, l).phi, c.phi_b.p,
                                                                   (const int2*)d.pin_list.p, d.n_pin);

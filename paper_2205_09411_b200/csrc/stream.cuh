@@ -96,16 +96,22 @@ template <int S>
 struct PlanRing {
   static constexpr int PK = S + 2, PR = PK + 1;
   int4* ring;  // [PR][2] in shared memory
+  int rev_n = 0;  // > 0: the plan is walked backwards (entry n - 1 - p), see pidx
   int4 held;
+  // plan entry of local block b (the CTA's b-th: p = blockIdx.x + b G)
+  __device__ __forceinline__ int pidx(int b, int G) const {
+    const int p = (int)blockIdx.x + b * G;
+    return rev_n ? rev_n - 1 - p : p;
+  }
   __device__ __forceinline__ void init(const int4* __restrict__ plan, int nmine, int G) {  // caller syncs
     const int nb = nmine < PK ? nmine : PK;
     for (int q = threadIdx.x; q < 2 * nb; q += blockDim.x)
-      ring[((q >> 1) % PR) * 2 + (q & 1)] = __ldg(plan + 2 * ((int)blockIdx.x + (q >> 1) * G) + (q & 1));
+      ring[((q >> 1) % PR) * 2 + (q & 1)] = __ldg(plan + 2 * pidx(q >> 1, G) + (q & 1));
   }
   __device__ __forceinline__ void advance(const int4* __restrict__ plan, int it, int nmine, int G) {
     if (threadIdx.x < 2) {
       if (it >= 1 && it - 1 + PK < nmine) ring[((it - 1 + PK) % PR) * 2 + threadIdx.x] = held;
-      if (it + PK < nmine) held = __ldg(plan + 2 * ((int)blockIdx.x + (it + PK) * G) + threadIdx.x);
+      if (it + PK < nmine) held = __ldg(plan + 2 * pidx(it + PK, G) + threadIdx.x);
     }
   }
   __device__ __forceinline__ BlockPlan get(int b) const {
@@ -326,10 +332,14 @@ __device__ __forceinline__ void gs_stream_column(const LevelView& L, const doubl
 // GS-RB half-sweep of the lean 3D blocks (UNIFORM / IFACE blocks without
 // coarse-fine faces, in plan order).  Special rows are left alone: k_gs_cut
 // updates the cut rows afterwards, inside rows keep their pin.
+// rev: walk the plan backwards.  Alternating the direction between the two
+// half-sweeps makes each sweep start on the blocks the previous one wrote
+// last -- the ones still in the 126 MB L2.
 template <int N, int S_STAGES, int MINB, int TH>
 __global__ void __launch_bounds__(Stream3<N, TH>::THR, MINB) k_gs_stream(LevelView L, int parity,
                                                                         const double* __restrict__ phi_b,
-                                                                        const int4* __restrict__ plan, int n) {
+                                                                        const int4* __restrict__ plan, int n,
+                                                                        int rev) {
   pdl_begin();
   using S = Stream3<N, TH>;
   constexpr int NI = N * N * N;
@@ -342,7 +352,7 @@ __global__ void __launch_bounds__(Stream3<N, TH>::THR, MINB) k_gs_stream(LevelVi
   const int nmine = (int)blockIdx.x < n ? (n - 1 - (int)blockIdx.x) / G + 1 : 0;
   if (nmine == 0) return;
   __shared__ int4 pring[PlanRing<S_STAGES>::PR * 2];
-  PlanRing<S_STAGES> R{pring};
+  PlanRing<S_STAGES> R{pring, rev ? n : 0};
   if (t == 0) {
     for (int s = 0; s < S_STAGES; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
@@ -1249,10 +1259,12 @@ __device__ __forceinline__ void pr_issue_async(const LevelView& Lp, const int4& 
 // V-cycle's first post-smoothing half-sweep, multigrid.hpp:491-498), so in
 // blocks without a physical / coarse-fine face -- where no ghost reads a cell
 // of that colour -- those cells are neither read nor written.
+// rev: walk the plan backwards, so that the first post-smoothing half-sweep
+// (forward) starts on the blocks written last (still in L2).
 template <int N, int S_STAGES, int MINB, bool FULL>
 __global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(LevelView Lf, LevelView Lp,
                                                                           const int4* __restrict__ plan, int n,
-                                                                          int dead) {
+                                                                          int dead, int rev) {
   pdl_begin();
   using S = PStream3<N>;
   constexpr int NI = N * N * N, HN = S::HN, PE = S::PE;
@@ -1273,6 +1285,7 @@ __global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(Level
   }
   __syncthreads();
   auto issue = [&](int p, int s) {
+    if (rev) p = n - 1 - p;
     const int4 a = __ldg(plan + 2 * p), b = __ldg(plan + 2 * p + 1);
     double* st = sm + s * S::STAGE;
     if (t == 0) {
