@@ -336,24 +336,46 @@ def run_b200(args, case):
     import ctypes as C
     ptr = C.c_void_p(pinned.data_ptr())
 
-    def e2e_step():
+    def e2e_serial_step():
         dev._check(dev.lib.pmg_b200_upload_level_field(dev.h, VAR_RHS, L, ptr, LAYOUT_INTERIOR))
         sol.v_cycle_async()
         return sol.cycle_result()
 
-    for _ in range(max(1, args.warmup)):
-        e2e_step()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        e2e_step()
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    if ws > 1:
-        tt = torch.tensor([e2e_s], device="cuda")
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(tt.item())
+    def e2e_run(steps):
+        """K steps through the public API, double-buffered as a time-stepping
+        caller would: step k's rhs is staged (H2D on the copy stream) while step
+        k-1's V-cycle runs, committed (scattered into the field) at the start
+        of step k; every one of the K uploads and K stats reads is inside the
+        timed region (the first upload is not overlapped)."""
+        dev._check(dev.lib.pmg_b200_stage_field_async(dev.h, VAR_RHS, L, ptr, LAYOUT_INTERIOR))
+        for k in range(steps):
+            dev._check(dev.lib.pmg_b200_commit_staged_field(dev.h))
+            sol.v_cycle_async()
+            if k + 1 < steps:
+                dev._check(dev.lib.pmg_b200_stage_field_async(dev.h, VAR_RHS, L, ptr, LAYOUT_INTERIOR))
+            sol.cycle_result()
+
+    def timed(fn):
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        fn()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if ws > 1:
+            tt = torch.tensor([dt], device="cuda")
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            dt = float(tt.item())
+        return dt
+
+    e2e_run(max(3, args.warmup))
+    e2e_s = timed(lambda: e2e_run(args.steps))
     e2e_val = leaf * ws * args.steps / e2e_s
+    for _ in range(max(1, args.warmup)):
+        e2e_serial_step()
+    e2e_serial_s = timed(lambda: [e2e_serial_step() for _ in range(args.steps)])
+    e2e_serial_val = leaf * ws * args.steps / e2e_serial_s
     kernels = sol.kernel_count(0)
 
     cpu = None
@@ -384,7 +406,10 @@ def run_b200(args, case):
                                 "unit": "GB/s", "frac": vc_gbs / peak,
                                 "bytes_per_unknown": BV / leaf},
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(gL.nbytes),
-                    "d2h_bytes_per_step": 16 + 16 + 4},
+                    "d2h_bytes_per_step": 16 + 16 + 4,
+                    "mode": "public API per step: finest rhs H2D from pinned host memory (double-buffered: "
+                            "overlaps the previous step's V-cycle) + V-cycle + stats D2H",
+                    "serial_value": e2e_serial_val},
             "gpu_launches": kernels * args.steps,
             "kernels_per_step": kernels,
             "clocks": clk.summary(),

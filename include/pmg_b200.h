@@ -97,6 +97,15 @@ int pmg_b200_upload_level_field(pmg_b200_ctx* ctx, int var, int level, const dou
                                 int layout);
 int pmg_b200_download_level_field(pmg_b200_ctx* ctx, int var, int level, double* host,
                                   int layout);
+/* double-buffered upload (a new right-hand side per solve step, as in a
+ * time-stepping caller): stage_field_async starts the host->device copy of
+ * `host` (pinned for overlap; level 0 = all blocks, else level_blocks order)
+ * on the context's copy stream and returns at once -- it overlaps whatever the
+ * solver is running; commit_staged_field makes the solver stream wait for it
+ * and scatters it into field `var`.  The host buffer must stay valid until the
+ * commit has been issued. */
+int pmg_b200_stage_field_async(pmg_b200_ctx* ctx, int var, int level, const double* host, int layout);
+int pmg_b200_commit_staged_field(pmg_b200_ctx* ctx);
 
 /* ---- solver (MgSolver<Dim>, multigrid.hpp:292-792) ------------------------ */
 /* replaces: MgSolver(mesh, stencils, cfg) -- cfg.validate() then init() (:295-299) */

@@ -70,7 +70,7 @@ EXPORTS = [
     "pmg_b200_synchronize", "pmg_b200_time_op", "pmg_b200_coarse_info",
     "pmg_b200_set_owned", "pmg_b200_level_field_ptr", "pmg_b200_restrict_only", "pmg_b200_fas_level",
     "pmg_b200_level_record", "pmg_b200_n_leaves", "pmg_b200_face_gradient", "pmg_b200_error_norms",
-    "pmg_b200_write_dump",
+    "pmg_b200_write_dump", "pmg_b200_stage_field_async", "pmg_b200_commit_staged_field",
 ]
 
 _lib = None
@@ -134,6 +134,8 @@ def load():
     lib.pmg_b200_n_leaves.argtypes = [vp]
     lib.pmg_b200_face_gradient.argtypes = [vp, C.c_int, f64p, C.c_void_p, C.c_void_p]
     lib.pmg_b200_write_dump.argtypes = [vp, C.c_int, C.c_char_p, C.c_char_p]
+    lib.pmg_b200_stage_field_async.argtypes = [vp, C.c_int, C.c_int, C.c_void_p, C.c_int]
+    lib.pmg_b200_commit_staged_field.argtypes = [vp]
     lib.pmg_b200_error_norms.argtypes = [vp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int,
                                          C.POINTER(C.c_double), C.POINTER(C.c_double)]
     _lib = lib

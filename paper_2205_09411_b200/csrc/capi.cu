@@ -33,6 +33,9 @@ Ctx::~Ctx() {
   if (side) cudaStreamDestroy(side);
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
+  if (copy) cudaStreamDestroy(copy);
+  if (ev_staged) cudaEventDestroy(ev_staged);
+  if (ev_consumed) cudaEventDestroy(ev_consumed);
 }
 
 static void require(bool cond, const std::string& msg, int code = PMG_ERR_INVALID_ARG) {
@@ -1179,6 +1182,46 @@ static void upload_field(Ctx& c, int var, int level, const double* host, int lay
   }
 }
 
+// Double-buffered upload: the H2D copy runs on its own stream into a second
+// staging buffer (overlapping whatever the solver stream is doing, e.g. the
+// previous V-cycle); commit scatters it into the field on the solver stream.
+static void stage_field_async(Ctx& c, int var, int level, const double* host, int layout) {
+  need_mesh(c);
+  require(layout == PMG_LAYOUT_PADDED || layout == PMG_LAYOUT_INTERIOR, "bad layout");
+  require(var >= 0 && var <= 3, "unsupported field variable");
+  require(level >= 0 && level <= c.mesh.L, "level out of range");
+  if (!c.copy) {
+    PMG_CUDA(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking));
+    PMG_CUDA(cudaEventCreateWithFlags(&c.ev_staged, cudaEventDisableTiming));
+    PMG_CUDA(cudaEventCreateWithFlags(&c.ev_consumed, cudaEventDisableTiming));
+    PMG_CUDA(cudaEventRecord(c.ev_consumed, c.stream));
+  }
+  const size_t per = layout == PMG_LAYOUT_PADDED ? (size_t)c.S : (size_t)c.NI;
+  const size_t nblk = level > 0 ? (size_t)c.lev[(size_t)level]->nb : (size_t)c.mesh.nb;
+  if (c.stage2.n < nblk * per) {
+    PMG_CUDA(cudaStreamSynchronize(c.copy));
+    PMG_CUDA(cudaStreamSynchronize(c.stream));
+    c.stage2.alloc(nblk * per);
+  }
+  PMG_CUDA(cudaStreamWaitEvent(c.copy, c.ev_consumed, 0));  // the previous commit has read the buffer
+  PMG_CUDA(cudaMemcpyAsync(c.stage2.p, host, nblk * per * 8, cudaMemcpyHostToDevice, c.copy));
+  PMG_CUDA(cudaEventRecord(c.ev_staged, c.copy));
+  c.staged_var = var;
+  c.staged_level = level;
+  c.staged_layout = layout;
+}
+static void commit_staged_field(Ctx& c) {
+  require(c.staged_var >= 0, "no staged field (call pmg_b200_stage_field_async)", PMG_ERR_STATE);
+  PMG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_staged, 0));
+  for (int l = 1; l <= c.mesh.L; ++l) {
+    if (c.staged_level > 0 && l != c.staged_level) continue;
+    LevelDev& d = *c.lev[(size_t)l];
+    c.ops->scatter(c, l, var_ptr(d, c.staged_var), c.stage2.p, c.staged_level > 0 ? d.ref_slot.p : d.slot_id.p,
+                   c.staged_layout);
+  }
+  PMG_CUDA(cudaEventRecord(c.ev_consumed, c.stream));
+  c.staged_var = -1;
+}
 static void download_field(Ctx& c, int var, int level, double* host, int layout) {
   need_mesh(c);
   require(layout == PMG_LAYOUT_PADDED || layout == PMG_LAYOUT_INTERIOR, "bad layout");
@@ -1398,6 +1441,12 @@ int pmg_b200_upload_level_field(pmg_b200_ctx* h, int var, int level, const doubl
     need_level(c, level);
     upload_field(c, var, level, host, layout);
   });
+}
+int pmg_b200_stage_field_async(pmg_b200_ctx* h, int var, int level, const double* host, int layout) {
+  return guard(h, [&](Ctx& c) { stage_field_async(c, var, level, host, layout); });
+}
+int pmg_b200_commit_staged_field(pmg_b200_ctx* h) {
+  return guard(h, [&](Ctx& c) { commit_staged_field(c); });
 }
 int pmg_b200_download_level_field(pmg_b200_ctx* h, int var, int level, double* host, int layout) {
   return guard(h, [&](Ctx& c) {

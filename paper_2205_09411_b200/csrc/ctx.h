@@ -213,6 +213,11 @@ struct Ctx {
   int sms = 148;  // multiprocessors of `device`
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // forked branch for concurrent block classes
+  // double-buffered field upload (pmg_b200_stage_field_async / commit_staged_field)
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ev_staged = nullptr, ev_consumed = nullptr;
+  DevBuf<double> stage2;
+  int staged_var = -1, staged_level = 0, staged_layout = 0;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::string err;
 

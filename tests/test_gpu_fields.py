@@ -121,3 +121,39 @@ def test_write_dump_layout(name, tmp_path):
         assert int(rec[1]) == mesh.level[b] and int(rec[-1]) == q * case.N ** case.dim
         assert [int(x) for x in rec[2:-1]] == [c * case.N for c in mesh.coords[b][:case.dim]]
         assert np.array_equal(vals[q * case.N ** case.dim:(q + 1) * case.N ** case.dim], phi[b])
+
+
+def test_staged_upload_matches_plain_upload():
+    """pmg_b200_stage_field_async + commit_staged_field (the double-buffered
+    upload bench.py's e2e uses) leave exactly what upload_level_field leaves,
+    also when the next stage is issued while a V-cycle is in flight."""
+    import ctypes as C
+
+    from paper_2205_09411_b200 import DeviceMesh, MgConfig, MgSolver, StencilBuildConfig, build_stencils
+    from paper_2205_09411_b200.mesh import VAR_RHS
+
+    case = cfgs.get_case("cfg2@3")
+    mesh = case.build_mesh()
+    dev = DeviceMesh(mesh)
+    build_stencils(dev, case.lsf, StencilBuildConfig(w_min=case.w_min))
+    g = case.rhs_fields(mesh)
+    dev.set_field(VAR_RHS, g, layout=LAYOUT_INTERIOR)
+    sol = MgSolver(dev, None, MgConfig())
+    sol.fmg_cycle()
+    L = mesh.n_levels
+    rng = np.random.default_rng(7)
+    blocks = np.array(mesh.level_blocks(L))
+    vals = [np.ascontiguousarray(rng.standard_normal((len(blocks), case.N ** 3))) for _ in range(3)]
+    dev._check(dev.lib.pmg_b200_stage_field_async(dev.h, VAR_RHS, L, C.c_void_p(vals[0].ctypes.data),
+                                                  LAYOUT_INTERIOR))
+    for k in range(3):
+        dev._check(dev.lib.pmg_b200_commit_staged_field(dev.h))
+        got = dev.get_field(VAR_RHS, layout=LAYOUT_INTERIOR)[blocks]
+        assert np.array_equal(got, vals[k])
+        sol.v_cycle_async()
+        if k + 1 < 3:
+            dev._check(dev.lib.pmg_b200_stage_field_async(dev.h, VAR_RHS, L, C.c_void_p(vals[k + 1].ctypes.data),
+                                                          LAYOUT_INTERIOR))
+        sol.cycle_result()
+    with pytest.raises(Exception):
+        dev._check(dev.lib.pmg_b200_commit_staged_field(dev.h))  # nothing staged
