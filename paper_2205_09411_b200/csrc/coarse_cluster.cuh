@@ -71,7 +71,10 @@ __global__ void __launch_bounds__(CC<N, PPC>::THR, 1) k_coarse_cluster(LevelView
                                                                     const double* __restrict__ phi_b,
                                                                     Rec* rec, int* status,
                                                                     double* diag_out) {
-  pdl_begin();
+  // programmatic dependent launch: the static per-cell operator data below is
+  // loaded before waiting for the previous kernel (the FAS of level 1); PHI,
+  // the right-hand side and phi_b are read only after griddepcontrol.wait
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   using G = Geo<3, N>;
   using K = CC<N, PPC>;
   cg::cluster_group cl = cg::this_cluster();
@@ -109,11 +112,13 @@ __global__ void __launch_bounds__(CC<N, PPC>::THR, 1) k_coarse_cluster(LevelView
   double sc[6] = {0, 0, 0, 0, 0, 0};  // special-row off-diagonals, loaded once
   if (f & 0x80)
     for (int d = 0; d < 6; ++d) sc[d] = C.spec_c[(size_t)C.spec[ii] * 6 + d];
+  const double c0v = C.c0[ii];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const size_t a = G::addr(0, x, y, z);
   double xv = unk ? L.phi[a] : 0.0;
   double bv = 0;
   if (unk) {
-    bv = L.rhs[a] + C.c0[ii];
+    bv = L.rhs[a] + c0v;
     for (int q = C.ob_start[ii]; q < C.ob_start[ii + 1]; ++q) bv += C.ob_val[q] * phi_b[C.ob_obj[q]];
   }
   // Cluster-wide deterministic sum of (a, b) plus the scalar recurrence that

@@ -55,6 +55,23 @@ inline void pdl_launch(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStr
   PMG_CUDA(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
 }
 
+// the same, always with programmatic stream serialization (kernels that load
+// their static data before griddepcontrol.wait)
+template <typename... KArgs, typename... Args>
+inline void pdl_launch_on(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  PMG_CUDA(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
+}
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;

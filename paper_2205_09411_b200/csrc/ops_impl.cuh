@@ -42,8 +42,8 @@ struct OpsImpl final : Ops {
     if (L.nb <= kSmallLevel && !(L.exp & 32768)) {
       const LevelDev& d = *c.lev[(size_t)l];
       if (d.has_tab && !(L.exp & 65536))
-        pdl_launch(k_gs_tab<D, N>, grid_for((long long)L.nb * G::H), 256, 0, c.stream, L, c.phi_b.p,
-                   (const int4*)d.tab.p, (const double*)d.tgbc.p, parity);
+        pdl_launch_on(k_gs_tab<D, N>, grid_for((long long)L.nb * G::H), 256, 0, c.stream, L, c.phi_b.p,
+                      (const int4*)d.tab.p, (const double*)d.tgbc.p, parity);
       else
         pdl_launch(k_gs<D, N>, grid_for((long long)L.nb * G::H), kThreads, 0, c.stream, L, Vc(c, l), c.phi_b.p,
                    parity);
@@ -179,13 +179,13 @@ struct OpsImpl final : Ops {
       if (d.has_tab && !(Lf.exp & 65536)) {
         const LevelView& Lp = V(c, l - 1);
         if (mode == RM_RES)
-          pdl_launch(k_restrict_tab<D, N, RM_RES>, g, 256, 0, c.stream, Lf, Lp, c.phi_b.p, (const int4*)d.tab.p,
+          pdl_launch_on(k_restrict_tab<D, N, RM_RES>, g, 256, 0, c.stream, Lf, Lp, c.phi_b.p, (const int4*)d.tab.p,
                      (const double*)d.tgbc.p);
         else if (mode == RM_RHS)
-          pdl_launch(k_restrict_tab<D, N, RM_RHS>, g, 256, 0, c.stream, Lf, Lp, c.phi_b.p, (const int4*)d.tab.p,
+          pdl_launch_on(k_restrict_tab<D, N, RM_RHS>, g, 256, 0, c.stream, Lf, Lp, c.phi_b.p, (const int4*)d.tab.p,
                      (const double*)d.tgbc.p);
         else
-          pdl_launch(k_restrict_tab<D, N, RM_FUSED>, g, 256, 0, c.stream, Lf, Lp, c.phi_b.p,
+          pdl_launch_on(k_restrict_tab<D, N, RM_FUSED>, g, 256, 0, c.stream, Lf, Lp, c.phi_b.p,
                      (const int4*)d.tab.p, (const double*)d.tgbc.p);
         check();
         return;
@@ -275,10 +275,10 @@ struct OpsImpl final : Ops {
       const LevelDev& d = *c.lev[(size_t)lc];
       if (L.nb <= kSmallLevel && d.has_tab && !(L.exp & 98304)) {
         if (f)
-          pdl_launch(k_fas_tab<D, N, true>, grid_for((long long)L.nb * G::NI, 256), 256, 0, c.stream, L, c.phi_b.p,
+          pdl_launch_on(k_fas_tab<D, N, true>, grid_for((long long)L.nb * G::NI, 256), 256, 0, c.stream, L, c.phi_b.p,
                      (const int4*)d.tab.p, (const double*)d.tgbc.p);
         else
-          pdl_launch(k_fas_tab<D, N, false>, grid_for((long long)L.nb * G::NI, 256), 256, 0, c.stream, L,
+          pdl_launch_on(k_fas_tab<D, N, false>, grid_for((long long)L.nb * G::NI, 256), 256, 0, c.stream, L,
                      c.phi_b.p, (const int4*)d.tab.p, (const double*)d.tgbc.p);
         check();
         return;
@@ -459,7 +459,7 @@ struct OpsImpl final : Ops {
       at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       at[1].val.programmaticStreamSerializationAllowed = 1;
       cfgl.attrs = at;
-      cfgl.numAttrs = pdl_enabled() ? 2 : 1;
+      cfgl.numAttrs = (V(c, 1).exp & 1) ? 1 : 2;  // PDL: the static prologue overlaps the FAS of level 1
       PMG_CUDA(cudaLaunchKernelEx(&cfgl, k_coarse_cluster<N, PPC>, V(c, 1), F, (const double*)c.phi_b.p, c.rec.p,
                                   c.status.p, c.diag.p));
     }

@@ -19,11 +19,15 @@
 
 namespace pmgdev {
 
-template <int D>
+// the cell's table entry is static (host-built at setup), its values are not:
+// with programmatic dependent launch (PDL) the entry is loaded before
+// griddepcontrol.wait, overlapping the previous kernel's drain
+template <int D, bool PDL = false>
 __device__ __forceinline__ void tab_load(const LevelView& L, const int4* __restrict__ T,
                                          const double* __restrict__ gbc, int a, int& code, int& leaf,
                                          double& self, double* p) {
   const int4 e0 = T[2 * a], e1 = T[2 * a + 1];
+  if (PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
   code = e0.x;
   leaf = e1.w;
   const int na[6] = {e0.y, e0.z, e0.w, e1.x, e1.y, e1.z};
@@ -35,7 +39,7 @@ __device__ __forceinline__ void tab_load(const LevelView& L, const int4* __restr
 
 // gsrb_block half-sweep (multigrid.hpp:621-695) of cell gid of the colour
 // (gid < nb * H): the body of k_gs_tab and of the cluster tail (tail.cuh)
-template <int D, int N>
+template <int D, int N, bool PDL = false>
 __device__ __forceinline__ void gs_tab_cell(const LevelView& L, const double* __restrict__ phi_b,
                                             const int4* __restrict__ T, const double* __restrict__ gbc, int parity,
                                             int gid) {
@@ -44,7 +48,7 @@ __device__ __forceinline__ void gs_tab_cell(const LevelView& L, const double* __
   const int a = (gid / G::H) * G::NI + parity * G::H + gid % G::H;
   int code, leaf;
   double self, p[2 * D];
-  tab_load<D>(L, T, gbc, a, code, leaf, self, p);
+  tab_load<D, PDL>(L, T, gbc, a, code, leaf, self, p);
   if (code <= -3) return;  // inside: pinned
   const double g = L.rhs[a];
   const double h2 = L.h2;
@@ -83,16 +87,16 @@ template <int D, int N>
 __global__ void __launch_bounds__(256) k_gs_tab(LevelView L, const double* __restrict__ phi_b,
                                                const int4* __restrict__ T, const double* __restrict__ gbc,
                                                int parity) {
-  pdl_begin();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // PDL: see tab_load
   using G = Geo<D, N>;
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= L.nb * G::H) return;
-  gs_tab_cell<D, N>(L, phi_b, T, gbc, parity, gid);
+  gs_tab_cell<D, N, true>(L, phi_b, T, gbc, parity, gid);
 }
 
 // FAS right-hand side g = L(phi) + R(r) on non-leaf blocks, OLD <- PHI
 // (multigrid.hpp:380-397) of cell a (a < nb * NI)
-template <int D, int N, bool FAS>
+template <int D, int N, bool FAS, bool PDL = false>
 __device__ __forceinline__ void fas_tab_cell(const LevelView& L, const double* __restrict__ phi_b,
                                              const int4* __restrict__ T, const double* __restrict__ gbc, int a) {
   using G = Geo<D, N>;
@@ -100,13 +104,14 @@ __device__ __forceinline__ void fas_tab_cell(const LevelView& L, const double* _
   if (FAS) {
     int code, leaf;
     double self, p[2 * D];
-    tab_load<D>(L, T, gbc, a, code, leaf, self, p);
+    tab_load<D, PDL>(L, T, gbc, a, code, leaf, self, p);
     if (!leaf) {
       const double out = code <= -3 ? 0.0 : apply_value<D>(L, phi_b, code >= 0 ? code : -1, self, p);
       L.rhs[a] = out + L.rhs[a];
     }
     L.old[a] = self;
   } else {
+    if (PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
     L.old[a] = L.phi[a];
   }
 }
@@ -114,11 +119,11 @@ __device__ __forceinline__ void fas_tab_cell(const LevelView& L, const double* _
 template <int D, int N, bool FAS>
 __global__ void __launch_bounds__(256) k_fas_tab(LevelView L, const double* __restrict__ phi_b,
                                                 const int4* __restrict__ T, const double* __restrict__ gbc) {
-  pdl_begin();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // PDL: see tab_load
   using G = Geo<D, N>;
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= L.nb * G::NI) return;
-  fas_tab_cell<D, N, FAS>(L, phi_b, T, gbc, a);
+  fas_tab_cell<D, N, FAS, true>(L, phi_b, T, gbc, a);
 }
 
 // residual + restriction of a small level (multigrid.hpp:374-418, 697-722):
@@ -126,7 +131,7 @@ __global__ void __launch_bounds__(256) k_fas_tab(LevelView L, const double* __re
 // x-fastest order, pins the parent (apply_pins(l-1)) and writes it.  gid is
 // the child item; every lane of the warp must call it (the group sum is a
 // shuffle), items past the level are idle lanes.
-template <int D, int N, int MODE>
+template <int D, int N, int MODE, bool PDL = false>
 __device__ __forceinline__ void restrict_tab_item(const LevelView& Lf, const LevelView& Lp,
                                                   const double* __restrict__ phi_b, const int4* __restrict__ T,
                                                   const double* __restrict__ gbc, int gid) {
@@ -144,13 +149,15 @@ __device__ __forceinline__ void restrict_tab_item(const LevelView& Lf, const Lev
     if (MODE == RM_FUSED) {
       int code, leaf;
       double p[2 * D];
-      tab_load<D>(Lf, T, gbc, a, code, leaf, vphi, p);
+      tab_load<D, PDL>(Lf, T, gbc, a, code, leaf, vphi, p);
       vq = code <= -3 ? 0.0 : resid_value<D>(Lf, phi_b, code >= 0 ? code : -1, vphi, p, Lf.rhs[a]);
     } else {
+      if (PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
       vphi = Lf.phi[a];
       vq = MODE == RM_RES ? Lf.res[a] : Lf.rhs[a];
     }
   }
+  if (PDL && !live) asm volatile("griddepcontrol.wait;" ::: "memory");  // idle lanes: before the writes below
   const int base = threadIdx.x & ~(NC - 1) & 31;
   double sphi = 0, sq = 0;
 #pragma unroll
@@ -174,8 +181,8 @@ __device__ __forceinline__ void restrict_tab_item(const LevelView& Lf, const Lev
 template <int D, int N, int MODE>
 __global__ void __launch_bounds__(256) k_restrict_tab(LevelView Lf, LevelView Lp, const double* __restrict__ phi_b,
                                                      const int4* __restrict__ T, const double* __restrict__ gbc) {
-  pdl_begin();
-  restrict_tab_item<D, N, MODE>(Lf, Lp, phi_b, T, gbc, blockIdx.x * blockDim.x + threadIdx.x);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // PDL: see tab_load
+  restrict_tab_item<D, N, MODE, true>(Lf, Lp, phi_b, T, gbc, blockIdx.x * blockDim.x + threadIdx.x);
 }
 
 // leaf-residual record of cell a of a small level: accumulates into (mx, ss, cnt)
