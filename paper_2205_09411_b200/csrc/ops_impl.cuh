@@ -112,8 +112,12 @@ struct OpsImpl final : Ops {
         attr = true;
       }
       const int grid = std::min(d.n_gs, c.sms * MINB);
-      pdl_launch(k_gs_stream<N, ST, MINB, TH>, grid, S::THR, smem, c.stream, L, parity, c.phi_b.p,
-                 (const int4*)d.gs_plan.p, d.n_gs, (L.exp & 8) ? 0 : parity);
+      if (L.exp & 1)
+        pdl_launch(k_gs_stream<N, ST, MINB, TH>, grid, S::THR, smem, c.stream, L, parity, c.phi_b.p,
+                   (const int4*)d.gs_plan.p, d.n_gs, (L.exp & 8) ? 0 : parity);
+      else  // PDL: the prologue overlaps the previous kernel's drain
+        pdl_launch_on(k_gs_stream<N, ST, MINB, TH>, grid, S::THR, smem, c.stream, L, parity, c.phi_b.p,
+                      (const int4*)d.gs_plan.p, d.n_gs, (L.exp & 8) ? 0 : parity);
     }
   }
   // residual-streaming kernels: k_restrict_stream (one thread per parent) or

@@ -340,7 +340,9 @@ __global__ void __launch_bounds__(Stream3<N, TH>::THR, MINB) k_gs_stream(LevelVi
                                                                         const double* __restrict__ phi_b,
                                                                         const int4* __restrict__ plan, int n,
                                                                         int rev) {
-  pdl_begin();
+  // PDL: barrier setup and the (static) plan entries happen before waiting
+  // for the previous kernel, overlapping its drain
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   using S = Stream3<N, TH>;
   constexpr int NI = N * N * N;
   extern __shared__ __align__(128) double sm[];
@@ -358,6 +360,7 @@ __global__ void __launch_bounds__(Stream3<N, TH>::THR, MINB) k_gs_stream(LevelVi
     fence_mbar_init();
   }
   R.init(plan, nmine, G);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
   for (int s = 0; s < S_STAGES; ++s) {
     if (s < nmine) {
