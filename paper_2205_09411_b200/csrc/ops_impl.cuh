@@ -223,7 +223,7 @@ struct OpsImpl final : Ops {
         }
         const LevelDev& dp = *c.lev[(size_t)(l - 1)];
         if (dp.n_pin > 0)  // apply_pins(l-1)
-          pdl_launch(k_pin_list, grid_for(dp.n_pin, 256), 256, 0, c.stream, V(c, l - 1).phi, c.phi_b.p,
+          pdl_launch_on(k_pin_list, grid_for(dp.n_pin, 256), 256, 0, c.stream, V(c, l - 1).phi, c.phi_b.p,
                                                                     (const int2*)dp.pin_list.p, dp.n_pin);
         check();
         return;
@@ -326,7 +326,7 @@ struct OpsImpl final : Ops {
           V(c, l), V(c, l - 1), (const int4*)d.pp_plan.p, d.n_pp, FULL ? -1 : c.prolong_dead,
           (V(c, l).exp & 8) ? 0 : 1);
       if (d.n_pin > 0)  // inside cells were interpolated too: restore their pins
-        pdl_launch(k_pin_list, grid_for(d.n_pin, 256), 256, 0, c.stream, V(c, l).phi, c.phi_b.p,
+        pdl_launch_on(k_pin_list, grid_for(d.n_pin, 256), 256, 0, c.stream, V(c, l).phi, c.phi_b.p,
                                                                   (const int2*)d.pin_list.p, d.n_pin);
     }
   }

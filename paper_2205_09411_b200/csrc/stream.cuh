@@ -1124,11 +1124,19 @@ __global__ void __launch_bounds__(128) k_restrict_fix(LevelView Lf, LevelView Lp
 }
 
 // apply_pins (stencil.hpp:225-237) over a list of (cell address, object) pairs
+// the list and phi_b are static: loaded before griddepcontrol.wait (PDL)
 static __global__ void __launch_bounds__(256) k_pin_list(double* __restrict__ phi, const double* __restrict__ phi_b,
                                                  const int2* __restrict__ list, int n) {
-  pdl_begin();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q < n) phi[list[q].x] = phi_b[list[q].y];
+  int2 e = make_int2(0, 0);
+  double v = 0.0;
+  if (q < n) {
+    e = list[q];
+    v = phi_b[e.y];
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (q < n) phi[e.x] = v;
 }
 
 // Cut rows of the lean interface blocks after the streaming sweep
