@@ -239,6 +239,64 @@ def run_reference(args, case):
     return 0
 
 
+def run_partitioned(args, case):
+    """--partitioned: ONE problem Morton-partitioned over the torchrun ranks
+    (distributed.DistributedMgSolver: face-layer exchange after every phase
+    over torch.distributed / NCCL, coarse tail on rank 0).
+    Strong scaling; the time of a V-cycle is the max over ranks.  The driver
+    is host-orchestrated (one C-ABI call per operation), so this measures the
+    decomposition, not the single-GPU graph's speed."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2205_09411_b200 import DeviceMesh, MgConfig, StencilBuildConfig, build_stencils
+    from paper_2205_09411_b200.distributed import DistributedMgSolver
+    from paper_2205_09411_b200.mesh import VAR_RHS
+    from paper_2205_09411_b200.solver import LAYOUT_INTERIOR
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    mesh = case.build_mesh()
+    dev = DeviceMesh(mesh, device=local)
+    build_stencils(dev, case.lsf, StencilBuildConfig(w_min=case.w_min))
+    dev.set_field(VAR_RHS, case.rhs_fields(mesh), layout=LAYOUT_INTERIOR)
+    sol = DistributedMgSolver(dev, MgConfig())
+    for _ in range(args.warmup):
+        sol.v_cycle()
+    times = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        st = sol.v_cycle()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if ws > 1:
+            tt = torch.tensor([dt], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = float(tt.item())
+        times.append(dt)
+    leaf = case.leaf_cells(mesh)
+    t = sum(times)
+    if rank == 0:
+        line = {"metric": METRIC, "value": leaf * len(times) / t, "unit": UNIT, "n_gpus": ws,
+                "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * t / len(times),
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic",
+                "config": {"workload": f"{case.name}: {case.notes}; step = one V-cycle, one problem "
+                                       f"Morton-partitioned over {ws} rank(s)",
+                           "leaf_cells": leaf, "parallelism": f"morton x{ws}",
+                           "split_level": int(sol.part.split_level)},
+                "final_max_resid": st.max_resid}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def run_b200(args, case):
     import torch
     from paper_2205_09411_b200 import (DeviceMesh, MgConfig, MgSolver, StencilBuildConfig,
@@ -435,12 +493,16 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="one problem Morton-partitioned over the ranks (host-driven, strong scaling)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     from paper_2205_09411_b200 import configs as cfgs
     case = cfgs.get_case(args.config)
     if args.impl == "reference":
         return run_reference(args, case)
+    if args.partitioned:
+        return run_partitioned(args, case)
     return run_b200(args, case)
 
 
