@@ -83,6 +83,8 @@ struct OpsImpl final : Ops {
           if (L.exp & (1 << 28)) launch_gs_stream<2, 3, T256>(c, L, d, parity);
           else if (L.exp & (1 << 29)) launch_gs_stream<2, 4, T256>(c, L, d, parity);
           else if (L.exp & (1 << 30)) launch_gs_stream<3, 2, T256>(c, L, d, parity);
+          else if (T256 && d.n_gs <= c.sms * 4 && !(L.exp & 16))  // one block per CTA, all resident at once
+            launch_gs_stream<1, 4, T256>(c, L, d, parity);
           else if (d.n_gs <= 1024) launch_gs_stream<2, 3, T256>(c, L, d, parity);  // 7.7 vs 8.0 us at 512 blocks
           else launch_gs_stream<kStreamStages, kStreamCtasPerSm, 0>(c, L, d, parity);
         }

@@ -372,7 +372,9 @@ __global__ void __launch_bounds__(Stream3<N, TH>::THR, MINB) k_gs_stream(LevelVi
     cp_async_commit();
   }
   const double h2 = L.h2;
-  static_assert(S_STAGES >= 2, "g of block it+1 is read through meta[] one iteration ahead");
+  // S_STAGES == 1 only with at most one block per CTA (the launcher's
+  // grid >= n): g of block it+1 is read through meta[] one iteration ahead
+  static_assert(S_STAGES >= 1, "stages");
   __syncthreads();  // meta of the first stages
   double gcur[S::PER], gnext[S::PER];
   // this thread's entries: e(q) = gbase + q * gstep (column order, or t + q * THR)
