@@ -38,18 +38,41 @@ __device__ __forceinline__ void tab_load(const LevelView& L, const int4* __restr
 }
 
 // gsrb_block half-sweep (multigrid.hpp:621-695) of cell gid of the colour
-// (gid < nb * H): the body of k_gs_tab and of the cluster tail (tail.cuh)
+// (gid < nb * H): the body of k_gs_tab.  Everything static -- the cell's
+// entry, its Dirichlet face values and a cut row's coefficients (bc * phi_b
+// folded, rebuilt with the graphs on set_boundary_value) -- is loaded before
+// griddepcontrol.wait (PDL); only phi and g after it.
 template <int D, int N, bool PDL = false>
 __device__ __forceinline__ void gs_tab_cell(const LevelView& L, const double* __restrict__ phi_b,
                                             const int4* __restrict__ T, const double* __restrict__ gbc, int parity,
                                             int gid) {
   using G = Geo<D, N>;
-  if (!owned(L, gid / G::H)) return;
+  if (!owned(L, gid / G::H)) {
+    if (PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
+    return;
+  }
   const int a = (gid / G::H) * G::NI + parity * G::H + gid % G::H;
-  int code, leaf;
-  double self, p[2 * D];
-  tab_load<D, PDL>(L, T, gbc, a, code, leaf, self, p);
+  const int4 e0 = T[2 * a], e1 = T[2 * a + 1];
+  const int code = e0.x;
+  const int na[6] = {e0.y, e0.z, e0.w, e1.x, e1.y, e1.z};
+  double gb[2 * D], cf[14];
+#pragma unroll
+  for (int d = 0; d < 2 * D; ++d) gb[d] = na[d] == -2 ? gbc[(size_t)a * 6 + d] : 0.0;
+  if (code >= 0) {
+    const double2* c2 = reinterpret_cast<const double2*>(L.r_coef) + (size_t)code * 8;
+#pragma unroll
+    for (int u = 0; u < 7; ++u) {
+      const double2 v = c2[u];
+      cf[2 * u] = v.x;
+      cf[2 * u + 1] = v.y;
+    }
+  }
+  if (PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
   if (code <= -3) return;  // inside: pinned
+  const double self = L.phi[a];
+  double p[2 * D];
+#pragma unroll
+  for (int d = 0; d < 2 * D; ++d) p[d] = na[d] >= 0 ? L.phi[na[d]] : (na[d] == -1 ? self : 2.0 * gb[d] - self);
   const double g = L.rhs[a];
   const double h2 = L.h2;
   double nv;
@@ -59,18 +82,10 @@ __device__ __forceinline__ void gs_tab_cell(const LevelView& L, const double* __
     else
       nv = 0.25 * (p[0] + p[1] + p[2] + p[3] - h2 * g);  // :640-641
   } else if (code == -2) {
-    double s = -h2 * g;  // :668-671
-    for (int d = 0; d < 2 * D; ++d) s += p[d];
-    nv = -s * (-1.0 / (2.0 * D));
-  } else {  // :677-683, from the row-coefficient table (bc * phi_b folded: one round trip)
-    const double2* c2 = reinterpret_cast<const double2*>(L.r_coef) + (size_t)code * 8;
-    double cf[14];
-#pragma unroll
-    for (int u = 0; u < 7; ++u) {
-      const double2 v = c2[u];
-      cf[2 * u] = v.x;
-      cf[2 * u + 1] = v.y;
-    }
+    double sv = -h2 * g;  // :668-671
+    for (int d = 0; d < 2 * D; ++d) sv += p[d];
+    nv = -sv * (-1.0 / (2.0 * D));
+  } else {  // :677-683
     const int bm = (int)cf[13];
     double num = g;
 #pragma unroll
@@ -90,7 +105,10 @@ __global__ void __launch_bounds__(256) k_gs_tab(LevelView L, const double* __res
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // PDL: see tab_load
   using G = Geo<D, N>;
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= L.nb * G::H) return;
+  if (gid >= L.nb * G::H) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    return;
+  }
   gs_tab_cell<D, N, true>(L, phi_b, T, gbc, parity, gid);
 }
 
