@@ -37,6 +37,66 @@ __device__ __forceinline__ void tab_load(const LevelView& L, const int4* __restr
     p[d] = na[d] >= 0 ? L.phi[na[d]] : (na[d] == -1 ? self : 2.0 * gbc[(size_t)a * 6 + d] - self);
 }
 
+// The static part of a cell's operator (its table entry, Dirichlet face
+// values, a special row's coefficients with bc * phi_b folded), loaded before
+// griddepcontrol.wait under PDL; tab_apply evaluates L(phi) at the cell from
+// it with the reference's operation order (stencil.hpp:273-322).
+template <int D>
+struct TabPre {
+  int code, leaf;
+  int na[2 * D];
+  double gb[2 * D], cf[14];
+};
+template <int D>
+__device__ __forceinline__ TabPre<D> tab_pre(const LevelView& L, const int4* __restrict__ T,
+                                             const double* __restrict__ gbc, int a) {
+  TabPre<D> P;
+  const int4 e0 = T[2 * a], e1 = T[2 * a + 1];
+  P.code = e0.x;
+  P.leaf = e1.w;
+  const int na[6] = {e0.y, e0.z, e0.w, e1.x, e1.y, e1.z};
+#pragma unroll
+  for (int d = 0; d < 2 * D; ++d) {
+    P.na[d] = na[d];
+    P.gb[d] = na[d] == -2 ? gbc[(size_t)a * 6 + d] : 0.0;
+  }
+  if (P.code >= 0) {
+    const double2* c2 = reinterpret_cast<const double2*>(L.r_coef) + (size_t)P.code * 8;
+#pragma unroll
+    for (int u = 0; u < 7; ++u) {
+      const double2 v = c2[u];
+      P.cf[2 * u] = v.x;
+      P.cf[2 * u + 1] = v.y;
+    }
+  }
+  return P;
+}
+template <int D>
+__device__ __forceinline__ void tab_values(const LevelView& L, const TabPre<D>& P, int a, double& self,
+                                           double* p) {
+  self = L.phi[a];
+#pragma unroll
+  for (int d = 0; d < 2 * D; ++d)
+    p[d] = P.na[d] >= 0 ? L.phi[P.na[d]] : (P.na[d] == -1 ? self : 2.0 * P.gb[d] - self);
+}
+// L(phi) at a solved cell (code > -3): uniform row (-2D self + sum p) w, special row center self + sum (nb p + bc phi_b)
+template <int D>
+__device__ __forceinline__ double tab_apply(const LevelView& L, const TabPre<D>& P, double self, const double* p) {
+  if (P.code < 0) {
+    double s = -2.0 * D * self;
+    for (int d = 0; d < 2 * D; ++d) s += p[d];
+    return s * L.w;
+  }
+  const int bm = (int)P.cf[13];
+  double s = P.cf[0] * self;
+#pragma unroll
+  for (int d = 0; d < 2 * D; ++d) {
+    s += P.cf[1 + d] * p[d];
+    if ((bm >> d) & 1) s += P.cf[7 + d];
+  }
+  return s;
+}
+
 // gsrb_block half-sweep (multigrid.hpp:621-695) of cell gid of the colour
 // (gid < nb * H): the body of k_gs_tab.  Everything static -- the cell's
 // entry, its Dirichlet face values and a cut row's coefficients (bc * phi_b
@@ -120,11 +180,12 @@ __device__ __forceinline__ void fas_tab_cell(const LevelView& L, const double* _
   using G = Geo<D, N>;
   if (!owned(L, a / G::NI)) return;
   if (FAS) {
-    int code, leaf;
+    const TabPre<D> P = tab_pre<D>(L, T, gbc, a);
+    if (PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
     double self, p[2 * D];
-    tab_load<D, PDL>(L, T, gbc, a, code, leaf, self, p);
-    if (!leaf) {
-      const double out = code <= -3 ? 0.0 : apply_value<D>(L, phi_b, code >= 0 ? code : -1, self, p);
+    tab_values<D>(L, P, a, self, p);
+    if (!P.leaf) {
+      const double out = P.code <= -3 ? 0.0 : tab_apply<D>(L, P, self, p);
       L.rhs[a] = out + L.rhs[a];
     }
     L.old[a] = self;
@@ -160,22 +221,42 @@ __device__ __forceinline__ void restrict_tab_item(const LevelView& Lf, const Lev
   const bool live = t < Lf.nb * NQ && owned(Lf, slot);
   const int q = live ? t % NQ : 0;
   const int qx = q % HN, qy = (q / HN) % HN, qz = D == 3 ? q / (HN * HN) : 0;
+  // static: the parent cell and its pin (the group's first lane) and, fused,
+  // the child's operator -- all before griddepcontrol.wait under PDL
+  size_t pa = 0;
+  bool pinned = false;
+  double pin = 0.0;
+  if (live && d == 0) {
+    const int P = Lf.parent[slot];
+    int cp[3] = {0, 0, 0};
+    for (int a2 = 0; a2 < D; ++a2) cp[a2] = (Lf.coords[slot * D + a2] & 1) * HN;
+    const int pi = cp[0] + qx, pj = cp[1] + qy, pk = D == 3 ? cp[2] + qz : 0;
+    pa = (size_t)P * G::NI + (size_t)(G::colour(pi, pj, pk) * G::H + G::entry(pi, pj, pk));
+    const int r = row_index<D, N>(Lp, P, G::colour(pi, pj, pk), G::entry(pi, pj, pk));
+    if (r >= 0 && Lp.r_mask[r] == 1) pinned = true, pin = phi_b[Lp.r_pin[r]];
+  }
   double vphi = 0, vq = 0;
+  int a = 0;
   if (live) {
     const int fi = 2 * qx + (d & 1), fj = 2 * qy + ((d >> 1) & 1), fk = D == 3 ? 2 * qz + ((d >> 2) & 1) : 0;
-    const int a = slot * G::NI + G::colour(fi, fj, fk) * G::H + G::entry(fi, fj, fk);
-    if (MODE == RM_FUSED) {
-      int code, leaf;
+    a = slot * G::NI + G::colour(fi, fj, fk) * G::H + G::entry(fi, fj, fk);
+  }
+  if (MODE == RM_FUSED) {
+    TabPre<D> Pc;
+    if (live) Pc = tab_pre<D>(Lf, T, gbc, a);
+    if (PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (live) {
       double p[2 * D];
-      tab_load<D, PDL>(Lf, T, gbc, a, code, leaf, vphi, p);
-      vq = code <= -3 ? 0.0 : resid_value<D>(Lf, phi_b, code >= 0 ? code : -1, vphi, p, Lf.rhs[a]);
-    } else {
-      if (PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
+      tab_values<D>(Lf, Pc, a, vphi, p);
+      vq = Pc.code <= -3 ? 0.0 : Lf.rhs[a] - tab_apply<D>(Lf, Pc, vphi, p);  // stencil.hpp:336-358
+    }
+  } else {
+    if (PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (live) {
       vphi = Lf.phi[a];
       vq = MODE == RM_RES ? Lf.res[a] : Lf.rhs[a];
     }
   }
-  if (PDL && !live) asm volatile("griddepcontrol.wait;" ::: "memory");  // idle lanes: before the writes below
   const int base = threadIdx.x & ~(NC - 1) & 31;
   double sphi = 0, sq = 0;
 #pragma unroll
@@ -184,15 +265,7 @@ __device__ __forceinline__ void restrict_tab_item(const LevelView& Lf, const Lev
     sq += __shfl_sync(0xffffffffu, vq, base + u);
   }
   if (!live || d != 0) return;
-  const int P = Lf.parent[slot];
-  int cp[3] = {0, 0, 0};
-  for (int a2 = 0; a2 < D; ++a2) cp[a2] = (Lf.coords[slot * D + a2] & 1) * HN;
-  const int pi = cp[0] + qx, pj = cp[1] + qy, pk = D == 3 ? cp[2] + qz : 0;
-  const size_t pa = (size_t)P * G::NI + (size_t)(G::colour(pi, pj, pk) * G::H + G::entry(pi, pj, pk));
-  double pv = sphi / (double)NC;
-  const int r = row_index<D, N>(Lp, P, G::colour(pi, pj, pk), G::entry(pi, pj, pk));
-  if (r >= 0 && Lp.r_mask[r] == 1) pv = phi_b[Lp.r_pin[r]];
-  Lp.phi[pa] = pv;
+  Lp.phi[pa] = pinned ? pin : sphi / (double)NC;
   Lp.rhs[pa] = sq / (double)NC;
 }
 
