@@ -231,28 +231,32 @@ __global__ void __launch_bounds__(kThreads) k_cfold(LevelView L, LevelView Lc) {
 }
 
 // ---------------------------------------------------------------- prolongation
-// fine cell t (t < nb * NI); the body of k_prolong and of the cluster tail (tail.cuh)
-template <int D, int N, bool FULL>
+// fine cell t (t < nb * NI); the body of k_prolong.  PDL: the static lookups
+// (inside test, parent, octant) come before griddepcontrol.wait, the field
+// values after it
+template <int D, int N, bool FULL, bool PDL = false>
 __device__ __forceinline__ void prolong_cell(const LevelView& Lf, const LevelView& Lp, const LevelView& Lpp,
                                              long long t) {
   using G = Geo<D, N>;
   const int slot = (int)(t / G::NI);
   const int ce = (int)(t % G::NI);
   const int c = ce / G::H, e = ce % G::H;
-  if (!owned(Lf, slot)) return;
-  if (Lf.kind[slot] != KIND_UNIFORM) {
+  bool skip = !owned(Lf, slot);
+  if (!skip && Lf.kind[slot] != KIND_UNIFORM) {
     const int r = Lf.row_of[(size_t)Lf.srow[slot] * G::NI + ce];
-    if (r >= 0 && Lf.r_mask[r] == 1) return;  // inside cells are skipped
+    skip = r >= 0 && Lf.r_mask[r] == 1;  // inside cells are skipped
   }
   int fc[3];
   G::cell_of(c, e, fc[0], fc[1], fc[2]);
-  const int P = Lf.parent[slot];
+  const int P = skip ? 0 : Lf.parent[slot];
   int pc[3] = {0, 0, 0}, sg[3] = {0, 0, 0};
-  for (int a = 0; a < D; ++a) {
+  for (int a = 0; a < D && !skip; ++a) {
     const int gk = ((Lf.coords[slot * D + a] & 1) ? N : 0) + fc[a];
     pc[a] = gk >> 1;
     sg[a] = (gk & 1) ? 1 : -1;
   }
+  if (PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (skip) return;
   const size_t fa = (size_t)slot * G::NI + ce;
   if (FULL) {
     double val = (1.0 - 0.25 * D) * phi_at<D, N>(Lp, Lpp, P, pc[0], pc[1], pc[2]);
@@ -277,11 +281,11 @@ __device__ __forceinline__ void prolong_cell(const LevelView& Lf, const LevelVie
 
 template <int D, int N, bool FULL>
 __global__ void __launch_bounds__(kThreads) k_prolong(LevelView Lf, LevelView Lp, LevelView Lpp) {
-  pdl_begin();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // PDL: see prolong_cell
   using G = Geo<D, N>;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long long)Lf.nb * G::NI) return;
-  prolong_cell<D, N, FULL>(Lf, Lp, Lpp, t);
+  prolong_cell<D, N, FULL, true>(Lf, Lp, Lpp, t);
 }
 
 // ---------------------------------------------------------------- pins

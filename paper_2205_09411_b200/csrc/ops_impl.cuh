@@ -360,9 +360,9 @@ struct OpsImpl final : Ops {
       }
     }
     if (full)
-      pdl_launch(k_prolong<D, N, true>, g, kThreads, 0, c.stream, Lf, Lp, Lpp);
+      pdl_launch_on(k_prolong<D, N, true>, g, kThreads, 0, c.stream, Lf, Lp, Lpp);
     else
-      pdl_launch(k_prolong<D, N, false>, g, kThreads, 0, c.stream, Lf, Lp, Lpp);
+      pdl_launch_on(k_prolong<D, N, false>, g, kThreads, 0, c.stream, Lf, Lp, Lpp);
     check();
   }
   void record(Ctx& c, int l) override {
