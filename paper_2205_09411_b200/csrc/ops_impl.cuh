@@ -180,7 +180,10 @@ struct OpsImpl final : Ops {
   void restrict_(Ctx& c, int l, int mode) override {
     const LevelView& Lf = V(c, l);
     const unsigned g = grid_for((long long)Lf.nb * G::NI);  // k_restrict: one thread per child cell
-    if (Lf.nb <= kSmallLevel && !(Lf.exp & 32768)) {
+    // 3D N=16 levels of more than 8 blocks restrict with the streaming kernel
+    // (one block per CTA there); PMG_EXP bit 11 keeps them on the table kernel
+    const bool stream_small = D == 3 && N == 16 && Lf.nb > 8 && mode == RM_FUSED && !(Lf.exp & 2048);
+    if (Lf.nb <= kSmallLevel && !(Lf.exp & 32768) && !stream_small) {
       const LevelDev& d = *c.lev[(size_t)l];
       if (d.has_tab && !(Lf.exp & 65536)) {
         const LevelView& Lp = V(c, l - 1);
