@@ -157,8 +157,8 @@ struct OpsImpl final : Ops {
           attr = true;
         }
         const int grid = std::min(d.n_rs, c.sms * MINB);
-        pdl_launch(k_restrict_stream<N, ST, MINB, MODE>, grid, RStream3<N>::THR, smem, c.stream, Lf, Lp, c.phi_b.p,
-                   (const int4*)d.rs_plan.p, d.n_rs, partial, rec, (unsigned int*)nullptr);
+        pdl_launch_on(k_restrict_stream<N, ST, MINB, MODE>, grid, RStream3<N>::THR, smem, c.stream, Lf, Lp,
+                      c.phi_b.p, (const int4*)d.rs_plan.p, d.n_rs, partial, rec, (unsigned int*)nullptr);
       } else if (Lf.exp & (1 << 27)) {
         launch_resid_stream<MODE, 3, 1, 1024>(c, Lf, Lp, d, partial, rec);
       } else {
@@ -327,7 +327,7 @@ struct OpsImpl final : Ops {
         attr = true;
       }
       const int grid = std::min(d.n_pp, c.sms * MINB);
-      pdl_launch(k_prolong_stream<N, ST, MINB, FULL>, grid, PStream3<N>::THR, smem, c.stream, 
+      pdl_launch_on(k_prolong_stream<N, ST, MINB, FULL>, grid, PStream3<N>::THR, smem, c.stream, 
           V(c, l), V(c, l - 1), (const int4*)d.pp_plan.p, d.n_pp, FULL ? -1 : c.prolong_dead,
           (V(c, l).exp & 8) ? 0 : 1);
       if (d.n_pin > 0)  // inside cells were interpolated too: restore their pins

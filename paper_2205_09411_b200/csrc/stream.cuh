@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
                                                                            const int4* __restrict__ plan, int n,
                                                                            Rec* __restrict__ partial, Rec* rec,
                                                                            unsigned int* counter) {
-  pdl_begin();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // PDL: prologue before the wait
   constexpr bool RECORD = MODE == 1, FASM = MODE == 2;
   using S = RStream3<N>;
   constexpr int NI = N * N * N;
@@ -617,6 +617,7 @@ __global__ void __launch_bounds__(RStream3<N>::THR, MINB) k_restrict_stream(Leve
     fence_mbar_init();
   }
   R.init(plan, nmine, G);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
   for (int s = 0; s < S_STAGES; ++s) {
     if (s < nmine) {
@@ -1278,7 +1279,7 @@ template <int N, int S_STAGES, int MINB, bool FULL>
 __global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(LevelView Lf, LevelView Lp,
                                                                           const int4* __restrict__ plan, int n,
                                                                           int dead, int rev) {
-  pdl_begin();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // PDL: prologue before the wait
   using S = PStream3<N>;
   constexpr int NI = N * N * N, HN = S::HN, PE = S::PE;
   constexpr int NE = (S::PS + S::THR - 1) / S::THR;
@@ -1297,6 +1298,7 @@ __global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(Level
     fence_mbar_init();
   }
   __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   auto issue = [&](int p, int s) {
     if (rev) p = n - 1 - p;
     const int4 a = __ldg(plan + 2 * p), b = __ldg(plan + 2 * p + 1);
