@@ -497,9 +497,11 @@ struct OpsImpl final : Ops {
       if constexpr (D == 3 && (N == 8 || N == 16)) {
         if (!(V(c, 1).exp & 32)) {
           // planes of the root block spread over a thread-block cluster
-          if (V(c, 1).exp & (1 << 22)) launch_coarse_cluster<1>(c, F);
+          // one plane per CTA (N CTAs, a 16-CTA non-portable cluster at N=16):
+          // 786 vs 796 us per V-cycle with two planes per CTA (PMG_EXP bit 22)
+          if (V(c, 1).exp & (1 << 22)) launch_coarse_cluster<2>(c, F);
           else if (V(c, 1).exp & (1 << 23)) launch_coarse_cluster<4>(c, F);
-          else launch_coarse_cluster<2>(c, F);
+          else launch_coarse_cluster<1>(c, F);
           check();
           return;
         }
