@@ -10,6 +10,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <tuple>
 
 #include "ctx.h"
 
@@ -87,8 +88,6 @@ static void set_views(Ctx& c) {
     v.cfold = d.cfold.p;
     v.cfoff = d.has_cfold ? d.cfoff.p : nullptr;
     for (int k = 0; k < 6; ++k) v.bctype[k] = c.bctype[k];
-    const char* ex = getenv("PMG_EXP");
-    v.exp = ex ? atoi(ex) : 0;
     v.dense = d.dense ? 1 : 0;
     v.nside = 1 << (l - 1);
     v.bczero = d.bczero ? 1 : 0;
@@ -809,17 +808,24 @@ static void assemble_coarse(Ctx& c) {
 }
 
 // ---------------------------------------------------------------- cycle sequences
-static void enq_restrict_level(Ctx& c, int l) {
-  // residual_level(l) + restrict_level(l): fused unless level l has
-  // coarse-fine faces (their ghosts read level l-1 cells being restricted)
+// residual_level(l) + restrict_level(l) up to apply_pins(l-1): one pass unless
+// level l has coarse-fine faces (their ghosts read level l-1 cells being restricted)
+static void enq_restrict_only(Ctx& c, int l) {
   if (c.lev[(size_t)l]->has_cf) {
     c.ops->residual(c, l);
     c.ops->restrict_(c, l, pmgdev::RM_RES);
   } else {
     c.ops->restrict_(c, l, pmgdev::RM_FUSED);
   }
+}
+// the rest of restrict_level(l): the FAS right-hand side and OLD of level l-1
+static void enq_fas_level(Ctx& c, int l) {
   c.ops->fas(c, l - 1, true);
   if (c.lev[(size_t)(l - 1)]->has_cfold) c.ops->cfold(c, l - 1);
+}
+static void enq_restrict_level(Ctx& c, int l) {
+  enq_restrict_only(c, l);
+  enq_fas_level(c, l);
 }
 static void enq_restrict_level_no_guess(Ctx& c, int l) {
   c.ops->restrict_(c, l, pmgdev::RM_RHS);
@@ -846,8 +852,7 @@ static void enq_v_span(Ctx& c, int top) {
   for (int l = 2; l <= top; ++l) {
     // the red half-sweep that follows overwrites every red cell the
     // prolongation would write, except where a physical-face ghost reads it
-    const char* ex = getenv("PMG_EXP");
-    c.prolong_dead = c.cfg.n_up > 0 && !(ex && (atoi(ex) & 2)) ? 0 : -1;
+    c.prolong_dead = c.cfg.n_up > 0 ? 0 : -1;
     c.ops->prolong(c, l, false);
     c.prolong_dead = -1;
     enq_smooth(c, l, c.cfg.n_up);
@@ -1752,6 +1757,7 @@ int pmg_b200_time_op(pmg_b200_ctx* h, int op, int level, int reps, double* ms_av
         case 5: PMG_CUDA(cudaGraphLaunch(graph_for(c, CK_V).exec, c.stream)); break;
         case 7: c.ops->restrict_(c, level, c.lev[(size_t)level]->has_cf ? pmgdev::RM_RES : pmgdev::RM_FUSED); break;
         case 8: c.ops->fas(c, level - 1, true); break;
+
         default: PMG_CUDA(cudaGraphLaunch(graph_for(c, CK_FMG_GUESS).exec, c.stream)); break;
       }
     };

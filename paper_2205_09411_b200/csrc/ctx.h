@@ -4,6 +4,7 @@
 
 #include <cstdlib>
 #include <memory>
+#include <unordered_set>
 #include <utility>
 #include <stdexcept>
 #include <string>
@@ -280,7 +281,21 @@ struct Ctx {
   Graph g_v, g_fmg[2], g_measure;
   bool graphs_dirty = true;
 
+  // kernels whose >48 KB dynamic shared memory / non-portable cluster
+  // attribute is set: cudaFuncSetAttribute is per device, a context is one device
+  std::unordered_set<const void*> attr_done;
+  int cluster16 = -1;  // 16-CTA coarse-solve cluster schedulable (-1: not yet queried)
+
   ~Ctx();
 };
+
+inline void set_smem_attr(Ctx& c, const void* fn, size_t smem) {
+  if (!c.attr_done.insert(fn).second) return;
+  PMG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+}
+inline void set_cluster_attr(Ctx& c, const void* fn) {
+  if (!c.attr_done.insert(fn).second) return;
+  PMG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+}
 
 }  // namespace pmghost

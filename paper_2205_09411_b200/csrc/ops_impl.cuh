@@ -8,6 +8,7 @@
 #include "coarse.cuh"
 #include "coarse_cluster.cuh"
 #include "stream.cuh"
+#include "brick.cuh"
 #include "small.cuh"
 #include "fields.cuh"
 
@@ -37,11 +38,9 @@ struct OpsImpl final : Ops {
 
   void gs(Ctx& c, int l, int parity) override {
     const LevelView& L = V(c, l);
-    if ((L.exp & (1 << 19)) && L.nb <= kSmallLevel) return;          // timing experiment only
-    if ((L.exp & (1 << 20)) && l < (int)c.mesh.L) return;            // timing experiment only
-    if (L.nb <= kSmallLevel && !(L.exp & 32768)) {
+    if (L.nb <= kSmallLevel) {
       const LevelDev& d = *c.lev[(size_t)l];
-      if (d.has_tab && !(L.exp & 65536))
+      if (d.has_tab)
         pdl_launch_on(k_gs_tab<D, N>, grid_for((long long)L.nb * G::H), 256, 0, c.stream, L, c.phi_b.p,
                       (const int4*)d.tab.p, (const double*)d.tgbc.p, parity);
       else
@@ -59,10 +58,10 @@ struct OpsImpl final : Ops {
       // only the other colour (plus, in k_gs_fix, the cut cell's own value).
       bool stream = false;
       if constexpr (D == 3 && (N == 8 || N == 16))
-        stream = d.n_gs > ((L.exp & 262144) ? 1024 : 0) && !(L.exp & 256);
+        stream = d.n_gs > 0;
       const int nfix = stream ? 0 : d.n_fix[parity];
       const bool lean_work = stream || d.n_fast > 0;
-      const int ncut = stream && !(L.exp & (1 << 24)) ? d.n_cut[parity] : 0;  // bit 24: timing experiment
+      const int ncut = stream ? d.n_cut[parity] : 0;
       const bool fork = lean_work && (d.n_slow > 0 || nfix > 0 || ncut > 0);
       if (fork) {
         PMG_CUDA(cudaEventRecord(c.ev_fork, c.stream));
@@ -80,10 +79,7 @@ struct OpsImpl final : Ops {
       if (stream) {
         if constexpr (D == 3 && (N == 8 || N == 16)) {
           constexpr int T256 = N == 16 ? 256 : 0;
-          if (L.exp & (1 << 28)) launch_gs_stream<2, 3, T256>(c, L, d, parity);
-          else if (L.exp & (1 << 29)) launch_gs_stream<2, 4, T256>(c, L, d, parity);
-          else if (L.exp & (1 << 30)) launch_gs_stream<3, 2, T256>(c, L, d, parity);
-          else if (T256 && d.n_gs <= c.sms * 4 && !(L.exp & 16))  // one block per CTA, all resident at once
+          if (T256 && d.n_gs <= c.sms * 4)  // one block per CTA, all resident at once
             launch_gs_stream<1, 4, T256>(c, L, d, parity);
           else if (d.n_gs <= 1024) launch_gs_stream<2, 3, T256>(c, L, d, parity);  // 7.7 vs 8.0 us at 512 blocks
           else launch_gs_stream<kStreamStages, kStreamCtasPerSm, 0>(c, L, d, parity);
@@ -107,35 +103,23 @@ struct OpsImpl final : Ops {
     if constexpr (D == 3 && (N == 8 || N == 16)) {
       using S = Stream3<N, TH>;
       constexpr size_t smem = (size_t)ST * S::STAGE * sizeof(double);
-      static bool attr = false;
-      if (!attr) {
-        PMG_CUDA(cudaFuncSetAttribute(k_gs_stream<N, ST, MINB, TH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-        attr = true;
-      }
+      set_smem_attr(c, (const void*)k_gs_stream<N, ST, MINB, TH>, smem);
       const int grid = std::min(d.n_gs, c.sms * MINB);
-      if (L.exp & 1)
-        pdl_launch(k_gs_stream<N, ST, MINB, TH>, grid, S::THR, smem, c.stream, L, parity, c.phi_b.p,
-                   (const int4*)d.gs_plan.p, d.n_gs, (L.exp & 8) ? 0 : parity);
-      else  // PDL: the prologue overlaps the previous kernel's drain
-        pdl_launch_on(k_gs_stream<N, ST, MINB, TH>, grid, S::THR, smem, c.stream, L, parity, c.phi_b.p,
-                      (const int4*)d.gs_plan.p, d.n_gs, (L.exp & 8) ? 0 : parity);
+      // PDL: the prologue overlaps the previous kernel's drain; parity 1 walks
+      // the plan backwards (starts on the blocks the red half-sweep wrote last)
+      pdl_launch_on(k_gs_stream<N, ST, MINB, TH>, grid, S::THR, smem, c.stream, L, parity, c.phi_b.p,
+                    (const int4*)d.gs_plan.p, d.n_gs, parity);
     }
   }
-  // residual-streaming kernels: k_restrict_stream (one thread per parent) or
-  // k_resid_stream (GS mapping); PMG_EXP bit 26 swaps them (timing comparisons)
+  // residual-streaming kernels: k_restrict_stream (one thread per parent) for
+  // the restriction, k_resid_stream (column mapping) for the record and FAS
   template <int MODE, int ST, int MINB, int TT>
   void launch_resid_stream(Ctx& c, const LevelView& Lf, const LevelView& Lp, const LevelDev& d, Rec* partial,
                            Rec* rec) {
     if constexpr (D == 3 && N == 16) {
       using Q = QStream3<N, TT>;
       constexpr size_t smem = (size_t)ST * Q::STAGE * sizeof(double);
-      static bool attr = false;
-      if (!attr) {
-        PMG_CUDA(cudaFuncSetAttribute(k_resid_stream<N, ST, MINB, MODE, TT>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-      }
+      set_smem_attr(c, (const void*)k_resid_stream<N, ST, MINB, MODE, TT>, smem);
       const int grid = std::min(d.n_rs, c.sms * MINB);
       pdl_launch(k_resid_stream<N, ST, MINB, MODE, TT>, grid, Q::THR, smem, c.stream, Lf, Lp, c.phi_b.p,
                  (const int4*)d.rs_plan.p, d.n_rs, partial, rec, (unsigned int*)nullptr);
@@ -144,23 +128,23 @@ struct OpsImpl final : Ops {
   template <int MODE>
   void launch_rstream(Ctx& c, const LevelView& Lf, const LevelView& Lp, const LevelDev& d, Rec* partial, Rec* rec) {
     if constexpr (D == 3 && N == 16) {
+      if (MODE == 1) {  // record: the 16-byte-access brick kernel (68 vs 85 us for the column kernel at 256^3)
+        constexpr int ST = 2;
+        constexpr size_t smem = (size_t)ST * QStream3<N, 512>::STAGE * sizeof(double);
+        set_smem_attr(c, (const void*)k_record_brick<N, ST>, smem);
+        pdl_launch(k_record_brick<N, ST>, rstream_grid(c, Lf, d), kBrickThreads, smem, c.stream, Lf,
+                   (const int4*)d.rs_plan.p, d.n_rs, partial);
+        return;
+      }
       // restriction: the one-thread-per-parent kernel (85 us at 256^3 vs 93 us
       // for the column kernel); record / FAS: the column kernel
-      const bool old_kernel = MODE == 0 ? !(Lf.exp & (1 << 26)) : (Lf.exp & (1 << 26)) != 0;
-      if (old_kernel) {
+      if (MODE == 0) {
         constexpr int ST = 2, MINB = 1;
         constexpr size_t smem = (size_t)ST * RStream3<N>::STAGE * sizeof(double);
-        static bool attr = false;
-        if (!attr) {
-          PMG_CUDA(cudaFuncSetAttribute(k_restrict_stream<N, ST, MINB, MODE>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-          attr = true;
-        }
+        set_smem_attr(c, (const void*)k_restrict_stream<N, ST, MINB, MODE>, smem);
         const int grid = std::min(d.n_rs, c.sms * MINB);
         pdl_launch_on(k_restrict_stream<N, ST, MINB, MODE>, grid, RStream3<N>::THR, smem, c.stream, Lf, Lp,
                       c.phi_b.p, (const int4*)d.rs_plan.p, d.n_rs, partial, rec, (unsigned int*)nullptr);
-      } else if (Lf.exp & (1 << 27)) {
-        launch_resid_stream<MODE, 3, 1, 1024>(c, Lf, Lp, d, partial, rec);
       } else {
         launch_resid_stream<MODE, 3, 1, 512>(c, Lf, Lp, d, partial, rec);
       }
@@ -168,7 +152,7 @@ struct OpsImpl final : Ops {
   }
   // number of CTAs launch_rstream uses (record partials)
   int rstream_grid(Ctx& c, const LevelView& Lf, const LevelDev& d) {
-    const int minb = 1;  // MODE 1: every variant runs one CTA per SM
+    const int minb = 2;  // MODE 1 = k_record_brick: two CTAs per SM
     return std::min(d.n_rs, c.sms * minb);
   }
   void residual(Ctx& c, int l) override {
@@ -181,11 +165,11 @@ struct OpsImpl final : Ops {
     const LevelView& Lf = V(c, l);
     const unsigned g = grid_for((long long)Lf.nb * G::NI);  // k_restrict: one thread per child cell
     // 3D N=16 levels of more than 8 blocks restrict with the streaming kernel
-    // (one block per CTA there); PMG_EXP bit 11 keeps them on the table kernel
-    const bool stream_small = D == 3 && N == 16 && Lf.nb > 8 && mode == RM_FUSED && !(Lf.exp & 2048);
-    if (Lf.nb <= kSmallLevel && !(Lf.exp & 32768) && !stream_small) {
+    // (one block per CTA there)
+    const bool stream_small = D == 3 && N == 16 && Lf.nb > 8 && mode == RM_FUSED;
+    if (Lf.nb <= kSmallLevel && !stream_small) {
       const LevelDev& d = *c.lev[(size_t)l];
-      if (d.has_tab && !(Lf.exp & 65536)) {
+      if (d.has_tab) {
         const LevelView& Lp = V(c, l - 1);
         if (mode == RM_RES)
           pdl_launch_on(k_restrict_tab<D, N, RM_RES>, g, 256, 0, c.stream, Lf, Lp, c.phi_b.p, (const int4*)d.tab.p,
@@ -210,10 +194,10 @@ struct OpsImpl final : Ops {
     }
     if constexpr (D == 3 && N == 16) {
       const LevelDev& d = *c.lev[(size_t)l];
-      if (mode == RM_FUSED && !d.has_cf && d.n_rs == d.n_own && !(Lf.exp & 8192)) {
+      if (mode == RM_FUSED && !d.has_cf && d.n_rs == d.n_own) {
         // parents with a cut child: k_restrict_fix on the forked stream (the
         // streaming kernel leaves them alone; both only read level l)
-        const bool fix = d.n_rfix > 0 && !(Lf.exp & (1 << 25));
+        const bool fix = d.n_rfix > 0;
         if (fix) {
           PMG_CUDA(cudaEventRecord(c.ev_fork, c.stream));
           PMG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
@@ -258,7 +242,7 @@ struct OpsImpl final : Ops {
     const unsigned g = grid_for((long long)L.nb * G::NI);
     if constexpr (D == 3 && N == 16) {
       const LevelDev& d = *c.lev[(size_t)lc];
-      if (f && L.nb > kSmallLevel && !d.has_cf && d.n_rs == d.n_own && !(L.exp & 8192)) {
+      if (f && L.nb > kSmallLevel && !d.has_cf && d.n_rs == d.n_own) {
         // streaming FAS (the residual kernel in FAS mode) and the cut rows
         // cut rows on the forked stream: the streaming kernel writes g only at
         // the other rows (and OLD everywhere), k_fas_fix reads phi and g of
@@ -282,7 +266,7 @@ struct OpsImpl final : Ops {
     }
     {
       const LevelDev& d = *c.lev[(size_t)lc];
-      if (L.nb <= kSmallLevel && d.has_tab && !(L.exp & 98304)) {
+      if (L.nb <= kSmallLevel && d.has_tab) {
         if (f)
           pdl_launch_on(k_fas_tab<D, N, true>, grid_for((long long)L.nb * G::NI, 256), 256, 0, c.stream, L, c.phi_b.p,
                      (const int4*)d.tab.p, (const double*)d.tgbc.p);
@@ -294,7 +278,7 @@ struct OpsImpl final : Ops {
       }
     }
     if constexpr (TILE) {
-      if (!(L.nb <= kSmallLevel && !(L.exp & 32768))) {
+      if (L.nb > kSmallLevel) {
         if (f)
           pdl_launch(k_fas_tile<D, N, true>, L.nb, TT::THREADS, 0, c.stream, L, Vc(c, lc), c.phi_b.p);
         else
@@ -320,16 +304,11 @@ struct OpsImpl final : Ops {
       const LevelDev& d = *c.lev[(size_t)l];
       constexpr int ST = 2, MINB = 2;
       constexpr size_t smem = (size_t)ST * PStream3<N>::STAGE * sizeof(double);
-      static bool attr = false;
-      if (!attr) {
-        PMG_CUDA(cudaFuncSetAttribute(k_prolong_stream<N, ST, MINB, FULL>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-      }
+      set_smem_attr(c, (const void*)k_prolong_stream<N, ST, MINB, FULL>, smem);
       const int grid = std::min(d.n_pp, c.sms * MINB);
       pdl_launch_on(k_prolong_stream<N, ST, MINB, FULL>, grid, PStream3<N>::THR, smem, c.stream, 
           V(c, l), V(c, l - 1), (const int4*)d.pp_plan.p, d.n_pp, FULL ? -1 : c.prolong_dead,
-          (V(c, l).exp & 8) ? 0 : 1);
+          1);
       if (d.n_pin > 0)  // inside cells were interpolated too: restore their pins
         pdl_launch_on(k_pin_list, grid_for(d.n_pin, 256), 256, 0, c.stream, V(c, l).phi, c.phi_b.p,
                                                                   (const int2*)d.pin_list.p, d.n_pin);
@@ -344,8 +323,8 @@ struct OpsImpl final : Ops {
       const LevelDev& d = *c.lev[(size_t)l];
       // streaming down to 64-block levels too (one block per CTA: 6.9 vs 10.1 us
       // for the generic per-cell kernel's chain of ghost lookups at 64 blocks,
-      // but slower at 8); PMG_EXP bit 4 keeps small levels on the per-cell kernel
-      if ((Lf.nb > kSmallLevel || (Lf.nb > 16 && !(Lf.exp & 4))) && d.n_pp > 0 && !(Lf.exp & 131072)) {
+      // but slower at 8)
+      if (Lf.nb > 16 && d.n_pp > 0) {
         if (full) launch_prolong_stream<true>(c, l);
         else launch_prolong_stream<false>(c, l);
         check();
@@ -353,7 +332,7 @@ struct OpsImpl final : Ops {
       }
     }
     if constexpr (TILE) {
-      if (!(Lf.nb <= kSmallLevel && !(Lf.exp & 32768))) {
+      if (Lf.nb > kSmallLevel) {
         if (full)
           pdl_launch(k_prolong_tile<D, N, true>, Lf.nb, TT::THREADS, 0, c.stream, Lf, Lp, Lpp);
         else
@@ -374,7 +353,7 @@ struct OpsImpl final : Ops {
     if (c.lev[(size_t)l]->n_leaf == 0) return;
     {
       const LevelDev& d = *c.lev[(size_t)l];
-      if (L.nb <= kSmallLevel && d.has_tab && !(L.exp & 98304)) {
+      if (L.nb <= kSmallLevel && d.has_tab) {
         const int gr = (int)grid_for((long long)L.nb * G::NI, 256);
         pdl_launch(k_record_tab<D, N>, gr, 256, 0, c.stream, L, c.phi_b.p, (const int4*)d.tab.p,
                    (const double*)d.tgbc.p, c.partial.p);
@@ -385,7 +364,7 @@ struct OpsImpl final : Ops {
     }
     if constexpr (D == 3 && N == 16) {
       const LevelDev& d = *c.lev[(size_t)l];
-      if (d.n_rs > 0 && L.nb > kSmallLevel && !(L.exp & 16384)) {
+      if (d.n_rs > 0 && L.nb > kSmallLevel) {
         // streaming record of every block without coarse-fine faces (special
         // rows excluded), the cut rows from their table and the remaining
         // blocks by k_record_tile, each into its own partials: [0, G) per
@@ -445,16 +424,37 @@ struct OpsImpl final : Ops {
     pdl_launch(k_pins<D, N>, grid_for((long long)L.nb * G::NI), kThreads, 0, c.stream, L, c.phi_b.p);
     check();
   }
+  // can a 16-CTA cluster of k_coarse_cluster<N, 1> be scheduled on this device?
+  bool coarse_cluster16_ok(Ctx& c) {
+    if constexpr (D == 3 && (N == 8 || N == 16)) {
+      using K = CC<N, 1>;
+      if (K::NC <= 8) return true;
+      if (c.cluster16 < 0) {
+        set_cluster_attr(c, (const void*)k_coarse_cluster<N, 1>);
+        cudaLaunchConfig_t cfgl = {};
+        cfgl.gridDim = dim3(K::NC, 1, 1);
+        cfgl.blockDim = dim3(K::THR, 1, 1);
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = K::NC;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfgl.attrs = at;
+        cfgl.numAttrs = 1;
+        int n = 0;
+        const cudaError_t e = cudaOccupancyMaxActiveClusters(&n, (const void*)k_coarse_cluster<N, 1>, &cfgl);
+        if (e != cudaSuccess) (void)cudaGetLastError();
+        c.cluster16 = (e == cudaSuccess && n > 0) ? 1 : 0;
+      }
+      return c.cluster16 == 1;
+    }
+    return false;
+  }
   template <int PPC>
   void launch_coarse_cluster(Ctx& c, const CoarseFast& F) {
     if constexpr (D == 3 && (N == 8 || N == 16)) {
       using K = CC<N, PPC>;
-      static bool cattr = false;
-      if (!cattr) {
-        if (K::NC > 8)
-          PMG_CUDA(cudaFuncSetAttribute(k_coarse_cluster<N, PPC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        cattr = true;
-      }
+      if (K::NC > 8) set_cluster_attr(c, (const void*)k_coarse_cluster<N, PPC>);
       cudaLaunchConfig_t cfgl = {};
       cfgl.gridDim = dim3(K::NC, 1, 1);
       cfgl.blockDim = dim3(K::THR, 1, 1);
@@ -468,13 +468,12 @@ struct OpsImpl final : Ops {
       at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       at[1].val.programmaticStreamSerializationAllowed = 1;
       cfgl.attrs = at;
-      cfgl.numAttrs = (V(c, 1).exp & 1) ? 1 : 2;  // PDL: the static prologue overlaps the FAS of level 1
+      cfgl.numAttrs = 2;  // PDL: the static prologue overlaps the FAS of level 1
       PMG_CUDA(cudaLaunchKernelEx(&cfgl, k_coarse_cluster<N, PPC>, V(c, 1), F, (const double*)c.phi_b.p, c.rec.p,
                                   c.status.p, c.diag.p));
     }
   }
   void coarse(Ctx& c) override {
-    if (V(c, 1).exp & (1 << 21)) return;  // timing experiment only
     if constexpr (FASTC) {
       CoarseFast F{};
       F.flags = c.cf_flags.p;
@@ -495,23 +494,18 @@ struct OpsImpl final : Ops {
       F.pins = (const int2*)c.lev[1]->pin_list.p;
       F.n_pins = c.lev[1]->n_pin;
       if constexpr (D == 3 && (N == 8 || N == 16)) {
-        if (!(V(c, 1).exp & 32)) {
-          // planes of the root block spread over a thread-block cluster
-          // one plane per CTA (N CTAs, a 16-CTA non-portable cluster at N=16):
-          // 786 vs 796 us per V-cycle with two planes per CTA (PMG_EXP bit 22)
-          if (V(c, 1).exp & (1 << 22)) launch_coarse_cluster<2>(c, F);
-          else if (V(c, 1).exp & (1 << 23)) launch_coarse_cluster<4>(c, F);
-          else launch_coarse_cluster<1>(c, F);
-          check();
-          return;
-        }
+        // planes of the root block spread over a thread-block cluster, one
+        // plane per CTA (N CTAs: a 16-CTA non-portable cluster at N=16; 786 vs
+        // 796 us per V-cycle with two planes per CTA), or two planes per CTA on
+        // the portable 8-CTA cluster where 16 co-resident CTAs cannot be placed
+        // (MPS / green-context SM limits, partitioned devices)
+        if (coarse_cluster16_ok(c)) launch_coarse_cluster<1>(c, F);
+        else launch_coarse_cluster<2>(c, F);
+        check();
+        return;
       }
       constexpr size_t smem = coarse_fast_smem<D, N>();
-      static bool attr = false;
-      if (!attr) {
-        PMG_CUDA(cudaFuncSetAttribute(k_coarse_fast<D, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-      }
+      set_smem_attr(c, (const void*)k_coarse_fast<D, N>, smem);
       pdl_launch(k_coarse_fast<D, N>, 1, kCoarseThreads, smem, c.stream, V(c, 1), F, c.phi_b.p, c.rec.p,
                                                                    c.status.p, c.diag.p);
       check();

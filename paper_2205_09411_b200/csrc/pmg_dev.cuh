@@ -72,7 +72,6 @@ struct LevelView {
   double* cfold;          // AMR: VAR_OLD ghosts on coarse-fine faces
   const int32_t* cfoff;   // [nb*2D] offset into cfold or -1
   int bctype[6];          // per domain face: 0 Dirichlet, 1 Neumann-zero (mesh.hpp:22-32)
-  int exp;                // performance-experiment switches (PMG_EXP, 0 in production)
   int dense;              // 1: all (2^(l-1))^D blocks present and slot == Morton code
   int nside;              // blocks per axis on this level (dense levels)
   int bczero;             // 1: no Dirichlet face values on this level (all zero)

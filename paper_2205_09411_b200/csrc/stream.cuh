@@ -173,11 +173,10 @@ __device__ __forceinline__ void xface_of(int c, int u, int& side, int& j, int& k
 // Thread-issued async copies of one block: the strided x-face values (the
 // neighbour's X value, or the own value on a physical face) and, for an
 // interface block, this thread's row_of entries.
-template <int N, int TH>
-__device__ __forceinline__ void gs_issue_async(const LevelView& L, const BlockPlan& P, int c, double* st) {
+template <int N, int TH, bool ROWQ = true>
+__device__ __forceinline__ void gs_issue_async(const LevelView& L, const BlockPlan& P, int c, double* st, int t) {
   using S = Stream3<N, TH>;
   constexpr int NI = N * N * N;
-  const int t = threadIdx.x;
   for (int u = t; u < N * N; u += S::THR) {
     int side, j, k;
     xface_of<N>(c, u, side, j, k);
@@ -202,7 +201,7 @@ __device__ __forceinline__ void gs_issue_async(const LevelView& L, const BlockPl
       src = L.phi + (size_t)P.slot() * NI + (size_t)c * S::H + (size_t)k * S::FH + (side ? (N - 1) * S::HN : 0);
     cp_async16(st + S::OY + side * S::FH + k * S::HN + 2 * ch, src + 2 * ch);
   }
-  if (P.kind() == KIND_IFACE) {  // this block's row_of page (colour c), 16-B chunks
+  if (ROWQ && P.kind() == KIND_IFACE) {  // this block's row_of page (colour c), 16-B chunks
     const int32_t* rof = L.row_of + (size_t)P.srow() * NI + (size_t)c * S::H;
     int32_t* rq = reinterpret_cast<int32_t*>(st + S::ORQ);
     for (int q = t; q < S::H / 4; q += S::THR) cp_async16(rq + 4 * q, rof + 4 * q);
@@ -212,10 +211,11 @@ __device__ __forceinline__ void gs_issue_async(const LevelView& L, const BlockPl
 // Physical faces: the staged own-colour values become ghosts 2 bc - f1
 // (Dirichlet) or stay f1 (Neumann), mesh.hpp:538-552.
 template <int N>
-__device__ __forceinline__ void gs_phys_faces(const LevelView& L, int slot, int pmask, int c, double* st) {
+__device__ __forceinline__ void gs_phys_faces(const LevelView& L, int slot, int pmask, int c, double* st, int t0,
+                                              int nt) {
   using S = Stream3<N>;
   constexpr int NX = N * N;  // x rows (two sides)
-  for (int q = threadIdx.x; q < NX + 4 * S::FH; q += blockDim.x) {
+  for (int q = t0; q < NX + 4 * S::FH; q += nt) {
     int dir, i, tj;
     double* h;
     if (q < NX) {
@@ -261,13 +261,14 @@ __device__ __forceinline__ int gs_column_base(int t) {
   const int m = t % S::HN, j = (t / S::HN) % N, kq = t / S::FH;
   return m + S::HN * j + S::FH * S::PER * kq;
 }
-template <int N, int TH>
+// SKG: the special-row kinds of an interface block come from the global
+// skind page (int8, srow) instead of the row_of page staged at ORQ.
+template <int N, int TH, bool SKG = false>
 __device__ __forceinline__ void gs_stream_column(const LevelView& L, const double* __restrict__ st, int c, int kind,
-                                                 double h2, int slot, const double* gcur) {
+                                                 double h2, int slot, const double* gcur, int t, int srow = 0) {
   using S = Stream3<N, TH>;
   constexpr int NI = N * N * N, HN = S::HN, FH = S::FH, PER = S::PER, KS = S::THR / S::FH;
   static_assert(PER * KS == N, "columns cover the block");
-  const int t = threadIdx.x;
   const int m = t % HN, j = (t / HN) % N, kq = t / FH;
   const int eb = m + HN * j + FH * PER * kq;  // entry of q = 0
   const int o0 = (c + j + kq * PER) & 1;       // x offset of q = 0; flips with q
@@ -310,9 +311,13 @@ __device__ __forceinline__ void gs_stream_column(const LevelView& L, const doubl
     for (int q = 0; q < PER; ++q) dst[q * FH] = v[q];
   } else {  // interface block (multigrid.hpp:665-684)
     const int32_t* rq = reinterpret_cast<const int32_t*>(st + S::ORQ);
+    const int8_t* skg = L.skind + (size_t)srow * NI + (size_t)c * S::H;
+    int uni[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) uni[q] = SKG ? (skg[eb + q * FH] == 0 ? -1 : 0) : rq[eb + q * FH];
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
-      const int r = rq[eb + q * FH];
+      const int r = uni[q];
       double xm, xp, ym, yp;
       nbrs(q, xm, xp, ym, yp);
       if (r < 0) {  // uniform row (:667-672)
@@ -367,7 +372,7 @@ __global__ void __launch_bounds__(Stream3<N, TH>::THR, MINB) k_gs_stream(LevelVi
       const BlockPlan P = R.get(s);
       if (t == 0) gs_issue<N>(L, P, c, sm + s * S::STAGE, &full[s]);
       if (t == 0) meta[s][0] = P.slot(), meta[s][1] = P.a.y;
-      gs_issue_async<N, TH>(L, P, c, sm + s * S::STAGE);
+      gs_issue_async<N, TH>(L, P, c, sm + s * S::STAGE, t);
     }
     cp_async_commit();
   }
@@ -377,9 +382,9 @@ __global__ void __launch_bounds__(Stream3<N, TH>::THR, MINB) k_gs_stream(LevelVi
   static_assert(S_STAGES >= 1, "stages");
   __syncthreads();  // meta of the first stages
   double gcur[S::PER], gnext[S::PER];
-  // this thread's entries: e(q) = gbase + q * gstep (column order, or t + q * THR)
-  const int gbase = (L.exp & 4096) ? t : gs_column_base<N, TH>(t);
-  const int gstep = (L.exp & 4096) ? S::THR : S::FH;
+  // this thread's entries: e(q) = gbase + q * FH (column order)
+  const int gbase = gs_column_base<N, TH>(t);
+  constexpr int gstep = S::FH;
   {
     const double* gsrc = L.rhs + (size_t)meta[0][0] * NI + (size_t)c * S::H + gbase;
 #pragma unroll
@@ -400,82 +405,16 @@ __global__ void __launch_bounds__(Stream3<N, TH>::THR, MINB) k_gs_stream(LevelVi
       for (int q = 0; q < S::PER; ++q) gnext[q] = gsrc[q * gstep];
     }
     if (pmask) {  // block-uniform branch
-      gs_phys_faces<N>(L, slot, pmask, c, st);
+      gs_phys_faces<N>(L, slot, pmask, c, st, t, blockDim.x);
       __syncthreads();
     }
-    if (!(L.exp & 4096)) {
-      gs_stream_column<N, TH>(L, st, c, kind, h2, slot, gcur);
-    } else {
-      // Thread t owns entries e = t + q*THR: the same (m, j) and colour offset o
-      // for every q, z-plane k = k0 + q*KS.  Neighbour indices into the stage
-      // (own tile or halo layer) are chosen once per block; only the z layers at
-      // q = 0 / PER-1 are per-q choices.
-      constexpr int KS = S::THR / S::FH;
-      const int m = t % S::HN, j = (t / S::HN) % N, k0 = t / S::FH;
-      const int o = (c + j + k0) & 1;
-      const int rb = S::OX + (k0 * N + j) * S::HN + m;
-      constexpr int DT = KS * S::FH;  // tile step per q
-      int ixm = rb, dxm = DT, ixp = rb, dxp = DT, iym = rb - S::HN, dym = DT, iyp = rb + S::HN, dyp = DT;
-      if (!o) {
-        if (m > 0) ixm = rb - 1;
-        else ixm = S::OXF + k0 * N + j, dxm = KS * N;
-      } else {
-        if (m < S::HN - 1) ixp = rb + 1;
-        else ixp = S::OXF + N * N + k0 * N + j, dxp = KS * N;
-      }
-      if (j == 0) iym = S::OY + k0 * S::HN + m, dym = KS * S::HN;
-      if (j == N - 1) iyp = S::OY + S::FH + k0 * S::HN + m, dyp = KS * S::HN;
-      const int izm0 = k0 > 0 ? rb - S::FH : S::OZ + j * S::HN + m;
-      const int izpL = k0 < KS - 1 ? rb + (S::PER - 1) * DT + S::FH : S::OZ + S::FH + j * S::HN + m;
-      double* __restrict__ dst = L.phi + (size_t)slot * NI + (size_t)c * S::H + t;
-      if (!(L.exp & 512)) {
-        if (kind == KIND_UNIFORM) {  // multigrid.hpp:651-653: (sum of 6 - h^2 g) / 6.0
-          double sv[S::PER], v[S::PER];
-          bool ok = true;
-  #pragma unroll
-          for (int q = 0; q < S::PER; ++q) {
-            const double zm = st[q == 0 ? izm0 : rb + q * DT - S::FH];
-            const double zp = st[q == S::PER - 1 ? izpL : rb + q * DT + S::FH];
-            sv[q] = st[ixm + q * dxm] + st[ixp + q * dxp] + st[iym + q * dym] + st[iyp + q * dyp] + zm + zp -
-                    h2 * gcur[q];
-            v[q] = div6_fast(sv[q]);
-            ok = ok && div6_in_range(sv[q]);
-          }
-          if (!ok) {
-  #pragma unroll
-            for (int q = 0; q < S::PER; ++q) v[q] = div6_slow(sv[q]);
-          }
-  #pragma unroll
-          for (int q = 0; q < S::PER; ++q) dst[q * S::THR] = v[q];
-        } else {  // interface block (multigrid.hpp:665-684)
-          const int32_t* rq = reinterpret_cast<const int32_t*>(st + S::ORQ);
-  #pragma unroll
-          for (int q = 0; q < S::PER; ++q) {
-            const int r = rq[t + q * S::THR];
-            const double g = gcur[q];
-            const double p0 = st[ixm + q * dxm], p1 = st[ixp + q * dxp], p2 = st[iym + q * dym],
-                         p3 = st[iyp + q * dyp], p4 = st[q == 0 ? izm0 : rb + q * DT - S::FH],
-                         p5 = st[q == S::PER - 1 ? izpL : rb + q * DT + S::FH];
-            if (r < 0) {  // uniform row (:667-672)
-              double sv = -h2 * g;
-              sv += p0;
-              sv += p1;
-              sv += p2;
-              sv += p3;
-              sv += p4;
-              sv += p5;
-              dst[q * S::THR] = -sv * (-1.0 / 6.0);
-            }  // special rows: cut rows by k_gs_cut, inside rows keep their pin
-          }
-        }
-      }
-    }
+    gs_stream_column<N, TH>(L, st, c, kind, h2, slot, gcur, t);
     __syncthreads();  // stage s consumed
     if (it + S_STAGES < nmine) {
       const BlockPlan pf = R.get(it + S_STAGES);
       if (t == 0) gs_issue<N>(L, pf, c, st, &full[s]);
       if (t == 0) meta[s][0] = pf.slot(), meta[s][1] = pf.a.y;
-      gs_issue_async<N, TH>(L, pf, c, st);
+      gs_issue_async<N, TH>(L, pf, c, st, t);
     }
     cp_async_commit();
 #pragma unroll
@@ -551,8 +490,10 @@ __device__ __forceinline__ void rs_issue_async(const LevelView& L, const BlockPl
 }
 
 template <int N, class S = RStream3<N>>
-__device__ __forceinline__ void rs_phys_faces(const LevelView& L, int slot, int pmask, double* st) {
-  for (int q = threadIdx.x; q < 2 * N * N + 8 * S::FH; q += blockDim.x) {
+__device__ __forceinline__ void rs_phys_faces(const LevelView& L, int slot, int pmask, double* st, int t0 = -1,
+                                              int nt = 0) {
+  if (t0 < 0) t0 = threadIdx.x, nt = blockDim.x;
+  for (int q = t0; q < 2 * N * N + 8 * S::FH; q += nt) {
     int dir, tj;
     double* h;
     if (q < 2 * N * N) {
@@ -824,6 +765,140 @@ __device__ __forceinline__ void qs_issue(const LevelView& L, const BlockPlan& P,
   }
 }
 
+// Per-thread body of the column-mapped residual (k_resid_stream): from a
+// stage in the QStream3 layout
+// (both phi halves + both-colour face layers, physical ghosts already
+// formed) the own values col, L(phi) ap and r = g - L(phi) of this thread's
+// 2 x PER cells, with the reference's operation order (stencil.hpp:300-322,
+// 336-358).  rr: special-row kind per cell (0 uniform, 1 inside, 2 cut).
+template <int N, int TT>
+__device__ __forceinline__ void qs_cells(const double* __restrict__ st, int kind, double w,
+                                         const double (&gcur)[2][QStream3<N, TT>::PER],
+                                         const int (&rr)[2][QStream3<N, TT>::PER],
+                                         double (&col)[2][QStream3<N, TT>::PER],
+                                         double (&res)[2][QStream3<N, TT>::PER],
+                                         double (&ap)[2][QStream3<N, TT>::PER], int t) {
+  using S = QStream3<N, TT>;
+  constexpr int HN = S::HN, H = S::H, FH = S::FH, PER = S::PER, KS = S::KS;
+  const int m = t % HN, j = (t / HN) % N, kq = t / FH;
+  const int eb = m + HN * j + FH * PER * kq;  // entry of q = 0
+  const int jo = (j + kq * PER) & 1;          // o of colour 0 at q = 0; o_c(q) = jo ^ c ^ (q & 1)
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int q = 0; q < PER; ++q) col[c][q] = st[S::OP + c * H + eb + q * FH];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int X = 1 - c;
+    const int XB = S::OP + X * H + eb;
+    // neighbour bases (index of q = 0) and per-q steps: the other x
+    // neighbour for o = 0 (e - 1 or the -x face) and o = 1 (e + 1 or +x),
+    // y- / y+ (e -+ HN or the y face of colour c), z halo of colour c
+    const int bx0 = m > 0 ? XB - 1 : S::OXF + kq * PER * N + j, sx0 = m > 0 ? FH : N;
+    const int bx1 = m < HN - 1 ? XB + 1 : S::OXF + N * N + kq * PER * N + j, sx1 = m < HN - 1 ? FH : N;
+    const int bym = j > 0 ? XB - HN : S::OY + (0 * 2 + c) * FH + kq * PER * HN + m, sym = j > 0 ? FH : HN;
+    const int byp = j < N - 1 ? XB + HN : S::OY + (1 * 2 + c) * FH + kq * PER * HN + m, syp = j < N - 1 ? FH : HN;
+    const double zlo = st[kq > 0 ? XB - FH : S::OZ + (0 * 2 + c) * FH + j * HN + m];
+    const double zhi = st[kq < KS - 1 ? XB + PER * FH : S::OZ + (1 * 2 + c) * FH + j * HN + m];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int o = jo ^ c ^ (q & 1);
+      const double f = col[c][q];
+      const double xo = st[o ? bx1 + q * sx1 : bx0 + q * sx0];
+      const double xm = o ? col[X][q] : xo, xp = o ? xo : col[X][q];
+      const double ym = st[bym + q * sym], yp = st[byp + q * syp];
+      const double zm = q > 0 ? col[X][q - 1] : zlo, zp = q < PER - 1 ? col[X][q + 1] : zhi;
+      double sres = -2.0 * 3 * f;  // stencil.hpp:300-322, direction order
+      sres += xm;
+      sres += xp;
+      sres += ym;
+      sres += yp;
+      sres += zm;
+      sres += zp;
+      ap[c][q] = kind == KIND_ALL_INSIDE ? 0.0 : sres * w;
+      const int r8 = rr[c][q];
+      res[c][q] = (kind == KIND_ALL_INSIDE || r8 == 1) ? 0.0 : gcur[c][q] - ap[c][q];
+    }
+  }
+}
+
+// MODE 1 of the column residual: this thread's leaf-record totals
+// (record_leaf_residual, multigrid.hpp:529-562); inside rows excluded, cut
+// rows recorded from their table (k_record_cut).
+template <int PER>
+__device__ __forceinline__ void qs_record(bool leaf, int kind, const int (&rr)[2][PER], const double (&res)[2][PER],
+                                          double& rmx, double& rss, double& rcnt) {
+  if (!leaf || kind == KIND_ALL_INSIDE) return;
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      if (rr[c][q] != 0) continue;
+      rmx = fmax(rmx, fabs(res[c][q]));
+      rss += res[c][q] * res[c][q];
+      rcnt += 1.0;
+    }
+}
+
+// MODE 0 of the column residual: restriction into the parent (multigrid.hpp:
+// 697-722).  A parent's 2x2x2 children are the x pair of two consecutive
+// planes of this thread and of the thread with j + 1 (lane + 8): one shuffle
+// exchange, then the fold in x-fastest order.  Parents with a cut child
+// belong to k_restrict_fix, pinned parents are re-pinned by k_pin_list.
+// Every lane of the warp must call it (shuffles).
+template <int N, int TT>
+__device__ __forceinline__ void qs_restrict(const LevelView& Lp, int Pp, int cx, int cy, int cz,
+                                            const int (&rr)[2][QStream3<N, TT>::PER],
+                                            const double (&col)[2][QStream3<N, TT>::PER],
+                                            const double (&res)[2][QStream3<N, TT>::PER], int t) {
+  using S = QStream3<N, TT>;
+  constexpr int NI = N * N * N, HN = S::HN, H = S::H, FH = S::FH, PER = S::PER;
+  const int m = t % HN, j = (t / HN) % N, kq = t / FH;
+  const int jo = (j + kq * PER) & 1;
+#pragma unroll
+  for (int p2 = 0; p2 < PER / 2; ++p2) {
+    double rv[2][2], fv[2][2];  // [dz][dx]
+    int cut = 0;
+#pragma unroll
+    for (int dz = 0; dz < 2; ++dz) {
+      const int q = 2 * p2 + dz;
+      const int c0 = jo ^ (q & 1);  // colour of the dx = 0 cell (o_c = 0)
+#pragma unroll
+      for (int dx = 0; dx < 2; ++dx) {
+        const int c = c0 ^ dx;
+        rv[dz][dx] = c ? res[1][q] : res[0][q];
+        fv[dz][dx] = c ? col[1][q] : col[0][q];
+        cut |= (c ? rr[1][q] : rr[0][q]) == 2;
+      }
+    }
+    double rn[2][2], fn[2][2];
+#pragma unroll
+    for (int dz = 0; dz < 2; ++dz)
+#pragma unroll
+      for (int dx = 0; dx < 2; ++dx) {
+        rn[dz][dx] = __shfl_down_sync(0xffffffffu, rv[dz][dx], HN);
+        fn[dz][dx] = __shfl_down_sync(0xffffffffu, fv[dz][dx], HN);
+      }
+    cut |= __shfl_down_sync(0xffffffffu, cut, HN);
+    if (!(j & 1) && !cut) {  // multigrid.hpp:706-721: x-fastest order
+      double sr = 0.0, sf = 0.0;
+      sr += rv[0][0], sf += fv[0][0];
+      sr += rv[0][1], sf += fv[0][1];
+      sr += rn[0][0], sf += fn[0][0];
+      sr += rn[0][1], sf += fn[0][1];
+      sr += rv[1][0], sf += fv[1][0];
+      sr += rv[1][1], sf += fv[1][1];
+      sr += rn[1][0], sf += fn[1][0];
+      sr += rn[1][1], sf += fn[1][1];
+      const int pi = cx * HN + m, pj = cy * HN + (j >> 1), pk = cz * HN + kq * (PER / 2) + p2;
+      const int pc = (pi + pj + pk) & 1, pe = (pi + N * (pj + N * pk)) >> 1;
+      const size_t pa = (size_t)Pp * NI + (size_t)pc * H + pe;
+      Lp.phi[pa] = sf / 8.0;
+      Lp.rhs[pa] = sr / 8.0;
+    }
+  }
+}
+
 template <int N, int S_STAGES, int MINB, int MODE, int TT>
 __global__ void __launch_bounds__(QStream3<N, TT>::THR, MINB) k_resid_stream(LevelView Lf, LevelView Lp,
                                                                         const double* __restrict__ phi_b,
@@ -866,7 +941,6 @@ __global__ void __launch_bounds__(QStream3<N, TT>::THR, MINB) k_resid_stream(Lev
   __syncthreads();  // meta of the first stages
   const int m = t % HN, j = (t / HN) % N, kq = t / FH;
   const int eb = m + HN * j + FH * PER * kq;  // entry of q = 0
-  const int jo = (j + kq * PER) & 1;          // o of colour 0 at q = 0; o_c(q) = jo ^ c ^ (q & 1)
   const double w = Lf.w;
   double gcur[2][PER], gnext[2][PER];
   {
@@ -915,58 +989,10 @@ __global__ void __launch_bounds__(QStream3<N, TT>::THR, MINB) k_resid_stream(Lev
       rs_phys_faces<N, S>(Lf, slot, pmask, st);
       __syncthreads();
     }
-    // the two columns, then every cell
-    double col[2][PER];
-#pragma unroll
-    for (int c = 0; c < 2; ++c)
-#pragma unroll
-      for (int q = 0; q < PER; ++q) col[c][q] = st[S::OP + c * H + eb + q * FH];
-    double res[2][PER], ap[2][PER];
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const int X = 1 - c;
-      const int XB = S::OP + X * H + eb;
-      // neighbour bases (index of q = 0) and per-q steps: the other x
-      // neighbour for o = 0 (e - 1 or the -x face) and o = 1 (e + 1 or +x),
-      // y- / y+ (e -+ HN or the y face of colour c), z halo of colour c
-      const int bx0 = m > 0 ? XB - 1 : S::OXF + kq * PER * N + j, sx0 = m > 0 ? FH : N;
-      const int bx1 = m < HN - 1 ? XB + 1 : S::OXF + N * N + kq * PER * N + j, sx1 = m < HN - 1 ? FH : N;
-      const int bym = j > 0 ? XB - HN : S::OY + (0 * 2 + c) * FH + kq * PER * HN + m, sym = j > 0 ? FH : HN;
-      const int byp = j < N - 1 ? XB + HN : S::OY + (1 * 2 + c) * FH + kq * PER * HN + m, syp = j < N - 1 ? FH : HN;
-      const double zlo = st[kq > 0 ? XB - FH : S::OZ + (0 * 2 + c) * FH + j * HN + m];
-      const double zhi = st[kq < KS - 1 ? XB + PER * FH : S::OZ + (1 * 2 + c) * FH + j * HN + m];
-#pragma unroll
-      for (int q = 0; q < PER; ++q) {
-        const int o = jo ^ c ^ (q & 1);
-        const double f = col[c][q];
-        const double xo = st[o ? bx1 + q * sx1 : bx0 + q * sx0];
-        const double xm = o ? col[X][q] : xo, xp = o ? xo : col[X][q];
-        const double ym = st[bym + q * sym], yp = st[byp + q * syp];
-        const double zm = q > 0 ? col[X][q - 1] : zlo, zp = q < PER - 1 ? col[X][q + 1] : zhi;
-        double sres = -2.0 * 3 * f;  // stencil.hpp:300-322, direction order
-        sres += xm;
-        sres += xp;
-        sres += ym;
-        sres += yp;
-        sres += zm;
-        sres += zp;
-        ap[c][q] = kind == KIND_ALL_INSIDE ? 0.0 : sres * w;
-        const int r8 = rr[c][q];
-        res[c][q] = (kind == KIND_ALL_INSIDE || r8 == 1) ? 0.0 : gcur[c][q] - ap[c][q];
-      }
-    }
+    double col[2][PER], res[2][PER], ap[2][PER];
+    qs_cells<N, TT>(st, kind, w, gcur, rr, col, res, ap, t);
     if (MODE == 1) {
-      if (leaf && kind != KIND_ALL_INSIDE) {
-#pragma unroll
-        for (int c = 0; c < 2; ++c)
-#pragma unroll
-          for (int q = 0; q < PER; ++q) {
-            if (rr[c][q] != 0) continue;  // inside rows excluded, cut rows by k_record_cut
-            rmx = fmax(rmx, fabs(res[c][q]));
-            rss += res[c][q] * res[c][q];
-            rcnt += 1.0;
-          }
-      }
+      qs_record<PER>(leaf, kind, rr, res, rmx, rss, rcnt);
     } else if (MODE == 2) {
 #pragma unroll
       for (int c = 0; c < 2; ++c)
@@ -988,54 +1014,7 @@ __global__ void __launch_bounds__(QStream3<N, TT>::THR, MINB) k_resid_stream(Lev
       rs_issue_async<N, S>(Lf, pf, st);
     }
     cp_async_commit();
-    if (MODE == 0) {
-      // children of parent (m, j/2, kq*PER/2 + p2): x pair (dx = o of the
-      // colour) of planes 2 p2 (dz 0) and 2 p2 + 1 (dz 1), this thread (dy = j & 1)
-      // and the thread of j + 1 (lane + 8)
-#pragma unroll
-      for (int p2 = 0; p2 < PER / 2; ++p2) {
-        double rv[2][2], fv[2][2];  // [dz][dx]
-        int cut = 0;
-#pragma unroll
-        for (int dz = 0; dz < 2; ++dz) {
-          const int q = 2 * p2 + dz;
-          const int c0 = jo ^ (q & 1);  // colour of the dx = 0 cell (o_c = 0)
-#pragma unroll
-          for (int dx = 0; dx < 2; ++dx) {
-            const int c = c0 ^ dx;
-            rv[dz][dx] = c ? res[1][q] : res[0][q];
-            fv[dz][dx] = c ? col[1][q] : col[0][q];
-            cut |= (c ? rr[1][q] : rr[0][q]) == 2;
-          }
-        }
-        double rn[2][2], fn[2][2];
-#pragma unroll
-        for (int dz = 0; dz < 2; ++dz)
-#pragma unroll
-          for (int dx = 0; dx < 2; ++dx) {
-            rn[dz][dx] = __shfl_down_sync(0xffffffffu, rv[dz][dx], HN);
-            fn[dz][dx] = __shfl_down_sync(0xffffffffu, fv[dz][dx], HN);
-          }
-        cut |= __shfl_down_sync(0xffffffffu, cut, HN);
-        if (!(j & 1) && !cut) {  // multigrid.hpp:706-721: x-fastest order
-          double sr = 0.0, sf = 0.0;
-          sr += rv[0][0], sf += fv[0][0];
-          sr += rv[0][1], sf += fv[0][1];
-          sr += rn[0][0], sf += fn[0][0];
-          sr += rn[0][1], sf += fn[0][1];
-          sr += rv[1][0], sf += fv[1][0];
-          sr += rv[1][1], sf += fv[1][1];
-          sr += rn[1][0], sf += fn[1][0];
-          sr += rn[1][1], sf += fn[1][1];
-          // pinned parents: re-pinned by k_pin_list afterwards
-          const int pi = cx * HN + m, pj = cy * HN + (j >> 1), pk = cz * HN + kq * (PER / 2) + p2;
-          const int pc = (pi + pj + pk) & 1, pe = (pi + N * (pj + N * pk)) >> 1;
-          const size_t pa = (size_t)Pp * NI + (size_t)pc * H + pe;
-          Lp.phi[pa] = sf / 8.0;
-          Lp.rhs[pa] = sr / 8.0;
-        }
-      }
-    }
+    if (MODE == 0) qs_restrict<N, TT>(Lp, Pp, cx, cy, cz, rr, col, res, t);
 #pragma unroll
     for (int c = 0; c < 2; ++c)
 #pragma unroll

@@ -158,8 +158,7 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_gs_tile(LevelView L, Le
   const int c = parity, X = 1 - c;
   const size_t base = (size_t)slot * G::NI;
   Halo<D, N> h;
-  const int ex = L.exp;
-  if (!(ex & 1)) h.prefetch(L, slot);
+  h.prefetch(L, slot);
   const uint8_t kind = L.kind[slot];
   const int sr = L.srow[slot];
   const double* __restrict__ src = L.phi + base + (size_t)X * G::H;
@@ -176,31 +175,17 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_gs_tile(LevelView L, Le
   const int32_t* rowp = sr < 0 ? nullptr : L.row_of + (size_t)sr * G::NI + c * G::H;
 #pragma unroll
   for (int q = 0; q < O::PER; ++q) rq[q] = rowp ? rowp[threadIdx.x + q * O::THR] : -1;
-  if (!(ex & 1)) h.issue(L, Lc, slot, X);
+  h.issue(L, Lc, slot, X);
   if (kind == KIND_ALL_INSIDE) return;  // whole CTA: no barrier is skipped unevenly
   double* __restrict__ dst = L.phi + base + (size_t)c * G::H;
-  if (ex & 2) {  // experiment: no shared memory, no compute
-#pragma unroll
-    for (int q = 0; q < O::PER; ++q) dst[threadIdx.x + q * O::THR] = ov[q] + gv[q];
-    return;
-  }
 #pragma unroll
   for (int q = 0; q < O::PER; ++q) {
     int j, k, B;
     O::at(q, j, k, B);
     T[B + ((X + j + k) & 1)] = ov[q];
   }
-  if (!(ex & 1)) h.store(T);
+  h.store(T);
   __syncthreads();
-  if (ex & 4) {  // experiment: smem round trip, trivial compute
-#pragma unroll
-    for (int q = 0; q < O::PER; ++q) {
-      int j, k, B;
-      O::at(q, j, k, B);
-      dst[threadIdx.x + q * O::THR] = T[B] + gv[q];
-    }
-    return;
-  }
 #pragma unroll
   for (int q = 0; q < O::PER; ++q) {
     int j, k, B;
@@ -276,7 +261,7 @@ __global__ void __launch_bounds__(Lean<D, N>::THR) k_gs_lean(LevelView L, int pa
   using TT = Tile<D, N>;
   using LN = Lean<D, N>;
   __shared__ double T[TT::SIZE];
-  const int slot = (L.exp & 128) ? (int)blockIdx.x : list[blockIdx.x];
+  const int slot = list[blockIdx.x];
   const int c = parity, X = 1 - c;
   const int t = threadIdx.x;
   const size_t base = (size_t)slot * G::NI;
@@ -286,7 +271,6 @@ __global__ void __launch_bounds__(Lean<D, N>::THR) k_gs_lean(LevelView L, int pa
   for (int u = 0; u < LN::HPER; ++u) {
     const int q = t + u * LN::THR;
     ns[u] = q < LN::HQ ? nbr_slot<D>(L, slot, q / LN::HT) : 0;  // -1: physical face
-    if (L.exp & 64) ns[u] = 0;
   }
   double ov[LN::PER], gv[LN::PER];
 #pragma unroll

@@ -163,12 +163,14 @@ def test_coarse_solve_single_level():
 
 
 @pytest.mark.timeout(900)
-@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4"])
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4", "cfg5@6"])
 def test_full_size_cycles_match_reference(name):
     """BASELINE configs 2 (256^3, FMG + 8 V, the headline), 3 (AMR, effective
-    512^3, 10 V) and 4 (512^3, 32 spheres, 12 V) at full size, GPU stencils, against the unmodified reference
-    solver run on the host's cores: residual histories within the floor-aware
-    bound, final phi within 1e-10 max|phi|."""
+    512^3, 10 V) and 4 (512^3, 32 spheres, 12 V) at full size, and config 5's
+    geometry and plan (two spheres at phi_b = +-1, Gaussian g, 10 V from phi = 0)
+    at 512^3, GPU stencils, against the unmodified reference solver run on the
+    host's cores: residual histories within the floor-aware bound, final phi
+    within 1e-10 max|phi|."""
     if "ref" not in ORACLES:
         pytest.skip("reference build (oracle/_ref) absent")
     case = cfgs.get_case(name)
@@ -177,24 +179,50 @@ def test_full_size_cycles_match_reference(name):
     assert hist[-1][0].max_resid < 1e-6 * hist[0][0].max_resid
 
 
+def _host_ram_gb():
+    try:
+        import psutil
+        return psutil.virtual_memory().available / 2**30
+    except Exception:
+        return 0.0
+
+
+@pytest.mark.slow
+@pytest.mark.timeout(2400)
+def test_config5_1024_matches_reference():
+    """BASELINE config 5 at its full 1024^3 (1.07e9 unknowns, 10 V from
+    phi = 0) against the unmodified reference on the host's cores.  The
+    reference's padded AoS fields need ~70 GB of host memory, so the test runs
+    where the host has room (the B200 box has ~196 GB)."""
+    if "ref" not in ORACLES:
+        pytest.skip("reference build (oracle/_ref) absent")
+    if _host_ram_gb() < 150:
+        pytest.skip(f"needs ~150 GB of free host memory for the reference at 1024^3 ({_host_ram_gb():.0f} GB)")
+    case = cfgs.get_case("cfg5")
+    rel, hist = _run_cycles(case, which="ref", gpu_stencils=True, threads=os.cpu_count() or 1)
+    assert rel <= 1e-10, rel
+    assert hist[-1][0].max_resid < 1e-5 * hist[0][0].max_resid
+
+
 @pytest.mark.timeout(900)
 def test_config5_full_size_properties():
     """BASELINE config 5 (1024^3, two spheres at phi_b = +-1, Gaussian g) at full
-    size on the GPU alone (the reference would need ~70 GB of host memory):
-    FMG + 10 V-cycles converge at the rate the reduced-size parity runs show,
-    the records are finite and strictly decreasing, and the solution respects
-    the boundary values (max |phi| within the pinned range plus the g effect)."""
+    size on the GPU alone, with BASELINE's plan (10 V-cycles from phi = 0, no
+    FMG): the records are finite and strictly decreasing, every cycle reduces
+    the residual at the rate the reference-checked sizes show (5-6x), and ten
+    cycles reduce it by more than 1e5."""
     from paper_2205_09411_b200 import DeviceMesh, MgConfig, MgSolver, StencilBuildConfig, build_stencils
     case = cfgs.get_case("cfg5")
+    assert not case.fmg_first and case.v_cycles == 10
     mesh = case.build_mesh()
     dev = DeviceMesh(mesh)
     build_stencils(dev, case.lsf, StencilBuildConfig(w_min=case.w_min))
     dev.set_field(VAR_RHS, case.rhs_fields(mesh), layout=LAYOUT_INTERIOR)
     sol = MgSolver(dev, None, MgConfig())
-    h = [sol.measure_residual(), sol.fmg_cycle()] + [sol.v_cycle() for _ in range(10)]
+    h = [sol.measure_residual()] + [sol.v_cycle() for _ in range(case.v_cycles)]
     r = np.array([x.max_resid for x in h])
     assert np.all(np.isfinite(r))
-    assert np.all(np.diff(r[1:]) < 0)
-    red = np.exp(np.mean(np.log(r[2:-1] / r[3:])))
+    assert np.all(np.diff(r) < 0), r
+    red = np.exp(np.mean(np.log(r[1:-1] / r[2:])))
     assert red > 3.0, red  # about 5-6x per V-cycle at every size tested against the reference
-    assert r[-1] < 1e-7 * r[0]
+    assert r[-1] < 1e-5 * r[0], r

@@ -1,5 +1,5 @@
-"""Per-level op times of config 2 under the PMG_EXP settings given on the
-command line (one subprocess each): python tools/exp_ops.py 0 268435456 ..."""
+"""Per-level in-graph op times of config 2 (each op captured 20x into one
+CUDA graph): python tools/exp_ops.py"""
 import os
 import subprocess
 import sys
@@ -33,8 +33,5 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "child":
         child()
         sys.exit(0)
-    for e in sys.argv[1:]:
-        env = dict(os.environ, PMG_EXP=e)
-        out = subprocess.run([sys.executable, __file__, "child"], capture_output=True, text=True, env=env)
-        print(f"PMG_EXP={e}", flush=True)
-        print(out.stdout.rstrip() if out.returncode == 0 else out.stderr[-2000:], flush=True)
+    out = subprocess.run([sys.executable, __file__, "child"], capture_output=True, text=True)
+    print(out.stdout.rstrip() if out.returncode == 0 else out.stderr[-2000:], flush=True)
