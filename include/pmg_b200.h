@@ -164,6 +164,36 @@ int pmg_b200_restrict_only(pmg_b200_ctx* ctx, int level);
 int pmg_b200_fas_level(pmg_b200_ctx* ctx, int level);
 int pmg_b200_level_record(pmg_b200_ctx* ctx, int level, double* out3);
 
+/* ---- the Morton-partitioned V-cycle (csrc/dist.h) ----------
+ * The reference has no multi-process path: this is the B200 decomposition of
+ * MgSolver::v_cycle (multigrid.hpp:483-499) over one context per GPU.
+ * set_partition: this context is rank `rank` of `world`; owner_of_block gives
+ *   the rank of every block id on the levels >= split_level (paper_2205_09411_b200
+ *   partition.morton_partition: Morton ranges of the split level, subtrees
+ *   follow); the levels below belong to rank 0.  Restricts every kernel to the
+ *   owned blocks and builds the device-resident halo plans (per level, per
+ *   peer, per colour).  Call after set_mesh and the stencils, before
+ *   solver_create.
+ * nccl_unique_id: 128 bytes for ncclCommInitRank, made on rank 0 and passed
+ *   to every rank by the caller.  dist_init_nccl: the NCCL transport (libnccl
+ *   resolved at run time); the whole cycle -- halo pack / unpack kernels and
+ *   grouped ncclSend / ncclRecv, the coarse-tail gather and broadcast, the
+ *   record all-gather -- is captured into one CUDA graph.
+ * dist_local_group: the in-process transport: ctxs[r] is rank r; each context
+ *   must then be driven by its own host thread (device copies between the
+ *   contexts, ordered by events; used to check the decomposition on one GPU).
+ * dist_v_cycle: one partitioned V-cycle; the stats are every rank's records
+ *   combined in rank order (the same on every rank).
+ * dist_info: out4 = {world, split level, transport (0 none, 1 NCCL,
+ *   2 in-process), halo cells received per V-cycle level sweep (both colours)}. */
+int pmg_b200_set_partition(pmg_b200_ctx* ctx, int world, int rank, int split_level, const int32_t* owner_of_block);
+int pmg_b200_nccl_unique_id(unsigned char* out128);
+int pmg_b200_dist_init_nccl(pmg_b200_ctx* ctx, const unsigned char* id128);
+int pmg_b200_dist_local_group(int n, pmg_b200_ctx* const* ctxs);
+int pmg_b200_dist_v_cycle(pmg_b200_ctx* ctx, pmg_cycle_stats_t* out);
+int pmg_b200_dist_v_cycle_async(pmg_b200_ctx* ctx);
+int pmg_b200_dist_info(pmg_b200_ctx* ctx, int32_t* out4);
+
 /* ---- post-solve fields -------------------------
  * pmg::face_gradient (proj/include/pmg/fields.hpp:149-232): the staggered
  * gradient of PHI on the faces of every leaf cell -- centred difference on

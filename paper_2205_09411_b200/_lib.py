@@ -71,6 +71,9 @@ EXPORTS = [
     "pmg_b200_set_owned", "pmg_b200_level_field_ptr", "pmg_b200_restrict_only", "pmg_b200_fas_level",
     "pmg_b200_level_record", "pmg_b200_n_leaves", "pmg_b200_face_gradient", "pmg_b200_error_norms",
     "pmg_b200_write_dump", "pmg_b200_stage_field_async", "pmg_b200_commit_staged_field",
+    "pmg_b200_set_partition", "pmg_b200_nccl_unique_id", "pmg_b200_dist_init_nccl",
+    "pmg_b200_dist_local_group", "pmg_b200_dist_v_cycle", "pmg_b200_dist_v_cycle_async",
+    "pmg_b200_dist_info",
 ]
 
 _lib = None
@@ -138,6 +141,13 @@ def load():
     lib.pmg_b200_commit_staged_field.argtypes = [vp]
     lib.pmg_b200_error_norms.argtypes = [vp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int,
                                          C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    lib.pmg_b200_set_partition.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_void_p]
+    lib.pmg_b200_nccl_unique_id.argtypes = [C.c_void_p]
+    lib.pmg_b200_dist_init_nccl.argtypes = [vp, C.c_void_p]
+    lib.pmg_b200_dist_local_group.argtypes = [C.c_int, C.POINTER(vp)]
+    lib.pmg_b200_dist_v_cycle.argtypes = [vp, C.POINTER(StatsT)]
+    lib.pmg_b200_dist_v_cycle_async.argtypes = [vp]
+    lib.pmg_b200_dist_info.argtypes = [vp, C.POINTER(C.c_int32)]
     _lib = lib
     return lib
 

@@ -13,6 +13,7 @@
 #include <tuple>
 
 #include "ctx.h"
+#include "dist.h"
 
 using namespace pmghost;
 using pmgdev::LevelView;
@@ -24,6 +25,7 @@ struct pmg_b200_ctx {
 namespace pmghost {
 
 Ctx::~Ctx() {
+  dist.reset();
   g_v.reset();
   g_fmg[0].reset();
   g_fmg[1].reset();
@@ -95,6 +97,7 @@ static void set_views(Ctx& c) {
 }
 
 static void invalidate_graphs(Ctx& c) {
+  if (c.dist) c.dist->g.reset(), c.dist->graph_failed = false;
   c.g_v.reset();
   c.g_fmg[0].reset();
   c.g_fmg[1].reset();
@@ -966,6 +969,143 @@ static void need_mesh(Ctx& c) { require(c.have_mesh, "mesh not set (call pmg_b20
 static void need_level(Ctx& c, int l, int lo = 1) {
   need_mesh(c);
   require(l >= lo && l <= c.mesh.L, "level out of range");
+}
+
+// ---------------------------------------------------------------- partitioned cycle (dist.h)
+static void enq_smooth_dist(Ctx& c, int l, int steps) {
+  for (int s = 0; s < steps; ++s)
+    for (int par = 0; par < 2; ++par) {
+      c.ops->gs(c, l, par);
+      dist_xchg(c, PMG_VAR_PHI, l, par);  // the colour just updated
+    }
+}
+// v_cycle (multigrid.hpp:483-499) over this rank's blocks, exchanging halo
+// layers after every phase that changes them; the coarse tail on rank 0
+static void enq_dist_cycle(Ctx& c) {
+  DistState& ds = *c.dist;
+  const int L = c.mesh.L, g = ds.split;
+  enq_clear_status(c);
+  enq_reset_records(c);
+  // halo phi as the owners hold it now (after init, an upload or the last cycle)
+  for (int l = g; l <= L; ++l) dist_xchg(c, PMG_VAR_PHI, l, 2);
+  for (int l = L; l >= std::max(g, 2); --l) {
+    enq_smooth_dist(c, l, c.cfg.n_down);
+    enq_restrict_only(c, l);  // restriction into l-1 and its pins, owned parents
+    if (l - 1 >= g) {
+      dist_xchg(c, PMG_VAR_PHI, l - 1, 2);
+      enq_fas_level(c, l);
+      dist_xchg(c, PMG_VAR_OLD, l - 1, 2);
+    } else {  // the split level's parents: octants gathered to rank 0, pinned there
+      dist_move(c, -1, 0, level_var(c, PMG_VAR_PHI, l - 1));
+      dist_move(c, -1, 0, level_var(c, PMG_VAR_RHS, l - 1));
+      if (ds.rank == 0) {
+        c.ops->pins(c, l - 1);
+        enq_fas_level(c, l);
+      }
+    }
+  }
+  if (g >= 2) {
+    if (ds.rank == 0) enq_v_span(c, g - 1);  // the coarse tail alone
+    dist_bcast_level(c, PMG_VAR_PHI, g - 1);
+    dist_bcast_level(c, PMG_VAR_OLD, g - 1);
+  } else {
+    enq_coarse(c);
+  }
+  for (int l = std::max(g, 2); l <= L; ++l) {
+    c.prolong_dead = c.cfg.n_up > 0 ? 0 : -1;
+    c.ops->prolong(c, l, false);
+    c.prolong_dead = -1;
+    dist_xchg(c, PMG_VAR_PHI, l, 2);
+    enq_smooth_dist(c, l, c.cfg.n_up);
+    c.ops->record(c, l);
+  }
+  dist_records(c);
+  PMG_CUDA(cudaMemcpyAsync(c.h_out, c.stats.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  PMG_CUDA(cudaMemcpyAsync(c.h_out + 2, c.diag.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  PMG_CUDA(cudaMemcpyAsync(c.h_status, c.status.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+}
+// one partitioned V-cycle: a CUDA graph (no transport, or NCCL -- pack kernels
+// and NCCL calls captured together), eager with the in-process transport
+static void launch_dist_cycle(Ctx& c) {
+  require(c.solver, "solver not created (call pmg_b200_solver_create)", PMG_ERR_STATE);
+  require(c.dist != nullptr, "no partition (call pmg_b200_set_partition)", PMG_ERR_STATE);
+  DistState& ds = *c.dist;
+  require(ds.world == 1 || ds.transport != TR_NONE, "partition over several ranks without a transport "
+          "(pmg_b200_dist_init_nccl / pmg_b200_dist_local_group)", PMG_ERR_STATE);
+  if (ds.transport == TR_LOCAL || ds.graph_failed) {
+    enq_dist_cycle(c);
+  } else {
+    if (!ds.g.exec) {
+      cudaGraph_t graph = nullptr;
+      PMG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+      bool ok = true;
+      try {
+        enq_dist_cycle(c);
+      } catch (...) {
+        ok = false;
+      }
+      const cudaError_t e = cudaStreamEndCapture(c.stream, &graph);
+      if (ok && e == cudaSuccess && graph && cudaGraphInstantiate(&ds.g.exec, graph, 0) == cudaSuccess) {
+        cudaGraphDestroy(graph);
+      } else {  // a transport that cannot be captured: replay the enqueue every cycle
+        if (graph) cudaGraphDestroy(graph);
+        (void)cudaGetLastError();
+        ds.g.exec = nullptr;
+        ds.graph_failed = true;
+        enq_dist_cycle(c);
+        c.have_guess = true;
+        return;
+      }
+    }
+    PMG_CUDA(cudaGraphLaunch(ds.g.exec, c.stream));
+  }
+  c.have_guess = true;
+}
+
+// ownership from the caller's partition (owner rank per block id on the
+// levels >= split; the levels below belong to rank 0), then the halo plans
+static void set_partition(Ctx& c, int world, int rank, int split, const int32_t* owner) {
+  need_mesh(c);
+  const HostMesh& m = c.mesh;
+  require(world >= 1 && rank >= 0 && rank < world, "bad world / rank");
+  require(split >= 1 && split <= m.L, "split level out of range");
+  require(world == 1 || split >= 2, "a partition over several ranks needs a split level >= 2 "
+          "(the coarse solve of level 1 runs on rank 0)");
+  auto ds = std::make_unique<DistState>();
+  ds->world = world;
+  ds->rank = rank;
+  ds->split = world == 1 ? 1 : split;
+  ds->owner.assign((size_t)m.nb, 0);
+  if (owner) ds->owner.assign(owner, owner + m.nb);
+  for (int id = 0; id < m.nb; ++id)
+    require(ds->owner[(size_t)id] >= 0 && ds->owner[(size_t)id] < world, "owner rank out of range");
+  for (int id = 0; id < m.nb; ++id) {  // a subtree stays on its split-level ancestor's rank
+    const int p = m.parent[(size_t)id];
+    if (m.level[(size_t)id] > ds->split && p >= 0)
+      require(ds->owner[(size_t)id] == ds->owner[(size_t)p], "a block and its parent on different ranks");
+  }
+  PMG_CUDA(cudaEventCreateWithFlags(&ds->ev_packed, cudaEventDisableTiming));
+  PMG_CUDA(cudaEventCreateWithFlags(&ds->ev_copied, cudaEventDisableTiming));
+  c.dist = std::move(ds);
+  c.owned.assign((size_t)m.L + 1, {});
+  for (int l = 1; l <= m.L; ++l) {
+    LevelDev& d = *c.lev[(size_t)l];
+    auto& o = c.owned[(size_t)l];
+    o.assign((size_t)d.nb, 0);
+    d.n_own = 0;
+    for (int s = 0; s < d.nb; ++s) {
+      o[(size_t)s] = dist_owner_slot(c, l, s) == rank ? 1 : 0;
+      d.n_own += o[(size_t)s];
+    }
+    d.own.upload(o, c.stream);
+    d.has_own = world > 1;
+    if (!d.has_own) o.clear();
+  }
+  if (c.st.valid) upload_stencils(c);
+  build_dist_plans(c);
+  set_views(c);
+  invalidate_graphs(c);
+  PMG_CUDA(cudaStreamSynchronize(c.stream));
 }
 
 static void set_mesh(Ctx& c, int nb, const int32_t* level, const int32_t* coords,
@@ -1864,6 +2004,80 @@ int pmg_b200_coarse_info(pmg_b200_ctx* h, int32_t* iters, double* rel) {
     *rel = c.h_out[2];
   });
 }
+int pmg_b200_set_partition(pmg_b200_ctx* h, int world, int rank, int split_level, const int32_t* owner_of_block) {
+  return guard(h, [&](Ctx& c) { set_partition(c, world, rank, split_level, owner_of_block); });
+}
+int pmg_b200_nccl_unique_id(unsigned char* out) {
+  if (!out) return PMG_ERR_INVALID_ARG;
+  NcclApi& n = nccl_api();
+  if (!n.ok) return PMG_ERR_CUDA;
+  ncclUniqueId id;
+  if (n.GetUniqueId(&id) != ncclSuccess) return PMG_ERR_CUDA;
+  std::memcpy(out, id.internal, sizeof(id.internal));
+  return PMG_OK;
+}
+int pmg_b200_dist_init_nccl(pmg_b200_ctx* h, const unsigned char* id) {
+  return guard(h, [&](Ctx& c) {
+    require(c.dist != nullptr, "no partition (call pmg_b200_set_partition)", PMG_ERR_STATE);
+    NcclApi& n = nccl_api();
+    require(n.ok, "NCCL unavailable: " + n.why, PMG_ERR_CUDA);
+    ncclUniqueId uid;
+    std::memcpy(uid.internal, id, sizeof(uid.internal));
+    DistState& ds = *c.dist;
+    if (ds.comm) {
+      PMG_NCCL(n.CommDestroy(ds.comm));
+      ds.comm = nullptr;
+    }
+    PMG_NCCL(n.CommInitRank(&ds.comm, ds.world, uid, ds.rank));
+    ds.transport = TR_NCCL;
+    invalidate_graphs(c);
+  });
+}
+int pmg_b200_dist_local_group(int n, pmg_b200_ctx* const* ctxs) {
+  if (n < 1 || !ctxs) return PMG_ERR_INVALID_ARG;
+  auto grp = std::make_shared<LocalGroup>();
+  for (int r = 0; r < n; ++r) {
+    if (!ctxs[r] || !ctxs[r]->c.dist) return PMG_ERR_STATE;
+    grp->ctx.push_back(&ctxs[r]->c);
+  }
+  for (int r = 0; r < n; ++r) {
+    DistState& ds = *ctxs[r]->c.dist;
+    if (ds.world != n || ds.rank != r) {
+      ctxs[r]->c.err = "local group: context " + std::to_string(r) + " is not rank " + std::to_string(r) +
+                       " of a " + std::to_string(n) + "-rank partition";
+      return PMG_ERR_STATE;
+    }
+  }
+  for (int r = 0; r < n; ++r) {
+    DistState& ds = *ctxs[r]->c.dist;
+    ds.group = grp;
+    ds.transport = TR_LOCAL;
+    invalidate_graphs(ctxs[r]->c);
+  }
+  return PMG_OK;
+}
+int pmg_b200_dist_v_cycle_async(pmg_b200_ctx* h) {
+  return guard(h, [&](Ctx& c) { launch_dist_cycle(c); });
+}
+int pmg_b200_dist_v_cycle(pmg_b200_ctx* h, pmg_cycle_stats_t* out) {
+  return guard(h, [&](Ctx& c) {
+    launch_dist_cycle(c);
+    cycle_result(c, out);
+  });
+}
+int pmg_b200_dist_info(pmg_b200_ctx* h, int32_t* out4) {
+  return guard(h, [&](Ctx& c) {
+    require(c.dist != nullptr, "no partition", PMG_ERR_STATE);
+    const DistState& ds = *c.dist;
+    long long halo = 0;
+    for (const auto& lv : ds.halo) halo += lv[2].nr;
+    out4[0] = ds.world;
+    out4[1] = ds.split;
+    out4[2] = ds.transport;
+    out4[3] = (int32_t)std::min<long long>(halo, INT32_MAX);
+  });
+}
+
 int pmg_b200_synchronize(pmg_b200_ctx* h) {
   return guard(h, [&](Ctx& c) { PMG_CUDA(cudaStreamSynchronize(c.stream)); });
 }

@@ -80,6 +80,15 @@ struct DevBuf {
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p, n = o.n;
+      o.p = nullptr, o.n = 0;
+    }
+    return *this;
+  }
   ~DevBuf() { release(); }
   void release() {
     if (p) cudaFree(p);
@@ -183,6 +192,7 @@ struct LevelDev {
 };
 
 struct Ctx;
+struct DistState;  // dist.h: the Morton-partitioned cycle
 
 // Launchers, templated on (Dim, N) inside ops.cu.
 struct Ops {
@@ -285,6 +295,7 @@ struct Ctx {
   // attribute is set: cudaFuncSetAttribute is per device, a context is one device
   std::unordered_set<const void*> attr_done;
   int cluster16 = -1;  // 16-CTA coarse-solve cluster schedulable (-1: not yet queried)
+  std::unique_ptr<DistState> dist;  // pmg_b200_set_partition (nullptr: one context, whole mesh)
 
   ~Ctx();
 };
