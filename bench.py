@@ -1,22 +1,27 @@
 #!/usr/bin/env python3
-"""Benchmark of the B200 V-cycle hot path on BASELINE config 2 (the headline).
+"""Benchmark of the B200 V-cycle hot path.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--config cfg2] [--no-cpu-baseline]
+                    [--config cfgX] [--replicas] [--no-cpu-baseline]
 
-Workload (BASELINE.json configs[1]): 3D [0,1]^3, 256^3 fp64 cells in 16^3
-blocks (L=5), sphere c=(.5,.5,.5) R=0.2 with phi=1, phi=0 on the outer faces,
-g = seeded 1e-2*U[-1,1); setup + GPU stencil build + FMG, then a STEP is one
-V-cycle (2+2 GS-RB) over the whole mesh.  Inputs are synthetic, generated on
-the host (configs.py) and resident in HBM when the timed region starts.
-The finest level alone (phi + rhs = 268 MB) exceeds the 126 MB L2, so no
-explicit L2 flush is needed between steps.
+N = 1 (default): BASELINE config 2, the headline (BASELINE.json configs[1]):
+3D [0,1]^3, 256^3 fp64 cells in 16^3 blocks (L=5), sphere c=(.5,.5,.5) R=0.2
+with phi=1, phi=0 on the outer faces, g = seeded 1e-2*U[-1,1); setup + GPU
+stencil build + FMG, then a STEP is one V-cycle (2+2 GS-RB) over the whole
+mesh, replayed as one CUDA graph.  Inputs are synthetic, generated on the host
+(configs.py) and resident in HBM when the timed region starts.  The finest
+level alone (phi + rhs = 268 MB) exceeds the 126 MB L2, so no explicit L2
+flush is needed between steps.
 
-N > 1 (torchrun): every rank solves its own replica of the workload (weak
-scaling, no data-path collective); time = max over ranks.  The
-Morton-partitioned single-problem path is the next row.
+N > 1 (torchrun, one rank per GPU): BASELINE config 5 -- ONE 1024^3 problem
+(two spheres at phi_b = +-1, Gaussian g) Morton-partitioned over the ranks
+(csrc/dist.h: per-rank blocks + halo in HBM, halo exchange over NCCL inside
+the per-rank CUDA graph, coarse tail on rank 0): strong scaling, the time of a
+step is the max over ranks.  ``--replicas`` instead runs N independent copies
+of the config (weak scaling).  ``--config`` picks another BASELINE config.
+
 ``--impl reference`` times the reference's own CPU solver (oracle/_ref,
-compiled from /root/reference) on the host's cores instead.
+compiled from /root/reference) on the host's cores for the same config.
 """
 from __future__ import annotations
 
@@ -219,7 +224,8 @@ def run_reference(args, case):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    r = cpu_reference_run(case, args.steps, args.warmup)
+    # a bounded sample: at most ~90 s of V-cycles (config 5 at 1024^3 takes ~6 s each on 16 cores)
+    r = cpu_reference_run(case, args.steps, args.warmup, budget_s=90.0)
     t = sum(r["times"])
     k = len(r["times"])
     value = r["leaf"] * k / t
@@ -240,12 +246,12 @@ def run_reference(args, case):
 
 
 def run_partitioned(args, case):
-    """--partitioned: ONE problem Morton-partitioned over the torchrun ranks
-    (distributed.DistributedMgSolver: face-layer exchange after every phase
-    over torch.distributed / NCCL, coarse tail on rank 0).
-    Strong scaling; the time of a V-cycle is the max over ranks.  The driver
-    is host-orchestrated (one C-ABI call per operation), so this measures the
-    decomposition, not the single-GPU graph's speed."""
+    """ONE problem Morton-partitioned over the torchrun ranks (SURVEY.md §8e;
+    distributed.DistributedMgSolver over csrc/dist.h): each rank holds its
+    blocks and their halo, runs its part of every V-cycle as one CUDA graph
+    with the NCCL halo exchange captured in it; the coarse tail runs on rank 0.
+    Strong scaling: value = the problem's unknowns x steps / (max over ranks of
+    the CUDA-event time)."""
     import torch
     import torch.distributed as dist
 
@@ -258,39 +264,94 @@ def run_partitioned(args, case):
     torch.cuda.set_device(local)
     if ws > 1 and not dist.is_initialized():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    t0 = time.perf_counter()
     mesh = case.build_mesh()
+    t_mesh = time.perf_counter() - t0
     dev = DeviceMesh(mesh, device=local)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
     build_stencils(dev, case.lsf, StencilBuildConfig(w_min=case.w_min))
+    t_stencil = time.perf_counter() - t0
     dev.set_field(VAR_RHS, case.rhs_fields(mesh), layout=LAYOUT_INTERIOR)
-    sol = DistributedMgSolver(dev, MgConfig())
-    for _ in range(args.warmup):
-        sol.v_cycle()
-    times = []
-    for _ in range(args.steps):
+    sol = DistributedMgSolver(dev, MgConfig(), world=ws, rank=rank)
+    stream = torch.cuda.ExternalStream(dev.stream, device=local)
+    L = mesh.n_levels
+
+    def barrier():
         torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
-        t0 = time.perf_counter()
-        st = sol.v_cycle()
+
+    def max_over_ranks(x):
+        if ws == 1:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # the config's plan (10 V from phi = 0 for config 5): residual history
+    hist = [sol.v_cycle().max_resid for _ in range(case.v_cycles)]
+    red = [hist[i] / hist[i + 1] for i in range(len(hist) - 1) if hist[i + 1] > 0]
+    reduction = math.exp(sum(math.log(x) for x in red) / len(red)) if red else None
+    for _ in range(args.warmup):
+        sol.v_cycle_async()
+    sol.cycle_result()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            sol.v_cycle_async()
+        e1.record(stream)
+        stats = sol.cycle_result()
         torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        if ws > 1:
-            tt = torch.tensor([dt], device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            dt = float(tt.item())
-        times.append(dt)
+    ms_total = max_over_ranks(e0.elapsed_time(e1))
+    # end to end through the public API: K cycles with the stats read back
+    # every step (host wall clock); the rank's rhs stays resident
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        sol.v_cycle()
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
     leaf = case.leaf_cells(mesh)
-    t = sum(times)
+    ms_step = ms_total / args.steps
+    peak, peak_kind = measured_peaks()
+    BV = vcycle_bytes(mesh, case.N, case.dim)
+    vc_gbs = BV / (ms_step * 1e-3) / 1e9
+    fbytes = max_over_ranks(sol.field_bytes())
+    info = sol.info()
+    kernels = info["graph_kernels"]
     if rank == 0:
-        line = {"metric": METRIC, "value": leaf * len(times) / t, "unit": UNIT, "n_gpus": ws,
-                "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * t / len(times),
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic",
-                "config": {"workload": f"{case.name}: {case.notes}; step = one V-cycle, one problem "
-                                       f"Morton-partitioned over {ws} rank(s)",
-                           "leaf_cells": leaf, "parallelism": f"morton x{ws}",
-                           "split_level": int(sol.part.split_level)},
-                "final_max_resid": st.max_resid}
+        line = {
+            "metric": METRIC, "value": leaf * args.steps / (ms_total * 1e-3), "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{case.name}: {case.notes}; step = one V-cycle of ONE problem "
+                                   f"Morton-partitioned over {ws} GPU(s)",
+                       "leaf_cells": leaf, "levels": L, "blocks": mesh.n_blocks,
+                       "parallelism": f"morton x{ws}" if ws > 1 else "1 GPU (partitioned path, one rank)",
+                       "split_level": info["split_level"],
+                       "l2_flush": "none needed: finest level > 126 MB L2 per rank"},
+            "vcycle_roofline": {"algorithmic_bytes": BV, "achieved": vc_gbs, "peak": peak * ws, "unit": "GB/s",
+                                "frac": vc_gbs / (peak * ws), "bytes_per_unknown": BV / leaf,
+                                "peak_kind": f"{peak_kind}, x {ws} GPUs"},
+            "e2e": {"value": leaf * args.steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 16 + 16 + 4,
+                    "mode": "public API per step (DistributedMgSolver.v_cycle: graph launch + stats read, "
+                            "host wall clock, max over ranks); rhs resident"},
+            "gpu_launches": kernels * args.steps,
+            "kernels_per_step_rank0": kernels,
+            "transport": {0: "none", 1: "nccl", 2: "in-process"}[info["transport"]],
+            "cycle_graph": bool(info["graph"]),
+            "field_bytes_per_rank_max": fbytes,
+            "halo_cells_per_level_sweep_rank0": info["halo_cells"],
+            "clocks": clk.summary(),
+            "residual_reduction_per_cycle": reduction,
+            "residual_history": hist,
+            "setup_s": {"mesh": t_mesh, "stencil_build_gpu": t_stencil},
+            "final_max_resid": stats.max_resid,
+        }
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
@@ -491,17 +552,22 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default=None,
+                    help="BASELINE config (default: cfg2 on one GPU, cfg5 partitioned on several)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: N independent copies of the config (weak scaling) instead of one partitioned problem")
     ap.add_argument("--partitioned", action="store_true",
-                    help="one problem Morton-partitioned over the ranks (host-driven, strong scaling)")
+                    help="the partitioned path even on one GPU (one rank)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    ws, _, _ = dist_env()
+    partitioned = args.partitioned or (ws > 1 and not args.replicas)
     from paper_2205_09411_b200 import configs as cfgs
-    case = cfgs.get_case(args.config)
+    case = cfgs.get_case(args.config or ("cfg5" if partitioned and ws > 1 else "cfg2"))
     if args.impl == "reference":
         return run_reference(args, case)
-    if args.partitioned:
+    if partitioned:
         return run_partitioned(args, case)
     return run_b200(args, case)
 

@@ -184,15 +184,21 @@ int pmg_b200_level_record(pmg_b200_ctx* ctx, int level, double* out3);
  *   contexts, ordered by events; used to check the decomposition on one GPU).
  * dist_v_cycle: one partitioned V-cycle; the stats are every rank's records
  *   combined in rank order (the same on every rank).
- * dist_info: out4 = {world, split level, transport (0 none, 1 NCCL,
- *   2 in-process), halo cells received per V-cycle level sweep (both colours)}. */
+ * dist_info: out6 = {world, split level, transport (0 none, 1 NCCL,
+ *   2 in-process), halo cells received per sweep of every partitioned level
+ *   (both colours), kernels in the captured cycle graph, graph captured (0/1)}. */
 int pmg_b200_set_partition(pmg_b200_ctx* ctx, int world, int rank, int split_level, const int32_t* owner_of_block);
 int pmg_b200_nccl_unique_id(unsigned char* out128);
 int pmg_b200_dist_init_nccl(pmg_b200_ctx* ctx, const unsigned char* id128);
 int pmg_b200_dist_local_group(int n, pmg_b200_ctx* const* ctxs);
 int pmg_b200_dist_v_cycle(pmg_b200_ctx* ctx, pmg_cycle_stats_t* out);
 int pmg_b200_dist_v_cycle_async(pmg_b200_ctx* ctx);
-int pmg_b200_dist_info(pmg_b200_ctx* ctx, int32_t* out4);
+int pmg_b200_dist_info(pmg_b200_ctx* ctx, int32_t* out6);
+/* device bytes held by the solution / rhs / OLD / residual arrays of every
+ * level: the whole mesh on one context; on a partitioned rank only its blocks
+ * and their halo blocks are backed (CUDA virtual memory), the coarse tail and
+ * levels of at most 64 blocks stay whole */
+int pmg_b200_field_bytes(pmg_b200_ctx* ctx, double* out);
 
 /* ---- post-solve fields -------------------------
  * pmg::face_gradient (proj/include/pmg/fields.hpp:149-232): the staggered

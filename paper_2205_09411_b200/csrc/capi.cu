@@ -1046,6 +1046,16 @@ static void launch_dist_cycle(Ctx& c) {
       }
       const cudaError_t e = cudaStreamEndCapture(c.stream, &graph);
       if (ok && e == cudaSuccess && graph && cudaGraphInstantiate(&ds.g.exec, graph, 0) == cudaSuccess) {
+        size_t nn = 0;
+        PMG_CUDA(cudaGraphGetNodes(graph, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        PMG_CUDA(cudaGraphGetNodes(graph, nodes.data(), &nn));
+        ds.g.kernels = 0;
+        for (auto nd : nodes) {
+          cudaGraphNodeType t;
+          PMG_CUDA(cudaGraphNodeGetType(nd, &t));
+          if (t == cudaGraphNodeTypeKernel) ++ds.g.kernels;
+        }
         cudaGraphDestroy(graph);
       } else {  // a transport that cannot be captured: replay the enqueue every cycle
         if (graph) cudaGraphDestroy(graph);
@@ -1103,6 +1113,7 @@ static void set_partition(Ctx& c, int world, int rank, int split, const int32_t*
   }
   if (c.st.valid) upload_stencils(c);
   build_dist_plans(c);
+  if (world > 1) shrink_fields(c);
   set_views(c);
   invalidate_graphs(c);
   PMG_CUDA(cudaStreamSynchronize(c.stream));
@@ -2065,19 +2076,32 @@ int pmg_b200_dist_v_cycle(pmg_b200_ctx* h, pmg_cycle_stats_t* out) {
     cycle_result(c, out);
   });
 }
-int pmg_b200_dist_info(pmg_b200_ctx* h, int32_t* out4) {
+int pmg_b200_dist_info(pmg_b200_ctx* h, int32_t* out6) {
   return guard(h, [&](Ctx& c) {
     require(c.dist != nullptr, "no partition", PMG_ERR_STATE);
     const DistState& ds = *c.dist;
     long long halo = 0;
     for (const auto& lv : ds.halo) halo += lv[2].nr;
-    out4[0] = ds.world;
-    out4[1] = ds.split;
-    out4[2] = ds.transport;
-    out4[3] = (int32_t)std::min<long long>(halo, INT32_MAX);
+    out6[0] = ds.world;
+    out6[1] = ds.split;
+    out6[2] = ds.transport;
+    out6[3] = (int32_t)std::min<long long>(halo, INT32_MAX);
+    out6[4] = ds.g.exec ? ds.g.kernels : 0;
+    out6[5] = ds.g.exec ? 1 : 0;
   });
 }
 
+int pmg_b200_field_bytes(pmg_b200_ctx* h, double* out) {
+  return guard(h, [&](Ctx& c) {
+    need_mesh(c);
+    double b = 0;
+    for (int l = 1; l <= c.mesh.L; ++l) {
+      const LevelDev& d = *c.lev[(size_t)l];
+      b += (double)(d.phi.bytes() + d.rhs.bytes() + d.old.bytes() + d.res.bytes());
+    }
+    *out = b;
+  });
+}
 int pmg_b200_synchronize(pmg_b200_ctx* h) {
   return guard(h, [&](Ctx& c) { PMG_CUDA(cudaStreamSynchronize(c.stream)); });
 }

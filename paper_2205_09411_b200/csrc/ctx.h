@@ -1,5 +1,6 @@
 // ctx.h -- host-side state of one solver context (one mesh on one device).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -73,28 +74,90 @@ inline void pdl_launch_on(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cuda
   PMG_CUDA(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
 }
 
+// Sparse device array (CUDA virtual memory management, driver entry points
+// resolved at run time): the whole index range is reserved, physical memory
+// is mapped only for the chunks a rank touches (its blocks and their halo
+// blocks), so a partitioned rank holds its share of the mesh, not all of it.
+struct VmmApi {
+  bool ok = false;
+  CUresult (*AddressReserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
+  CUresult (*AddressFree)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*Create)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long) = nullptr;
+  CUresult (*Release)(CUmemGenericAllocationHandle) = nullptr;
+  CUresult (*Map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
+  CUresult (*Unmap)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*SetAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
+  CUresult (*Granularity)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags) = nullptr;
+};
+inline VmmApi& vmm_api() {
+  static VmmApi a = [] {
+    VmmApi x;
+    auto get = [](const char* n) -> void* {
+      void* f = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint(n, &f, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+        return nullptr;
+      return f;
+    };
+    x.AddressReserve = (decltype(x.AddressReserve))get("cuMemAddressReserve");
+    x.AddressFree = (decltype(x.AddressFree))get("cuMemAddressFree");
+    x.Create = (decltype(x.Create))get("cuMemCreate");
+    x.Release = (decltype(x.Release))get("cuMemRelease");
+    x.Map = (decltype(x.Map))get("cuMemMap");
+    x.Unmap = (decltype(x.Unmap))get("cuMemUnmap");
+    x.SetAccess = (decltype(x.SetAccess))get("cuMemSetAccess");
+    x.Granularity = (decltype(x.Granularity))get("cuMemGetAllocationGranularity");
+    x.ok = x.AddressReserve && x.AddressFree && x.Create && x.Release && x.Map && x.Unmap && x.SetAccess &&
+           x.Granularity;
+    (void)cudaGetLastError();
+    return x;
+  }();
+  return a;
+}
+struct SparseAlloc {
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  std::vector<std::pair<size_t, size_t>> runs;  // mapped (offset, bytes)
+  std::vector<CUmemGenericAllocationHandle> handles;
+  size_t mapped = 0;
+  SparseAlloc() = default;
+  SparseAlloc(const SparseAlloc&) = delete;
+  SparseAlloc& operator=(const SparseAlloc&) = delete;
+  ~SparseAlloc() {
+    VmmApi& v = vmm_api();
+    for (size_t i = 0; i < runs.size(); ++i) {
+      v.Unmap(base + runs[i].first, runs[i].second);
+      v.Release(handles[i]);
+    }
+    if (base) v.AddressFree(base, size);
+  }
+};
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
+  std::shared_ptr<SparseAlloc> sp;  // set: p lies in a sparse (VMM) range
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), sp(std::move(o.sp)) { o.p = nullptr, o.n = 0; }
   DevBuf& operator=(DevBuf&& o) noexcept {
     if (this != &o) {
       release();
-      p = o.p, n = o.n;
+      p = o.p, n = o.n, sp = std::move(o.sp);
       o.p = nullptr, o.n = 0;
     }
     return *this;
   }
   ~DevBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (sp) sp.reset();
+    else if (p) cudaFree(p);
     p = nullptr;
     n = 0;
   }
+  size_t bytes() const { return sp ? sp->mapped : n * sizeof(T); }
   void alloc(size_t count) {
     release();
     if (count == 0) count = 1;

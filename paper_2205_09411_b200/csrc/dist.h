@@ -322,6 +322,91 @@ static void build_dist_plans(Ctx& c) {
   ds.recs.alloc((size_t)W * (size_t)(m.L + 1));
 }
 
+// ---------------------------------------------------------------- per-rank memory
+#define PMG_CU(x)                                                                                 \
+  do {                                                                                            \
+    CUresult r_ = (x);                                                                            \
+    if (r_ != CUDA_SUCCESS)                                                                       \
+      throw PmgError(PMG_ERR_CUDA, "CUDA driver error " + std::to_string((int)r_) + " at " #x);   \
+  } while (0)
+
+// Replace `buf` (slot-major, slot_bytes per block) by a sparse copy that maps
+// only the chunks holding the blocks flagged in `need`.
+static void make_sparse(Ctx& c, DevBuf<double>& buf, const std::vector<uint8_t>& need, size_t slot_bytes) {
+  VmmApi& v = vmm_api();
+  if (!v.ok) throw PmgError(PMG_ERR_CUDA, "CUDA virtual memory management unavailable");
+  CUmemAllocationProp prop = {};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = c.device;
+  size_t gran = 0;
+  PMG_CU(v.Granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM));
+  const size_t total = buf.n * sizeof(double), size = (total + gran - 1) / gran * gran, nch = size / gran;
+  std::vector<uint8_t> ch(nch, 0);
+  for (size_t s = 0; s < need.size(); ++s)
+    if (need[s])
+      for (size_t q = s * slot_bytes / gran; q <= ((s + 1) * slot_bytes - 1) / gran; ++q) ch[q] = 1;
+  auto sa = std::make_shared<SparseAlloc>();
+  sa->size = size;
+  PMG_CU(v.AddressReserve(&sa->base, size, gran, 0, 0));
+  CUmemAccessDesc acc = {};
+  acc.location = prop.location;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  for (size_t q = 0; q < nch;) {
+    if (!ch[q]) {
+      ++q;
+      continue;
+    }
+    size_t e = q;
+    while (e < nch && ch[e]) ++e;
+    const size_t off = q * gran, bytes = (e - q) * gran;
+    CUmemGenericAllocationHandle hnd;
+    PMG_CU(v.Create(&hnd, bytes, &prop, 0));
+    sa->runs.emplace_back(off, bytes);
+    sa->handles.push_back(hnd);
+    PMG_CU(v.Map(sa->base + off, bytes, 0, hnd, 0));
+    PMG_CU(v.SetAccess(sa->base + off, bytes, &acc, 1));
+    sa->mapped += bytes;
+    PMG_CUDA(cudaMemcpyAsync((char*)sa->base + off, (const char*)buf.p + off, std::min(bytes, total - off),
+                             cudaMemcpyDeviceToDevice, c.stream));
+    q = e;
+  }
+  PMG_CUDA(cudaStreamSynchronize(c.stream));
+  const size_t n = buf.n;
+  buf.release();
+  buf.p = (double*)sa->base;
+  buf.n = n;
+  buf.sp = sa;
+}
+
+// Fields of the levels >= split with more than kSmallLevel blocks keep only
+// this rank's blocks and their same-level face neighbours (the halo); the
+// small levels and the coarse tail stay whole.
+static void shrink_fields(Ctx& c) {
+  DistState& ds = *c.dist;
+  const HostMesh& m = c.mesh;
+  for (int l = ds.split; l <= m.L; ++l) {
+    LevelDev& d = *c.lev[(size_t)l];
+    if (d.nb <= kSmallLevel) continue;
+    std::vector<uint8_t> need((size_t)d.nb, 0);
+    for (int s = 0; s < d.nb; ++s) {
+      if (dist_owner_slot(c, l, s) != ds.rank) continue;
+      need[(size_t)s] = 1;
+      const int id = m.slots[(size_t)l][(size_t)s];
+      for (int f = 0; f < c.F; ++f) {
+        const int nid = m.nbr[(size_t)id * 6 + f];
+        if (nid >= 0) need[(size_t)m.slot_of[(size_t)nid]] = 1;
+      }
+    }
+    const size_t sb = (size_t)c.NI * sizeof(double);
+    make_sparse(c, d.phi, need, sb);
+    make_sparse(c, d.rhs, need, sb);
+    make_sparse(c, d.old, need, sb);
+    make_sparse(c, d.res, need, sb);
+  }
+  c.staging.release();  // whole-mesh upload staging: allocated again on demand
+}
+
 // ---------------------------------------------------------------- transport
 static double* level_var(Ctx& c, int var, int l) {
   LevelDev& d = *c.lev[(size_t)l];

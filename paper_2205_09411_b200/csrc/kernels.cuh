@@ -591,15 +591,18 @@ __global__ void __launch_bounds__(1024) k_coarse(LevelView L, CoarseDev C,
 // layout 0: padded (N+2)^D per block (reference Block::data slice, mesh.hpp:47)
 // layout 1: interior N^D per block, x fastest
 template <int D, int N>
+// own: a partitioned rank's blocks (nullptr: every block); the others are not
+// written (their storage may not even be mapped, dist.h)
 __global__ void __launch_bounds__(kThreads) k_scatter(int nb, double* __restrict__ dst,
                                                       const double* __restrict__ src,
                                                       const int32_t* __restrict__ slot_id,
-                                                      int layout) {
+                                                      int layout, const uint8_t* __restrict__ own) {
   pdl_begin();
   using G = Geo<D, N>;
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (long long)nb * G::NI) return;
   const int slot = (int)(t / G::NI);
+  if (own && !own[slot]) return;
   const int ii = (int)(t % G::NI);
   const int i = ii % N, j = (ii / N) % N, k = D == 3 ? ii / (N * N) : 0;
   const long long id = slot_id[slot];
@@ -641,7 +644,8 @@ __global__ void __launch_bounds__(kThreads) k_gather(LevelView L, LevelView Lc, 
   }
   const int out = (i < 0 || i >= N) + (j < 0 || j >= N) + (D == 3 && (k < 0 || k >= N));
   double v = 0.0;
-  if (out == 0) {
+  if (!owned(L, slot)) {  // a partitioned rank reports its own blocks (others: 0)
+  } else if (out == 0) {
     const double* arr = var == 0 ? L.phi : var == 1 ? L.rhs : var == 2 ? L.res : L.old;
     v = arr ? arr[G::addr(slot, i, j, k)] : 0.0;
   } else if (out == 1) {

@@ -576,7 +576,7 @@ struct OpsImpl final : Ops {
                int layout) override {
     const LevelView& L = V(c, l);
     pdl_launch(k_scatter<D, N>, grid_for((long long)L.nb * G::NI), kThreads, 0, c.stream, 
-        L.nb, dst, staging, slot_id, layout);
+        L.nb, dst, staging, slot_id, layout, L.own);
     check();
   }
   void gather(Ctx& c, int l, int var, double* staging, const int32_t* slot_id,

@@ -116,9 +116,17 @@ class DistributedMgSolver:
         return out
 
     def info(self):
-        out = (C.c_int32 * 4)()
+        out = (C.c_int32 * 6)()
         self.dev._check(self.lib.pmg_b200_dist_info(self.h, out))
-        return dict(world=out[0], split_level=out[1], transport=out[2], halo_cells=out[3])
+        return dict(world=out[0], split_level=out[1], transport=out[2], halo_cells=out[3],
+                    graph_kernels=out[4], graph=out[5])
+
+    def field_bytes(self) -> float:
+        """Device bytes of this rank's field arrays (its blocks + halo on the
+        large levels, the coarse tail whole)."""
+        out = C.c_double()
+        self.dev._check(self.lib.pmg_b200_field_bytes(self.h, C.byref(out)))
+        return out.value
 
     def v_cycle(self) -> CycleStats:
         st = _lib.StatsT()

@@ -24,6 +24,10 @@ from paper_2205_09411_b200.solver import LAYOUT_INTERIOR
 pytestmark = pytest.mark.gpu
 
 
+def case_ni(mesh):
+    return mesh.N ** mesh.dim
+
+
 def _setup(name):
     case = cfgs.get_case(name)
     mesh = case.build_mesh()
@@ -69,6 +73,12 @@ def test_partitioned_contexts_match_single(name, world):
     n_ref = sum(len(v) for l in range(part.split_level, mesh.n_levels + 1)
                 for c in (0, 1) for v in ref.recv.get((l, c), {}).values())
     assert info["halo_cells"] == n_ref
+    # per-rank memory: the large levels map only the chunks (2 MB = 64 blocks
+    # in Morton order) holding the rank's blocks and halo blocks -- at these
+    # sizes the halo touches most chunks, at 1024^3 a rank maps ~1/world + 5%
+    full = 4 * 8 * sum(len(mesh.level_blocks(l)) for l in range(1, mesh.n_levels + 1)) * case_ni(mesh)
+    for s in sols:
+        assert 0 < s.field_bytes() <= full, (s.field_bytes(), full)
     for k in range(cycles):
         hb = DistributedMgSolver.run_local(sols, lambda s: s.v_cycle())
         for r in range(world):  # every rank reports the combined records
