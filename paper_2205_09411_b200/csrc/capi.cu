@@ -158,12 +158,12 @@ static void build_cut_tables(Ctx& c) {
       bool no_cf = true, all_inside = true;
       for (int f = 0; f < F; ++f) no_cf = no_cf && !(m.nbr[(size_t)id * 6 + f] < 0 && m.cnbr[(size_t)id * 6 + f] >= 0);
       for (int ii = 0; ii < NI; ++ii) {
-        const int r = st.row_of[(size_t)id * NI + ii];
+        const int r = st.row_at((size_t)id, (size_t)ii);
         if (r < 0 || st.mask[(size_t)(r0 + r)] != PMG_INSIDE) all_inside = false;
       }
       if (no_cf && !all_inside && own_slot(c, l, s))
         for (int ii = 0; ii < NI; ++ii) {
-          const int r = st.row_of[(size_t)id * NI + ii];
+          const int r = st.row_at((size_t)id, (size_t)ii);
           if (r < 0 || st.mask[(size_t)(r0 + r)] == PMG_INSIDE) continue;
           const int i = ii % N, j = (ii / N) % N, k = D == 3 ? ii / (N * N) : 0;
           const int cc = (i + j + k) & 1;
@@ -247,7 +247,7 @@ static void build_small_tables(Ctx& c) {
         int32_t* e = tab.data() + a * 8;
         int code = -1;
         if (bnd) {
-          const int r = st.row_of[(size_t)id * NI + ii];
+          const int r = st.row_at((size_t)id, (size_t)ii);
           if (r < 0) code = -2;
           else if (st.mask[(size_t)(r0 + r)] == PMG_INSIDE) code = -3 - (base + r);
           else code = base + r;
@@ -301,7 +301,7 @@ static void cell_entry(const Ctx& c, int s, int id, int ii, int base, int32_t* e
   const int i = ii % N, j = (ii / N) % N, k = D == 3 ? ii / (N * N) : 0;
   int code = -1;
   if (st.valid && st.boundary[(size_t)id]) {
-    const int r = st.row_of[(size_t)id * NI + ii];
+    const int r = st.row_at((size_t)id, (size_t)ii);
     if (r < 0) code = -2;
     else if (st.mask[(size_t)(st.row_start[(size_t)id] + r)] == PMG_INSIDE) code = -3 - (base + r);
     else code = base + r;
@@ -338,34 +338,15 @@ static void cell_entry(const Ctx& c, int s, int id, int ii, int base, int32_t* e
 // product (formed exactly as the reference forms it, stencil.hpp:344-358), the
 // cut-direction mask, an inside flag -- 16 doubles, one 128-B line.
 static void build_row_coef(Ctx& c) {
-  const HostMesh& m = c.mesh;
-  const HostStencils& st = c.st;
-  const int F = c.F;
-  for (int l = 1; l <= m.L; ++l) {
+  for (int l = 1; l <= c.mesh.L; ++l) {
     LevelDev& d = *c.lev[(size_t)l];
-    std::vector<double> cf;
-    for (int s = 0; s < d.nb && st.valid; ++s) {
-      const int id = m.slots[(size_t)l][(size_t)s];
-      if (!st.boundary[(size_t)id]) continue;
-      const int r0 = st.row_start[(size_t)id], rc = st.row_count[(size_t)id];
-      for (int r = 0; r < rc; ++r) {
-        const size_t q = (size_t)(r0 + r);
-        double e[16] = {st.center[q]};
-        int bm = 0;
-        for (int f = 0; f < F; ++f) {
-          e[1 + f] = st.nb[q * F + f];
-          const double b = st.bc[q * F + f];
-          if (b != 0) {
-            bm |= 1 << f;
-            e[7 + f] = b * st.phi_b[(size_t)st.obj[q * F + f]];
-          }
-        }
-        e[13] = (double)bm;
-        e[14] = st.mask[q] == PMG_INSIDE ? 1.0 : 0.0;
-        cf.insert(cf.end(), e, e + 16);
-      }
-    }
-    d.r_coef.upload(cf, c.stream);
+    const int R = (int)d.n_rows;
+    d.r_coef.alloc((size_t)std::max(R, 1) * 16);
+    if (R > 0)
+      pdl_launch(pmgdev::k_row_coef, (unsigned)((R + 255) / 256), 256, 0, c.stream, R, c.F,
+                 (const double*)d.r_center.p, (const double*)d.r_nb.p, (const double*)d.r_bc.p,
+                 (const int8_t*)d.r_obj.p, (const uint8_t*)d.r_mask.p, (const double*)c.phi_b.p, d.r_coef.p);
+    PMG_CUDA(cudaGetLastError());
   }
 }
 
@@ -403,47 +384,76 @@ static void build_rfix_tables(Ctx& c) {
   }
 }
 
+// The StencilSet's rows on the device (block-id order, StencilSet row
+// numbering; row_of pages in row_page order): kept from the device build, or
+// uploaded once from a host StencilSet (set_stencils).
+static void ensure_devrows(Ctx& c) {
+  if (c.devrows) return;
+  const HostStencils& st = c.st;
+  auto R = std::make_unique<DevRows>();
+  const size_t nr = st.center.size(), F = (size_t)c.F;
+  R->center.upload(st.center, c.stream);
+  R->nb.upload(st.nb, c.stream);
+  R->bc.upload(st.bc, c.stream);
+  if (st.d.size() == nr * F) R->d.upload(st.d, c.stream);
+  else R->d.upload(std::vector<double>(nr * F, 1.0), c.stream);
+  R->obj.upload(st.obj, c.stream);
+  R->mask.upload(st.mask, c.stream);
+  R->pin.upload(st.pin, c.stream);
+  R->rowof.upload(st.row_pages, c.stream);
+  PMG_CUDA(cudaStreamSynchronize(c.stream));
+  c.devrows = std::move(R);
+}
+
 static void upload_stencils(Ctx& c) {
   const HostMesh& m = c.mesh;
   const HostStencils& st = c.st;
   const int NI = c.NI, H = NI / 2, F = c.F;
   std::vector<std::vector<uint8_t>> kindv((size_t)m.L + 1);
+  std::vector<int32_t> cs_perm((size_t)NI);  // interior index -> colour-split entry
+  for (int ii = 0; ii < NI; ++ii) cs_perm[(size_t)ii] = cs_addr(ii, c.N, c.dim, H);
+  ensure_devrows(c);
   for (int l = 1; l <= m.L; ++l) {
     LevelDev& d = *c.lev[(size_t)l];
-    std::vector<int32_t> srow((size_t)d.nb, -1), row_of;
-    std::vector<uint8_t> kind((size_t)d.nb, pmgdev::KIND_UNIFORM), mask;
-    std::vector<double> center, nbv, bcv, dv;
-    std::vector<int8_t> obj, pin;
-    int n_if = 0;
+    std::vector<int32_t> srow((size_t)d.nb, -1);
+    std::vector<uint8_t> kind((size_t)d.nb, pmgdev::KIND_UNIFORM);
+    std::vector<int4> rlist;  // per interface block in slot order: StencilSet page, first row, level row, count
+    int n_if = 0, base = 0;
     for (int s = 0; s < d.nb; ++s) {
       const int id = m.slots[(size_t)l][(size_t)s];
       if (!st.valid || !st.boundary[(size_t)id]) continue;
       srow[(size_t)s] = n_if++;
-      const int base = (int)center.size();
       const int r0 = st.row_start[(size_t)id];
       const int rc = st.row_count[(size_t)id];
-      bool all_inside = true;
-      row_of.resize((size_t)n_if * NI, -1);
-      int32_t* page = row_of.data() + (size_t)(n_if - 1) * NI;
-      for (int ii = 0; ii < NI; ++ii) {
-        const int32_t r = st.row_of[(size_t)id * NI + ii];
-        require(r < rc, "stencil row_of entry out of range");
-        page[cs_addr(ii, c.N, c.dim, H)] = r < 0 ? -1 : base + r;
-        if (r < 0 || st.mask[(size_t)(r0 + r)] != PMG_INSIDE) all_inside = false;
-      }
-      for (int r = 0; r < rc; ++r) {
-        const size_t q = (size_t)(r0 + r);
-        center.push_back(st.center[q]);
-        mask.push_back(st.mask[q]);
-        pin.push_back(st.pin[q]);
-        for (int f = 0; f < F; ++f) {
-          nbv.push_back(st.nb[q * F + f]);
-          bcv.push_back(st.bc[q * F + f]);
-          dv.push_back(st.d.empty() ? 1.0 : st.d[q * F + f]);
-          obj.push_back(st.obj[q * F + f]);
-        }
-      }
+      bool all_inside = rc == NI;
+      for (int r = 0; r < rc && all_inside; ++r) all_inside = st.mask[(size_t)(r0 + r)] == PMG_INSIDE;
       kind[(size_t)s] = all_inside ? pmgdev::KIND_ALL_INSIDE : pmgdev::KIND_IFACE;
+      rlist.push_back(make_int4(st.row_page[(size_t)id], r0, base, rc));
+      base += rc;
+    }
+    // the level's rows, row_of pages (colour-split, level row numbers) and
+    // special-row kinds, gathered on the device from the StencilSet's rows
+    d.n_rows = (size_t)base;
+    const size_t R1 = (size_t)std::max(base, 1);
+    d.r_center.alloc(R1);
+    d.r_mask.alloc(R1);
+    d.r_pin.alloc(R1);
+    d.r_nb.alloc(R1 * F);
+    d.r_bc.alloc(R1 * F);
+    d.r_d.alloc(R1 * F);
+    d.r_obj.alloc(R1 * F);
+    d.row_of.alloc((size_t)std::max(n_if, 1) * NI);
+    d.skind.alloc((size_t)std::max(n_if, 1) * NI);
+    if (n_if > 0) {
+      DevBuf<int4> dl;
+      dl.upload(rlist, c.stream);
+      const DevRows& R = *c.devrows;
+      pdl_launch(pmgdev::k_level_rows, (unsigned)n_if, 256, 0, c.stream, (const int4*)dl.p, c.N, c.dim, F,
+                 (const int32_t*)R.rowof.p, (const double*)R.center.p, (const double*)R.nb.p, (const double*)R.bc.p,
+                 (const double*)R.d.p, (const int8_t*)R.obj.p, (const uint8_t*)R.mask.p, (const int8_t*)R.pin.p,
+                 d.row_of.p, d.skind.p, d.r_center.p, d.r_nb.p, d.r_bc.p, d.r_d.p, d.r_obj.p, d.r_mask.p,
+                 d.r_pin.p);
+      PMG_CUDA(cudaStreamSynchronize(c.stream));  // dl
     }
     d.srow.upload(srow, c.stream);
     d.kind.upload(kind, c.stream);
@@ -477,12 +487,15 @@ static void upload_stencils(Ctx& c) {
         (no_cf && kind[(size_t)s] == pmgdev::KIND_UNIFORM ? ufast : uslow).push_back(s);
         // cut (non-inside) rows of lean interface blocks, per colour, for k_gs_fix
         if (no_cf && kind[(size_t)s] == pmgdev::KIND_IFACE) {
-          const int32_t* page = row_of.data() + (size_t)srow[(size_t)s] * NI;
-          for (int cc = 0; cc < 2; ++cc)
-            for (int e = 0; e < H; ++e) {
-              const int32_t r = page[cc * H + e];
-              if (r >= 0 && mask[(size_t)r] != PMG_INSIDE) fix[cc].push_back(s), fix[cc].push_back(e);
+          const int32_t* page = st.page((size_t)id);
+          const int r0 = st.row_start[(size_t)id];
+          for (int ii = 0; ii < NI; ++ii) {
+            const int32_t r = page[ii];
+            if (r >= 0 && st.mask[(size_t)(r0 + r)] != PMG_INSIDE) {
+              const int a = cs_perm[(size_t)ii];
+              fix[a / H].push_back(s), fix[a / H].push_back(a % H);
             }
+          }
         }
       }
       d.n_gs = (int)gsl.size() / 8;
@@ -504,20 +517,6 @@ static void upload_stencils(Ctx& c) {
         d.fix_list[cc].upload(fix[cc], c.stream);
       }
     }
-    d.row_of.upload(row_of, c.stream);
-    {  // special-row kind per entry (stream.cuh): 0 uniform, 1 inside, 2 cut
-      std::vector<int8_t> sk(row_of.size(), 0);
-      for (size_t q = 0; q < row_of.size(); ++q)
-        if (row_of[q] >= 0) sk[q] = mask[(size_t)row_of[q]] == PMG_INSIDE ? 1 : 2;
-      d.skind.upload(sk, c.stream);
-    }
-    d.r_center.upload(center, c.stream);
-    d.r_nb.upload(nbv, c.stream);
-    d.r_d.upload(dv, c.stream);
-    d.r_bc.upload(bcv, c.stream);
-    d.r_obj.upload(obj, c.stream);
-    d.r_mask.upload(mask, c.stream);
-    d.r_pin.upload(pin, c.stream);
   }
   // k_restrict_fix lists (3D): parents of level l-1 whose fused restriction
   // needs the general path -- a child with a special row, or a pinned parent
@@ -525,7 +524,7 @@ static void upload_stencils(Ctx& c) {
     const int N = c.N, HN = N / 2;
     auto row_at = [&](int id, int i, int j, int k) -> int {
       if (!st.valid || !st.boundary[(size_t)id]) return -1;
-      const int r = st.row_of[(size_t)id * NI + (size_t)(i + N * (j + N * k))];
+      const int r = st.row_at((size_t)id, (size_t)(i + N * (j + N * k)));
       return r < 0 ? -1 : st.row_start[(size_t)id] + r;
     };
     for (int l = 2; l <= m.L; ++l) {
@@ -598,7 +597,7 @@ static void upload_stencils(Ctx& c) {
         const int id = m.slots[(size_t)l][(size_t)s];
         if (!st.boundary[(size_t)id] || !own_slot(c, l, s)) continue;
         for (int ii = 0; ii < NI; ++ii) {
-          const int r = st.row_of[(size_t)id * NI + ii];
+          const int r = st.row_at((size_t)id, (size_t)ii);
           if (r < 0) continue;
           const size_t q = (size_t)(st.row_start[(size_t)id] + r);
           if (st.mask[q] != PMG_INSIDE) continue;
@@ -625,7 +624,10 @@ static void default_stencils(Ctx& c) {
   st.boundary.assign((size_t)c.mesh.nb, 0);
   st.row_count.assign((size_t)c.mesh.nb, 0);
   st.row_start.assign((size_t)c.mesh.nb + 1, 0);
-  st.row_of.assign((size_t)c.mesh.nb * c.NI, -1);
+  st.NI = c.NI;
+  st.row_page.assign((size_t)c.mesh.nb, -1);
+  st.row_pages.clear();
+  c.devrows.reset();
 }
 
 // ---------------------------------------------------------------- coarse assembly
@@ -646,7 +648,7 @@ static void assemble_coarse(Ctx& c) {
   const int r0 = st.row_start[(size_t)id];
   auto row_ptr = [&](int ii) -> int {
     if (!bnd) return -1;
-    const int r = st.row_of[(size_t)id * NI + ii];
+    const int r = st.row_at((size_t)id, (size_t)ii);
     return r < 0 ? -1 : r0 + r;
   };
   auto inside = [&](int ii) {
@@ -1409,11 +1411,14 @@ static void set_stencils(Ctx& c, const int32_t* boundary, const int32_t* row_cou
   st.row_start.assign((size_t)nbk + 1, 0);
   for (int i = 0; i < nbk; ++i) st.row_start[(size_t)i + 1] = st.row_start[(size_t)i] + st.row_count[(size_t)i];
   const size_t R = (size_t)st.row_start[(size_t)nbk];
-  st.row_of.assign((size_t)nbk * c.NI, -1);
+  st.NI = c.NI;
+  st.row_page.assign((size_t)nbk, -1);
+  st.row_pages.clear();
   for (int i = 0; i < nbk; ++i)
-    if (st.boundary[(size_t)i])
-      std::copy(row_of + (size_t)i * c.NI, row_of + (size_t)(i + 1) * c.NI,
-                st.row_of.begin() + (long)i * c.NI);
+    if (st.boundary[(size_t)i]) {
+      st.row_page[(size_t)i] = (int32_t)(st.row_pages.size() / (size_t)c.NI);
+      st.row_pages.insert(st.row_pages.end(), row_of + (size_t)i * c.NI, row_of + (size_t)(i + 1) * c.NI);
+    }
   st.center.assign(center, center + R);
   st.nb.assign(nb, nb + R * F);
   st.bc.assign(bc, bc + R * F);
@@ -1430,6 +1435,7 @@ static void set_stencils(Ctx& c, const int32_t* boundary, const int32_t* row_cou
         require(st.obj[r * F + f] >= 0 && st.obj[r * F + f] < n_obj, "stencil object id out of range");
   }
   st.valid = true;
+  c.devrows.reset();
   upload_stencils(c);
   set_views(c);
   c.solver = false;
@@ -1559,7 +1565,7 @@ int pmg_b200_get_stencils(pmg_b200_ctx* h, int32_t* row_of, double* center, doub
     const HostStencils& st = c.st;
     for (int i = 0; i < c.mesh.nb; ++i)
       for (int q = 0; q < c.NI; ++q)
-        row_of[(size_t)i * c.NI + q] = st.boundary[(size_t)i] ? st.row_of[(size_t)i * c.NI + q] : -1;
+        row_of[(size_t)i * c.NI + q] = st.boundary[(size_t)i] ? st.row_at((size_t)i, (size_t)q) : -1;
     std::copy(st.center.begin(), st.center.end(), center);
     std::copy(st.nb.begin(), st.nb.end(), nb);
     std::copy(st.bc.begin(), st.bc.end(), bc);

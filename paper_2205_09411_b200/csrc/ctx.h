@@ -186,12 +186,29 @@ struct HostMesh {
 
 struct HostStencils {
   bool valid = false;
-  std::vector<int32_t> boundary, row_count, row_start, row_of;  // row_of nb*NI
+  std::vector<int32_t> boundary, row_count, row_start;
+  // row_of (StencilSet::row_of, one N^D page per block) kept for the boundary
+  // blocks only: row_page[id] = page index or -1 (every entry -1)
+  int NI = 0;
+  std::vector<int32_t> row_page, row_pages;
+  int32_t row_at(size_t id, size_t ii) const {
+    const int32_t p = row_page[id];
+    return p < 0 ? -1 : row_pages[(size_t)p * (size_t)NI + ii];
+  }
+  const int32_t* page(size_t id) const { return row_pages.data() + (size_t)row_page[id] * (size_t)NI; }
   std::vector<double> center, nb, bc, d;
   std::vector<int8_t> obj, pin;
   std::vector<uint8_t> mask;
   std::vector<int32_t> lin;
   std::vector<double> phi_b;
+};
+
+// the StencilSet's rows on the device (capi.cu ensure_devrows)
+struct DevRows {
+  DevBuf<double> center, nb, bc, d;
+  DevBuf<int8_t> obj, pin;
+  DevBuf<uint8_t> mask;
+  DevBuf<int32_t> rowof;  // pages in HostStencils::row_page order
 };
 
 struct HostCoarse {
@@ -211,7 +228,8 @@ struct LevelDev {
   DevBuf<int32_t> nbr, cnbr, coords, parent, child, srow, bcoff, cfoff, row_of, slot_id;
   DevBuf<uint8_t> leaf, kind, r_mask;
   DevBuf<double> phi, rhs, old, res, bcval, cfold, r_center, r_nb, r_bc, r_d;
-  DevBuf<double> r_coef;  // 16 per row (capi.cu build_row_coef)
+  DevBuf<double> r_coef;  // 16 per row (k_row_coef)
+  size_t n_rows = 0;      // special rows of the level's interface blocks
   DevBuf<int8_t> r_obj, r_pin, skind;
   DevBuf<int32_t> ref_slot;  // level_blocks order position -> slot
   // block classes: "fast" = uniform stencil and all 2D faces same-level
@@ -319,6 +337,7 @@ struct Ctx {
   std::vector<int32_t> face_off[6];  // per dir, per block: offset into face_vals[dir] or -1
 
   HostStencils st;
+  std::unique_ptr<DevRows> devrows;
   HostCoarse coarse;
   std::vector<std::unique_ptr<LevelDev>> lev;  // index 0 unused
   DevBuf<double> phi_b;

@@ -364,6 +364,75 @@ __global__ void __launch_bounds__(kThreads) k_record(LevelView L, LevelView Lc,
 }
 
 // CycleStats from the level records (multigrid.hpp:564-575).
+// Per special row of a level, the folded coefficients the gather-entry
+// kernels read: center, nb[6], bc * phi_b[obj] per cut direction (formed as
+// the reference forms it, stencil.hpp:344-358), the cut mask, inside flag.
+static __global__ void __launch_bounds__(256) k_row_coef(int R, int F, const double* __restrict__ center,
+                                                         const double* __restrict__ nb, const double* __restrict__ bc,
+                                                         const int8_t* __restrict__ obj,
+                                                         const uint8_t* __restrict__ mask,
+                                                         const double* __restrict__ phi_b, double* __restrict__ out) {
+  pdl_begin();
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= R) return;
+  double e[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) e[k] = 0.0;
+  e[0] = center[r];
+  int bm = 0;
+  for (int f = 0; f < F; ++f) {
+    e[1 + f] = nb[(size_t)r * F + f];
+    const double b = bc[(size_t)r * F + f];
+    if (b != 0) {
+      bm |= 1 << f;
+      e[7 + f] = b * phi_b[obj[(size_t)r * F + f]];
+    }
+  }
+  e[13] = (double)bm;
+  e[14] = mask[r] == 1 ? 1.0 : 0.0;  // PMG_INSIDE
+  double2* o = reinterpret_cast<double2*>(out + (size_t)r * 16);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) o[k] = make_double2(e[2 * k], e[2 * k + 1]);
+}
+
+// One CTA per interface block of a level (list: StencilSet page, first row,
+// level row, row count): the block's rows copied into the level's row arrays
+// and its row_of page in the colour-split cell order with level row numbers,
+// plus the special-row kind of every cell (0 uniform, 1 inside, 2 cut).
+static __global__ void __launch_bounds__(256) k_level_rows(
+    const int4* __restrict__ list, int N, int D, int F, const int32_t* __restrict__ rowof,
+    const double* __restrict__ center, const double* __restrict__ nb, const double* __restrict__ bc,
+    const double* __restrict__ dd, const int8_t* __restrict__ obj, const uint8_t* __restrict__ mask,
+    const int8_t* __restrict__ pin, int32_t* __restrict__ o_rowof, int8_t* __restrict__ o_skind,
+    double* __restrict__ o_center, double* __restrict__ o_nb, double* __restrict__ o_bc, double* __restrict__ o_d,
+    int8_t* __restrict__ o_obj, uint8_t* __restrict__ o_mask, int8_t* __restrict__ o_pin) {
+  pdl_begin();
+  const int4 e = list[blockIdx.x];  // {page, src row, dst row, count}
+  const int NI = D == 2 ? N * N : N * N * N, H = NI / 2;
+  const int32_t* src = rowof + (size_t)e.x * NI;
+  int32_t* dpg = o_rowof + (size_t)blockIdx.x * NI;
+  int8_t* spg = o_skind + (size_t)blockIdx.x * NI;
+  for (int ii = threadIdx.x; ii < NI; ii += blockDim.x) {
+    const int r = src[ii];
+    const int i = ii % N, j = (ii / N) % N, k = D == 3 ? ii / (N * N) : 0;
+    const int a = ((i + j + k) & 1) * H + (ii >> 1);
+    dpg[a] = r < 0 ? -1 : e.z + r;
+    spg[a] = r < 0 ? 0 : (mask[e.y + r] == 1 ? 1 : 2);  // PMG_INSIDE
+  }
+  for (int q = threadIdx.x; q < e.w; q += blockDim.x) {
+    const size_t sr = (size_t)e.y + q, dr = (size_t)e.z + q;
+    o_center[dr] = center[sr];
+    o_mask[dr] = mask[sr];
+    o_pin[dr] = pin[sr];
+    for (int f = 0; f < F; ++f) {
+      o_nb[dr * F + f] = nb[sr * F + f];
+      o_bc[dr * F + f] = bc[sr * F + f];
+      o_d[dr * F + f] = dd[sr * F + f];
+      o_obj[dr * F + f] = obj[sr * F + f];
+    }
+  }
+}
+
 static __global__ void k_combine(const Rec* __restrict__ rec, int nlev, double* out) {
   pdl_begin();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;

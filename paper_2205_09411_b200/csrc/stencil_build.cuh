@@ -7,7 +7,9 @@
 //                     (stencil.hpp:143-161)
 //   2. k_cell_rows    one thread per interior cell of a flagged block: inside
 //                     row with pin_obj, or 2D line searches (golden bracketing +
-//                     bisection), thin-object rescue, make_row (stencil.hpp:166-191)
+//                     bisection), thin-object rescue, make_row (stencil.hpp:166-191);
+//      k_cell_search  for composites of many objects, one WARP per boundary
+//                     candidate: the lanes evaluate the children (WarpEval)
 //   3. k_compact      one CTA per flagged block: rows compacted in interior-index
 //                     order (BlockStencil::set_row order, stencil.hpp:75-79)
 // Every decision is an fp64 threshold test; with --fmad=false and the
@@ -157,26 +159,69 @@ __device__ __forceinline__ int lsf_attaining(const LsfDev& L, const double* x) {
   return best;
 }
 
+// Level-set evaluators for the line searches.  SeqEval: one thread evaluates
+// the composite min child by child (lsf_eval / lsf_attaining).  WarpEval: the
+// 32 lanes of a warp evaluate the children of a composite in parallel (lane k
+// takes children k, k+32, ...) and reduce (value, index) lexicographically --
+// the minimum value and the first child attaining it, exactly what the
+// sequential strict-< scan yields (levelset.hpp:127-148), so decisions stay
+// bit-identical.  Every lane returns the same result; the callers' control
+// flow is then uniform across the warp.
 template <int D>
-__device__ __forceinline__ void lsf_gradient(const LsfDev& L, const double* x, double dx,
-                                             double* g) {
+struct SeqEval {
+  LsfDev L;
+  __device__ __forceinline__ double f(const double* x) const { return lsf_eval<D>(L, x); }
+  __device__ __forceinline__ int obj(const double* x) const { return lsf_attaining<D>(L, x); }
+};
+template <int D>
+struct WarpEval {
+  LsfDev L;
+  __device__ __forceinline__ void reduce(const double* x, double& v, int& idx) const {
+    v = DBL_MAX * 2.0;
+    idx = 0x7fffffff;
+    for (int i = 1 + (int)(threadIdx.x & 31); i < L.n; i += 32) {
+      const double e = eval_simple<D>(L.d[i], x);
+      if (e < v) v = e, idx = i;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+      if (ov < v || (!(v < ov) && oi < idx)) v = ov, idx = oi;
+    }
+  }
+  __device__ __forceinline__ double f(const double* x) const {
+    double v;
+    int i;
+    reduce(x, v, i);
+    return v;
+  }
+  __device__ __forceinline__ int obj(const double* x) const {
+    double v;
+    int i;
+    reduce(x, v, i);
+    return i - 1;
+  }
+};
+
+template <int D, class E>
+__device__ __forceinline__ void lsf_gradient(const E& ev, const double* x, double dx, double* g) {
   for (int k = 0; k < D; ++k) {
     double xp[3], xm[3];
     for (int a = 0; a < D; ++a) xp[a] = xm[a] = x[a];
     xp[k] += dx;
     xm[k] -= dx;
-    g[k] = (lsf_eval<D>(L, xp) - lsf_eval<D>(L, xm)) / (2 * dx);
+    g[k] = (ev.f(xp) - ev.f(xm)) / (2 * dx);
   }
 }
 
 // boundary_candidate (levelset.hpp:277-289)
-template <int D>
-__device__ __forceinline__ bool boundary_candidate(const LsfDev& L, const double* x, double dx,
-                                                   double safety) {
+template <int D, class E>
+__device__ __forceinline__ bool boundary_candidate(const E& ev, const double* x, double dx, double safety) {
   const double Ls = safety * sqrt((double)D) * dx;
   double g[3];
-  lsf_gradient<D>(L, x, dx, g);
-  return fabs(lsf_eval<D>(L, x)) < Ls * vnorm<D>(g);
+  lsf_gradient<D>(ev, x, dx, g);
+  return fabs(ev.f(x)) < Ls * vnorm<D>(g);
 }
 
 // p = a + t (b - a)   (Vec operator*, operator+, core.hpp:27-55)
@@ -185,14 +230,13 @@ __device__ __forceinline__ void along(const double* a, const double* b, double t
   for (int k = 0; k < D; ++k) p[k] = a[k] + (b[k] - a[k]) * t;
 }
 
-template <int D>
-__device__ double bisect_t(const LsfDev& L, const double* a, const double* b, double lo,
-                           double hi, double eps) {
+template <int D, class E>
+__device__ double bisect_t(const E& ev, const double* a, const double* b, double lo, double hi, double eps) {
   while (hi - lo > eps) {
     const double mid = 0.5 * (lo + hi);
     double p[3];
     along<D>(a, b, mid, p);
-    if (lsf_eval<D>(L, p) > 0)
+    if (ev.f(p) > 0)
       lo = mid;
     else
       hi = mid;
@@ -201,22 +245,21 @@ __device__ double bisect_t(const LsfDev& L, const double* a, const double* b, do
 }
 
 // find_root_position (levelset.hpp:223-257)
-template <int D>
-__device__ double find_root_position(const LsfDev& L, const double* a, const double* b,
-                                     const pmg_stencil_cfg_t& cfg) {
-  const double fa = lsf_eval<D>(L, a);
-  if (fa * lsf_eval<D>(L, b) <= 0) return bisect_t<D>(L, a, b, 0.0, 1.0, cfg.eps_tol);
+template <int D, class E>
+__device__ double find_root_position(const E& ev, const double* a, const double* b, const pmg_stencil_cfg_t& cfg) {
+  const double fa = ev.f(a);
+  if (fa * ev.f(b) <= 0) return bisect_t<D>(ev, a, b, 0.0, 1.0, cfg.eps_tol);
   const double invphi = 0.6180339887498949;
   double lo = 0.0, hi = 1.0;
   double t1 = hi - invphi * (hi - lo);
   double t2 = lo + invphi * (hi - lo);
   double p[3];
   along<D>(a, b, t1, p);
-  double g1 = fa * lsf_eval<D>(L, p);
+  double g1 = fa * ev.f(p);
   along<D>(a, b, t2, p);
-  double g2 = fa * lsf_eval<D>(L, p);
-  if (g1 <= 0) return bisect_t<D>(L, a, b, 0.0, t1, cfg.eps_tol);
-  if (g2 <= 0) return bisect_t<D>(L, a, b, 0.0, t2, cfg.eps_tol);
+  double g2 = fa * ev.f(p);
+  if (g1 <= 0) return bisect_t<D>(ev, a, b, 0.0, t1, cfg.eps_tol);
+  if (g2 <= 0) return bisect_t<D>(ev, a, b, 0.0, t2, cfg.eps_tol);
   for (int it = 0; it < cfg.max_bracket_iters && hi - lo > cfg.eps_tol; ++it) {
     if (g1 <= g2) {
       hi = t2;
@@ -224,16 +267,16 @@ __device__ double find_root_position(const LsfDev& L, const double* a, const dou
       g2 = g1;
       t1 = hi - invphi * (hi - lo);
       along<D>(a, b, t1, p);
-      g1 = fa * lsf_eval<D>(L, p);
-      if (g1 <= 0) return bisect_t<D>(L, a, b, 0.0, t1, cfg.eps_tol);
+      g1 = fa * ev.f(p);
+      if (g1 <= 0) return bisect_t<D>(ev, a, b, 0.0, t1, cfg.eps_tol);
     } else {
       lo = t1;
       t1 = t2;
       g1 = g2;
       t2 = lo + invphi * (hi - lo);
       along<D>(a, b, t2, p);
-      g2 = fa * lsf_eval<D>(L, p);
-      if (g2 <= 0) return bisect_t<D>(L, a, b, 0.0, t2, cfg.eps_tol);
+      g2 = fa * ev.f(p);
+      if (g2 <= 0) return bisect_t<D>(ev, a, b, 0.0, t2, cfg.eps_tol);
     }
   }
   return -1.0;
@@ -263,17 +306,38 @@ struct BuildArgs {
   uint8_t* flag;            // [nb]
 };
 
+// lip1: every piece of the level set is a Euclidean distance (spheres, rods),
+// so f is 1-Lipschitz and each central-difference gradient component is at
+// most 1: a block whose padded cells all lie farther than the mask band from
+// the boundary is decided from its centre alone (no cell can be inside or
+// pass |f| < L ||grad f|| <= L sqrt(D)); the same flag, without the per-cell work.
 template <int D, int N>
 __global__ void __launch_bounds__(256) k_block_flag(LsfDev L, const double* __restrict__ origin,
                                                     const double* __restrict__ dx, int nb,
-                                                    double safety, uint8_t* flag) {
+                                                    double safety, uint8_t* flag, int lip1) {
   pdl_begin();
   __shared__ int any;
   const int b = blockIdx.x;
   if (b >= nb) return;
+  const double h = dx[b];
+  if (lip1) {
+    double xc[3];
+    for (int k = 0; k < D; ++k) xc[k] = origin[b * 3 + k] + 0.5 * N * h;
+    const double fc = lsf_eval<D>(L, xc);
+    const double reach = sqrt((double)D) * 0.5 * (N + 1) * h;  // centre to the farthest padded cell centre
+    const double band = safety * sqrt((double)D) * h * sqrt((double)D);
+    const double slack = 1e-9 * (1.0 + fabs(fc) + h);
+    if (fc - reach > band + slack) {  // every padded cell outside and beyond the band
+      if (threadIdx.x == 0) flag[b] = 0;
+      return;
+    }
+    if (fc + 0.5 * N * h * sqrt((double)D) < -slack) {  // every interior cell inside
+      if (threadIdx.x == 0) flag[b] = 1;
+      return;
+    }
+  }
   if (threadIdx.x == 0) any = 0;
   __syncthreads();
-  const double h = dx[b];
   constexpr int NI = D == 2 ? N * N : N * N * N;
   for (int ii = threadIdx.x; ii < NI; ii += blockDim.x) {
     const int i[3] = {ii % N, (ii / N) % N, D == 3 ? ii / (N * N) : 0};
@@ -290,27 +354,14 @@ __global__ void __launch_bounds__(256) k_block_flag(LsfDev L, const double* __re
       const int i[3] = {q % S1 - 1, (q / S1) % S1 - 1, D == 3 ? q / (S1 * S1) - 1 : 0};
       double x[3];
       for (int k = 0; k < D; ++k) x[k] = origin[b * 3 + k] + (i[k] + 0.5) * h;
-      if (boundary_candidate<D>(L, x, h, 0.0 + safety)) any = 1;
+      if (boundary_candidate<D>(SeqEval<D>{L}, x, h, 0.0 + safety)) any = 1;
     }
     __syncthreads();
   }
   if (threadIdx.x == 0) flag[b] = any ? 1 : 0;
 }
 
-template <int D, int N>
-__global__ void __launch_bounds__(128) k_cell_rows(LsfDev L, BuildArgs A, pmg_stencil_cfg_t cfg) {
-  pdl_begin();
-  constexpr int NI = D == 2 ? N * N : N * N * N;
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long long)A.nflag * NI) return;
-  const int fb = (int)(t / NI);
-  const int ii = (int)(t % NI);
-  const int b = A.flagged[fb];
-  const double h = A.dx[b];
-  const int i[3] = {ii % N, (ii / N) % N, D == 3 ? ii / (N * N) : 0};
-  double x[3];
-  for (int k = 0; k < D; ++k) x[k] = A.origin[b * 3 + k] + (i[k] + 0.5) * h;
-  RowScratch r;
+__device__ __forceinline__ void row_init(RowScratch& r) {
   r.center = 0;
   for (int f = 0; f < 6; ++f) {
     r.nb[f] = 0;
@@ -321,102 +372,166 @@ __global__ void __launch_bounds__(128) k_cell_rows(LsfDev L, BuildArgs A, pmg_st
   r.mask = PMG_SOLVED;
   r.pin = -1;
   r.has = 0;
-  const double fc = lsf_eval<D>(L, x);
+}
+
+// cell centre of interior cell t of the flagged-block list
+template <int D, int N>
+__device__ __forceinline__ void cell_at(const BuildArgs& A, long long t, double* x, double& h) {
+  constexpr int NI = D == 2 ? N * N : N * N * N;
+  const int b = A.flagged[(int)(t / NI)];
+  const int ii = (int)(t % NI);
+  h = A.dx[b];
+  const int i[3] = {ii % N, (ii / N) % N, D == 3 ? ii / (N * N) : 0};
+  for (int k = 0; k < D; ++k) x[k] = A.origin[b * 3 + k] + (i[k] + 0.5) * h;
+}
+
+// A boundary-candidate cell (not inside): cell_distances, the thin-object
+// rescue and make_row (stencil.hpp:166-191, levelset.hpp:293-382).
+template <int D, class E>
+__device__ void cell_search(const E& ev, const double* x, double h, double fc, const pmg_stencil_cfg_t& cfg,
+                            RowScratch& r) {
+  double dd[6];
+  int8_t ob[6];
+  for (int f = 0; f < 2 * D; ++f) {
+    dd[f] = 1.0;
+    ob[f] = -1;
+  }
+  bool cut = false;
+  for (int f = 0; f < 2 * D; ++f) {  // cell_distances (levelset.hpp:313-327)
+    double nbp[3];
+    for (int k = 0; k < D; ++k) nbp[k] = x[k];
+    nbp[f >> 1] += ((f & 1) ? 1 : -1) * h;
+    const double tr = find_root_position<D>(ev, x, nbp, cfg);
+    if (tr < 0) continue;
+    const double d = clampd(tr, cfg.d_min, 1.0);
+    if (d < 1.0) {
+      double p[3];
+      along<D>(x, nbp, tr, p);
+      dd[f] = d;
+      ob[f] = (int8_t)ev.obj(p);
+      cut = true;
+    }
+  }
+  if (!cut && cfg.thin_rescue && h > cfg.w_min) {
+    // resolve_thin_boundary (levelset.hpp:344-382)
+    const double fa = fc;
+    const int max_steps = (int)(h / cfg.w_min);
+    double y[3];
+    for (int k = 0; k < D; ++k) y[k] = x[k];
+    for (int step = 0; step < max_steps; ++step) {
+      double g[3];
+      lsf_gradient<D>(ev, y, h, g);
+      const double gn = vnorm<D>(g);
+      if (gn == 0) break;
+      const double sc = cfg.w_min / gn;
+      for (int k = 0; k < D; ++k) y[k] -= g[k] * sc;
+      if (fa * ev.f(y) > 0) continue;
+      const double tt = bisect_t<D>(ev, x, y, 0.0, 1.0, cfg.eps_tol);
+      double root[3], rc[3];
+      along<D>(x, y, tt, root);
+      for (int k = 0; k < D; ++k) rc[k] = root[k] - x[k];
+      const double hd = clampd(vnorm<D>(rc) / h, cfg.d_min, 1.0);
+      const int hobj = ev.obj(root);
+      int hdir = 0;
+      double best = DBL_MAX * 2.0;
+      for (int f = 0; f < 2 * D; ++f) {
+        double nbp[3];
+        for (int k = 0; k < D; ++k) nbp[k] = x[k];
+        nbp[f >> 1] += ((f & 1) ? 1 : -1) * h;
+        double rn[3];
+        for (int k = 0; k < D; ++k) rn[k] = root[k] - nbp[k];
+        const double dist = vnorm<D>(rn);
+        if (dist < best) {
+          best = dist;
+          hdir = f;
+        }
+      }
+      dd[hdir] = hd;
+      ob[hdir] = (int8_t)hobj;
+      cut = hd < 1.0;
+      for (int f = 0; f < 2 * D && !cut; ++f) cut = dd[f] < 1.0;
+      break;
+    }
+  }
+  if (cut) {  // make_row (stencil.hpp:84-110)
+    const double inv2 = 1.0 / (h * h);
+    for (int a = 0; a < D; ++a) {
+      const double dm = dd[2 * a], dp = dd[2 * a + 1];
+      const double cm = 2.0 / ((dp + dm) * dm) * inv2;
+      const double cp = 2.0 / ((dp + dm) * dp) * inv2;
+      r.center -= 2.0 / (dm * dp) * inv2;
+      if (dm < 1.0) {
+        r.bc[2 * a] = cm;
+        r.obj[2 * a] = ob[2 * a];
+      } else {
+        r.nb[2 * a] = cm;
+      }
+      if (dp < 1.0) {
+        r.bc[2 * a + 1] = cp;
+        r.obj[2 * a + 1] = ob[2 * a + 1];
+      } else {
+        r.nb[2 * a + 1] = cp;
+      }
+    }
+    for (int f = 0; f < 2 * D; ++f) r.d[f] = dd[f];
+    r.has = 1;
+  }
+}
+
+// One thread per interior cell of a flagged block.  cand == nullptr: the
+// whole row here (a plain or few-child level set).  Otherwise the boundary
+// candidates are only listed in cand[] for k_cell_search.
+template <int D, int N>
+__global__ void __launch_bounds__(128) k_cell_rows(LsfDev L, BuildArgs A, pmg_stencil_cfg_t cfg,
+                                                   long long* cand, int* n_cand) {
+  pdl_begin();
+  constexpr int NI = D == 2 ? N * N : N * N * N;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)A.nflag * NI) return;
+  const int fb = (int)(t / NI);
+  double x[3], h;
+  cell_at<D, N>(A, t, x, h);
+  RowScratch r;
+  row_init(r);
+  const SeqEval<D> ev{L};
+  const double fc = ev.f(x);
   if (fc <= 0) {  // inside: identity row pinned to the attaining object
     r.mask = PMG_INSIDE;
-    r.pin = (int8_t)lsf_attaining<D>(L, x);
+    r.pin = (int8_t)ev.obj(x);
     r.center = 1.0;
     r.has = 1;
-  } else if (boundary_candidate<D>(L, x, h, cfg.boundary_safety)) {
-    double dd[6];
-    int8_t ob[6];
-    for (int f = 0; f < 2 * D; ++f) {
-      dd[f] = 1.0;
-      ob[f] = -1;
+  } else if (boundary_candidate<D>(ev, x, h, cfg.boundary_safety)) {
+    if (cand) {
+      cand[atomicAdd(n_cand, 1)] = t;
+      return;  // the row is written by k_cell_search
     }
-    bool cut = false;
-    for (int f = 0; f < 2 * D; ++f) {  // cell_distances (levelset.hpp:313-327)
-      double nbp[3];
-      for (int k = 0; k < D; ++k) nbp[k] = x[k];
-      nbp[f >> 1] += ((f & 1) ? 1 : -1) * h;
-      const double tr = find_root_position<D>(L, x, nbp, cfg);
-      if (tr < 0) continue;
-      const double d = clampd(tr, cfg.d_min, 1.0);
-      if (d < 1.0) {
-        double p[3];
-        along<D>(x, nbp, tr, p);
-        dd[f] = d;
-        ob[f] = (int8_t)lsf_attaining<D>(L, p);
-        cut = true;
-      }
-    }
-    if (!cut && cfg.thin_rescue && h > cfg.w_min) {
-      // resolve_thin_boundary (levelset.hpp:344-382)
-      const double fa = fc;
-      const int max_steps = (int)(h / cfg.w_min);
-      double y[3];
-      for (int k = 0; k < D; ++k) y[k] = x[k];
-      for (int step = 0; step < max_steps; ++step) {
-        double g[3];
-        lsf_gradient<D>(L, y, h, g);
-        const double gn = vnorm<D>(g);
-        if (gn == 0) break;
-        const double sc = cfg.w_min / gn;
-        for (int k = 0; k < D; ++k) y[k] -= g[k] * sc;
-        if (fa * lsf_eval<D>(L, y) > 0) continue;
-        const double tt = bisect_t<D>(L, x, y, 0.0, 1.0, cfg.eps_tol);
-        double root[3], rc[3];
-        along<D>(x, y, tt, root);
-        for (int k = 0; k < D; ++k) rc[k] = root[k] - x[k];
-        const double hd = clampd(vnorm<D>(rc) / h, cfg.d_min, 1.0);
-        const int hobj = lsf_attaining<D>(L, root);
-        int hdir = 0;
-        double best = DBL_MAX * 2.0;
-        for (int f = 0; f < 2 * D; ++f) {
-          double nbp[3];
-          for (int k = 0; k < D; ++k) nbp[k] = x[k];
-          nbp[f >> 1] += ((f & 1) ? 1 : -1) * h;
-          double rn[3];
-          for (int k = 0; k < D; ++k) rn[k] = root[k] - nbp[k];
-          const double dist = vnorm<D>(rn);
-          if (dist < best) {
-            best = dist;
-            hdir = f;
-          }
-        }
-        dd[hdir] = hd;
-        ob[hdir] = (int8_t)hobj;
-        cut = hd < 1.0;
-        for (int f = 0; f < 2 * D && !cut; ++f) cut = dd[f] < 1.0;
-        break;
-      }
-    }
-    if (cut) {  // make_row (stencil.hpp:84-110)
-      const double inv2 = 1.0 / (h * h);
-      for (int a = 0; a < D; ++a) {
-        const double dm = dd[2 * a], dp = dd[2 * a + 1];
-        const double cm = 2.0 / ((dp + dm) * dm) * inv2;
-        const double cp = 2.0 / ((dp + dm) * dp) * inv2;
-        r.center -= 2.0 / (dm * dp) * inv2;
-        if (dm < 1.0) {
-          r.bc[2 * a] = cm;
-          r.obj[2 * a] = ob[2 * a];
-        } else {
-          r.nb[2 * a] = cm;
-        }
-        if (dp < 1.0) {
-          r.bc[2 * a + 1] = cp;
-          r.obj[2 * a + 1] = ob[2 * a + 1];
-        } else {
-          r.nb[2 * a + 1] = cp;
-        }
-      }
-      for (int f = 0; f < 2 * D; ++f) r.d[f] = dd[f];
-      r.has = 1;
-    }
+    cell_search<D>(ev, x, h, fc, cfg, r);
   }
   A.rows[t] = r;
   if (r.has) atomicAdd(&A.counts[fb], 1);
+}
+
+// One warp per boundary-candidate cell of a composite level set with many
+// children: the lanes evaluate the children (WarpEval), so the line searches
+// run without divergence.
+template <int D, int N>
+__global__ void __launch_bounds__(128) k_cell_search(LsfDev L, BuildArgs A, pmg_stencil_cfg_t cfg,
+                                                     const long long* __restrict__ cand, const int* n_cand) {
+  pdl_begin();
+  constexpr int NI = D == 2 ? N * N : N * N * N;
+  const int w = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (w >= *n_cand) return;
+  const long long t = cand[w];
+  double x[3], h;
+  cell_at<D, N>(A, t, x, h);
+  RowScratch r;
+  row_init(r);
+  const WarpEval<D> ev{L};
+  cell_search<D>(ev, x, h, ev.f(x), cfg, r);
+  if ((threadIdx.x & 31) == 0) {
+    A.rows[t] = r;
+    if (r.has) atomicAdd(&A.counts[(int)(t / NI)], 1);
+  }
 }
 
 // One CTA per flagged block: exclusive scan of `has` in interior order.
@@ -485,6 +600,10 @@ __global__ void __launch_bounds__(1024) k_compact(BuildArgs A, const int32_t* __
 
 namespace pmghost {
 
+// composite level sets with at least this many children search their
+// boundary cells one warp per cell (the lanes evaluate the children)
+constexpr int kWarpSearchChildren = 8;
+
 template <int D, int N>
 void run_stencil_build(Ctx& c, const pmg_lsf_t* lsf, int n_lsf, const pmg_stencil_cfg_t* cfg) {
   using namespace pmgdev;
@@ -511,8 +630,11 @@ void run_stencil_build(Ctx& c, const pmg_lsf_t* lsf, int n_lsf, const pmg_stenci
   d_dx.upload(m.dx, c.stream);
   DevBuf<uint8_t> d_flag;
   d_flag.alloc((size_t)nb);
+  int lip1 = 1;  // only Euclidean-distance pieces (k_block_flag's far-block test)
+  for (const auto& dsc : descs)
+    if (dsc.shape != PMG_SHAPE_SPHERE && dsc.shape != PMG_SHAPE_ROD && dsc.shape != PMG_SHAPE_COMPOSITE_MIN) lip1 = 0;
   k_block_flag<D, N><<<nb, 256, 0, c.stream>>>(L, d_origin.p, d_dx.p, nb, cfg->boundary_safety,
-                                               d_flag.p);
+                                               d_flag.p, lip1);
   PMG_CUDA(cudaGetLastError());
   std::vector<uint8_t> flag((size_t)nb);
   PMG_CUDA(cudaMemcpyAsync(flag.data(), d_flag.p, (size_t)nb, cudaMemcpyDeviceToHost, c.stream));
@@ -522,11 +644,14 @@ void run_stencil_build(Ctx& c, const pmg_lsf_t* lsf, int n_lsf, const pmg_stenci
     if (flag[(size_t)b]) flagged.push_back(b);
   HostStencils& st = c.st;
   st = HostStencils{};
+  c.devrows.reset();
   st.valid = true;
   st.boundary.assign((size_t)nb, 0);
   st.row_count.assign((size_t)nb, 0);
   st.row_start.assign((size_t)nb + 1, 0);
-  st.row_of.assign((size_t)nb * NI, -1);
+  st.NI = NI;
+  st.row_page.assign((size_t)nb, -1);
+  st.row_pages.clear();
   st.phi_b.resize((size_t)n_obj);
   for (int o = 0; o < n_obj; ++o) st.phi_b[(size_t)o] = composite ? lsf[o + 1].boundary_value : lsf[0].boundary_value;
   const int nf = (int)flagged.size();
@@ -539,8 +664,27 @@ void run_stencil_build(Ctx& c, const pmg_lsf_t* lsf, int n_lsf, const pmg_stenci
     d_rows.alloc((size_t)nf * NI);
     BuildArgs A{nf, d_flagged.p, d_origin.p, d_dx.p, d_rows.p, d_counts.p, d_flag.p};
     const long long tot = (long long)nf * NI;
-    k_cell_rows<D, N><<<(unsigned)((tot + 127) / 128), 128, 0, c.stream>>>(L, A, *cfg);
-    PMG_CUDA(cudaGetLastError());
+    if (composite && n_obj >= kWarpSearchChildren) {
+      // candidates listed by k_cell_rows, searched one warp per cell
+      DevBuf<long long> d_cand;
+      DevBuf<int> d_ncand;
+      d_cand.alloc((size_t)tot);
+      d_ncand.alloc(1);
+      PMG_CUDA(cudaMemsetAsync(d_ncand.p, 0, sizeof(int), c.stream));
+      k_cell_rows<D, N><<<(unsigned)((tot + 127) / 128), 128, 0, c.stream>>>(L, A, *cfg, d_cand.p, d_ncand.p);
+      PMG_CUDA(cudaGetLastError());
+      int ncand = 0;
+      PMG_CUDA(cudaMemcpyAsync(&ncand, d_ncand.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+      PMG_CUDA(cudaStreamSynchronize(c.stream));
+      if (ncand > 0)
+        k_cell_search<D, N><<<(unsigned)(((long long)ncand * 32 + 127) / 128), 128, 0, c.stream>>>(
+            L, A, *cfg, d_cand.p, d_ncand.p);
+      PMG_CUDA(cudaGetLastError());
+    } else {
+      k_cell_rows<D, N><<<(unsigned)((tot + 127) / 128), 128, 0, c.stream>>>(L, A, *cfg, (long long*)nullptr,
+                                                                              (int*)nullptr);
+      PMG_CUDA(cudaGetLastError());
+    }
     std::vector<int32_t> counts((size_t)nf), offs((size_t)nf + 1, 0);
     PMG_CUDA(cudaMemcpyAsync(counts.data(), d_counts.p, (size_t)nf * 4, cudaMemcpyDeviceToHost, c.stream));
     PMG_CUDA(cudaStreamSynchronize(c.stream));
@@ -563,7 +707,8 @@ void run_stencil_build(Ctx& c, const pmg_lsf_t* lsf, int n_lsf, const pmg_stenci
     k_compact<D, N><<<nf, 1024, 0, c.stream>>>(A, d_offs.p, d_rowof.p, d_center.p, d_nb.p, d_bc.p,
                                                d_d.p, d_obj.p, d_mask.p, d_pin.p, d_lin.p);
     PMG_CUDA(cudaGetLastError());
-    std::vector<int32_t> rowof((size_t)nf * NI);
+    std::vector<int32_t>& rowof = st.row_pages;  // the flagged blocks' pages, in block-id order
+    rowof.resize((size_t)nf * NI);
     st.center.resize(R);
     st.nb.resize(R * F);
     st.bc.resize(R * F);
@@ -585,13 +730,23 @@ void run_stencil_build(Ctx& c, const pmg_lsf_t* lsf, int n_lsf, const pmg_stenci
     dl(st.mask.data(), d_mask.p, R);
     dl(st.lin.data(), d_lin.p, R * 4);
     PMG_CUDA(cudaStreamSynchronize(c.stream));
+    // the device copy the per-level row arrays are gathered from (upload_stencils)
+    auto DR = std::make_unique<DevRows>();
+    DR->center = std::move(d_center);
+    DR->nb = std::move(d_nb);
+    DR->bc = std::move(d_bc);
+    DR->d = std::move(d_d);
+    DR->obj = std::move(d_obj);
+    DR->pin = std::move(d_pin);
+    DR->mask = std::move(d_mask);
+    DR->rowof = std::move(d_rowof);
+    c.devrows = std::move(DR);
     // rows are concatenated in block-id order; flagged[] is increasing
     for (int i = 0; i < nf; ++i) {
       const int b = flagged[(size_t)i];
       st.boundary[(size_t)b] = 1;
       st.row_count[(size_t)b] = counts[(size_t)i];
-      std::copy(rowof.begin() + (long)i * NI, rowof.begin() + (long)(i + 1) * NI,
-                st.row_of.begin() + (long)b * NI);
+      st.row_page[(size_t)b] = i;
     }
   }
   for (int b = 0; b < nb; ++b) st.row_start[(size_t)b + 1] = st.row_start[(size_t)b] + st.row_count[(size_t)b];

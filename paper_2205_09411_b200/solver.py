@@ -14,6 +14,7 @@ Names, argument meaning and error behaviour follow pmg::MgSolver
 from __future__ import annotations
 
 import ctypes as C
+from collections.abc import Mapping
 import os
 from dataclasses import dataclass
 
@@ -246,7 +247,37 @@ class DeviceMesh:
         return s
 
 
-def build_stencils(dev: DeviceMesh, lsf: LevelSetSpec, cfg: StencilBuildConfig) -> StencilSet:
+class DeviceStencils(Mapping):
+    """The StencilSet built on the device (build_stencils).  The solver reads
+    the device copy; the host image (a StencilSet) is read back only when an
+    item is first accessed (parity checks, the C++ drop-in's bit comparison)."""
+
+    def __init__(self, dev: DeviceMesh, phi_b):
+        self._dev, self._phi_b, self._s = dev, list(phi_b), None
+
+    def host(self) -> StencilSet:
+        if self._s is None:
+            self._s = self._dev.get_stencils(self._phi_b)
+        return self._s
+
+    def __getitem__(self, k):
+        return self.host()[k]
+
+    def __setitem__(self, k, v):
+        self.host()[k] = v
+
+    def __iter__(self):
+        return iter(self.host())
+
+    def __len__(self):
+        return len(self.host())
+
+    @property
+    def n_rows(self):
+        return self.host().n_rows
+
+
+def build_stencils(dev: DeviceMesh, lsf: LevelSetSpec, cfg: StencilBuildConfig) -> DeviceStencils:
     """pmg::build_stencils (stencil.hpp:207-222), evaluated on the GPU."""
     descs = lsf.as_descs()
     arr = _lsf_array(descs)
@@ -255,7 +286,7 @@ def build_stencils(dev: DeviceMesh, lsf: LevelSetSpec, cfg: StencilBuildConfig) 
     dev._check(dev.lib.pmg_b200_build_stencils(dev.h, C.cast(arr, C.c_void_p), len(descs),
                                                C.byref(c)))
     phi_b = [lsf.object(i).boundary_value for i in range(lsf.n_objects())]
-    return dev.get_stencils(phi_b)
+    return DeviceStencils(dev, phi_b)
 
 
 class MgSolver:
@@ -265,8 +296,8 @@ class MgSolver:
         self.dev = dev
         self.lib = dev.lib
         self.h = dev.h
-        if stencils is not None:
-            dev.set_stencils(stencils)
+        if stencils is not None and not (isinstance(stencils, DeviceStencils) and stencils._dev is dev):
+            dev.set_stencils(stencils if not isinstance(stencils, DeviceStencils) else stencils.host())
         self.stencils = stencils
         cfg = cfg or MgConfig()
         self.cfg = cfg
