@@ -65,6 +65,17 @@ def gs_traffic(name):
         return None
 
 
+def gs_traffic_source(name):
+    if name != "cfg2":
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_gs_traffic.json")) as f:
+            d = json.load(f)
+        return d.get("source", "profiles/r01_gs_traffic.json (ncu --set full capture of k_gs_stream)")
+    except Exception:
+        return None
+
+
 def vcycle_bytes(mesh, N, dim, nu1=2, nu2=2):
     """Algorithmic bytes of one V-cycle:
     B_V = sum_{l=2..L} [(24(nu1+nu2)+32) n_l + 32 n_l/2^D + 32 n_{l-1}] + 16 sum_l leaf_l."""
@@ -186,6 +197,29 @@ def dist_env():
     return ws, rank, local
 
 
+def workload_config(case, mesh):
+    """The config dict of a bench line -- identical in both arms (the problem,
+    not how an arm decomposes it; that is the line's "parallelism")."""
+    step = "one V-cycle after the FMG cycle" if case.fmg_first else "one V-cycle (10 V from phi = 0 is the plan)"
+    L = mesh.n_levels
+    n_fine = len(mesh.level_blocks(L)) * case.N ** case.dim
+    return {"workload": f"{case.name}: {case.notes}; step = {step}", "leaf_cells": case.leaf_cells(mesh),
+            "levels": L, "blocks": mesh.n_blocks,
+            "l2_flush": f"none needed: the finest level's phi + rhs ({2 * 8 * n_fine / 1e6:.0f} MB) exceed "
+                        "the 126 MB L2"}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_reference_run(case, steps, warmup, budget_s=None, threads=None):
     """The reference's own MgSolver (oracle/_ref/libpmgref.so) on host cores."""
     from oracle.oc import REF_SO, PORT_SO, Oracle
@@ -233,8 +267,8 @@ def run_reference(args, case):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
         "steps": k, "warmup": args.warmup, "ms_per_step": 1e3 * t / k, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{case.name}: {case.notes}; step = one V-cycle (after FMG)",
-                   "leaf_cells": r["leaf"], "parallelism": "host threads"},
+        "config": workload_config(case, case.build_mesh()),
+        "parallelism": f"host threads x{r['threads']} ({cpu_model()})",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["threads"], "kind": r["kind"],
                          "sample": f"{k} V-cycles of {case.name} after FMG "
                                    f"(median {1e3 * statistics.median(r['times']):.1f} ms)"},
@@ -327,12 +361,9 @@ def run_partitioned(args, case):
             "metric": METRIC, "value": leaf * args.steps / (ms_total * 1e-3), "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{case.name}: {case.notes}; step = one V-cycle of ONE problem "
-                                   f"Morton-partitioned over {ws} GPU(s)",
-                       "leaf_cells": leaf, "levels": L, "blocks": mesh.n_blocks,
-                       "parallelism": f"morton x{ws}" if ws > 1 else "1 GPU (partitioned path, one rank)",
-                       "split_level": info["split_level"],
-                       "l2_flush": "none needed: finest level > 126 MB L2 per rank"},
+            "config": workload_config(case, mesh),
+            "parallelism": (f"one problem Morton-partitioned over {ws} GPUs (split level {info['split_level']})"
+                            if ws > 1 else "1 GPU (the partitioned path, one rank)"),
             "vcycle_roofline": {"algorithmic_bytes": BV, "achieved": vc_gbs, "peak": peak * ws, "unit": "GB/s",
                                 "frac": vc_gbs / (peak * ws), "bytes_per_unknown": BV / leaf,
                                 "peak_kind": f"{peak_kind}, x {ws} GPUs"},
@@ -501,25 +532,27 @@ def run_b200(args, case):
     if rank == 0 and not args.no_cpu_baseline:
         r = cpu_reference_run(case, steps=40, warmup=1, budget_s=20.0)
         cpu = {"value": r["leaf"] * len(r["times"]) / sum(r["times"]), "unit": UNIT,
-               "cores": r["threads"], "kind": r["kind"],
+               "cores": r["threads"], "kind": r["kind"], "cpu_model": cpu_model(),
                "sample": f"{len(r['times'])} V-cycles of {case.name} after FMG on the host "
                          f"(reference MgSolver, {r['threads']} threads; median "
                          f"{1e3 * statistics.median(r['times']):.1f} ms/V-cycle)"}
+        r1 = cpu_reference_run(case, steps=5, warmup=0, budget_s=10.0, threads=1)
+        cpu["threads_1"] = {"value": r1["leaf"] * len(r1["times"]) / sum(r1["times"]), "unit": UNIT,
+                            "cores": 1, "sample": f"{len(r1['times'])} V-cycles, median "
+                                                  f"{1e3 * statistics.median(r1['times']):.1f} ms/V-cycle"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{case.name}: {case.notes}; step = one V-cycle (after FMG)",
-                       "leaf_cells": leaf, "levels": L, "blocks": mesh.n_blocks,
-                       "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
-                       "l2_flush": "none needed: finest phi+rhs = "
-                                   f"{2 * 8 * n_fine / 1e6:.0f} MB > 126 MB L2"},
+            "config": workload_config(case, mesh),
+            "parallelism": f"{ws} independent replicas (weak scaling)" if ws > 1 else "1 GPU",
             "roofline": {"bound": "hbm",
                          "kernel": "finest GS-RB half-sweep (k_gs_stream + concurrent k_gs_cut)",
                          "achieved": gs_gbs, "peak": peak, "unit": "GB/s",
                          "frac": gs_gbs / peak, "traffic": gs_traffic(case.name),
+                         "traffic_source": gs_traffic_source(case.name),
                          "bytes_per_launch": gs_bytes, "peak_kind": peak_kind},
             "vcycle_roofline": {"algorithmic_bytes": BV, "achieved": vc_gbs, "peak": peak,
                                 "unit": "GB/s", "frac": vc_gbs / peak,
@@ -540,10 +573,89 @@ def run_b200(args, case):
             "setup_s": {"mesh": t_mesh, "stencil_build_gpu": t_stencil},
             "final_max_resid": stats.max_resid,
         }
+        if ws == 1 and not args.no_extras:
+            line["extra_configs"] = extra_configs(args)
+            line["stencil_build"] = stencil_build_compare(args)
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def extra_configs(args, names=("cfg3", "cfg4")):
+    """V-cycle throughput of BASELINE configs 3 (AMR, byte model from the
+    actual n_l and leaf_l) and 4 (512^3, 32 spheres) on the same GPU."""
+    import torch
+    from paper_2205_09411_b200 import DeviceMesh, MgConfig, MgSolver, StencilBuildConfig, build_stencils
+    from paper_2205_09411_b200 import configs as cfgs
+    from paper_2205_09411_b200.mesh import VAR_RHS
+    from paper_2205_09411_b200.solver import LAYOUT_INTERIOR
+    out = {}
+    peak, _ = measured_peaks()
+    for name in names:
+        case = cfgs.get_case(name)
+        mesh = case.build_mesh()
+        dev = DeviceMesh(mesh)
+        build_stencils(dev, case.lsf, StencilBuildConfig(w_min=case.w_min))
+        dev.set_field(VAR_RHS, case.rhs_fields(mesh), layout=LAYOUT_INTERIOR)
+        sol = MgSolver(dev, None, MgConfig())
+        hist = [sol.v_cycle().max_resid for _ in range(case.v_cycles)]  # the config's plan
+        for _ in range(3):
+            sol.v_cycle_async()
+        sol.cycle_result()
+        stream = torch.cuda.ExternalStream(dev.stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        steps = max(5, args.steps)
+        e0.record(stream)
+        for _ in range(steps):
+            sol.v_cycle_async()
+        e1.record(stream)
+        sol.cycle_result()
+        ms = e0.elapsed_time(e1) / steps
+        leaf = case.leaf_cells(mesh)
+        BV = vcycle_bytes(mesh, case.N, case.dim)
+        red = [hist[i] / hist[i + 1] for i in range(len(hist) - 1) if hist[i + 1] > 0]
+        out[name] = {"workload": case.notes, "leaf_cells": leaf, "ms_per_step": ms,
+                     "value": leaf / (ms * 1e-3), "unit": UNIT,
+                     "vcycle_roofline": {"algorithmic_bytes": BV, "achieved": BV / (ms * 1e-3) / 1e9,
+                                         "peak": peak, "unit": "GB/s", "frac": BV / (ms * 1e-3) / 1e9 / peak,
+                                         "bytes_per_unknown": BV / leaf},
+                     "residual_reduction_per_cycle": (math.exp(sum(math.log(x) for x in red) / len(red))
+                                                      if red else None)}
+        del sol, dev
+    return out
+
+
+def stencil_build_compare(args, names=("cfg2", "cfg4")):
+    """K5 end to end (pmg_b200_build_stencils: the device build and every
+    device table the solver needs) against the reference's build_stencils on
+    all host threads, same host, same inputs."""
+    from oracle.oc import REF_SO, Oracle
+    from paper_2205_09411_b200 import DeviceMesh, StencilBuildConfig, build_stencils
+    from paper_2205_09411_b200 import configs as cfgs
+    out = {}
+    for name in names:
+        case = cfgs.get_case(name)
+        mesh = case.build_mesh()
+        dev = DeviceMesh(mesh)
+        ts = []
+        for _ in range(2):
+            t0 = time.perf_counter()
+            build_stencils(dev, case.lsf, StencilBuildConfig(w_min=case.w_min))
+            ts.append(time.perf_counter() - t0)
+        del dev
+        rec = {"gpu_s_first": ts[0], "gpu_s": min(ts)}
+        if os.path.exists(REF_SO) and not args.no_cpu_baseline:
+            o = Oracle(case.dim, case.N, case.lo[:case.dim], case.hi[:case.dim], "ref")
+            o.build_uniform(case.levels)
+            t0 = time.perf_counter()
+            o.build_stencils(case.lsf.as_descs(), w_min=case.w_min)
+            rec["reference_s"] = time.perf_counter() - t0
+            rec["reference_threads"] = os.cpu_count()
+            rec["speedup"] = rec["reference_s"] / rec["gpu_s"]
+            del o
+        out[name] = rec
+    return out
 
 
 def main():
@@ -555,6 +667,8 @@ def main():
     ap.add_argument("--config", default=None,
                     help="BASELINE config (default: cfg2 on one GPU, cfg5 partitioned on several)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the extra lines (configs 3 / 4 throughput, stencil build vs the reference)")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: N independent copies of the config (weak scaling) instead of one partitioned problem")
     ap.add_argument("--partitioned", action="store_true",

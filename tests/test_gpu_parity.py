@@ -226,3 +226,49 @@ def test_config5_full_size_properties():
     red = np.exp(np.mean(np.log(r[1:-1] / r[2:])))
     assert red > 3.0, red  # about 5-6x per V-cycle at every size tested against the reference
     assert r[-1] < 1e-5 * r[0], r
+
+
+def test_coarse_stall_message_matches_reference():
+    """BiCGStab stall on a coarse system too large for the smoothing fallback
+    (n = 3960 > 8^3 + 1; multigrid.hpp:456-465): the same std::runtime_error
+    text as the reference -- iterations and unknowns exactly, the relative
+    residual (std::to_string) to its printed digits up to the dot-product
+    summation order."""
+    import re
+
+    from paper_2205_09411_b200 import MgConfig
+    from paper_2205_09411_b200._lib import PMG_ERR_COARSE_STALL, PmgError
+    case = cfgs.get_case("cfg2@3")
+    o, dev, sol, mesh, st = setup_pair(case, mg=MgConfig(coarse_max_iters=1))
+    with pytest.raises(PmgError) as ea:
+        sol.v_cycle()
+    with pytest.raises(RuntimeError) as eb:
+        o.v_cycle()
+    a, b = str(ea.value), str(eb.value)
+    assert ea.value.code == PMG_ERR_COARSE_STALL
+    pat = r"coarse solve failed: BiCGStab stalled at relative residual ([0-9.]+) after (\d+) iterations on (\d+) unknowns"
+    ma, mb = re.search(pat, a), re.search(pat, b)
+    assert ma and mb, (a, b)
+    assert ma.group(2) == mb.group(2) == "1" and ma.group(3) == mb.group(3) == "3960", (a, b)
+    assert abs(float(ma.group(1)) - float(mb.group(1))) <= 2e-6 + 1e-9 * float(mb.group(1)), (a, b)
+
+
+def test_gsrb_fallback_matches_reference():
+    """Config 1's coarse system (n = 52 <= 8^2 + 1) with BiCGStab capped at one
+    iteration: the reference writes the iterate back and finishes with GS-RB
+    sweeps (gsrb_fallback, multigrid.hpp:586-601); the GPU path does the same,
+    with residual histories and phi within the SURVEY 8c bounds."""
+    from paper_2205_09411_b200 import MgConfig
+    case = cfgs.get_case("cfg1")
+    o, dev, sol, mesh, st = setup_pair(case, mg=MgConfig(coarse_max_iters=1))
+    D, N = case.dim, case.N
+    dxf = mesh.level_dx(mesh.n_levels)
+    hist = []
+    for _ in range(4):
+        hist.append((sol.v_cycle(), o.v_cycle()))
+    pa = dev.get_field(VAR_PHI, layout=LAYOUT_INTERIOR)
+    pb = interior(o, VAR_PHI, D, N)
+    maxphi = float(np.max(np.abs(pb)))
+    for k, (a, b) in enumerate(hist):
+        assert abs(a.max_resid - b[0]) <= resid_tol(b[0], maxphi, dxf, D), (k, a.max_resid, b[0])
+    assert max_rel_diff(pa, pb) <= 1e-10
