@@ -144,6 +144,9 @@ int pmg_b200_cycle_kernel_count(pmg_b200_ctx* ctx, int kind);
 int pmg_b200_n_levels(pmg_b200_ctx* ctx);
 int pmg_b200_level_size(pmg_b200_ctx* ctx, int level);
 int pmg_b200_synchronize(pmg_b200_ctx* ctx);
+/* a page-locked host buffer of at least `bytes`, owned by the context and
+ * reused (the C++ drop-in's PHI copies to the host go through it) */
+void* pmg_b200_host_buffer(pmg_b200_ctx* ctx, size_t bytes);
 /* BiCGStab iterations and final relative residual of the most recent coarse
  * solve (KrylovResult, multigrid.hpp:200-204; the reference discards it) */
 int pmg_b200_coarse_info(pmg_b200_ctx* ctx, int32_t* iters, double* rel);

@@ -26,6 +26,7 @@
 #include <string>
 #include <vector>
 
+#include "pmg/fields.hpp"
 #include "pmg/multigrid.hpp"
 #include "pmg_b200.h"
 
@@ -42,6 +43,9 @@ inline void check(pmg_b200_ctx* h, int rc) {
 }
 
 template <int Dim>
+void upload_mesh(pmg_b200_ctx* h, const TreeMesh<Dim>& mesh);
+
+template <int Dim>
 pmg_b200_ctx* make_context(const TreeMesh<Dim>& mesh, int device) {
   double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
   for (int k = 0; k < Dim; ++k) {
@@ -50,11 +54,19 @@ pmg_b200_ctx* make_context(const TreeMesh<Dim>& mesh, int device) {
   }
   pmg_b200_ctx* h = pmg_b200_create(Dim, mesh.block_size(), lo, hi, device);
   if (!h) throw std::runtime_error("pmg_b200_create: out of memory");
-  if (*pmg_b200_last_error(h)) {
-    const std::string m = pmg_b200_last_error(h);
+  try {  // the context is destroyed on any failure below
+    if (*pmg_b200_last_error(h)) throw std::runtime_error(pmg_b200_last_error(h));
+    upload_mesh<Dim>(h, mesh);
+  } catch (...) {
     pmg_b200_destroy(h);
-    throw std::runtime_error(m);
+    throw;
   }
+  return h;
+}
+
+// topology and physical face values of the reference's mesh
+template <int Dim>
+void upload_mesh(pmg_b200_ctx* h, const TreeMesh<Dim>& mesh) {
   const int nb = mesh.n_blocks();
   std::vector<int32_t> level(nb), coords(nb * 3, 0), parent(nb), children(nb * 8, -1),
       nbr(nb * 6, -1), cnbr(nb * 6, -1);
@@ -108,7 +120,6 @@ pmg_b200_ctx* make_context(const TreeMesh<Dim>& mesh, int device) {
                                                                       : PMG_BC_DIRICHLET,
                                   vals.empty() ? nullptr : vals.data()));
   }
-  return h;
 }
 
 template <int Dim>
@@ -242,7 +253,7 @@ template <int Dim>
 class MgSolver {
  public:
   MgSolver(TreeMesh<Dim>& mesh, StencilSet<Dim>& stencils, const MgConfig& cfg, int device = 0)
-      : mesh_(mesh), set_(stencils), cfg_(cfg) {
+      : mesh_(mesh), set_(stencils), cfg_(cfg), pool_(cfg.threads) {
     cfg_.validate();
     h_ = detail::make_context(mesh_, device);
     try {
@@ -282,7 +293,10 @@ class MgSolver {
   void prolong_full(int level) { op(pmg_b200_prolong_full(h_, level)); }
   void coarse_solve() { op(pmg_b200_coarse_solve(h_)); }
   void set_have_guess(bool v) { detail::check(h_, pmg_b200_set_have_guess(h_, v ? 1 : 0)); }
-  const CoarseSystem& coarse_system() {
+  /// The host thread pool (MgSolver::pool, multigrid.hpp:475): the cycles
+  /// run on the GPU; host-side helpers a caller runs over the mesh use it.
+  ThreadPool& pool() { return pool_; }
+  const CoarseSystem& coarse_system() const {
     int32_t n, nnz, no;
     detail::check(h_, pmg_b200_coarse_sizes(h_, &n, &nnz, &no));
     cs_.n = n;
@@ -302,13 +316,64 @@ class MgSolver {
     return cs_;
   }
 
+  /// pmg::error_norms (fields.hpp:35-69) of PHI against an AnalyticSolution,
+  /// evaluated on the device: no copy of PHI to the host.
+  ErrorNorms error_norms(const AnalyticSolution& sol, bool volume_weighted = false) const {
+    ErrorNorms e;
+    const int tag = sol.tag == AnalyticSolution::Case::sphere3d ? 1 : 0;
+    detail::check(h_, pmg_b200_error_norms(h_, VAR_PHI, tag, sol.phi_b, sol.a, sol.R, volume_weighted ? 1 : 0,
+                                           &e.linf, &e.l2));
+    return e;
+  }
+  /// pmg::face_gradient (fields.hpp:149-232) of PHI on the device; the
+  /// cell-centred magnitude goes to mesh.field(id, var_out) of every leaf when
+  /// var_out >= 0, as the reference writes it.
+  FaceField<Dim> face_gradient(int var_out = -1) {
+    const int nl = pmg_b200_n_leaves(h_);
+    if (nl < 0) detail::check(h_, -nl);
+    const int N = mesh_.block_size();
+    size_t ni = 1, per_axis = (size_t)N + 1;
+    for (int k = 0; k < Dim; ++k) ni *= (size_t)N;
+    for (int k = 1; k < Dim; ++k) per_axis *= (size_t)N;
+    std::vector<double> faces((size_t)nl * Dim * per_axis), mag(var_out >= 0 ? (size_t)nl * ni : 1);
+    std::vector<int32_t> ids((size_t)nl);
+    detail::check(h_, pmg_b200_face_gradient(h_, VAR_PHI, faces.data(), var_out >= 0 ? mag.data() : nullptr,
+                                             ids.data()));
+    FaceField<Dim> ff;
+    ff.block_ids.assign(ids.begin(), ids.end());
+    ff.faces.resize((size_t)nl);
+    for (int q = 0; q < nl; ++q)
+      for (int a = 0; a < Dim; ++a)
+        ff.faces[(size_t)q][(size_t)a].assign(faces.begin() + (long)((size_t)q * Dim + a) * (long)per_axis,
+                                              faces.begin() + (long)((size_t)q * Dim + a + 1) * (long)per_axis);
+    if (var_out >= 0) {
+      IVec<Dim> zero{}, nn;
+      nn.fill(N);
+      for (int q = 0; q < nl; ++q) {
+        double* out = mesh_.field(ids[(size_t)q], var_out);
+        size_t c = 0;
+        for_box<Dim>(zero, nn, [&](const IVec<Dim>& i) { out[mesh_.lin(i)] = mag[(size_t)q * ni + c++]; });
+      }
+    }
+    return ff;
+  }
+  /// pmg::write_dump (io.hpp:23-71) of PHI streamed from the device.
+  void write_dump(const std::string& path, const std::string& field_name) {
+    detail::check(h_, pmg_b200_write_dump(h_, VAR_PHI, path.c_str(), field_name.c_str()));
+  }
+
   /// Copy PHI (ghost layers included) from the GPU into mesh.field(id, VAR_PHI).
+  /// The copy goes through the context's page-locked buffer and is scattered
+  /// into the blocks by the solver's thread pool.
   void sync_to_host() {
     const size_t S = mesh_.var_stride();
-    std::vector<double> buf((size_t)mesh_.n_blocks() * S);
-    detail::check(h_, pmg_b200_download_field(h_, VAR_PHI, buf.data(), PMG_LAYOUT_PADDED));
-    for (int id = 0; id < mesh_.n_blocks(); ++id)
-      std::memcpy(mesh_.field(id, VAR_PHI), buf.data() + (size_t)id * S, S * sizeof(double));
+    const size_t bytes = (size_t)mesh_.n_blocks() * S * sizeof(double);
+    double* buf = static_cast<double*>(pmg_b200_host_buffer(h_, bytes));
+    if (!buf) detail::check(h_, PMG_ERR_CUDA);
+    detail::check(h_, pmg_b200_download_field(h_, VAR_PHI, buf, PMG_LAYOUT_PADDED));
+    parallel_for(&pool_, mesh_.n_blocks(), [&](int id) {
+      std::memcpy(mesh_.field(id, VAR_PHI), buf + (size_t)id * S, S * sizeof(double));
+    });
   }
   /// Drop-in default true: PHI is copied back after every cycle/operation.
   void set_sync_to_host(bool v) { sync_ = v; }
@@ -339,9 +404,10 @@ class MgSolver {
   TreeMesh<Dim>& mesh_;
   StencilSet<Dim>& set_;
   MgConfig cfg_;
+  ThreadPool pool_;
   pmg_b200_ctx* h_ = nullptr;
   bool sync_ = true;
-  CoarseSystem cs_;
+  mutable CoarseSystem cs_;
 };
 
 }  // namespace b200

@@ -73,7 +73,7 @@ EXPORTS = [
     "pmg_b200_write_dump", "pmg_b200_stage_field_async", "pmg_b200_commit_staged_field",
     "pmg_b200_set_partition", "pmg_b200_nccl_unique_id", "pmg_b200_dist_init_nccl",
     "pmg_b200_dist_local_group", "pmg_b200_dist_v_cycle", "pmg_b200_dist_v_cycle_async",
-    "pmg_b200_dist_info", "pmg_b200_field_bytes",
+    "pmg_b200_dist_info", "pmg_b200_field_bytes", "pmg_b200_host_buffer",
 ]
 
 _lib = None
@@ -149,6 +149,8 @@ def load():
     lib.pmg_b200_dist_v_cycle_async.argtypes = [vp]
     lib.pmg_b200_dist_info.argtypes = [vp, C.POINTER(C.c_int32)]
     lib.pmg_b200_field_bytes.argtypes = [vp, C.POINTER(C.c_double)]
+    lib.pmg_b200_host_buffer.argtypes = [vp, C.c_size_t]
+    lib.pmg_b200_host_buffer.restype = C.c_void_p
     _lib = lib
     return lib
 

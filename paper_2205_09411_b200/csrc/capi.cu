@@ -31,6 +31,7 @@ Ctx::~Ctx() {
   g_fmg[1].reset();
   g_measure.reset();
   if (h_out) cudaFreeHost(h_out);
+  if (h_buf) cudaFreeHost(h_buf);
   if (h_status) cudaFreeHost(h_status);
   if (stream) cudaStreamDestroy(stream);
   if (side) cudaStreamDestroy(side);
@@ -2107,6 +2108,20 @@ int pmg_b200_field_bytes(pmg_b200_ctx* h, double* out) {
     }
     *out = b;
   });
+}
+void* pmg_b200_host_buffer(pmg_b200_ctx* h, size_t bytes) {
+  void* out = nullptr;
+  guard(h, [&](Ctx& c) {
+    if (c.h_buf_bytes < bytes) {
+      if (c.h_buf) PMG_CUDA(cudaFreeHost(c.h_buf));
+      c.h_buf = nullptr;
+      c.h_buf_bytes = 0;
+      PMG_CUDA(cudaMallocHost(&c.h_buf, bytes));
+      c.h_buf_bytes = bytes;
+    }
+    out = c.h_buf;
+  });
+  return out;
 }
 int pmg_b200_synchronize(pmg_b200_ctx* h) {
   return guard(h, [&](Ctx& c) { PMG_CUDA(cudaStreamSynchronize(c.stream)); });

@@ -361,6 +361,8 @@ struct Ctx {
   double cf_w = 0;
 
   double* h_out = nullptr;  // pinned: stats[2], diag[2]
+  void* h_buf = nullptr;    // pinned transfer buffer (pmg_b200_host_buffer)
+  size_t h_buf_bytes = 0;
   int* h_status = nullptr;  // pinned
 
   pmg_mg_cfg_t cfg{2, 2, 1e-6, 2000, 1};

@@ -20,3 +20,18 @@ def test_cpp_dropin_matches_reference_solver():
     print(p.stdout)
     assert p.returncode == 0, p.stdout + p.stderr
     assert "ALL OK" in p.stdout
+
+
+HARNESS = os.path.join(ROOT, "oracle", "_ref", "harness_dropin")
+
+
+@pytest.mark.skipif(not os.path.exists(HARNESS), reason="make -C oracle dropin (needs the reference headers)")
+def test_harness_on_gpu_matches_reference_harness():
+    """Every case the reference harness knows (harness.hpp:47-54) through
+    pmg::b200::run_case and pmg::run_case: residuals.csv, errors.csv,
+    mesh_stats.txt, config_resolved.cfg and the dumps agree (oracle/harness_dropin.cpp)."""
+    p = subprocess.run([HARNESS], capture_output=True, text=True, timeout=1200)
+    print(p.stdout)
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert "ALL OK" in p.stdout
+    assert p.stdout.count("\nok ") + p.stdout.startswith("ok ") >= 15
