@@ -55,11 +55,11 @@ def measured_peaks():
 
 def gs_traffic(name):
     """DRAM bytes per launch of the finest GS kernel from the committed ncu
-    capture (profiles/r01_gs_traffic.json), for the headline config only."""
+    capture (profiles/r02_gs_traffic.json), for the headline config only."""
     if name != "cfg2":
         return None
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_gs_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02_gs_traffic.json")) as f:
             return float(json.load(f)["dram_bytes_per_launch"])
     except Exception:
         return None
@@ -69,9 +69,9 @@ def gs_traffic_source(name):
     if name != "cfg2":
         return None
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_gs_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02_gs_traffic.json")) as f:
             d = json.load(f)
-        return d.get("source", "profiles/r01_gs_traffic.json (ncu --set full capture of k_gs_stream)")
+        return d.get("source", "profiles/r02_gs_traffic.json (ncu --set full capture of k_gs_stream)")
     except Exception:
         return None
 

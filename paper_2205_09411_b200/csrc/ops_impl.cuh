@@ -150,11 +150,8 @@ struct OpsImpl final : Ops {
       }
     }
   }
-  // number of CTAs launch_rstream uses (record partials)
-  int rstream_grid(Ctx& c, const LevelView& Lf, const LevelDev& d) {
-    const int minb = 2;  // MODE 1 = k_record_brick: two CTAs per SM
-    return std::min(d.n_rs, c.sms * minb);
-  }
+  // number of CTAs launch_rstream uses (record partials): k_record_brick runs two per SM
+  int rstream_grid(Ctx& c, const LevelView& Lf, const LevelDev& d) { return std::min(d.n_rs, c.sms * 2); }
   void residual(Ctx& c, int l) override {
     const LevelView& L = V(c, l);
     pdl_launch(k_residual<D, N>, grid_for((long long)L.nb * G::NI), kThreads, 0, c.stream, L, Vc(c, l),

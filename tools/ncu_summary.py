@@ -36,8 +36,8 @@ _UNIT = {("nsecond", "us"): 1e-3, ("usecond", "us"): 1.0, ("msecond", "us"): 1e3
          ("Kbyte", "KB"): 1.0, ("byte", "KB"): 1e-3}
 
 
-def _conv(v, unit, target):
-    return v * _UNIT.get((unit, target), 1.0)
+def _conv(v, unit, target, scale=1.0):
+    return v * _UNIT.get((unit, target), scale)
 
 
 def _num(s):
@@ -87,11 +87,11 @@ def full_report(path, regex=None):
             continue
         name = r[h.index("Kernel Name")].split("(")[0] if "Kernel Name" in h else "?"
         val = {}
-        for key, label, _, unit in METRICS:
+        for key, label, scale, unit in METRICS:
             if key in h:
                 v = _num(r[h.index(key)])
                 if v is not None:
-                    val[key] = _conv(v, units[h.index(key)], unit)
+                    val[key] = _conv(v, units[h.index(key)], unit, scale)
         lines.append(f"### `{name}`\n\n| metric | value |\n|---|---:|")
         for key, label, _, unit in METRICS:
             if key in val:
