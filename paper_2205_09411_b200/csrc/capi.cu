@@ -148,11 +148,12 @@ static void build_cut_tables(Ctx& c) {
   const int N = c.N, D = c.dim, NI = c.NI, H = NI / 2, F = c.F;
   for (int l = 1; l <= m.L; ++l) {
     LevelDev& d = *c.lev[(size_t)l];
-    std::vector<int32_t> ent[2];
+    std::vector<int32_t> ent[2], off[2];
     std::vector<double> gbc[2], coef[2];
     int base = 0;  // row offset of the block within the level's row arrays (upload_stencils order)
     for (int s = 0; s < d.nb && st.valid; ++s) {
       const int id = m.slots[(size_t)l][(size_t)s];
+      for (int cc = 0; cc < 2; ++cc) off[cc].push_back((int32_t)(ent[cc].size() / 8));  // k_gs_coop row ranges
       if (!st.boundary[(size_t)id]) continue;
       const int rc = st.row_count[(size_t)id];
       const int r0 = st.row_start[(size_t)id];
@@ -215,6 +216,9 @@ static void build_cut_tables(Ctx& c) {
       base += rc;
     }
     for (int cc = 0; cc < 2; ++cc) {
+      off[cc].resize((size_t)d.nb, (int32_t)(ent[cc].size() / 8));
+      off[cc].push_back((int32_t)(ent[cc].size() / 8));
+      d.cut_off[cc].upload(off[cc], c.stream);
       d.n_cut[cc] = (int)ent[cc].size() / 8;
       d.cut_ent[cc].upload(ent[cc], c.stream);
       d.cut_gbc[cc].upload(gbc[cc], c.stream);
@@ -500,6 +504,7 @@ static void upload_stencils(Ctx& c) {
         }
       }
       d.n_gs = (int)gsl.size() / 8;
+      d.coop = -1;
       d.gs_plan.upload(gsl, c.stream);
       d.n_rs = (int)rsl.size() / 8;
       d.rs_plan.upload(rsl, c.stream);
@@ -839,6 +844,7 @@ static void enq_restrict_level_no_guess(Ctx& c, int l) {
   if (c.lev[(size_t)(l - 1)]->has_cfold) c.ops->cfold(c, l - 1);
 }
 static void enq_smooth(Ctx& c, int l, int steps) {
+  if (c.ops->smooth(c, l, steps)) return;  // one cooperative launch (coop.cuh)
   for (int s = 0; s < steps; ++s) {
     c.ops->gs(c, l, 0);
     c.ops->gs(c, l, 1);
@@ -976,6 +982,7 @@ static void need_level(Ctx& c, int l, int lo = 1) {
 
 // ---------------------------------------------------------------- partitioned cycle (dist.h)
 static void enq_smooth_dist(Ctx& c, int l, int steps) {
+  if (c.dist->world == 1 && c.ops->smooth(c, l, steps)) return;  // no exchange between half-sweeps
   for (int s = 0; s < steps; ++s)
     for (int par = 0; par < 2; ++par) {
       c.ops->gs(c, l, par);
@@ -1495,6 +1502,8 @@ pmg_b200_ctx* pmg_b200_create(int dim, int N, const double* lo, const double* hi
     PMG_CUDA(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
     PMG_CUDA(cudaMallocHost(&c.h_out, 4 * sizeof(double)));
     PMG_CUDA(cudaMallocHost(&c.h_status, sizeof(int)));
+    c.gbar.alloc(2);
+    PMG_CUDA(cudaMemset(c.gbar.p, 0, 2 * sizeof(unsigned)));
     c.ops = make_ops(dim, N);
   } catch (const std::exception& e) {
     c.err = e.what();
@@ -1903,8 +1912,8 @@ int pmg_b200_time_op(pmg_b200_ctx* h, int op, int level, int reps, double* ms_av
     // in-cycle cost of a small op, launch gaps as inside the cycle graphs)
     const bool in_graph = op >= 100;
     if (in_graph) op -= 100;
-    require(reps >= 1 && op >= 0 && op <= 8 && !(in_graph && (op == 5 || op == 6)), "bad op/reps");
-    if (op <= 3 || op >= 7) need_level(c, level, op == 0 || op == 3 ? 1 : 2);
+    require(reps >= 1 && op >= 0 && op <= 10 && !(in_graph && (op == 5 || op == 6)), "bad op/reps");
+    if (op <= 3 || op >= 7) need_level(c, level, op == 0 || op == 3 || op == 9 ? 1 : 2);
     auto one = [&](int k) {
       switch (op) {
         case 0: c.ops->gs(c, level, k & 1); break;
@@ -1915,6 +1924,12 @@ int pmg_b200_time_op(pmg_b200_ctx* h, int op, int level, int reps, double* ms_av
         case 5: PMG_CUDA(cudaGraphLaunch(graph_for(c, CK_V).exec, c.stream)); break;
         case 7: c.ops->restrict_(c, level, c.lev[(size_t)level]->has_cf ? pmgdev::RM_RES : pmgdev::RM_FUSED); break;
         case 8: c.ops->fas(c, level - 1, true); break;
+        case 9: enq_smooth(c, level, 1); break;  // one smoothing step (both colours)
+        case 10:  // the V-cycle's prolongation (red cells left to the next half-sweep)
+          c.prolong_dead = 0;
+          c.ops->prolong(c, level, false);
+          c.prolong_dead = -1;
+          break;
 
         default: PMG_CUDA(cudaGraphLaunch(graph_for(c, CK_FMG_GUESS).exec, c.stream)); break;
       }

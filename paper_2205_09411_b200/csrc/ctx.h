@@ -263,6 +263,8 @@ struct LevelDev {
   DevBuf<double> cut_gbc[2];
   DevBuf<double> cut_coef[2];  // 16 per cut row: center, nb[6], bc*phi_b[6], bc mask
   int n_cut[2] = {0, 0};
+  DevBuf<int32_t> cut_off[2];  // nb + 1 per colour: cut rows of slot s (k_gs_coop)
+  int coop = -1;               // k_gs_coop smooths this level (-1: not yet decided)
   DevBuf<int32_t> fix_list[2];  // (slot, entry) pairs of special rows in lean interface blocks
   int n_fix[2] = {0, 0};
   bool has_cf = false;       // some block has a coarse-fine face
@@ -279,6 +281,8 @@ struct DistState;  // dist.h: the Morton-partitioned cycle
 struct Ops {
   virtual ~Ops() = default;
   virtual void gs(Ctx& c, int l, int parity) = 0;
+  // smooth(l, steps) as one cooperative launch; false: not eligible (use gs)
+  virtual bool smooth(Ctx& c, int l, int steps) = 0;
   virtual void residual(Ctx& c, int l) = 0;
   virtual void restrict_(Ctx& c, int l, int mode) = 0;
   virtual void fas(Ctx& c, int lc, bool fas) = 0;
@@ -378,6 +382,7 @@ struct Ctx {
   // kernels whose >48 KB dynamic shared memory / non-portable cluster
   // attribute is set: cudaFuncSetAttribute is per device, a context is one device
   std::unordered_set<const void*> attr_done;
+  DevBuf<unsigned> gbar;  // k_gs_coop grid barrier {count, generation}
   int cluster16 = -1;  // 16-CTA coarse-solve cluster schedulable (-1: not yet queried)
   std::unique_ptr<DistState> dist;  // pmg_b200_set_partition (nullptr: one context, whole mesh)
 

@@ -9,6 +9,7 @@
 #include "coarse_cluster.cuh"
 #include "stream.cuh"
 #include "brick.cuh"
+#include "coop.cuh"
 #include "small.cuh"
 #include "fields.cuh"
 
@@ -97,6 +98,47 @@ struct OpsImpl final : Ops {
       pdl_launch(k_gs<D, N>, grid_for((long long)L.nb * G::H), kThreads, 0, c.stream, L, Vc(c, l),
                                                                              c.phi_b.p, parity);
     check();
+  }
+  // smooth(l, steps) in one cooperative launch (coop.cuh): 3D N = 8 / 16
+  // levels whose blocks are all lean, one CTA per plan block, all co-resident
+  bool smooth(Ctx& c, int l, int steps) override {
+    if constexpr (D == 3 && (N == 8 || N == 16)) {
+      LevelDev& d = *c.lev[(size_t)l];
+      if (steps <= 0 || !kCoopEnabled) return false;
+      if (d.coop < 0) {
+        d.coop = 0;
+        if (!d.has_cf && d.n_slow == 0 && d.n_gs > 0 && d.n_gs <= kCoopMaxBlocks) {
+          constexpr size_t smem = (size_t)Coop3<N>::SMEM * sizeof(double);
+          set_smem_attr(c, (const void*)k_gs_coop<N>, smem);
+          int per_sm = 0;
+          PMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_coop<N>, kCoopThreads, smem));
+          d.coop = (long long)per_sm * c.sms >= d.n_gs ? 1 : 0;
+        }
+      }
+      if (!d.coop) return false;
+      const LevelView& L = V(c, l);
+      CutTabs cut;
+      for (int cc = 0; cc < 2; ++cc) {
+        cut.ent[cc] = (const int32_t*)d.cut_ent[cc].p;
+        cut.gbc[cc] = (const double*)d.cut_gbc[cc].p;
+        cut.coef[cc] = (const double*)d.cut_coef[cc].p;
+        cut.off[cc] = (const int32_t*)d.cut_off[cc].p;
+      }
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)d.n_gs);
+      cfg.blockDim = dim3(kCoopThreads);
+      cfg.dynamicSmemBytes = (size_t)Coop3<N>::SMEM * sizeof(double);
+      cfg.stream = c.stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeCooperative;
+      at[0].val.cooperative = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      PMG_CUDA(cudaLaunchKernelEx(&cfg, k_gs_coop<N>, L, (const int4*)d.gs_plan.p, d.n_gs, 2 * steps, cut,
+                                  c.gbar.p));
+      return true;
+    }
+    return false;
   }
   template <int ST, int MINB, int TH>
   void launch_gs_stream(Ctx& c, const LevelView& L, const LevelDev& d, int parity) {

@@ -265,7 +265,8 @@ __device__ __forceinline__ int gs_column_base(int t) {
 // skind page (int8, srow) instead of the row_of page staged at ORQ.
 template <int N, int TH, bool SKG = false>
 __device__ __forceinline__ void gs_stream_column(const LevelView& L, const double* __restrict__ st, int c, int kind,
-                                                 double h2, int slot, const double* gcur, int t, int srow = 0) {
+                                                 double h2, int slot, const double* gcur, int t, int srow = 0,
+                                                 double* sdst = nullptr) {
   using S = Stream3<N, TH>;
   constexpr int NI = N * N * N, HN = S::HN, FH = S::FH, PER = S::PER, KS = S::THR / S::FH;
   static_assert(PER * KS == N, "columns cover the block");
@@ -309,6 +310,10 @@ __device__ __forceinline__ void gs_stream_column(const LevelView& L, const doubl
     }
 #pragma unroll
     for (int q = 0; q < PER; ++q) dst[q * FH] = v[q];
+    if (sdst) {  // k_gs_coop keeps the block's colour-c half in shared memory
+#pragma unroll
+      for (int q = 0; q < PER; ++q) sdst[eb + q * FH] = v[q];
+    }
   } else {  // interface block (multigrid.hpp:665-684)
     const int32_t* rq = reinterpret_cast<const int32_t*>(st + S::ORQ);
     const int8_t* skg = L.skind + (size_t)srow * NI + (size_t)c * S::H;
@@ -328,7 +333,9 @@ __device__ __forceinline__ void gs_stream_column(const LevelView& L, const doubl
         sv += yp;
         sv += xc[q];
         sv += xc[q + 2];
-        dst[q * FH] = -sv * (-1.0 / 6.0);
+        const double v = -sv * (-1.0 / 6.0);
+        dst[q * FH] = v;
+        if (sdst) sdst[eb + q * FH] = v;
       }  // special rows: cut rows by k_gs_cut, inside rows keep their pin
     }
   }
@@ -1126,13 +1133,11 @@ static __global__ void __launch_bounds__(256) k_pin_list(double* __restrict__ ph
 // the row index and the six neighbour addresses (-1: Neumann ghost f1,
 // -2: Dirichlet ghost 2 bc - f1 with bc in gbc), so a thread needs two
 // dependent round trips.  One thread per cut row of the active colour.
+// gs_cut_row: one row of the table; returns the cell address, `out` its new value
 template <int D>
-__global__ void __launch_bounds__(128) k_gs_cut(LevelView L, const int32_t* __restrict__ ent,
-                                               const double* __restrict__ gbc, const double* __restrict__ coef,
-                                               int n) {
-  pdl_begin();
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= n) return;
+__device__ __forceinline__ int gs_cut_row(const LevelView& L, const int32_t* __restrict__ ent,
+                                          const double* __restrict__ gbc, const double* __restrict__ coef, int q,
+                                          double& out) {
   const int4 e0 = reinterpret_cast<const int4*>(ent)[2 * q];
   const int4 e1 = reinterpret_cast<const int4*>(ent)[2 * q + 1];
   const double2* cf2 = reinterpret_cast<const double2*>(coef) + (size_t)q * 8;
@@ -1157,7 +1162,20 @@ __global__ void __launch_bounds__(128) k_gs_cut(LevelView L, const int32_t* __re
     num -= cf[1 + d] * p[d];
     if ((bm >> d) & 1) num -= cf[7 + d];
   }
-  L.phi[a] = num / cf[0];
+  out = num / cf[0];
+  return a;
+}
+
+template <int D>
+__global__ void __launch_bounds__(128) k_gs_cut(LevelView L, const int32_t* __restrict__ ent,
+                                               const double* __restrict__ gbc, const double* __restrict__ coef,
+                                               int n) {
+  pdl_begin();
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  double v;
+  const int a = gs_cut_row<D>(L, ent, gbc, coef, q, v);
+  L.phi[a] = v;
 }
 
 // ------------------------------------------------------------------ prolongation
@@ -1213,24 +1231,33 @@ __device__ __forceinline__ PElem pr_elem(int q) {
   return E;
 }
 // parent-block cell of element E for octant `oct`: block (P or the
-// neighbour across the parent face, -1 physical) and colour-split address
+// neighbour across the parent face, -1 physical) and colour-split address.
+// Scalar coordinates (no runtime-indexed arrays: they went to local memory).
 template <int N>
-__device__ __forceinline__ size_t pr_addr(const PElem& E, int oct, int P, const int* pn, int& phys, int c3[3]) {
+__device__ __forceinline__ size_t pr_addr(const PElem& E, int oct, int P, const int* pn, int& phys, int& x0,
+                                          int& x1, int& x2) {
   constexpr int NI = N * N * N, HN = N / 2, H = NI / 2;
-  for (int d = 0; d < 3; ++d) c3[d] = ((oct >> d) & 1) * HN + E.t3[d];
+  x0 = (oct & 1) * HN + E.t3[0];
+  x1 = ((oct >> 1) & 1) * HN + E.t3[1];
+  x2 = ((oct >> 2) & 1) * HN + E.t3[2];
   int blk = P;
   phys = 0;
-  if (E.ax >= 0 && ((oct >> E.ax) & 1) == E.side) {  // leaves the parent block
-    const int nb = E.ax == 0 ? pn[0] : E.ax == 1 ? pn[1] : pn[2];
+  const int ax = E.ax;
+  if (ax >= 0 && ((oct >> ax) & 1) == E.side) {  // leaves the parent block
+    const int nb = ax == 0 ? pn[0] : ax == 1 ? pn[1] : pn[2];
+    int v;
     if (nb >= 0) {
       blk = nb;
-      c3[E.ax] = E.side ? 0 : N - 1;
+      v = E.side ? 0 : N - 1;
     } else {  // physical face: the parent's own boundary cell, made a ghost after the wait
-      c3[E.ax] = E.side ? N - 1 : 0;
+      v = E.side ? N - 1 : 0;
       phys = 1;
     }
+    x0 = ax == 0 ? v : x0;
+    x1 = ax == 1 ? v : x1;
+    x2 = ax == 2 ? v : x2;
   }
-  return (size_t)blk * NI + (size_t)(((c3[0] + c3[1] + c3[2]) & 1) * H) + (size_t)((c3[0] + N * (c3[1] + N * c3[2])) >> 1);
+  return (size_t)blk * NI + (size_t)(((x0 + x1 + x2) & 1) * H) + (size_t)((x0 + N * (x1 + N * x2)) >> 1);
 }
 
 template <int N, bool FULL, int NE>
@@ -1241,8 +1268,8 @@ __device__ __forceinline__ void pr_issue_async(const LevelView& Lp, const int4& 
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
     if (E[e].q < 0) continue;
-    int phys, c3[3];
-    const size_t ad = pr_addr<N>(E[e], a.z, a.y, pn, phys, c3);
+    int phys, x0, x1, x2;
+    const size_t ad = pr_addr<N>(E[e], a.z, a.y, pn, phys, x0, x1, x2);
     cp_async8(st + S::ORP + E[e].q, Lp.phi + ad);
     if (!FULL) cp_async8(st + S::ORO + E[e].q, Lp.old + ad);
   }
@@ -1278,9 +1305,17 @@ __global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(Level
   }
   __syncthreads();
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  auto issue = [&](int p, int s) {
+  // plan entry of the next block to issue, loaded one block ahead (its
+  // latency overlaps the current block instead of delaying the next issue)
+  int4 qa = make_int4(0, 0, 0, 0), qb = qa;
+  auto fetch = [&](int idx) {
+    int p = blockIdx.x + idx * G;
     if (rev) p = n - 1 - p;
-    const int4 a = __ldg(plan + 2 * p), b = __ldg(plan + 2 * p + 1);
+    qa = __ldg(plan + 2 * p);
+    qb = __ldg(plan + 2 * p + 1);
+  };
+  auto issue = [&](int s) {
+    const int4 a = qa, b = qb;
     double* st = sm + s * S::STAGE;
     if (t == 0) {
       meta[s][0] = a;
@@ -1299,17 +1334,27 @@ __global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(Level
     pr_issue_async<N, FULL, NE>(Lp, a, b, st, E);
   };
   for (int s = 0; s < S_STAGES; ++s) {
-    if (s < nmine) issue(blockIdx.x + s * G, s);
+    if (s < nmine) {
+      fetch(s);
+      issue(s);
+    }
     cp_async_commit();
   }
-  // fine-cell geometry of this thread: entries e = t + q*THR, both colours;
-  // j and the parity of k are fixed, the parent z row advances 2 planes per q
-  const int m = t % HN, j = (t / HN) % N, k0 = t / (HN * N);
-  constexpr int KS = S::THR / (HN * N);  // planes per q
-  static_assert(KS % 2 == 0, "the parent row advances by whole planes");
-  const int c0 = (j + k0) & 1;  // colour of i = 2m (x sign -1); i = 2m+1 has +1
-  const int ctr0 = (((k0 >> 1) + 1) * PE + (j >> 1) + 1) * PE + m + 1;
-  const int dyo = (j & 1) ? PE : -PE, dzo = (k0 & 1) ? PE * PE : -PE * PE;
+  if (S_STAGES < nmine) fetch(S_STAGES);
+  // fine-cell geometry of this thread: the column of PER consecutive fine
+  // planes k = kz*PER + q of entry column (m, j), both colours -- the cells
+  // (2m, j, k) and (2m+1, j, k), parent (m, j/2, k/2).  The column's parents
+  // span PER/2 planes, so the tile is read once per parent plane (centre, x-,
+  // x+, y) plus the plane below and above (the z neighbours): 2 + 2 PER loads
+  // for 2 PER fine cells.
+  constexpr int KZ = S::THR / (HN * N);  // columns along z
+  static_assert(KZ * S::PER == N && S::PER % 2 == 0, "columns of whole parent planes");
+  constexpr int PPL = S::PER / 2;  // parent planes per column
+  const int m = t % HN, j = (t / HN) % N, kz = t / (HN * N);
+  const int ebase = m + HN * j + HN * N * S::PER * kz;  // entry of q = 0
+  const int pz0 = PPL * kz;                            // first parent plane
+  const int ctr0 = ((pz0 + 1) * PE + (j >> 1) + 1) * PE + m + 1;
+  const int dyo = (j & 1) ? PE : -PE;
   for (int it = 0; it < nmine; ++it) {
     const int s = it % S_STAGES;
     double* st = sm + s * S::STAGE;
@@ -1331,10 +1376,10 @@ __global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(Level
         if ((ax == 0 ? pn[0] : ax == 1 ? pn[1] : pn[2]) < 0) {
           const int dir = 2 * ax + E[e].side;
           if (Lp.bctype[dir] != 1) {
-            int phys, c3[3];
-            (void)pr_addr<N>(E[e], oct, P, pn, phys, c3);
+            int phys, x0, x1, x2;
+            (void)pr_addr<N>(E[e], oct, P, pn, phys, x0, x1, x2);
             const int bo = Lp.bcoff[P * 6 + dir];
-            const int tj = ax == 0 ? c3[1] + N * c3[2] : ax == 1 ? c3[0] + N * c3[2] : c3[0] + N * c3[1];
+            const int tj = ax == 0 ? x1 + N * x2 : ax == 1 ? x0 + N * x2 : x0 + N * x1;
             const double bcv = bo < 0 ? 0.0 : Lp.bcval[bo + tj];
             vp = 2.0 * bcv - vp;
             vo = 2.0 * bcv - vo;
@@ -1347,19 +1392,28 @@ __global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(Level
     const double* Dt = st + S::ORP;
     double* __restrict__ dst = Lf.phi + (size_t)slot * NI;
     const int skipc = (!FULL && dead >= 0 && !b.w) ? dead : -1;
+    double zc[PPL + 2], xm[PPL], xp[PPL], yv[PPL];
+#pragma unroll
+    for (int u = 0; u < PPL + 2; ++u) zc[u] = Dt[ctr0 + (u - 1) * PE * PE];
+#pragma unroll
+    for (int u = 0; u < PPL; ++u) {
+      xm[u] = Dt[ctr0 + u * PE * PE - 1];
+      xp[u] = Dt[ctr0 + u * PE * PE + 1];
+      yv[u] = Dt[ctr0 + u * PE * PE + dyo];
+    }
 #pragma unroll
     for (int q = 0; q < S::PER; ++q) {
-      const int ctr = ctr0 + q * (KS / 2) * PE * PE;
-      const double dc = Dt[ctr], dxm = Dt[ctr - 1], dxp = Dt[ctr + 1];
-      const double dy = Dt[ctr + dyo];
-      const double dz = Dt[ctr + dzo];
-      const int e = t + q * S::THR;
+      const int u = q >> 1;  // parent plane of fine plane k = kz*PER + q (k parity = q parity)
+      const double dc = zc[u + 1], dy = yv[u];
+      const double dz = zc[(q & 1) ? u + 2 : u];
+      const int c0 = (j + q) & 1;  // colour of i = 2m (x neighbour -1); i = 2m+1 has +1
+      const int e = ebase + q * HN * N;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int c = h ? 1 - c0 : c0;
         if (c == skipc) continue;
         double v = (1.0 - 0.25 * 3) * dc;  // multigrid.hpp:742-752
-        v += 0.25 * (h ? dxp : dxm);
+        v += 0.25 * (h ? xp[u] : xm[u]);
         v += 0.25 * dy;
         v += 0.25 * dz;
         const size_t ad = (size_t)c * S::H + e;
@@ -1367,7 +1421,10 @@ __global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(Level
       }
     }
     __syncthreads();  // stage s consumed
-    if (it + S_STAGES < nmine) issue(blockIdx.x + (it + S_STAGES) * G, s);
+    if (it + S_STAGES < nmine) {
+      issue(s);
+      if (it + S_STAGES + 1 < nmine) fetch(it + S_STAGES + 1);
+    }
     cp_async_commit();
   }
 }

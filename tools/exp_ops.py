@@ -26,7 +26,8 @@ def child():
     print(f"  vcycle {us5:.1f} us  coarse {us(4, 1):.1f} us")
     for l in range(mesh.n_levels, 1, -1):
         print(f"  level {l} ({len(mesh.level_blocks(l))} blocks): gs {us(0, l):7.1f}  restrict {us(1, l):7.1f}"
-              f"  prolong {us(2, l):7.1f}  record {us(3, l):7.1f}  fas {us(8, l):7.1f} us")
+              f"  prolong {us(2, l):7.1f}  record {us(3, l):7.1f}  fas {us(8, l):7.1f}"
+              f"  smooth step {us(9, l):7.1f}  prolong(in-cycle) {us(10, l):7.1f} us")
 
 
 if __name__ == "__main__":
