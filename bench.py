@@ -100,8 +100,9 @@ class ClockSampler:
            ("sw_thermal_slowdown", "SwThermalSlowdown"), ("sw_power_cap", "SwPowerCap"),
            ("hw_power_brake_slowdown", "HwPowerBrakeSlowdown"))
 
-    def __init__(self, device):
+    def __init__(self, device, period_s=None):
         self.device = device
+        self.period_s = float(os.environ.get("PMG_CLOCK_POLL_S", "0.0005")) if period_s is None else period_s
         self.sm, self.max_mhz, self.reasons = [], None, set()
         self._stop = None
         self.proc = None
@@ -143,7 +144,7 @@ class ClockSampler:
                         self.reasons.update(n for n, bit in bits.items() if bit and (r & bit))
                     except Exception:
                         pass
-                    self._stop.wait(0.0005)
+                    self._stop.wait(self.period_s)
 
             self._th = threading.Thread(target=poll, daemon=True)
             self._th.start()

@@ -242,6 +242,45 @@ int pmg_b200_face_gradient(pmg_b200_ctx* ctx, int var, double* faces, double* ma
  * Ops 1-8 modify the solution exactly as the solver would. */
 int pmg_b200_time_op(pmg_b200_ctx* ctx, int op, int level, int reps, double* ms_avg);
 
+/* ---- the block tree on the device ------------------------------------------- */
+/* replaces: TreeMesh<Dim>'s topology and its refinement (mesh.hpp:66-82,
+ * 157-175, 198, 206-216, 253-320, 429-469) and refine_by_criterion
+ * (harness.hpp:295-321).  The tree lives in HBM; flags are evaluated, the 2:1
+ * balance closure is formed, new blocks are numbered and the level lists and
+ * neighbour tables are rebuilt by kernels (csrc/tree.cu).  Block ids, level
+ * lists and neighbour tables are identical to the reference's. */
+typedef struct pmg_b200_tree pmg_b200_tree;
+/* TreeMesh(lo, hi, block_size): the root block (mesh.hpp:66-82) */
+pmg_b200_tree* pmg_b200_tree_create(int dim, int N, const double* lo, const double* hi, int device);
+void pmg_b200_tree_destroy(pmg_b200_tree* tree);
+const char* pmg_b200_tree_last_error(pmg_b200_tree* tree);
+int pmg_b200_tree_n_blocks(pmg_b200_tree* tree);  /* TreeMesh::n_blocks (mesh.hpp:94) */
+int pmg_b200_tree_n_levels(pmg_b200_tree* tree);  /* TreeMesh::n_levels (mesh.hpp:100) */
+int pmg_b200_tree_adapt_passes(pmg_b200_tree* tree);
+/* TreeMesh::refine_all(times, max_level) (mesh.hpp:206-216); build_uniform = create + refine_all(levels-1) */
+int pmg_b200_tree_refine_all(pmg_b200_tree* tree, int times, int max_level);
+/* TreeMesh::adapt(flags, max_level), refine flags (mesh.hpp:157-175,198): flags[id] == 1
+ * (RefineFlag::refine) on a leaf refines it; the 2:1 balance forces more.
+ * flags may be a host or a device pointer (flags_on_device). */
+int pmg_b200_tree_adapt(pmg_b200_tree* tree, const uint8_t* flags, int n_flags, int flags_on_device,
+                        int max_level, int* n_refined);
+/* refine_by_criterion(mesh, max_level, want) (harness.hpp:295-321) with `want` evaluated on
+ * the device at every cell centre of every leaf below max_level:
+ *   kind 0  |f(x)| < p0 * b.dx, f the level set (lsf, n_lsf as in pmg_b200_build_stencils)
+ *   kind 1  b.dx > p0 * max(1, ||x - centre|| / p1)   (harness.hpp:351-355, sphere_refined)
+ *   kind 2  b.dx > p0 && ||x - centre|| < p1          (harness.hpp:413-418, two_electrodes) */
+int pmg_b200_tree_refine_by_criterion(pmg_b200_tree* tree, int kind, const pmg_lsf_t* lsf, int n_lsf,
+                                      double p0, double p1, const double* centre, int max_level);
+/* the Block table (mesh.hpp:37-55) in the layout of pmg_b200_set_mesh; NULL outputs are skipped */
+int pmg_b200_tree_get(pmg_b200_tree* tree, int32_t* level, int32_t* coords, double* origin, double* dx,
+                      int32_t* parent, int32_t* children, int32_t* nbr, int32_t* cnbr);
+/* TreeMesh::level_blocks(level) (mesh.hpp:102-105): ids sorted by coords */
+int pmg_b200_tree_level_blocks(pmg_b200_tree* tree, int level, int32_t* ids, int* n);
+/* device pointers of the table: level, coords, origin, dx, parent, children, nbr, cnbr */
+int pmg_b200_tree_device_arrays(pmg_b200_tree* tree, const void** out8);
+/* pmg_b200_set_mesh from the device tree */
+int pmg_b200_set_mesh_from_tree(pmg_b200_ctx* ctx, pmg_b200_tree* tree);
+
 #ifdef __cplusplus
 }
 #endif

@@ -9,7 +9,11 @@
 //   * pmg::b200::build_stencils == pmg::build_stencils, every field bit-exact;
 //   * the residual history of an FMG cycle + 3 V-cycles within
 //     |dr| <= 1e-6 r + 16 eps (2D/dx^2) max|phi|;
-//   * final PHI (with ghosts) within 1e-10 max|phi|  (§8c(ii)).
+//   * final PHI (with ghosts) within 1e-10 max|phi|  (§8c(ii));
+//   * the mesh of every case rebuilt on the device (pmg::b200::DeviceTree,
+//     include/pmg_b200/tree.hpp: refine_all / refine_by_criterion with
+//     build_case's criteria, harness.hpp:332-357, 384-419) is the reference's
+//     TreeMesh: ids, geometry, level lists and neighbour tables identical.
 // Prints one line per case and exits non-zero on the first mismatch.
 // Built by `make -C oracle dropin` into oracle/_ref/ (needs /root/reference);
 // run on the GPU box by tests/test_gpu_cpp_dropin.py.
@@ -22,6 +26,7 @@
 #include "pmg/harness.hpp"
 #include "pmg/io.hpp"
 #include "pmg_b200/solver.hpp"
+#include "pmg_b200/tree.hpp"
 
 using namespace pmg;
 
@@ -157,12 +162,36 @@ void diagnose(const std::string& name, TreeMesh<Dim> mesh, StencilSet<Dim> set) 
   std::printf("  op sequence agrees\n");
 }
 
+// build_case's mesh (harness.hpp:324-441) rebuilt on the device
+template <int Dim>
+bool tree_matches(const CaseConfig& cfg, const TreeMesh<Dim>& mesh, std::string& why) {
+  const std::string& id = cfg.case_id;
+  b200::DeviceTree<Dim> tree(mesh.domain_lo(), mesh.domain_hi(), cfg.block_size);
+  const double dx_min = mesh.level_dx(cfg.max_level);
+  if (id == "sphere_refined") {  // harness.hpp:348-356
+    tree.refine_radial(dx_min, cfg.radius, Vec<Dim>{}, cfg.max_level);
+  } else if (id == "two_electrodes") {  // harness.hpp:384-419
+    const int base = std::max(1, cfg.max_level - 2);
+    tree.refine_all(base - 1, base);
+    Vec<Dim> tip{};  // the reference sets the tip in 3D only (harness.hpp:398-403)
+    if constexpr (Dim == 3) tip = Vec<Dim>{{0.5, 0.5, 0.8}};
+    tree.refine_ball(dx_min, cfg.tip_refine_radius, tip, cfg.max_level);
+  } else {  // build_uniform (mesh.hpp:565-572)
+    tree.refine_all(cfg.max_level - 1, cfg.max_level);
+  }
+  return tree.same_as(mesh, &why);
+}
+
 template <int Dim>
 void run(CaseConfig cfg) {
   const std::string name = cfg.case_id + "/" + std::to_string(Dim) + "D/L" + std::to_string(cfg.max_level);
   if (cfg.w_min <= 0) cfg.w_min = 1.0 / (cfg.block_size * (1 << (cfg.max_level - 1)));
   detail::CaseSetup<Dim> setup = detail::build_case<Dim>(cfg);
   TreeMesh<Dim>& mesh = setup.mesh;
+  {
+    std::string why;
+    if (!tree_matches<Dim>(cfg, mesh, why)) return fail(name, "device tree differs: " + why);
+  }
   if (setup.rhs) {
     IVec<Dim> zero{}, nn;
     nn.fill(mesh.block_size());

@@ -111,6 +111,8 @@ def load(path):
     lib.oc_last_error.argtypes = [vp]
     lib.oc_build_uniform.argtypes = [vp, C.c_int]
     lib.oc_refine_band.argtypes = [vp, C.c_void_p, C.c_int, C.c_double, C.c_int]
+    lib.oc_refine_crit.argtypes = [vp, C.c_int, C.c_double, C.c_double, _f64p, C.c_int]
+    lib.oc_adapt.argtypes = [vp, C.c_void_p, C.c_int, C.c_int]
     lib.oc_n_blocks.argtypes = [vp]
     lib.oc_n_levels.argtypes = [vp]
     lib.oc_get_topology.argtypes = [vp, _i32p, _i32p, _f64p, _f64p, _i32p, _i32p, _i32p, _i32p]
@@ -181,6 +183,16 @@ class Oracle:
         arr = lsf_array(lsf_specs)
         self._check(self.lib.oc_refine_band(self.h, C.cast(arr, C.c_void_p), len(lsf_specs),
                                             band, max_level))
+
+    def refine_crit(self, kind, p0, p1, centre, max_level):
+        c = np.zeros(3)
+        c[:len(centre)] = centre
+        self._check(self.lib.oc_refine_crit(self.h, kind, p0, p1, c, max_level))
+
+    def adapt_refine(self, ids, max_level):
+        flags = np.zeros(self.n_blocks, np.uint8)
+        flags[np.asarray(list(ids), np.int64)] = 1
+        self._check(self.lib.oc_adapt(self.h, flags.ctypes.data_as(C.c_void_p), flags.size, max_level))
 
     @property
     def n_blocks(self):

@@ -40,6 +40,11 @@ const char* oc_last_error(oc_ctx* h);
  * with want(b, x) = |lsf(x)| < band * b.dx) */
 int oc_build_uniform(oc_ctx* h, int levels);
 int oc_refine_band(oc_ctx* h, const pmg_lsf_t* lsf, int n_lsf, double band, int max_level);
+/* refine_by_criterion with build_case's criteria: kind 1 b.dx > p0 max(1, |x - c| / p1)
+ * (harness.hpp:351-355), kind 2 b.dx > p0 && |x - c| < p1 (harness.hpp:413-418) */
+int oc_refine_crit(oc_ctx* h, int kind, double p0, double p1, const double* centre, int max_level);
+/* TreeMesh::adapt with refine flags (mesh.hpp:157-175,198): flags[id] == 1 refines leaf id */
+int oc_adapt(oc_ctx* h, const uint8_t* flags, int n, int max_level);
 int oc_n_blocks(oc_ctx* h);
 int oc_n_levels(oc_ctx* h);
 /* per block: level[nb], coords[nb*3], origin[nb*3], dx[nb], parent[nb],

@@ -1241,6 +1241,46 @@ int oc_refine_band(oc_ctx* h, const pmg_lsf_t* l, int n, double band, int max_le
     return 0;
   });
 }
+int oc_adapt(oc_ctx* h, const uint8_t* flags, int n, int max_level) {
+  return guard(h, [&](Ctx& c) {  // TreeMesh::adapt, refine flags (mesh.hpp:157-175,198)
+    std::vector<int> ids;
+    for (int id = 0; id < c.nblocks() && id < n; ++id)
+      if (flags[id] == 1) ids.push_back(id);
+    adapt_refine(c, ids, max_level);
+    c.st.assign((size_t)c.nblocks(), BlockSt{});
+    c.have_solver = false;
+    return 0;
+  });
+}
+int oc_refine_crit(oc_ctx* h, int kind, double p0, double p1, const double* centre, int max_level) {
+  return guard(h, [&](Ctx& c) {  // harness.hpp:295-321 with the criteria of :351-355 (1) and :413-418 (2)
+    for (;;) {
+      std::vector<int> flags;
+      for (int lv = 1; lv <= c.nlevels(); ++lv)
+        for (int id : c.levels[(size_t)lv]) {
+          if (!leaf(c, id) || c.lvl[(size_t)id] >= max_level) continue;
+          bool f = false;
+          const double bdx = c.bdx[(size_t)id];
+          c.each([&](int i, int j, int k, int) {
+            if (f) return;
+            double x[3];
+            c.center(id, i, j, k, x);
+            double ss = 0;
+            for (int a = 0; a < c.D; ++a) ss += (x[a] - centre[a]) * (x[a] - centre[a]);
+            const double r = std::sqrt(ss);
+            const bool w = kind == 1 ? bdx > p0 * std::max(1.0, r / p1) : (bdx > p0 && r < p1);
+            if (w) f = true;
+          });
+          if (f) flags.push_back(id);
+        }
+      if (flags.empty()) break;
+      adapt_refine(c, flags, max_level);
+    }
+    c.st.assign((size_t)c.nblocks(), BlockSt{});
+    c.have_solver = false;
+    return 0;
+  });
+}
 int oc_n_blocks(oc_ctx* h) { return h ? h->c.nblocks() : -1; }
 int oc_n_levels(oc_ctx* h) { return h ? h->c.nlevels() : -1; }
 int oc_get_topology(oc_ctx* h, int32_t* level, int32_t* coords, double* origin, double* dx,

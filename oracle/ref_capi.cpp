@@ -9,6 +9,8 @@
 // Forwarding map (reference file:line):
 //   oc_build_uniform       -> pmg::build_uniform            mesh.hpp:565-572
 //   oc_refine_band         -> pmg::detail::refine_by_criterion harness.hpp:295-321
+//   oc_refine_crit         -> the same with build_case's criteria  harness.hpp:351-355, 413-418
+//   oc_adapt               -> TreeMesh::adapt                mesh.hpp:157-204
 //   oc_fill_ghosts         -> TreeMesh::fill_ghosts          mesh.hpp:217-221
 //   oc_build_stencils      -> pmg::build_stencils            stencil.hpp:207-222
 //   oc_apply_pins          -> pmg::apply_pins                stencil.hpp:225-237
@@ -34,6 +36,8 @@ struct Base {
   std::string err;
   virtual int build_uniform(int levels) = 0;
   virtual int refine_band(const pmg_lsf_t* l, int n, double band, int max_level) = 0;
+  virtual int refine_crit(int kind, double p0, double p1, const double* centre, int max_level) = 0;
+  virtual int adapt(const uint8_t* flags, int n, int max_level) = 0;
   virtual int n_blocks() = 0;
   virtual int n_levels() = 0;
   virtual int topology(int32_t*, int32_t*, double*, double*, int32_t*, int32_t*, int32_t*,
@@ -126,6 +130,28 @@ struct Impl final : Base {
                                    [&](const Block<D>& b, const Vec<D>& x) {
                                      return std::abs(lsf_eval(s, x)) < band * b.dx;
                                    });
+    solver.reset();
+    return 0;
+  }
+  int refine_crit(int kind, double p0, double p1, const double* centre, int max_level) override {
+    Vec<D> c;
+    for (int k = 0; k < D; ++k) c[k] = centre[k];
+    if (kind == 1)
+      detail::refine_by_criterion<D>(mesh, max_level, [=](const Block<D>& b, const Vec<D>& x) {
+        return b.dx > p0 * std::max(1.0, norm(x - c) / p1);
+      });
+    else
+      detail::refine_by_criterion<D>(mesh, max_level, [=](const Block<D>& b, const Vec<D>& x) {
+        return b.dx > p0 && norm(x - c) < p1;
+      });
+    solver.reset();
+    return 0;
+  }
+  int adapt(const uint8_t* flags, int n, int max_level) override {
+    std::vector<RefineFlag> f(static_cast<size_t>(mesh.n_blocks()), RefineFlag::keep);
+    for (int id = 0; id < mesh.n_blocks() && id < n; ++id)
+      if (flags[id] == 1) f[static_cast<size_t>(id)] = RefineFlag::refine;
+    mesh.adapt(f, max_level);
     solver.reset();
     return 0;
   }
@@ -443,6 +469,12 @@ int oc_build_uniform(oc_ctx* h, int levels) {
 }
 int oc_refine_band(oc_ctx* h, const pmg_lsf_t* l, int n, double band, int max_level) {
   return guard(h, [&](Base& b) { return b.refine_band(l, n, band, max_level); });
+}
+int oc_refine_crit(oc_ctx* h, int kind, double p0, double p1, const double* centre, int max_level) {
+  return guard(h, [&](Base& b) { return b.refine_crit(kind, p0, p1, centre, max_level); });
+}
+int oc_adapt(oc_ctx* h, const uint8_t* flags, int n, int max_level) {
+  return guard(h, [&](Base& b) { return b.adapt(flags, n, max_level); });
 }
 int oc_n_blocks(oc_ctx* h) { return h && h->impl ? h->impl->n_blocks() : -1; }
 int oc_n_levels(oc_ctx* h) { return h && h->impl ? h->impl->n_levels() : -1; }

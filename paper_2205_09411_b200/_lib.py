@@ -74,6 +74,11 @@ EXPORTS = [
     "pmg_b200_set_partition", "pmg_b200_nccl_unique_id", "pmg_b200_dist_init_nccl",
     "pmg_b200_dist_local_group", "pmg_b200_dist_v_cycle", "pmg_b200_dist_v_cycle_async",
     "pmg_b200_dist_info", "pmg_b200_field_bytes", "pmg_b200_host_buffer",
+    "pmg_b200_tree_create", "pmg_b200_tree_destroy", "pmg_b200_tree_last_error",
+    "pmg_b200_tree_n_blocks", "pmg_b200_tree_n_levels", "pmg_b200_tree_adapt_passes",
+    "pmg_b200_tree_refine_all", "pmg_b200_tree_adapt", "pmg_b200_tree_refine_by_criterion",
+    "pmg_b200_tree_get", "pmg_b200_tree_level_blocks", "pmg_b200_tree_device_arrays",
+    "pmg_b200_set_mesh_from_tree",
 ]
 
 _lib = None
@@ -151,6 +156,22 @@ def load():
     lib.pmg_b200_field_bytes.argtypes = [vp, C.POINTER(C.c_double)]
     lib.pmg_b200_host_buffer.argtypes = [vp, C.c_size_t]
     lib.pmg_b200_host_buffer.restype = C.c_void_p
+    # the block tree on the device (csrc/tree.cu)
+    lib.pmg_b200_tree_create.restype = vp
+    lib.pmg_b200_tree_create.argtypes = [C.c_int, C.c_int, f64p, f64p, C.c_int]
+    lib.pmg_b200_tree_destroy.argtypes = [vp]
+    lib.pmg_b200_tree_last_error.restype = C.c_char_p
+    lib.pmg_b200_tree_last_error.argtypes = [vp]
+    for n in ("pmg_b200_tree_n_blocks", "pmg_b200_tree_n_levels", "pmg_b200_tree_adapt_passes"):
+        getattr(lib, n).argtypes = [vp]
+    lib.pmg_b200_tree_refine_all.argtypes = [vp, C.c_int, C.c_int]
+    lib.pmg_b200_tree_adapt.argtypes = [vp, C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]
+    lib.pmg_b200_tree_refine_by_criterion.argtypes = [vp, C.c_int, C.c_void_p, C.c_int, C.c_double,
+                                                      C.c_double, C.c_void_p, C.c_int]
+    lib.pmg_b200_tree_get.argtypes = [vp] + [C.c_void_p] * 8
+    lib.pmg_b200_tree_level_blocks.argtypes = [vp, C.c_int, C.c_void_p, C.POINTER(C.c_int)]
+    lib.pmg_b200_tree_device_arrays.argtypes = [vp, C.POINTER(C.c_void_p)]
+    lib.pmg_b200_set_mesh_from_tree.argtypes = [vp, vp]
     _lib = lib
     return lib
 

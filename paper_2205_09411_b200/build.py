@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libpmg_b200.so")
 
-SOURCES = ["capi.cu", "ops.cu"] + [f"ops_{d}_{n}.cu" for d in (2, 3) for n in (4, 8, 16, 32)]
+SOURCES = ["capi.cu", "ops.cu", "tree.cu"] + [f"ops_{d}_{n}.cu" for d in (2, 3) for n in (4, 8, 16, 32)]
 HEADERS = ["ctx.h", "kernels.cuh", "cells.cuh", "pmg_dev.cuh", "stencil_build.cuh", "ops_impl.cuh", "tiles.cuh", "coarse.cuh", "tile_kernels.cuh", "coarse_cluster.cuh", "stream.cuh", "small.cuh", "fields.cuh", "brick.cuh", "dist.h", "coop.cuh"]
 
 NVCC_FLAGS = [

@@ -38,9 +38,6 @@ __device__ __forceinline__ double2 ldg2(const double* p) { return *reinterpret_c
 __device__ __forceinline__ void stg2(double* p, double a, double b) {
   *reinterpret_cast<double2*>(p) = make_double2(a, b);
 }
-__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 
 // Residuals of one quarter-row (4 cells x 0..3 at row j, plane k) from the
 // stage: own values f[4], L(phi) ap[4] and r[4] = g - L(phi).

@@ -32,7 +32,6 @@ Ctx::~Ctx() {
   g_measure.reset();
   if (h_out) cudaFreeHost(h_out);
   if (h_buf) cudaFreeHost(h_buf);
-  if (h_status) cudaFreeHost(h_status);
   if (stream) cudaStreamDestroy(stream);
   if (side) cudaStreamDestroy(side);
   if (ev_fork) cudaEventDestroy(ev_fork);
@@ -874,25 +873,37 @@ static void enq_v_span(Ctx& c, int top) {
 static void enq_reset_records(Ctx& c) {
   PMG_CUDA(cudaMemsetAsync(c.rec.p, 0, c.rec.n * sizeof(pmgdev::Rec), c.stream));
 }
+// stats, diag and status to the host in one copy (Ctx::outbuf)
+static void enq_copy_out(Ctx& c) {
+  PMG_CUDA(cudaMemcpyAsync(c.h_out, c.outbuf.p, 5 * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+}
 static void enq_finish(Ctx& c) {
+  if (c.finished) {  // the last record wrote the stats and the host copy (ops record)
+    c.finished = false;
+    return;
+  }
   pdl_launch(pmgdev::k_combine, 1, 32, 0, c.stream, c.rec.p, c.mesh.L, c.stats.p);
   PMG_CUDA(cudaGetLastError());
-  PMG_CUDA(cudaMemcpyAsync(c.h_out, c.stats.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
-  PMG_CUDA(cudaMemcpyAsync(c.h_out + 2, c.diag.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
-  PMG_CUDA(cudaMemcpyAsync(c.h_status, c.status.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  enq_copy_out(c);
 }
 static void enq_clear_status(Ctx& c) {
   PMG_CUDA(cudaMemsetAsync(c.status.p, 0, sizeof(int), c.stream));
+}
+// status and the level records, adjacent in Ctx::outbuf: one memset
+static void enq_clear_cycle(Ctx& c) {
+  PMG_CUDA(cudaMemsetAsync(c.status.p, 0, sizeof(double) + c.rec.n * sizeof(pmgdev::Rec), c.stream));
 }
 
 enum CycleKind { CK_V = 0, CK_FMG_NOGUESS = 1, CK_FMG_GUESS = 2, CK_MEASURE = 3 };
 
 static void enq_cycle(Ctx& c, int kind) {
   const int L = c.mesh.L;
-  enq_clear_status(c);
-  enq_reset_records(c);
+  enq_clear_cycle(c);
+  c.finished = false;
   if (kind == CK_V) {
+    c.finish_level = L;
     enq_v_span(c, L);
+    c.finish_level = 0;
   } else if (kind == CK_MEASURE) {
     for (int l = 1; l <= L; ++l) c.ops->record(c, l);
   } else {
@@ -904,7 +915,9 @@ static void enq_cycle(Ctx& c, int kind) {
     enq_coarse(c);
     for (int l = 2; l <= L; ++l) {
       c.ops->prolong(c, l, !guess);
+      c.finish_level = l == L ? L : 0;
       enq_v_span(c, l);
+      c.finish_level = 0;
     }
   }
   enq_finish(c);
@@ -994,8 +1007,7 @@ static void enq_smooth_dist(Ctx& c, int l, int steps) {
 static void enq_dist_cycle(Ctx& c) {
   DistState& ds = *c.dist;
   const int L = c.mesh.L, g = ds.split;
-  enq_clear_status(c);
-  enq_reset_records(c);
+  enq_clear_cycle(c);
   // halo phi as the owners hold it now (after init, an upload or the last cycle)
   for (int l = g; l <= L; ++l) dist_xchg(c, PMG_VAR_PHI, l, 2);
   for (int l = L; l >= std::max(g, 2); --l) {
@@ -1030,9 +1042,7 @@ static void enq_dist_cycle(Ctx& c) {
     c.ops->record(c, l);
   }
   dist_records(c);
-  PMG_CUDA(cudaMemcpyAsync(c.h_out, c.stats.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
-  PMG_CUDA(cudaMemcpyAsync(c.h_out + 2, c.diag.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
-  PMG_CUDA(cudaMemcpyAsync(c.h_status, c.status.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  enq_copy_out(c);
 }
 // one partitioned V-cycle: a CUDA graph (no transport, or NCCL -- pack kernels
 // and NCCL calls captured together), eager with the in-process transport
@@ -1276,12 +1286,18 @@ static void set_mesh(Ctx& c, int nb, const int32_t* level, const int32_t* coords
   int maxnb = 0;
   for (int l = 1; l <= m.L; ++l) maxnb = std::max(maxnb, c.lev[(size_t)l]->nb);
   c.partial.alloc((size_t)maxnb + 8192);  // + per-CTA partials of k_record_cut
-  c.rec.alloc(pmgdev::kMaxLevels + 1);
+  {
+    static_assert(sizeof(pmgdev::Rec) == 3 * sizeof(double), "records follow the five output doubles");
+    const size_t nrec = pmgdev::kMaxLevels + 1;
+    c.outbuf.alloc(5 + 3 * nrec);
+    PMG_CUDA(cudaMemsetAsync(c.outbuf.p, 0, c.outbuf.n * sizeof(double), c.stream));
+    c.stats.p = c.outbuf.p, c.stats.n = 2;
+    c.diag.p = c.outbuf.p + 2, c.diag.n = 2;
+    c.status.p = reinterpret_cast<int*>(c.outbuf.p + 4), c.status.n = 1;
+    c.rec.p = reinterpret_cast<pmgdev::Rec*>(c.outbuf.p + 5), c.rec.n = nrec;
+  }
   c.counter.alloc(1);
   PMG_CUDA(cudaMemsetAsync(c.counter.p, 0, sizeof(unsigned), c.stream));
-  c.stats.alloc(2);
-  c.status.alloc(1);
-  c.diag.alloc(2);
   c.have_mesh = true;
   c.solver = false;
   default_stencils(c);
@@ -1500,8 +1516,13 @@ pmg_b200_ctx* pmg_b200_create(int dim, int N, const double* lo, const double* hi
     PMG_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
     PMG_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
     PMG_CUDA(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming));
-    PMG_CUDA(cudaMallocHost(&c.h_out, 4 * sizeof(double)));
-    PMG_CUDA(cudaMallocHost(&c.h_status, sizeof(int)));
+    PMG_CUDA(cudaHostAlloc(&c.h_out, 5 * sizeof(double), cudaHostAllocMapped));
+    std::memset(c.h_out, 0, 5 * sizeof(double));
+    if (cudaHostGetDevicePointer(&c.h_out_dev, c.h_out, 0) != cudaSuccess) {
+      c.h_out_dev = nullptr;  // no mapped access: the cycles end with a copy node
+      cudaGetLastError();
+    }
+    c.h_status = reinterpret_cast<int*>(c.h_out + 4);
     c.gbar.alloc(2);
     PMG_CUDA(cudaMemset(c.gbar.p, 0, 2 * sizeof(unsigned)));
     c.ops = make_ops(dim, N);
@@ -1733,8 +1754,7 @@ int pmg_b200_coarse_solve(pmg_b200_ctx* h) {
     require(c.solver, "solver not created", PMG_ERR_STATE);
     enq_clear_status(c);
     enq_coarse(c);
-    PMG_CUDA(cudaMemcpyAsync(c.h_out + 2, c.diag.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
-    PMG_CUDA(cudaMemcpyAsync(c.h_status, c.status.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    enq_copy_out(c);
     cycle_result(c, nullptr);
   });
 }
@@ -1927,10 +1947,9 @@ int pmg_b200_time_op(pmg_b200_ctx* h, int op, int level, int reps, double* ms_av
         case 9: enq_smooth(c, level, 1); break;  // one smoothing step (both colours)
         case 10:  // the V-cycle's prolongation (red cells left to the next half-sweep)
           c.prolong_dead = 0;
-          c.ops->prolong(c, level, false);
-          c.prolong_dead = -1;
+                c.ops->prolong(c, level, false);
+                c.prolong_dead = -1;
           break;
-
         default: PMG_CUDA(cudaGraphLaunch(graph_for(c, CK_FMG_GUESS).exec, c.stream)); break;
       }
     };

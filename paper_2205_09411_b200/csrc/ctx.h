@@ -345,13 +345,21 @@ struct Ctx {
   HostCoarse coarse;
   std::vector<std::unique_ptr<LevelDev>> lev;  // index 0 unused
   DevBuf<double> phi_b;
-  DevBuf<pmgdev::Rec> rec, partial;
+  // outbuf: stats[2], diag[2], status (int32 in one double), then the level
+  // records -- one D2H copy and one memset per cycle instead of three and two
+  DevBuf<double> outbuf;
+  template <typename T>
+  struct View {
+    T* p = nullptr;
+    size_t n = 0;
+  };
+  View<pmgdev::Rec> rec;
+  DevBuf<pmgdev::Rec> partial;
   DevBuf<int2> leaf_tab;            // (level, slot) of every leaf in dump order (io.hpp:17-21)
   DevBuf<double> ff_faces, ff_mag;  // face_gradient scratch
   DevBuf<unsigned int> counter;
-  DevBuf<double> stats;
-  DevBuf<int> status;
-  DevBuf<double> diag;
+  View<double> stats, diag;
+  View<int> status;
   DevBuf<double> staging;
   // coarse system on device
   DevBuf<int32_t> c_rp, c_ci, c_uaddr;
@@ -364,10 +372,16 @@ struct Ctx {
   DevBuf<int8_t> cf_ob_obj;
   double cf_w = 0;
 
-  double* h_out = nullptr;  // pinned: stats[2], diag[2]
+  double* h_out = nullptr;  // pinned image of outbuf's first 5 doubles: stats[2], diag[2], status
   void* h_buf = nullptr;    // pinned transfer buffer (pmg_b200_host_buffer)
   size_t h_buf_bytes = 0;
-  int* h_status = nullptr;  // pinned
+  int* h_status = nullptr;  // = (int*)(h_out + 4)
+  double* h_out_dev = nullptr;  // device address of h_out (mapped pinned memory)
+  // the cycle's last record (level finish_level) writes the CycleStats and
+  // the host copy itself (k_record_fold's FinishArgs); `finished` tells
+  // enq_finish that it did
+  int finish_level = 0;
+  bool finished = false;
 
   pmg_mg_cfg_t cfg{2, 2, 1e-6, 2000, 1};
   bool solver = false;

@@ -396,7 +396,8 @@ struct OpsImpl final : Ops {
         const int gr = (int)grid_for((long long)L.nb * G::NI, 256);
         pdl_launch(k_record_tab<D, N>, gr, 256, 0, c.stream, L, c.phi_b.p, (const int4*)d.tab.p,
                    (const double*)d.tgbc.p, c.partial.p);
-        pdl_launch(k_record_fold, 1, 256, 0, c.stream, (const Rec*)c.partial.p, gr, c.rec.p + L.level);
+        pdl_launch(k_record_fold, 1, 256, 0, c.stream, (const Rec*)c.partial.p, gr, c.rec.p + L.level,
+                   FinishArgs{});
         check();
         return;
       }
@@ -428,8 +429,14 @@ struct OpsImpl final : Ops {
           PMG_CUDA(cudaEventRecord(c.ev_join, c.side));
           PMG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
         }
+        // the cycle's last record also writes the CycleStats and the host copy
+        FinishArgs fin{};
+        if (c.finish_level == l && c.h_out_dev) {
+          fin = FinishArgs{c.rec.p, c.mesh.L, l, c.outbuf.p, c.h_out_dev};
+          c.finished = true;
+        }
         pdl_launch(k_record_fold, 1, 256, 0, c.stream, (const Rec*)c.partial.p,
-                   grid + gcut + (d.n_slow > 0 ? L.nb : 0), c.rec.p + L.level);
+                   grid + gcut + (d.n_slow > 0 ? L.nb : 0), c.rec.p + L.level, fin);
         check();
         return;
       }

@@ -50,6 +50,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// bulk prefetch into L2 (bytes % 16 == 0)
+__device__ __forceinline__ void l2_prefetch(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
@@ -406,7 +411,7 @@ __global__ void __launch_bounds__(Stream3<N, TH>::THR, MINB) k_gs_stream(LevelVi
     __syncthreads();
     const int slot = meta[s][0], flags = meta[s][1];
     const int kind = flags & 0xff, pmask = (flags >> 8) & 63;
-    if (it + 1 < nmine) {  // this thread's g of the next block, in flight during this one
+    if (S_STAGES > 1 && it + 1 < nmine) {  // this thread's g of the next block, in flight during this one
       const double* gsrc = L.rhs + (size_t)meta[(it + 1) % S_STAGES][0] * NI + (size_t)c * S::H + gbase;
 #pragma unroll
       for (int q = 0; q < S::PER; ++q) gnext[q] = gsrc[q * gstep];
@@ -424,8 +429,10 @@ __global__ void __launch_bounds__(Stream3<N, TH>::THR, MINB) k_gs_stream(LevelVi
       gs_issue_async<N, TH>(L, pf, c, st, t);
     }
     cp_async_commit();
+    if (S_STAGES > 1) {
 #pragma unroll
-    for (int q = 0; q < S::PER; ++q) gcur[q] = gnext[q];
+      for (int q = 0; q < S::PER; ++q) gcur[q] = gnext[q];
+    }
   }
 }
 
@@ -1472,7 +1479,19 @@ __global__ void __launch_bounds__(256) k_record_cut(LevelView L, const double* _
 }
 
 // rec = fold of partial[0 .. n) in index order (combine_records' per-level record)
-static __global__ void __launch_bounds__(256) k_record_fold(const Rec* __restrict__ partial, int n, Rec* out) {
+// fin != nullptr: this is the cycle's last record -- thread 0 also forms the
+// CycleStats over all levels (k_combine's loop, multigrid.hpp:564-575, with
+// this level's totals in place) and writes stats, diag and status to the
+// mapped host buffer, so the cycle graph ends here (no combine kernel, no
+// device-to-host copy node).
+struct FinishArgs {
+  const Rec* rec;     // all level records, [0 .. nlev]
+  int nlev, level;    // level being folded
+  double* outbuf;     // device: stats[2], diag[2], status
+  double* host_out;   // mapped pinned image of outbuf
+};
+static __global__ void __launch_bounds__(256) k_record_fold(const Rec* __restrict__ partial, int n, Rec* out,
+                                                            FinishArgs fin) {
   pdl_begin();
   __shared__ double red[72];
   double mx = 0.0, ss = 0.0, cc = 0.0;
@@ -1488,6 +1507,24 @@ static __global__ void __launch_bounds__(256) k_record_fold(const Rec* __restric
     out->max = mx;
     out->sumsq = ss;
     out->count = (long long)cc;
+    if (fin.host_out) {
+      double m = 0, s = 0;
+      long long c = 0;
+      for (int l = 0; l <= fin.nlev; ++l) {
+        const bool me = l == fin.level;
+        m = fmax(m, me ? mx : fin.rec[l].max);
+        s += me ? ss : fin.rec[l].sumsq;
+        c += me ? (long long)cc : fin.rec[l].count;
+      }
+      const double l2 = c > 0 ? sqrt(s / (double)c) : 0.0;
+      fin.outbuf[0] = m;
+      fin.outbuf[1] = l2;
+      fin.host_out[0] = m;
+      fin.host_out[1] = l2;
+      fin.host_out[2] = fin.outbuf[2];
+      fin.host_out[3] = fin.outbuf[3];
+      fin.host_out[4] = fin.outbuf[4];
+    }
   }
 }
 

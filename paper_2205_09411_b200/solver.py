@@ -123,8 +123,13 @@ class DeviceMesh:
     """A TreeMesh bound to one GPU context: topology, face BCs and every cell
     field (VAR_PHI/RHS/RES/OLD) in HBM."""
 
-    def __init__(self, mesh: TreeMesh, device: int = 0):
+    def __init__(self, mesh: TreeMesh, device: int = 0, tree=None):
+        """mesh: the host TreeMesh mirror.  tree: a DeviceTree (tree.py) -- the
+        topology then comes from the device tables (pmg_b200_set_mesh_from_tree)
+        and `mesh` may be None (a mirror is filled from the same tables)."""
         self.lib = _lib.load()
+        if tree is not None and mesh is None:
+            mesh = tree.to_host_mesh()
         self.mesh = mesh
         self.dim, self.N = mesh.dim, mesh.N
         self.NI = self.N ** self.dim
@@ -136,10 +141,13 @@ class DeviceMesh:
         if not self.h:
             raise MemoryError("pmg_b200_create failed")
         self._check_err()
-        t = mesh.topology_arrays()
-        self._check(self.lib.pmg_b200_set_mesh(self.h, mesh.n_blocks, t["level"], t["coords"],
-                                               t["origin"], t["dx"], t["parent"],
-                                               t["children"], t["nbr"], t["cnbr"]))
+        if tree is not None:
+            self._check(self.lib.pmg_b200_set_mesh_from_tree(self.h, tree.h))
+        else:
+            t = mesh.topology_arrays()
+            self._check(self.lib.pmg_b200_set_mesh(self.h, mesh.n_blocks, t["level"], t["coords"],
+                                                   t["origin"], t["dx"], t["parent"],
+                                                   t["children"], t["nbr"], t["cnbr"]))
         self.sync_face_bc()
 
     def __del__(self):
