@@ -191,6 +191,49 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.sm)}
 
 
+def time_plan_cycles(torch, dev, sol, mesh, case, stream, steps, barrier=None):
+    """Device time of `steps` V-cycles OF THE CONFIG'S PLAN (e.g. config 2: the
+    8 V-cycles that follow the FMG cycle): passes of at most case.v_cycles
+    back-to-back cycles, each pass right after the plan's start -- phi = 0 with
+    the pins applied, then the FMG cycle where the plan has one -- which is
+    rebuilt outside the timed region.  CUDA events bracket every pass on the
+    launching stream (device idle and synchronised on both sides); the pass
+    times are summed.  Cycles beyond the plan run on a converged solution,
+    where the coarse BiCGStab solves for round-off noise and needs a third more
+    iterations (profiles/r02_cycle_by_cycle.txt): they are reported separately
+    (`converged_state`), not as the step time.
+    Returns (total ms, last CycleStats, max residual after a full pass or None)."""
+    import numpy as np
+    from paper_2205_09411_b200.mesh import VAR_PHI
+    from paper_2205_09411_b200.solver import LAYOUT_INTERIOR
+    zeros = np.zeros((mesh.n_blocks, case.N ** case.dim))
+    L = mesh.n_levels
+    total, done, stats, full_pass_resid = 0.0, 0, None, None
+    while done < steps:
+        n = min(case.v_cycles, steps - done)
+        dev.set_field(VAR_PHI, zeros, layout=LAYOUT_INTERIOR)
+        for l in range(1, L + 1):
+            sol.apply_pins(l)
+        sol.set_have_guess(False)
+        torch.cuda.synchronize()
+        if barrier:
+            barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if case.fmg_first:
+            sol.fmg_cycle_async()  # untimed: e0 is recorded behind it on the stream
+        e0.record(stream)
+        for _ in range(n):
+            sol.v_cycle_async()
+        e1.record(stream)
+        stats = sol.cycle_result()
+        torch.cuda.synchronize()
+        total += e0.elapsed_time(e1)
+        if n == case.v_cycles:
+            full_pass_resid = stats.max_resid
+        done += n
+    return total, stats, full_pass_resid
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -435,24 +478,29 @@ def run_b200(args, case):
     red = [plan_v[i] / plan_v[i + 1] for i in range(len(plan_v) - 1) if plan_v[i + 1] > 0]
     reduction = math.exp(sum(math.log(x) for x in red) / len(red)) if red else None
 
-    # warmup (untimed)
-    for _ in range(args.warmup):
+    # converged state (cycles beyond the plan), reported beside the step time
+    for _ in range(max(3, args.warmup)):
         sol.v_cycle_async()
     sol.cycle_result()
-    if ws > 1:
-        torch.distributed.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        sol.v_cycle_async()
+    e1.record(stream)
+    sol.cycle_result()
+    torch.cuda.synchronize()
+    converged_ms = e0.elapsed_time(e1) / args.steps
+    converged_coarse_iters = sol.coarse_info()[0]
+
+    # warmup (untimed): W V-cycles of the plan; then the K timed steps
+    bar = torch.distributed.barrier if ws > 1 else None
+    time_plan_cycles(torch, dev, sol, mesh, case, stream, max(3, args.warmup), bar)
     with ClockSampler(dev_id) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            sol.v_cycle_async()
-        e1.record(stream)
-        stats = sol.cycle_result()
-        torch.cuda.synchronize()
+        ms_total, stats, replay_resid = time_plan_cycles(torch, dev, sol, mesh, case, stream, args.steps, bar)
+    plan_coarse_iters = sol.coarse_info()[0]
     if ws > 1:
         torch.distributed.barrier()
-    ms_total = e0.elapsed_time(e1)
     if ws > 1:
         tt = torch.tensor([ms_total], device="cuda")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
@@ -565,6 +613,19 @@ def run_b200(args, case):
                     "serial_value": e2e_serial_val},
             "gpu_launches": kernels * args.steps,
             "kernels_per_step": kernels,
+            "timing": {
+                "protocol": f"steps are V-cycles of the config's plan ({'FMG + ' if case.fmg_first else ''}"
+                            f"{case.v_cycles} V from phi = 0): passes of <= {case.v_cycles} back-to-back "
+                            "cycles timed with CUDA events on the launching stream and summed; before every "
+                            "pass phi is reset and the plan's start (pins"
+                            f"{', FMG cycle' if case.fmg_first else ''}) rebuilt outside the timed region",
+                "plan_replay_matches": (replay_resid == plan_v[-1]) if replay_resid is not None else None,
+                "coarse_iters_last_plan_cycle": plan_coarse_iters,
+                "converged_state": {
+                    "ms_per_step": converged_ms, "coarse_iters": converged_coarse_iters,
+                    "note": "back-to-back V-cycles on the converged solution (beyond the plan): the coarse "
+                            "BiCGStab then solves for round-off noise and runs more iterations"},
+            },
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "fmg_ms": t_fmg,
@@ -601,18 +662,11 @@ def extra_configs(args, names=("cfg3", "cfg4")):
         dev.set_field(VAR_RHS, case.rhs_fields(mesh), layout=LAYOUT_INTERIOR)
         sol = MgSolver(dev, None, MgConfig())
         hist = [sol.v_cycle().max_resid for _ in range(case.v_cycles)]  # the config's plan
-        for _ in range(3):
-            sol.v_cycle_async()
-        sol.cycle_result()
         stream = torch.cuda.ExternalStream(dev.stream)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         steps = max(5, args.steps)
-        e0.record(stream)
-        for _ in range(steps):
-            sol.v_cycle_async()
-        e1.record(stream)
-        sol.cycle_result()
-        ms = e0.elapsed_time(e1) / steps
+        time_plan_cycles(torch, dev, sol, mesh, case, stream, 3)  # warm-up
+        ms_total, _, _ = time_plan_cycles(torch, dev, sol, mesh, case, stream, steps)
+        ms = ms_total / steps
         leaf = case.leaf_cells(mesh)
         BV = vcycle_bytes(mesh, case.N, case.dim)
         red = [hist[i] / hist[i + 1] for i in range(len(hist) - 1) if hist[i + 1] > 0]

@@ -1932,7 +1932,7 @@ int pmg_b200_time_op(pmg_b200_ctx* h, int op, int level, int reps, double* ms_av
     // in-cycle cost of a small op, launch gaps as inside the cycle graphs)
     const bool in_graph = op >= 100;
     if (in_graph) op -= 100;
-    require(reps >= 1 && op >= 0 && op <= 10 && !(in_graph && (op == 5 || op == 6)), "bad op/reps");
+    require(reps >= 1 && op >= 0 && op <= 10 && !(in_graph && op == 6), "bad op/reps");
     if (op <= 3 || op >= 7) need_level(c, level, op == 0 || op == 3 || op == 9 ? 1 : 2);
     auto one = [&](int k) {
       switch (op) {
@@ -1941,7 +1941,10 @@ int pmg_b200_time_op(pmg_b200_ctx* h, int op, int level, int reps, double* ms_av
         case 2: c.ops->prolong(c, level, false); break;
         case 3: c.ops->record(c, level); break;
         case 4: enq_coarse(c); break;
-        case 5: PMG_CUDA(cudaGraphLaunch(graph_for(c, CK_V).exec, c.stream)); break;
+        case 5:  // in a graph: the V-cycle's nodes themselves, `reps` cycles in ONE graph
+          if (in_graph) enq_cycle(c, CK_V);
+          else PMG_CUDA(cudaGraphLaunch(graph_for(c, CK_V).exec, c.stream));
+          break;
         case 7: c.ops->restrict_(c, level, c.lev[(size_t)level]->has_cf ? pmgdev::RM_RES : pmgdev::RM_FUSED); break;
         case 8: c.ops->fas(c, level - 1, true); break;
         case 9: enq_smooth(c, level, 1); break;  // one smoothing step (both colours)

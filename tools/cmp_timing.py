@@ -30,7 +30,7 @@ for rep in range(3):
     if case.fmg_first:
         sol.fmg_cycle()
     rows = []
-    for k in range(14):
+    for k in range(26):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
