@@ -350,7 +350,14 @@ def run_partitioned(args, case):
     t0 = time.perf_counter()
     build_stencils(dev, case.lsf, StencilBuildConfig(w_min=case.w_min))
     t_stencil = time.perf_counter() - t0
-    dev.set_field(VAR_RHS, case.rhs_fields(mesh), layout=LAYOUT_INTERIOR)
+    # every rank generates the right-hand side of its own blocks only (the
+    # generator is counter-based: the values do not depend on who draws them)
+    only = None
+    if ws > 1:
+        from paper_2205_09411_b200.distributed import owner_of_blocks
+        from paper_2205_09411_b200.partition import morton_partition
+        only = owner_of_blocks(mesh, morton_partition(mesh, ws)) == rank
+    dev.set_field(VAR_RHS, case.rhs_fields(mesh, only=only), layout=LAYOUT_INTERIOR)
     sol = DistributedMgSolver(dev, MgConfig(), world=ws, rank=rank)
     stream = torch.cuda.ExternalStream(dev.stream, device=local)
     L = mesh.n_levels

@@ -75,8 +75,15 @@ class Case:
                                   lambda mesh, b, x: np.abs(lsf_eval(lsf, x)) < band * mesh.dx[b])
         return m
 
-    def rhs_fields(self, mesh: TreeMesh):
-        """Interior RHS (n_blocks, N^D) for leaf blocks, zeros elsewhere."""
+    def rhs_fields(self, mesh: TreeMesh, only=None, chunk=2048):
+        """Interior RHS (n_blocks, N^D) for leaf blocks, zeros elsewhere.
+
+        ``only``: boolean mask over block ids -- values are generated for those
+        leaves alone (a rank of the partitioned solve needs its own blocks; the
+        counter-based generator makes every cell's value independent of which
+        others are drawn).  Blocks are processed ``chunk`` at a time, so the
+        temporaries stay small at 1024^3 (the untouched rows of the zero array
+        are never committed)."""
         nb, NI = mesh.n_blocks, self.N ** self.dim
         out = np.zeros((nb, NI))
         if self.rhs == "zero":
@@ -85,24 +92,24 @@ class Case:
         idx = np.indices((N,) * D)[::-1].reshape(D, -1).T  # x fastest
         for l in range(1, mesh.n_levels + 1):
             n = N << (l - 1)
-            ids = [b for b in mesh.level_blocks(l) if mesh.is_leaf(b)]
-            if not ids:
-                continue
-            crd = np.array([mesh.coords[b] for b in ids], np.int64)  # (nl, D)
-            g = crd[:, None, :] * N + idx[None, :, :]                 # (nl, NI, D)
-            k = g[..., 0].astype(np.uint64)
-            mul = np.uint64(n)
-            for a in range(1, D):
-                k = k + mul * g[..., a].astype(np.uint64)
-                mul = mul * np.uint64(n)
-            if self.rhs == "uniform":
-                u = uniform01(self.seed, k)
-                vals = self.rhs_amp * (2.0 * u - 1.0)
-            else:  # gauss: Box-Muller on draws 2k, 2k+1
-                u1 = uniform01(self.seed, np.uint64(2) * k)
-                u2 = uniform01(self.seed, np.uint64(2) * k + np.uint64(1))
-                vals = self.rhs_amp * np.sqrt(-2.0 * np.log(1.0 - u1)) * np.cos(2.0 * np.pi * u2)
-            out[np.array(ids)] = vals
+            ids_all = [b for b in mesh.level_blocks(l) if mesh.is_leaf(b) and (only is None or only[b])]
+            for c0 in range(0, len(ids_all), chunk):
+                ids = ids_all[c0:c0 + chunk]
+                crd = np.array([mesh.coords[b] for b in ids], np.int64)  # (nl, D)
+                g = crd[:, None, :] * N + idx[None, :, :]                 # (nl, NI, D)
+                k = g[..., 0].astype(np.uint64)
+                mul = np.uint64(n)
+                for a in range(1, D):
+                    k = k + mul * g[..., a].astype(np.uint64)
+                    mul = mul * np.uint64(n)
+                if self.rhs == "uniform":
+                    u = uniform01(self.seed, k)
+                    vals = self.rhs_amp * (2.0 * u - 1.0)
+                else:  # gauss: Box-Muller on draws 2k, 2k+1
+                    u1 = uniform01(self.seed, np.uint64(2) * k)
+                    u2 = uniform01(self.seed, np.uint64(2) * k + np.uint64(1))
+                    vals = self.rhs_amp * np.sqrt(-2.0 * np.log(1.0 - u1)) * np.cos(2.0 * np.pi * u2)
+                out[np.array(ids)] = vals
         return out
 
     def leaf_cells(self, mesh: TreeMesh):
