@@ -89,6 +89,7 @@ static void set_views(Ctx& c) {
     v.r_pin = d.r_pin.p;
     v.cfold = d.cfold.p;
     v.cfoff = d.has_cfold ? d.cfoff.p : nullptr;
+    v.cfc = nullptr;  // the launchers that read the table set it (ops_impl.cuh Vt)
     for (int k = 0; k < 6; ++k) v.bctype[k] = c.bctype[k];
     v.dense = d.dense ? 1 : 0;
     v.nside = 1 << (l - 1);
@@ -821,7 +822,7 @@ static void assemble_coarse(Ctx& c) {
 // residual_level(l) + restrict_level(l) up to apply_pins(l-1): one pass unless
 // level l has coarse-fine faces (their ghosts read level l-1 cells being restricted)
 static void enq_restrict_only(Ctx& c, int l) {
-  if (c.lev[(size_t)l]->has_cf) {
+  if (c.lev[(size_t)l]->has_cf && !c.ops->cf_table()) {
     c.ops->residual(c, l);
     c.ops->restrict_(c, l, pmgdev::RM_RES);
   } else {
@@ -927,6 +928,7 @@ static Graph& graph_for(Ctx& c, int kind) {
   Graph& g = kind == CK_V ? c.g_v : kind == CK_MEASURE ? c.g_measure : c.g_fmg[kind == CK_FMG_GUESS];
   if (g.exec) return g;
   cudaGraph_t graph;
+  cfc_all_dirty(c);  // a replay may start from any state: the graph rebuilds the cfc tables it reads
   PMG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
   try {
     enq_cycle(c, kind);
@@ -936,6 +938,7 @@ static Graph& graph_for(Ctx& c, int kind) {
     throw;
   }
   PMG_CUDA(cudaStreamEndCapture(c.stream, &graph));
+  cfc_all_dirty(c);  // nothing was executed
   size_t nn = 0;
   PMG_CUDA(cudaGraphGetNodes(graph, nullptr, &nn));
   std::vector<cudaGraphNode_t> nodes(nn);
@@ -1057,6 +1060,7 @@ static void launch_dist_cycle(Ctx& c) {
   } else {
     if (!ds.g.exec) {
       cudaGraph_t graph = nullptr;
+      cfc_all_dirty(c);
       PMG_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
       bool ok = true;
       try {
@@ -1065,6 +1069,7 @@ static void launch_dist_cycle(Ctx& c) {
         ok = false;
       }
       const cudaError_t e = cudaStreamEndCapture(c.stream, &graph);
+      cfc_all_dirty(c);
       if (ok && e == cudaSuccess && graph && cudaGraphInstantiate(&ds.g.exec, graph, 0) == cudaSuccess) {
         size_t nn = 0;
         PMG_CUDA(cudaGraphGetNodes(graph, nullptr, &nn));
@@ -1278,6 +1283,18 @@ static void set_mesh(Ctx& c, int nb, const int32_t* level, const int32_t* coords
     d.has_cfold = n > 0;
     d.cfoff.upload(cfo, c.stream);
     d.cfold.alloc((size_t)std::max(n, 1));
+    // the same faces, listed, and their cfc pages (LevelView::cfc)
+    std::vector<int32_t> cff;
+    for (int s = 0; s < d.nb; ++s)
+      for (int f = 0; f < F; ++f)
+        if (cfo[(size_t)s * F + f] >= 0) {
+          cff.push_back(s);
+          cff.push_back(f);
+        }
+    d.n_cf = (int)(cff.size() / 2);
+    if (d.n_cf > 0) d.cf_faces.upload(cff, c.stream);
+    d.cfc.alloc((size_t)std::max(n, 1));
+    d.cfc_dirty = true;
   }
   for (int f = 0; f < 6; ++f) {
     c.face_vals[f].clear();
@@ -1476,6 +1493,8 @@ static int guard(pmg_b200_ctx* h, Fn&& fn) {
   try {
     h->c.err.clear();
     PMG_CUDA(cudaSetDevice(h->c.device));
+    // the caller may have written PHI through pmg_b200_level_field_ptr
+    pmghost::cfc_all_dirty(h->c);
     fn(h->c);
     return PMG_OK;
   } catch (const PmgError& e) {
@@ -1945,7 +1964,9 @@ int pmg_b200_time_op(pmg_b200_ctx* h, int op, int level, int reps, double* ms_av
           if (in_graph) enq_cycle(c, CK_V);
           else PMG_CUDA(cudaGraphLaunch(graph_for(c, CK_V).exec, c.stream));
           break;
-        case 7: c.ops->restrict_(c, level, c.lev[(size_t)level]->has_cf ? pmgdev::RM_RES : pmgdev::RM_FUSED); break;
+        case 7:
+          c.ops->restrict_(c, level, c.lev[(size_t)level]->has_cf && !c.ops->cf_table() ? pmgdev::RM_RES : pmgdev::RM_FUSED);
+          break;
         case 8: c.ops->fas(c, level - 1, true); break;
         case 9: enq_smooth(c, level, 1); break;  // one smoothing step (both colours)
         case 10:  // the V-cycle's prolongation (red cells left to the next half-sweep)
@@ -2021,12 +2042,7 @@ void* pmg_b200_level_field_ptr(pmg_b200_ctx* h, int var, int level) {
 int pmg_b200_restrict_only(pmg_b200_ctx* h, int level) {
   return guard(h, [&](Ctx& c) {
     need_level(c, level, 2);
-    if (c.lev[(size_t)level]->has_cf) {
-      c.ops->residual(c, level);
-      c.ops->restrict_(c, level, pmgdev::RM_RES);
-    } else {
-      c.ops->restrict_(c, level, pmgdev::RM_FUSED);
-    }
+    enq_restrict_only(c, level);
     PMG_CUDA(cudaStreamSynchronize(c.stream));
   });
 }

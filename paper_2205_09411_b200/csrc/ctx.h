@@ -269,6 +269,13 @@ struct LevelDev {
   int n_fix[2] = {0, 0};
   bool has_cf = false;       // some block has a coarse-fine face
   bool has_cfold = false;
+  // coarse parts of the coarse-fine ghosts (LevelView::cfc): the level's
+  // coarse-fine faces {slot, dir}, the table, and whether level l-1's PHI
+  // changed since the table was built
+  DevBuf<int32_t> cf_faces;
+  int n_cf = 0;
+  DevBuf<double> cfc;
+  bool cfc_dirty = true;
   bool dense = false;   // all blocks present, slot == Morton code
   bool bczero = true;   // no Dirichlet face values (all zero)
   pmgdev::LevelView view{};
@@ -287,6 +294,10 @@ struct Ops {
   virtual void restrict_(Ctx& c, int l, int mode) = 0;
   virtual void fas(Ctx& c, int lc, bool fas) = 0;
   virtual void cfold(Ctx& c, int lc) = 0;
+  virtual void cfc_build(Ctx& c, int l) = 0;
+  // the block-per-CTA kernels read coarse-fine ghosts from the cfc table, so
+  // residual + restriction of a level with coarse-fine faces is one pass
+  virtual bool cf_table() const = 0;
   virtual void prolong(Ctx& c, int l, bool full) = 0;
   virtual void record(Ctx& c, int l) = 0;
   virtual void pins(Ctx& c, int l) = 0;
@@ -402,6 +413,21 @@ struct Ctx {
 
   ~Ctx();
 };
+
+// PHI of level l was (or may have been) written: the cfc table of level l+1 is stale
+inline void phi_written(Ctx& c, int l) {
+  if (l >= 1 && l + 1 < (int)c.lev.size() && c.lev[(size_t)l + 1]) c.lev[(size_t)l + 1]->cfc_dirty = true;
+}
+inline void cfc_all_dirty(Ctx& c) {
+  for (auto& d : c.lev)
+    if (d) d->cfc_dirty = true;
+}
+inline void ensure_cfc(Ctx& c, int l) {
+  LevelDev& d = *c.lev[(size_t)l];
+  if (d.n_cf == 0 || !d.cfc_dirty) return;
+  c.ops->cfc_build(c, l);
+  d.cfc_dirty = false;
+}
 
 inline void set_smem_attr(Ctx& c, const void* fn, size_t smem) {
   if (!c.attr_done.insert(fn).second) return;

@@ -472,6 +472,7 @@ static void dist_xchg(Ctx& c, int var, int l, int k) {
   DistState& ds = *c.dist;
   if (ds.world == 1 || l < ds.split) return;
   dist_move(c, l, k, level_var(c, var, l));
+  phi_written(c, l);  // halo cells of level l changed (whatever `var`)
 }
 
 // whole level l of `var` from rank 0 to every rank
@@ -479,6 +480,7 @@ static void dist_bcast_level(Ctx& c, int var, int l) {
   DistState& ds = *c.dist;
   double* f = level_var(c, var, l);
   const size_t n = (size_t)c.lev[(size_t)l]->nb * c.NI;
+  phi_written(c, l);
   if (ds.transport == TR_NCCL) {
     PMG_NCCL(nccl_api().Broadcast(f, f, n, ncclFloat64, 0, ds.comm, c.stream));
   } else if (ds.transport == TR_LOCAL) {

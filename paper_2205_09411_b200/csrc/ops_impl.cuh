@@ -34,11 +34,30 @@ struct OpsImpl final : Ops {
   static constexpr bool FASTC = G::NI <= 4096;
   const LevelView& V(Ctx& c, int l) { return c.lev[(size_t)l]->view; }
   const LevelView& Vc(Ctx& c, int l) { return c.lev[(size_t)(l > 1 ? l - 1 : l)]->view; }
+  // level l's view with the cfc table (coarse parts of its coarse-fine ghosts)
+  // attached, rebuilt first if level l-1 changed since
+  LevelView Vt(Ctx& c, int l) {
+    LevelDev& d = *c.lev[(size_t)l];
+    LevelView v = d.view;
+    if (d.n_cf > 0) {
+      ensure_cfc(c, l);
+      v.cfc = d.cfc.p;
+    }
+    return v;
+  }
+  bool cf_table() const override { return TILE; }
+  void cfc_build(Ctx& c, int l) override {
+    const LevelDev& d = *c.lev[(size_t)l];
+    pdl_launch(k_cfc_build<D, N>, grid_for((long long)d.n_cf * G::NT, 256), 256, 0, c.stream, V(c, l), Vc(c, l),
+               (const int2*)d.cf_faces.p, d.n_cf, d.cfc.p);
+    check();
+  }
 
   void check() { PMG_CUDA(cudaGetLastError()); }
 
   void gs(Ctx& c, int l, int parity) override {
     const LevelView& L = V(c, l);
+    phi_written(c, l);
     if (L.nb <= kSmallLevel) {
       const LevelDev& d = *c.lev[(size_t)l];
       if (d.has_tab)
@@ -64,13 +83,14 @@ struct OpsImpl final : Ops {
       const bool lean_work = stream || d.n_fast > 0;
       const int ncut = stream ? d.n_cut[parity] : 0;
       const bool fork = lean_work && (d.n_slow > 0 || nfix > 0 || ncut > 0);
+      const LevelView Lt = d.n_slow > 0 ? Vt(c, l) : L;  // before the fork: a table rebuild runs on c.stream
       if (fork) {
         PMG_CUDA(cudaEventRecord(c.ev_fork, c.stream));
         PMG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
       }
       cudaStream_t s2 = fork ? c.side : c.stream;
       if (d.n_slow > 0)
-        pdl_launch(k_gs_tile<D, N>, d.n_slow, TT::THREADS, 0, s2, L, Vc(c, l), c.phi_b.p, parity, d.slow_list.p);
+        pdl_launch(k_gs_tile<D, N>, d.n_slow, TT::THREADS, 0, s2, Lt, Vc(c, l), c.phi_b.p, parity, d.slow_list.p);
       if (nfix > 0)
         pdl_launch(k_gs_fix<D, N>, grid_for(nfix, 128), 128, 0, s2, L, Vc(c, l), c.phi_b.p, parity,
                                                            (const int2*)d.fix_list[parity].p, nfix);
@@ -82,6 +102,8 @@ struct OpsImpl final : Ops {
           constexpr int T256 = N == 16 ? 256 : 0;
           if (T256 && d.n_gs <= c.sms * 4)  // one block per CTA, all resident at once
             launch_gs_stream<1, 4, T256>(c, L, d, parity);
+          else if (N == 8)  // 512-cell blocks: 128-thread CTAs, eight per SM (40.0 vs 45.1 us per
+            launch_gs_stream<2, 8, 128>(c, L, d, parity);  // half-sweep on cfg3's finest level with <2, 2, 256>)
           else if (d.n_gs <= 1024) launch_gs_stream<2, 3, T256>(c, L, d, parity);  // 7.7 vs 8.0 us at 512 blocks
           else launch_gs_stream<kStreamStages, kStreamCtasPerSm, 0>(c, L, d, parity);
         }
@@ -136,6 +158,7 @@ struct OpsImpl final : Ops {
       cfg.numAttrs = 1;
       PMG_CUDA(cudaLaunchKernelEx(&cfg, k_gs_coop<N>, L, (const int4*)d.gs_plan.p, d.n_gs, 2 * steps, cut,
                                   c.gbar.p));
+      phi_written(c, l);
       return true;
     }
     return false;
@@ -201,6 +224,10 @@ struct OpsImpl final : Ops {
     check();
   }
   void restrict_(Ctx& c, int l, int mode) override {
+    restrict_impl(c, l, mode);
+    phi_written(c, l - 1);  // after the launch: level l's own table (read above) is stale from here on
+  }
+  void restrict_impl(Ctx& c, int l, int mode) {
     const LevelView& Lf = V(c, l);
     const unsigned g = grid_for((long long)Lf.nb * G::NI);  // k_restrict: one thread per child cell
     // 3D N=16 levels of more than 8 blocks restrict with the streaming kernel
@@ -263,7 +290,7 @@ struct OpsImpl final : Ops {
       else if (mode == RM_RHS)
         pdl_launch(k_restrict_tile<D, N, RM_RHS>, Lf.nb, TT::THREADS, 0, c.stream, Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
       else
-        pdl_launch(k_restrict_tile<D, N, RM_FUSED>, Lf.nb, TT::THREADS, 0, c.stream, Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
+        pdl_launch(k_restrict_tile<D, N, RM_FUSED>, Lf.nb, TT::THREADS, 0, c.stream, Vt(c, l), Vc(c, l), V(c, l - 1), c.phi_b.p);
       check();
       return;
     }
@@ -319,7 +346,7 @@ struct OpsImpl final : Ops {
     if constexpr (TILE) {
       if (L.nb > kSmallLevel) {
         if (f)
-          pdl_launch(k_fas_tile<D, N, true>, L.nb, TT::THREADS, 0, c.stream, L, Vc(c, lc), c.phi_b.p);
+          pdl_launch(k_fas_tile<D, N, true>, L.nb, TT::THREADS, 0, c.stream, Vt(c, lc), Vc(c, lc), c.phi_b.p);
         else
           pdl_launch(k_fas_tile<D, N, false>, L.nb, TT::THREADS, 0, c.stream, L, Vc(c, lc), c.phi_b.p);
         check();
@@ -355,6 +382,7 @@ struct OpsImpl final : Ops {
   }
   void prolong(Ctx& c, int l, bool full) override {
     const LevelView& Lf = V(c, l);
+    phi_written(c, l);
     const LevelView& Lp = V(c, l - 1);
     const LevelView& Lpp = Vc(c, l - 1);
     const unsigned g = grid_for((long long)Lf.nb * G::NI);
@@ -372,10 +400,11 @@ struct OpsImpl final : Ops {
     }
     if constexpr (TILE) {
       if (Lf.nb > kSmallLevel) {
+        const LevelView Lpt = Vt(c, l - 1);  // the parents' coarse-fine ghosts
         if (full)
-          pdl_launch(k_prolong_tile<D, N, true>, Lf.nb, TT::THREADS, 0, c.stream, Lf, Lp, Lpp);
+          pdl_launch(k_prolong_tile<D, N, true>, Lf.nb, TT::THREADS, 0, c.stream, Lf, Lpt, Lpp);
         else
-          pdl_launch(k_prolong_tile<D, N, false>, Lf.nb, TT::THREADS, 0, c.stream, Lf, Lp, Lpp);
+          pdl_launch(k_prolong_tile<D, N, false>, Lf.nb, TT::THREADS, 0, c.stream, Lf, Lpt, Lpp);
         check();
         return;
       }
@@ -414,12 +443,13 @@ struct OpsImpl final : Ops {
         const int ncut = d.n_cut[0] + d.n_cut[1];
         const int gcut = ncut > 0 ? (int)grid_for(ncut, 256) : 0;
         const bool fork = d.n_slow > 0 || ncut > 0;
+        const LevelView Lt = d.n_slow > 0 ? Vt(c, l) : L;
         if (fork) {
           PMG_CUDA(cudaEventRecord(c.ev_fork, c.stream));
           PMG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
         }
         if (d.n_slow > 0)
-          pdl_launch(k_record_tile<D, N>, d.n_slow, TT::THREADS, 0, c.side, L, Vc(c, l), c.phi_b.p,
+          pdl_launch(k_record_tile<D, N>, d.n_slow, TT::THREADS, 0, c.side, Lt, Vc(c, l), c.phi_b.p,
                      c.partial.p + grid + gcut, c.rec.p, (unsigned int*)nullptr, d.slow_list.p);
         if (ncut > 0)
           pdl_launch(k_record_cut<D>, gcut, 256, 0, c.side, L, c.phi_b.p, d.cut_ent[0].p, d.cut_gbc[0].p,
@@ -444,13 +474,14 @@ struct OpsImpl final : Ops {
     if constexpr (TILE) {
       const LevelDev& d = *c.lev[(size_t)l];
       const bool fork = d.n_ufast > 0 && d.n_uslow > 0;
+      const LevelView Lt = d.n_uslow > 0 ? Vt(c, l) : L;
       if (fork) {
         PMG_CUDA(cudaEventRecord(c.ev_fork, c.stream));
         PMG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
       }
       if (d.n_uslow > 0)
         pdl_launch(k_record_tile<D, N>, d.n_uslow, TT::THREADS, 0, fork ? c.side : c.stream, 
-            L, Vc(c, l), c.phi_b.p, c.partial.p, c.rec.p, c.counter.p, d.uslow_list.p);
+            Lt, Vc(c, l), c.phi_b.p, c.partial.p, c.rec.p, c.counter.p, d.uslow_list.p);
       if (d.n_ufast > 0)
         pdl_launch(k_record_lean<D, N>, d.n_ufast, TT::THREADS, 0, c.stream, L, c.partial.p, c.rec.p,
                                                                      c.counter.p, d.ufast_list.p);
@@ -467,6 +498,7 @@ struct OpsImpl final : Ops {
   }
   void pins(Ctx& c, int l) override {
     const LevelView& L = V(c, l);
+    phi_written(c, l);
     pdl_launch(k_pins<D, N>, grid_for((long long)L.nb * G::NI), kThreads, 0, c.stream, L, c.phi_b.p);
     check();
   }
@@ -520,6 +552,7 @@ struct OpsImpl final : Ops {
     }
   }
   void coarse(Ctx& c) override {
+    phi_written(c, 1);
     if constexpr (FASTC) {
       CoarseFast F{};
       F.flags = c.cf_flags.p;
@@ -621,6 +654,7 @@ struct OpsImpl final : Ops {
   void scatter(Ctx& c, int l, double* dst, const double* staging, const int32_t* slot_id,
                int layout) override {
     const LevelView& L = V(c, l);
+    phi_written(c, l);
     pdl_launch(k_scatter<D, N>, grid_for((long long)L.nb * G::NI), kThreads, 0, c.stream, 
         L.nb, dst, staging, slot_id, layout, L.own);
     check();

@@ -71,6 +71,12 @@ struct LevelView {
   const int8_t* r_pin;    // [R]
   double* cfold;          // AMR: VAR_OLD ghosts on coarse-fine faces
   const int32_t* cfoff;   // [nb*2D] offset into cfold or -1
+  // AMR: the slope-corrected coarse value of every coarse-fine ghost (the part
+  // of mesh.hpp:500-535 that only reads level l-1), rebuilt by k_cfc_build
+  // whenever level l-1 changed; face f of a block at cfoff[...], colour-split:
+  // [colour of the adjacent interior cell][transverse index >> 1].  nullptr:
+  // evaluate from level l-1 at the read (the launchers opt in, ops_impl.cuh Vt)
+  const double* cfc;
   int bctype[6];          // per domain face: 0 Dirichlet, 1 Neumann-zero (mesh.hpp:22-32)
   int dense;              // 1: all (2^(l-1))^D blocks present and slot == Morton code
   int nside;              // blocks per axis on this level (dense levels)
@@ -221,8 +227,8 @@ __device__ __forceinline__ double val_nocf(const LevelView& L, const double* __r
 // `dir` next to interior cell (i,j,k): mesh.hpp:500-535.  f1 = value of (i,j,k),
 // f2 = value of the next cell inward.
 template <int D, int N>
-__device__ __forceinline__ double cf_ghost(const LevelView& L, const LevelView& Lc, int slot,
-                                           int dir, int i, int j, int k, double f1, double f2) {
+__device__ __forceinline__ double cf_coarse(const LevelView& L, const LevelView& Lc, int slot,
+                                            int dir, int i, int j, int k) {
   using G = Geo<D, N>;
   const int axis = dir >> 1, side = dir & 1;
   const int cb = L.cnbr[slot * G::F + dir];
@@ -248,6 +254,20 @@ __device__ __forceinline__ double cf_ghost(const LevelView& L, const LevelView& 
     const double vd = val_nocf<D, N>(Lc, Lc.phi, cb, dn[0], dn[1], dn[2]);
     c += (double)sgn[a] * (vu - vd) / 8.0;
   }
+  return c;
+}
+// position of the ghost next to interior cell (i,j,k) inside its face's cfc page
+template <int D, int N>
+__device__ __forceinline__ int cfc_index(int axis, int i, int j, int k) {
+  using G = Geo<D, N>;
+  return G::colour(i, j, k) * (G::NT / 2) + (G::tindex(axis, i, j, k) >> 1);
+}
+template <int D, int N>
+__device__ __forceinline__ double cf_ghost(const LevelView& L, const LevelView& Lc, int slot,
+                                           int dir, int i, int j, int k, double f1, double f2) {
+  using G = Geo<D, N>;
+  const double c = L.cfc ? L.cfc[L.cfoff[slot * G::F + dir] + cfc_index<D, N>(dir >> 1, i, j, k)]
+                         : cf_coarse<D, N>(L, Lc, slot, dir, i, j, k);
   return 0.5 * c + 0.75 * f1 - 0.25 * f2;
 }
 

@@ -446,36 +446,20 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_restrict_tile(LevelView
   __shared__ double T1s[TT::SIZE];
   const int slot = blockIdx.x;
   const size_t base = (size_t)slot * G::NI;
-  load_both<D, N>(T0s, T1s, Lf, Lfc, slot, MODE == RM_FUSED);
-  cp_async_wait_all();
-  __syncthreads();
   const uint8_t kind = Lf.kind[slot];
-  const int32_t* rowp = kind == KIND_UNIFORM ? nullptr : Lf.row_of + (size_t)Lf.srow[slot] * G::NI;
+  const int fsr = Lf.srow[slot];
   const int P = Lf.parent[slot];
   int cp[3] = {0, 0, 0};
   for (int a = 0; a < D; ++a) cp[a] = (Lf.coords[slot * D + a] & 1) * HN;
   const int t = threadIdx.x;
   const int m = t % HN;
   const unsigned mask = THR >= 32 ? 0xffffffffu : ((1u << THR) - 1u);
-  auto cell = [&](int jj, int kk, int cc, double& phi_out) -> double {
-    const int e = m + HN * (jj + N * kk);
-    const int B = (D == 3 ? ((kk + 1) * TT::P + (jj + 1)) : (jj + 1)) * TT::RW + m;
-    const int o = (cc + jj + kk) & 1;
-    const double* Tc = cc ? T1s : T0s;
-    const double* To = cc ? T0s : T1s;
-    const double self = Tc[B + o];
-    phi_out = self;
-    const size_t a = base + (size_t)cc * G::H + e;
-    if (MODE == RM_RES) return Lf.res[a];
-    if (MODE == RM_RHS) return Lf.rhs[a];
-    const int r = rowp ? rowp[cc * G::H + e] : -1;
-    if (r >= 0 && Lf.r_mask[r] == 1) return 0.0;
-    double p[2 * D];
-    nbrs_at<D, N>(To, B, o, p);
-    return resid_value<D>(Lf, phi_b, r, self, p, Lf.rhs[a]);
-  };
-  for (int step = 0; step < STEPS; ++step) {
-    int kp, jj;
+  Both<D, N> both;
+  both.issue(Lf, Lfc, slot, MODE == RM_FUSED);
+  // every other global value this thread needs, in flight with the fields:
+  // the restricted quantity (or g for the residual), the special-row kind of
+  // each cell and of the parent cell (skind: only a cut row needs its row index)
+  auto where = [&](int step, int& kp, int& jj) {
     if (D == 3) {
       kp = t / (HN * N) + ZG * step;  // z-pair index
       jj = (t / HN) % N;
@@ -483,14 +467,72 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_restrict_tile(LevelView
       kp = 0;
       jj = t / HN + RPS * step;
     }
-    const bool active = D == 3 ? kp < N / 2 : jj < N;
+    return D == 3 ? kp < N / 2 : jj < N;
+  };
+  double gq[STEPS][2][2];
+  int8_t skq[STEPS][2][2], psk[STEPS];
+  const int psr = Lp.srow[P];
+#pragma unroll
+  for (int step = 0; step < STEPS; ++step) {
+    int kp, jj;
+    const bool active = where(step, kp, jj);
+    psk[step] = 0;
+#pragma unroll
+    for (int dz = 0; dz < 2; ++dz)
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        gq[step][dz][x] = 0.0;
+        skq[step][dz][x] = 0;
+      }
+    if (!active) continue;
+    for (int dz = 0; dz < (D == 3 ? 2 : 1); ++dz) {
+      const int kk = D == 3 ? 2 * kp + dz : 0;
+      const int c0 = (jj + kk) & 1;  // colour of i = 2m
+      const int e = m + HN * (jj + N * kk);
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        const int cc = x ? 1 - c0 : c0;
+        const size_t a = base + (size_t)cc * G::H + e;
+        gq[step][dz][x] = MODE == RM_RES ? Lf.res[a] : Lf.rhs[a];
+        if (MODE == RM_FUSED && kind != KIND_UNIFORM)
+          skq[step][dz][x] = Lf.skind[(size_t)fsr * G::NI + (size_t)cc * G::H + e];
+      }
+    }
+    if (!(jj & 1) && psr >= 0) {
+      const int pi = cp[0] + m, pj = cp[1] + (jj >> 1), pk = D == 3 ? cp[2] + kp : 0;
+      psk[step] = Lp.skind[(size_t)psr * G::NI + (size_t)(G::colour(pi, pj, pk) * G::H + G::entry(pi, pj, pk))];
+    }
+  }
+  both.store(T0s, T1s);
+  cp_async_wait_all();
+  __syncthreads();
+  const int32_t* rowp = kind == KIND_UNIFORM ? nullptr : Lf.row_of + (size_t)fsr * G::NI;
+  auto cell = [&](int jj, int kk, int cc, double g, int sk, double& phi_out) -> double {
+    const int e = m + HN * (jj + N * kk);
+    const int B = (D == 3 ? ((kk + 1) * TT::P + (jj + 1)) : (jj + 1)) * TT::RW + m;
+    const int o = (cc + jj + kk) & 1;
+    const double* Tc = cc ? T1s : T0s;
+    const double* To = cc ? T0s : T1s;
+    const double self = Tc[B + o];
+    phi_out = self;
+    if (MODE != RM_FUSED) return g;
+    if (sk == 1) return 0.0;
+    const int r = sk == 2 ? rowp[cc * G::H + e] : -1;
+    double p[2 * D];
+    nbrs_at<D, N>(To, B, o, p);
+    return resid_value<D>(Lf, phi_b, r, self, p, g);
+  };
+#pragma unroll
+  for (int step = 0; step < STEPS; ++step) {
+    int kp, jj;
+    const bool active = where(step, kp, jj);
     double r_[2][2] = {{0, 0}, {0, 0}}, f_[2][2] = {{0, 0}, {0, 0}};  // [z][x]
     if (active) {
       for (int dz = 0; dz < (D == 3 ? 2 : 1); ++dz) {
         const int kk = D == 3 ? 2 * kp + dz : 0;
         const int c0 = (jj + kk) & 1;  // colour of i = 2m
-        r_[dz][0] = cell(jj, kk, c0, f_[dz][0]);
-        r_[dz][1] = cell(jj, kk, 1 - c0, f_[dz][1]);
+        r_[dz][0] = cell(jj, kk, c0, gq[step][dz][0], skq[step][dz][0], f_[dz][0]);
+        r_[dz][1] = cell(jj, kk, 1 - c0, gq[step][dz][1], skq[step][dz][1], f_[dz][1]);
       }
     }
     double pr[2][2], pf[2][2];  // the y+1 partner's values
@@ -516,8 +558,7 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_restrict_tile(LevelView
     const int pc = G::colour(pi, pj, pk), pe = G::entry(pi, pj, pk);
     const size_t pa = (size_t)P * G::NI + (size_t)(pc * G::H + pe);
     double vphi = sf / (double)(1 << D);
-    const int rr = row_index<D, N>(Lp, P, pc, pe);
-    if (rr >= 0 && Lp.r_mask[rr] == 1) vphi = phi_b[Lp.r_pin[rr]];
+    if (psk[step] == 1) vphi = phi_b[Lp.r_pin[Lp.row_of[(size_t)psr * G::NI + (size_t)(pc * G::H + pe)]]];
     Lp.phi[pa] = vphi;
     Lp.rhs[pa] = sr / (double)(1 << D);
   }
@@ -540,18 +581,24 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_fas_tile(LevelView L, L
     for (int ce = threadIdx.x; ce < G::NI; ce += blockDim.x) L.old[base + ce] = L.phi[base + ce];
     return;
   }
-  load_both<D, N>(T0, T1, L, Lc, slot, true);
+  const uint8_t kind = L.kind[slot];
+  const int sr = L.srow[slot];
+  Both<D, N> b;
+  b.issue(L, Lc, slot, true);
   double rq[2][O::PER];
+  int8_t skq[2][O::PER];  // special-row kinds, in flight with the fields (k_record_tile)
 #pragma unroll
   for (int q = 0; q < O::PER; ++q) {
     const int e = threadIdx.x + q * O::THR;
     rq[0][q] = L.rhs[base + e];
     rq[1][q] = L.rhs[base + G::H + e];
+    skq[0][q] = kind == KIND_UNIFORM ? (int8_t)0 : L.skind[(size_t)sr * G::NI + e];
+    skq[1][q] = kind == KIND_UNIFORM ? (int8_t)0 : L.skind[(size_t)sr * G::NI + G::H + e];
   }
+  b.store(T0, T1);
   cp_async_wait_all();
   __syncthreads();
-  const uint8_t kind = L.kind[slot];
-  const int32_t* rowp = kind == KIND_UNIFORM ? nullptr : L.row_of + (size_t)L.srow[slot] * G::NI;
+  const int32_t* rowp = kind == KIND_UNIFORM ? nullptr : L.row_of + (size_t)sr * G::NI;
 #pragma unroll
   for (int q = 0; q < O::PER; ++q) {
     int j, k, B;
@@ -563,9 +610,9 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_fas_tile(LevelView L, L
       const double* Tc = c ? T1 : T0;
       const double* To = c ? T0 : T1;
       const double self = Tc[B + o];
-      const int r = rowp ? rowp[c * G::H + e] : -1;
+      const int r = skq[c][q] == 2 ? rowp[c * G::H + e] : -1;
       double out;
-      if (r >= 0 && L.r_mask[r] == 1) {
+      if (skq[c][q] == 1) {
         out = 0.0;
       } else {
         double p[2 * D];
@@ -602,6 +649,9 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_prolong_tile(LevelView 
   for (int a = 0; a < D; ++a) cp[a] = (Lf.coords[slot * D + a] & 1) * HN;
   // fine values in flight first
   double fv[2][O::PER];  // [h][q]: h = 0 -> cell i = 2m, h = 1 -> i = 2m+1
+  int8_t skq[2][O::PER];  // special-row kind (1 = inside: the cell keeps its pin)
+  const uint8_t kind = Lf.kind[slot];
+  const int sr = Lf.srow[slot];
 #pragma unroll
   for (int q = 0; q < O::PER; ++q) {
     int j, k, B;
@@ -610,6 +660,8 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_prolong_tile(LevelView 
     const int c0 = (j + k) & 1;
     fv[0][q] = FULL ? 0.0 : Lf.phi[base + (size_t)c0 * G::H + e];
     fv[1][q] = FULL ? 0.0 : Lf.phi[base + (size_t)(1 - c0) * G::H + e];
+    skq[0][q] = kind == KIND_UNIFORM ? (int8_t)0 : Lf.skind[(size_t)sr * G::NI + (size_t)c0 * G::H + e];
+    skq[1][q] = kind == KIND_UNIFORM ? (int8_t)0 : Lf.skind[(size_t)sr * G::NI + (size_t)(1 - c0) * G::H + e];
   }
   for (int q = threadIdx.x; q < PS; q += blockDim.x) {
     const int a = q % PE - 1, b = (q / PE) % PE - 1, cc = D == 3 ? q / (PE * PE) - 1 : 0;
@@ -622,8 +674,6 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_prolong_tile(LevelView 
       Dt[q] = phi_at<D, N>(Lp, Lpp, P, pi, pj, pk) - old_at<D, N>(Lp, P, pi, pj, pk);
   }
   __syncthreads();
-  const uint8_t kind = Lf.kind[slot];
-  const int32_t* rowp = kind == KIND_UNIFORM ? nullptr : Lf.row_of + (size_t)Lf.srow[slot] * G::NI;
   const int m = threadIdx.x % HN;
 #pragma unroll
   for (int q = 0; q < O::PER; ++q) {
@@ -642,10 +692,7 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_prolong_tile(LevelView 
 #pragma unroll
     for (int h = 0; h < 2; ++h) {  // h = 0: i = 2m, h = 1: i = 2m+1
       const int c = h ? 1 - c0 : c0;
-      if (rowp) {
-        const int r = rowp[c * G::H + e];
-        if (r >= 0 && Lf.r_mask[r] == 1) continue;
-      }
+      if (skq[h][q] == 1) continue;
       double v = (1.0 - 0.25 * D) * dc;
       v += 0.25 * (h ? dxp : dxm);
       v += 0.25 * dy;
@@ -671,9 +718,30 @@ __device__ __forceinline__ void record_finish(const LevelView& L, Rec* __restric
                                               Rec* rec, unsigned int* counter, int slot,
                                               double mx, double ss, double cnt, double* sm,
                                               bool* last, unsigned arrivals = 1u) {
-  mx = block_max(mx, sm);
-  ss = block_sum(ss, sm);
-  cnt = block_sum(cnt, sm);
+  {  // one barrier: warp butterflies, then thread 0 folds the warps in order
+     // (the same order as block_max / block_sum)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    mx = warp_max(mx);
+    ss = warp_sum(ss);
+    cnt = warp_sum(cnt);
+    if (lane == 0) {
+      sm[wid] = mx;
+      sm[24 + wid] = ss;
+      sm[48 + wid] = cnt;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m = 0, s = 0, n = 0;
+      for (int w = 0; w < nw; ++w) {
+        m = fmax(m, sm[w]);
+        s += sm[24 + w];
+        n += sm[48 + w];
+      }
+      mx = m;
+      ss = s;
+      cnt = n;
+    }
+  }
   if (threadIdx.x == 0) {
     partial[slot].max = mx;
     partial[slot].sumsq = ss;
@@ -726,21 +794,29 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_record_tile(LevelView L
   const size_t base = (size_t)slot * G::NI;
   double mx = 0, ss = 0, cnt = 0;
   const bool leaf = L.leaf[slot] != 0;
+  const uint8_t kind = L.kind[slot];
+  const int sr = L.srow[slot];
   double gq[2][O::PER];
+  // special-row kinds of this thread's cells (skind: 0 uniform, 1 inside, 2
+  // cut), in flight with the fields: only a cut row then needs its row index
+  int8_t skq[2][O::PER];
   if (leaf) {
-    load_both<D, N>(T0, T1, L, Lc, slot, true);
+    Both<D, N> b;
+    b.issue(L, Lc, slot, true);
 #pragma unroll
     for (int q = 0; q < O::PER; ++q) {
       const int e = threadIdx.x + q * O::THR;
       gq[0][q] = L.rhs[base + e];
       gq[1][q] = L.rhs[base + G::H + e];
+      skq[0][q] = kind == KIND_UNIFORM ? (int8_t)0 : L.skind[(size_t)sr * G::NI + e];
+      skq[1][q] = kind == KIND_UNIFORM ? (int8_t)0 : L.skind[(size_t)sr * G::NI + G::H + e];
     }
+    b.store(T0, T1);
   }
   cp_async_wait_all();
   __syncthreads();
   if (leaf) {
-    const uint8_t kind = L.kind[slot];
-    const int32_t* rowp = kind == KIND_UNIFORM ? nullptr : L.row_of + (size_t)L.srow[slot] * G::NI;
+    const int32_t* rowp = kind == KIND_UNIFORM ? nullptr : L.row_of + (size_t)sr * G::NI;
 #pragma unroll
     for (int q = 0; q < O::PER; ++q) {
       int j, k, B;
@@ -748,8 +824,8 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_record_tile(LevelView L
       const int e = threadIdx.x + q * O::THR;
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        const int r = rowp ? rowp[c * G::H + e] : -1;
-        if (r >= 0 && L.r_mask[r] == 1) continue;
+        if (skq[c][q] == 1) continue;
+        const int r = skq[c][q] == 2 ? rowp[c * G::H + e] : -1;
         const int o = (c + j + k) & 1;
         double p[2 * D];
         nbrs_at<D, N>(c ? T0 : T1, B, o, p);
