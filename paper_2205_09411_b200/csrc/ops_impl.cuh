@@ -437,8 +437,8 @@ struct OpsImpl final : Ops {
         // streaming record of every block without coarse-fine faces (special
         // rows excluded), the cut rows from their table and the remaining
         // blocks by k_record_tile, each into its own partials: [0, G) per
-        // streaming CTA, [G, G + gcut) per cut-row CTA, then one per slot of
-        // the remaining blocks; folded in that order
+        // streaming CTA, [G, G + gcut) per cut-row CTA, then one per block of
+        // the slow list; folded in that order
         const int grid = rstream_grid(c, L, d);
         const int ncut = d.n_cut[0] + d.n_cut[1];
         const int gcut = ncut > 0 ? (int)grid_for(ncut, 256) : 0;
@@ -466,7 +466,7 @@ struct OpsImpl final : Ops {
           c.finished = true;
         }
         pdl_launch(k_record_fold, 1, 256, 0, c.stream, (const Rec*)c.partial.p,
-                   grid + gcut + (d.n_slow > 0 ? L.nb : 0), c.rec.p + L.level, fin);
+                   grid + gcut + d.n_slow, c.rec.p + L.level, fin);
         check();
         return;
       }
@@ -479,16 +479,26 @@ struct OpsImpl final : Ops {
         PMG_CUDA(cudaEventRecord(c.ev_fork, c.stream));
         PMG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
       }
+      // one partial per listed block ([0, n_uslow) general, then the lean
+      // ones), folded in that order by k_record_fold: no atomic counter, and
+      // the cycle's last record writes the CycleStats and the host copy
       if (d.n_uslow > 0)
         pdl_launch(k_record_tile<D, N>, d.n_uslow, TT::THREADS, 0, fork ? c.side : c.stream, 
-            Lt, Vc(c, l), c.phi_b.p, c.partial.p, c.rec.p, c.counter.p, d.uslow_list.p);
+            Lt, Vc(c, l), c.phi_b.p, c.partial.p, c.rec.p, (unsigned int*)nullptr, d.uslow_list.p);
       if (d.n_ufast > 0)
-        pdl_launch(k_record_lean<D, N>, d.n_ufast, TT::THREADS, 0, c.stream, L, c.partial.p, c.rec.p,
-                                                                     c.counter.p, d.ufast_list.p);
+        pdl_launch(k_record_lean<D, N>, d.n_ufast, TT::THREADS, 0, c.stream, L, c.partial.p + d.n_uslow, c.rec.p,
+                                                                     (unsigned int*)nullptr, d.ufast_list.p);
       if (fork) {
         PMG_CUDA(cudaEventRecord(c.ev_join, c.side));
         PMG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
       }
+      FinishArgs fin{};
+      if (c.finish_level == l && c.h_out_dev) {
+        fin = FinishArgs{c.rec.p, c.mesh.L, l, c.outbuf.p, c.h_out_dev};
+        c.finished = true;
+      }
+      pdl_launch(k_record_fold, 1, 256, 0, c.stream, (const Rec*)c.partial.p, d.n_uslow + d.n_ufast,
+                 c.rec.p + L.level, fin);
       check();
       return;
     }

@@ -145,7 +145,7 @@ struct Halo {
 // then the opposite colour and the rhs (registers), then the halo values;
 // then one round of shared-memory stores, a barrier, and the updates.
 template <int D, int N>
-__global__ void __launch_bounds__(Tile<D, N>::THREADS) k_gs_tile(LevelView L, LevelView Lc,
+__global__ void __launch_bounds__(Tile<D, N>::THREADS, Tile<D, N>::MINB) k_gs_tile(LevelView L, LevelView Lc,
                                                                  const double* __restrict__ phi_b,
                                                                  int parity,
                                                                  const int32_t* __restrict__ list) {
@@ -429,7 +429,7 @@ __device__ __forceinline__ void load_both(double* __restrict__ T0, double* __res
 // pinned where the parent row is inside (apply_pins(l-1)); the restricted
 // residual (or rhs) goes to the parent's rhs slot for k_fas.
 template <int D, int N, int MODE>
-__global__ void __launch_bounds__(Tile<D, N>::THREADS) k_restrict_tile(LevelView Lf, LevelView Lfc,
+__global__ void __launch_bounds__(Tile<D, N>::THREADS, Tile<D, N>::MINB) k_restrict_tile(LevelView Lf, LevelView Lfc,
                                                                        LevelView Lp,
                                                                        const double* __restrict__ phi_b) {
   pdl_begin();
@@ -471,6 +471,7 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_restrict_tile(LevelView
   };
   double gq[STEPS][2][2];
   int8_t skq[STEPS][2][2], psk[STEPS];
+  int rwq[STEPS][2][2];
   const int psr = Lp.srow[P];
 #pragma unroll
   for (int step = 0; step < STEPS; ++step) {
@@ -483,6 +484,7 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_restrict_tile(LevelView
       for (int x = 0; x < 2; ++x) {
         gq[step][dz][x] = 0.0;
         skq[step][dz][x] = 0;
+        rwq[step][dz][x] = -1;
       }
     if (!active) continue;
     for (int dz = 0; dz < (D == 3 ? 2 : 1); ++dz) {
@@ -494,8 +496,10 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_restrict_tile(LevelView
         const int cc = x ? 1 - c0 : c0;
         const size_t a = base + (size_t)cc * G::H + e;
         gq[step][dz][x] = MODE == RM_RES ? Lf.res[a] : Lf.rhs[a];
-        if (MODE == RM_FUSED && kind != KIND_UNIFORM)
+        if (MODE == RM_FUSED && kind != KIND_UNIFORM) {
           skq[step][dz][x] = Lf.skind[(size_t)fsr * G::NI + (size_t)cc * G::H + e];
+          rwq[step][dz][x] = Lf.row_of[(size_t)fsr * G::NI + (size_t)cc * G::H + e];
+        }
       }
     }
     if (!(jj & 1) && psr >= 0) {
@@ -506,9 +510,7 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_restrict_tile(LevelView
   both.store(T0s, T1s);
   cp_async_wait_all();
   __syncthreads();
-  const int32_t* rowp = kind == KIND_UNIFORM ? nullptr : Lf.row_of + (size_t)fsr * G::NI;
-  auto cell = [&](int jj, int kk, int cc, double g, int sk, double& phi_out) -> double {
-    const int e = m + HN * (jj + N * kk);
+  auto cell = [&](int jj, int kk, int cc, double g, int sk, int r, double& phi_out) -> double {
     const int B = (D == 3 ? ((kk + 1) * TT::P + (jj + 1)) : (jj + 1)) * TT::RW + m;
     const int o = (cc + jj + kk) & 1;
     const double* Tc = cc ? T1s : T0s;
@@ -517,7 +519,6 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_restrict_tile(LevelView
     phi_out = self;
     if (MODE != RM_FUSED) return g;
     if (sk == 1) return 0.0;
-    const int r = sk == 2 ? rowp[cc * G::H + e] : -1;
     double p[2 * D];
     nbrs_at<D, N>(To, B, o, p);
     return resid_value<D>(Lf, phi_b, r, self, p, g);
@@ -531,8 +532,8 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_restrict_tile(LevelView
       for (int dz = 0; dz < (D == 3 ? 2 : 1); ++dz) {
         const int kk = D == 3 ? 2 * kp + dz : 0;
         const int c0 = (jj + kk) & 1;  // colour of i = 2m
-        r_[dz][0] = cell(jj, kk, c0, gq[step][dz][0], skq[step][dz][0], f_[dz][0]);
-        r_[dz][1] = cell(jj, kk, 1 - c0, gq[step][dz][1], skq[step][dz][1], f_[dz][1]);
+        r_[dz][0] = cell(jj, kk, c0, gq[step][dz][0], skq[step][dz][0], rwq[step][dz][0], f_[dz][0]);
+        r_[dz][1] = cell(jj, kk, 1 - c0, gq[step][dz][1], skq[step][dz][1], rwq[step][dz][1], f_[dz][1]);
       }
     }
     double pr[2][2], pf[2][2];  // the y+1 partner's values
@@ -566,7 +567,7 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_restrict_tile(LevelView
 
 // ------------------------------------------------------------------ FAS + OLD snapshot
 template <int D, int N, bool FAS>
-__global__ void __launch_bounds__(Tile<D, N>::THREADS) k_fas_tile(LevelView L, LevelView Lc,
+__global__ void __launch_bounds__(Tile<D, N>::THREADS, Tile<D, N>::MINB) k_fas_tile(LevelView L, LevelView Lc,
                                                                   const double* __restrict__ phi_b) {
   pdl_begin();
   if (!owned(L, blockIdx.x)) return;  // multi-GPU: another rank's block
@@ -586,7 +587,8 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_fas_tile(LevelView L, L
   Both<D, N> b;
   b.issue(L, Lc, slot, true);
   double rq[2][O::PER];
-  int8_t skq[2][O::PER];  // special-row kinds, in flight with the fields (k_record_tile)
+  int8_t skq[2][O::PER];  // special-row kinds and row indices, in flight with the fields (k_record_tile)
+  int rwq[2][O::PER];
 #pragma unroll
   for (int q = 0; q < O::PER; ++q) {
     const int e = threadIdx.x + q * O::THR;
@@ -594,11 +596,12 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_fas_tile(LevelView L, L
     rq[1][q] = L.rhs[base + G::H + e];
     skq[0][q] = kind == KIND_UNIFORM ? (int8_t)0 : L.skind[(size_t)sr * G::NI + e];
     skq[1][q] = kind == KIND_UNIFORM ? (int8_t)0 : L.skind[(size_t)sr * G::NI + G::H + e];
+    rwq[0][q] = kind == KIND_UNIFORM ? -1 : L.row_of[(size_t)sr * G::NI + e];
+    rwq[1][q] = kind == KIND_UNIFORM ? -1 : L.row_of[(size_t)sr * G::NI + G::H + e];
   }
   b.store(T0, T1);
   cp_async_wait_all();
   __syncthreads();
-  const int32_t* rowp = kind == KIND_UNIFORM ? nullptr : L.row_of + (size_t)sr * G::NI;
 #pragma unroll
   for (int q = 0; q < O::PER; ++q) {
     int j, k, B;
@@ -610,7 +613,7 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_fas_tile(LevelView L, L
       const double* Tc = c ? T1 : T0;
       const double* To = c ? T0 : T1;
       const double self = Tc[B + o];
-      const int r = skq[c][q] == 2 ? rowp[c * G::H + e] : -1;
+      const int r = rwq[c][q];
       double out;
       if (skq[c][q] == 1) {
         out = 0.0;
@@ -632,7 +635,7 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_fas_tile(LevelView L, L
 // A thread's entry e is an x-pair (i = 2m, 2m+1) under one parent column:
 // both cells share the centre, y and z terms and differ in the x term.
 template <int D, int N, bool FULL>
-__global__ void __launch_bounds__(Tile<D, N>::THREADS) k_prolong_tile(LevelView Lf, LevelView Lp,
+__global__ void __launch_bounds__(Tile<D, N>::THREADS, Tile<D, N>::MINB) k_prolong_tile(LevelView Lf, LevelView Lp,
                                                                       LevelView Lpp) {
   pdl_begin();
   if (!owned(Lf, blockIdx.x)) return;  // multi-GPU: another rank's block
@@ -777,7 +780,7 @@ __device__ __forceinline__ void record_finish(const LevelView& L, Rec* __restric
 }
 
 template <int D, int N>
-__global__ void __launch_bounds__(Tile<D, N>::THREADS) k_record_tile(LevelView L, LevelView Lc,
+__global__ void __launch_bounds__(Tile<D, N>::THREADS, Tile<D, N>::MINB) k_record_tile(LevelView L, LevelView Lc,
                                                                      const double* __restrict__ phi_b,
                                                                      Rec* __restrict__ partial,
                                                                      Rec* rec, unsigned int* counter,
@@ -800,6 +803,7 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_record_tile(LevelView L
   // special-row kinds of this thread's cells (skind: 0 uniform, 1 inside, 2
   // cut), in flight with the fields: only a cut row then needs its row index
   int8_t skq[2][O::PER];
+  int rwq[2][O::PER];  // and the row indices (used by the cut rows only)
   if (leaf) {
     Both<D, N> b;
     b.issue(L, Lc, slot, true);
@@ -810,22 +814,22 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_record_tile(LevelView L
       gq[1][q] = L.rhs[base + G::H + e];
       skq[0][q] = kind == KIND_UNIFORM ? (int8_t)0 : L.skind[(size_t)sr * G::NI + e];
       skq[1][q] = kind == KIND_UNIFORM ? (int8_t)0 : L.skind[(size_t)sr * G::NI + G::H + e];
+      rwq[0][q] = kind == KIND_UNIFORM ? -1 : L.row_of[(size_t)sr * G::NI + e];
+      rwq[1][q] = kind == KIND_UNIFORM ? -1 : L.row_of[(size_t)sr * G::NI + G::H + e];
     }
     b.store(T0, T1);
   }
   cp_async_wait_all();
   __syncthreads();
   if (leaf) {
-    const int32_t* rowp = kind == KIND_UNIFORM ? nullptr : L.row_of + (size_t)sr * G::NI;
 #pragma unroll
     for (int q = 0; q < O::PER; ++q) {
       int j, k, B;
       O::at(q, j, k, B);
-      const int e = threadIdx.x + q * O::THR;
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         if (skq[c][q] == 1) continue;
-        const int r = skq[c][q] == 2 ? rowp[c * G::H + e] : -1;
+        const int r = rwq[c][q];
         const int o = (c + j + k) & 1;
         double p[2 * D];
         nbrs_at<D, N>(c ? T0 : T1, B, o, p);
@@ -837,14 +841,15 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_record_tile(LevelView L
       }
     }
   }
-  record_finish(L, partial, rec, counter, slot, mx, ss, cnt, sm, &last);
+  // without a counter the partials are per list position, folded by k_record_fold
+  record_finish(L, partial, rec, counter, counter ? slot : (int)blockIdx.x, mx, ss, cnt, sm, &last);
 }
 
 // Lean record for interior uniform blocks: both colours asynchronously into
 // shared memory, halos gathered from the same-level neighbours, uniform
 // residual g - (sum_6 - 2D phi) w (stencil.hpp:336-342) for every cell.
 template <int D, int N>
-__global__ void __launch_bounds__(Tile<D, N>::THREADS) k_record_lean(LevelView L,
+__global__ void __launch_bounds__(Tile<D, N>::THREADS, Tile<D, N>::MINB) k_record_lean(LevelView L,
                                                                      Rec* __restrict__ partial,
                                                                      Rec* rec, unsigned int* counter,
                                                                      const int32_t* __restrict__ list) {
@@ -934,7 +939,8 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS) k_record_lean(LevelView L
       }
     }
   }
-  record_finish(L, partial, rec, counter, slot, mx, ss, cnt, sm, &last);
+  // without a counter the partials are per list position, folded by k_record_fold
+  record_finish(L, partial, rec, counter, counter ? slot : (int)blockIdx.x, mx, ss, cnt, sm, &last);
 }
 
 }  // namespace pmgdev

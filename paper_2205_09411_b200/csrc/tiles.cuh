@@ -24,6 +24,11 @@ struct Tile {
   // 3D N = 8: 128 threads (two entries each) -- twice as many blocks resident per
   // SM, which is what these latency-bound kernels need (cfg3: 1.29 -> 1.20 ms per cycle)
   static constexpr int THREADS = (D == 3 && N == 8) ? 128 : (Geo<D, N>::H < 256 ? Geo<D, N>::H : 256);
+  // resident CTAs per SM asked of the compiler (register cap)
+#ifndef PMG_TILE8_MINB
+#define PMG_TILE8_MINB 12
+#endif
+  static constexpr int MINB = (D == 3 && N == 8) ? PMG_TILE8_MINB : 1;
   __device__ __forceinline__ static int idx(int ip, int jp, int kp) {
     return (D == 3 ? kp * P + jp : jp) * RW + (ip >> 1);
   }
