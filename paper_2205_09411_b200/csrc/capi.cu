@@ -142,14 +142,44 @@ static void upload_bc(Ctx& c) {
 // block (no coarse-fine face), per level and colour, with its row index in
 // the level's row arrays and the addresses of its 2D neighbour values
 // (same block, same-level neighbour block, or a physical-face code).
+// 3D N = 8 / 16: the streaming GS kernel also takes blocks with coarse-fine
+// faces (their ghosts from the cfc table), unless a cut row sits on such a
+// face (k_gs_cut's gather entries cannot express a coarse-fine ghost)
+static bool stream_dn(const Ctx& c) { return c.dim == 3 && (c.N == 8 || c.N == 16); }
+static bool has_cf_face(const Ctx& c, int id) {
+  for (int f = 0; f < c.F; ++f)
+    if (c.mesh.nbr[(size_t)id * 6 + f] < 0 && c.mesh.cnbr[(size_t)id * 6 + f] >= 0) return true;
+  return false;
+}
+static bool cf_streamable(const Ctx& c, int id) {
+  const HostStencils& st = c.st;
+  if (!stream_dn(c) || !has_cf_face(c, id)) return false;
+  if (!st.valid || !st.boundary[(size_t)id]) return true;
+  const int N = c.N, r0 = st.row_start[(size_t)id];
+  for (int f = 0; f < c.F; ++f) {
+    if (!(c.mesh.nbr[(size_t)id * 6 + f] < 0 && c.mesh.cnbr[(size_t)id * 6 + f] >= 0)) continue;
+    const int ax = f >> 1, fix = (f & 1) ? N - 1 : 0;
+    for (int v = 0; v < N; ++v)
+      for (int u = 0; u < N; ++u) {
+        int q[3];
+        q[ax] = fix;
+        q[ax == 0 ? 1 : 0] = u;
+        q[ax == 2 ? 1 : 2] = v;
+        const int r = st.row_at((size_t)id, (size_t)(q[0] + N * (q[1] + N * q[2])));
+        if (r >= 0 && st.mask[(size_t)(r0 + r)] != PMG_INSIDE) return false;
+      }
+  }
+  return true;
+}
+
 static void build_cut_tables(Ctx& c) {
   const HostMesh& m = c.mesh;
   const HostStencils& st = c.st;
   const int N = c.N, D = c.dim, NI = c.NI, H = NI / 2, F = c.F;
   for (int l = 1; l <= m.L; ++l) {
     LevelDev& d = *c.lev[(size_t)l];
-    std::vector<int32_t> ent[2], off[2];
-    std::vector<double> gbc[2], coef[2];
+    std::vector<int32_t> ent[2], off[2], entc[2];
+    std::vector<double> gbc[2], coef[2], gbcc[2], coefc[2];  // ..c: blocks with coarse-fine faces (gs_cf)
     int base = 0;  // row offset of the block within the level's row arrays (upload_stencils order)
     for (int s = 0; s < d.nb && st.valid; ++s) {
       const int id = m.slots[(size_t)l][(size_t)s];
@@ -163,7 +193,8 @@ static void build_cut_tables(Ctx& c) {
         const int r = st.row_at((size_t)id, (size_t)ii);
         if (r < 0 || st.mask[(size_t)(r0 + r)] != PMG_INSIDE) all_inside = false;
       }
-      if (no_cf && !all_inside && own_slot(c, l, s))
+      const bool cfs = !no_cf && cf_streamable(c, id);
+      if ((no_cf || cfs) && !all_inside && own_slot(c, l, s))
         for (int ii = 0; ii < NI; ++ii) {
           const int r = st.row_at((size_t)id, (size_t)ii);
           if (r < 0 || st.mask[(size_t)(r0 + r)] == PMG_INSIDE) continue;
@@ -185,6 +216,7 @@ static void build_cut_tables(Ctx& c) {
               e[2 + f] = (int32_t)((size_t)m.slot_of[(size_t)nid] * NI + cs_addr(q[0] + N * (q[1] + N * q[2]), N, D, H));
               continue;
             }
+            require(m.cnbr[(size_t)id * 6 + f] < 0, "cut row on a coarse-fine face in a streamed block", PMG_ERR_STATE);
             if (c.bctype[f] == PMG_BC_NEUMANN_ZERO) {
               e[2 + f] = -1;
               continue;
@@ -195,8 +227,8 @@ static void build_cut_tables(Ctx& c) {
               gb[f] = c.face_vals[f][(size_t)c.face_off[f][(size_t)id] + t];
             }
           }
-          ent[cc].insert(ent[cc].end(), e, e + 8);
-          gbc[cc].insert(gbc[cc].end(), gb, gb + 6);
+          (cfs ? entc : ent)[cc].insert((cfs ? entc : ent)[cc].end(), e, e + 8);
+          (cfs ? gbcc : gbc)[cc].insert((cfs ? gbcc : gbc)[cc].end(), gb, gb + 6);
           // row coefficients, with each cut direction's bc * phi_b product formed
           // here exactly as the reference forms it (stencil.hpp:344-358)
           const size_t q = (size_t)(r0 + r);
@@ -211,7 +243,7 @@ static void build_cut_tables(Ctx& c) {
             }
           }
           cf[13] = (double)bm;
-          coef[cc].insert(coef[cc].end(), cf, cf + 16);
+          (cfs ? coefc : coef)[cc].insert((cfs ? coefc : coef)[cc].end(), cf, cf + 16);
         }
       base += rc;
     }
@@ -223,6 +255,10 @@ static void build_cut_tables(Ctx& c) {
       d.cut_ent[cc].upload(ent[cc], c.stream);
       d.cut_gbc[cc].upload(gbc[cc], c.stream);
       d.cut_coef[cc].upload(coef[cc], c.stream);
+      d.n_cutcf[cc] = (int)entc[cc].size() / 8;
+      d.cutcf_ent[cc].upload(entc[cc], c.stream);
+      d.cutcf_gbc[cc].upload(gbcc[cc], c.stream);
+      d.cutcf_coef[cc].upload(coefc[cc], c.stream);
     }
   }
 }
@@ -465,7 +501,8 @@ static void upload_stencils(Ctx& c) {
     kindv[(size_t)l] = kind;
     // block classes for the specialised kernels
     {
-      std::vector<int32_t> fast, slow, ufast, uslow, fix[2], gsl, rsl, url;
+      std::vector<int32_t> fast, slow, ufast, uslow, fix[2], gsl, rsl, url, gslow;
+      d.gs_cf = false;
       for (int s = 0; s < d.nb; ++s) {
         if (!own_slot(c, l, s)) continue;
         const int id = m.slots[(size_t)l][(size_t)s];
@@ -473,6 +510,29 @@ static void upload_stencils(Ctx& c) {
         for (int f = 0; f < F; ++f)
           no_cf = no_cf && !(m.nbr[(size_t)id * 6 + f] < 0 && m.cnbr[(size_t)id * 6 + f] >= 0);
         (no_cf ? fast : slow).push_back(s);
+        if (!no_cf && stream_dn(c)) {
+          // coarse-fine faces: streamed with the faces' cfc pages as neighbour
+          // codes -2 - page (stream.cuh BlockPlan), unless a cut row sits on one
+          if (kind[(size_t)s] == pmgdev::KIND_ALL_INSIDE) {
+            // nothing to sweep
+          } else if (cf_streamable(c, id)) {
+            int pm = 0;
+            int32_t ns[6] = {-1, -1, -1, -1, -1, -1};
+            for (int f = 0; f < F; ++f) {
+              const int nid = m.nbr[(size_t)id * 6 + f];
+              if (nid >= 0) ns[f] = m.slot_of[(size_t)nid];
+              else if (m.cnbr[(size_t)id * 6 + f] >= 0) ns[f] = -2 - d.cfoff_host[(size_t)s * F + f] / c.NT;
+              else pm |= 1 << f;
+            }
+            const int sr = srow[(size_t)s] < 0 ? 0 : srow[(size_t)s];
+            require(sr < (1 << 17), "too many interface blocks on one level for the streaming plan");
+            const int32_t e[8] = {s, (int32_t)kind[(size_t)s] | (pm << 8) | (sr << 14), ns[0], ns[1], ns[2], ns[3], ns[4], ns[5]};
+            gsl.insert(gsl.end(), e, e + 8);
+            d.gs_cf = true;
+          } else {
+            gslow.push_back(s);
+          }
+        }
         if (no_cf) {
           // stream.cuh BlockPlan: slot, kind | phys << 8 | srow << 14, 6 neighbour slots
           int pm = 0;
@@ -514,6 +574,8 @@ static void upload_stencils(Ctx& c) {
       d.n_slow = (int)slow.size();
       d.fast_list.upload(fast, c.stream);
       d.slow_list.upload(slow, c.stream);
+      d.n_gs_slow = (int)gslow.size();
+      d.gs_slow.upload(gslow, c.stream);
       d.n_ufast = (int)ufast.size();
       d.n_uslow = (int)uslow.size();
       d.ufast_list.upload(ufast, c.stream);
@@ -1281,6 +1343,7 @@ static void set_mesh(Ctx& c, int nb, const int32_t* level, const int32_t* coords
         }
     }
     d.has_cfold = n > 0;
+    d.cfoff_host = cfo;
     d.cfoff.upload(cfo, c.stream);
     d.cfold.alloc((size_t)std::max(n, 1));
     // the same faces, listed, and their cfc pages (LevelView::cfc)

@@ -274,6 +274,17 @@ struct LevelDev {
   // changed since the table was built
   DevBuf<int32_t> cf_faces;
   int n_cf = 0;
+  std::vector<int32_t> cfoff_host;  // cfoff as uploaded (the streaming plans carry the cfc page numbers)
+  // streaming GS of blocks with coarse-fine faces (3D N = 8 / 16): they join
+  // gs_plan with their faces' cfc pages (BlockPlan), their cut rows have
+  // their own k_gs_cut tables, and only blocks with a cut row ON a
+  // coarse-fine face stay with k_gs_tile (gs_slow)
+  bool gs_cf = false;
+  DevBuf<int32_t> gs_slow;
+  int n_gs_slow = 0;
+  DevBuf<int32_t> cutcf_ent[2];
+  DevBuf<double> cutcf_gbc[2], cutcf_coef[2];
+  int n_cutcf[2] = {0, 0};
   DevBuf<double> cfc;
   bool cfc_dirty = true;
   bool dense = false;   // all blocks present, slot == Morton code

@@ -82,25 +82,37 @@ struct OpsImpl final : Ops {
       const int nfix = stream ? 0 : d.n_fix[parity];
       const bool lean_work = stream || d.n_fast > 0;
       const int ncut = stream ? d.n_cut[parity] : 0;
-      const bool fork = lean_work && (d.n_slow > 0 || nfix > 0 || ncut > 0);
-      const LevelView Lt = d.n_slow > 0 ? Vt(c, l) : L;  // before the fork: a table rebuild runs on c.stream
+      // streaming: blocks with coarse-fine faces are in the plan too (gs_cf),
+      // except the few with a cut row on such a face (gs_slow)
+      const int n_tile = stream ? d.n_gs_slow : d.n_slow;
+      const int32_t* tile_list = stream ? d.gs_slow.p : d.slow_list.p;
+      const int ncutcf = stream ? d.n_cutcf[parity] : 0;
+      const bool fork = lean_work && (n_tile > 0 || nfix > 0 || ncut > 0 || ncutcf > 0);
+      const LevelView Lt = d.n_cf > 0 ? Vt(c, l) : L;  // before the fork: a table rebuild runs on c.stream
       if (fork) {
         PMG_CUDA(cudaEventRecord(c.ev_fork, c.stream));
         PMG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
       }
       cudaStream_t s2 = fork ? c.side : c.stream;
-      if (d.n_slow > 0)
-        pdl_launch(k_gs_tile<D, N>, d.n_slow, TT::THREADS, 0, s2, Lt, Vc(c, l), c.phi_b.p, parity, d.slow_list.p);
+      if (n_tile > 0)
+        pdl_launch(k_gs_tile<D, N>, n_tile, TT::THREADS, 0, s2, Lt, Vc(c, l), c.phi_b.p, parity, tile_list);
       if (nfix > 0)
         pdl_launch(k_gs_fix<D, N>, grid_for(nfix, 128), 128, 0, s2, L, Vc(c, l), c.phi_b.p, parity,
                                                            (const int2*)d.fix_list[parity].p, nfix);
       if (ncut > 0)  // cut rows: disjoint from the streaming kernel's cells and inputs
         pdl_launch(k_gs_cut<D>, grid_for(ncut, 128), 128, 0, s2, L, (const int32_t*)d.cut_ent[parity].p,
                    (const double*)d.cut_gbc[parity].p, (const double*)d.cut_coef[parity].p, ncut);
+      if (ncutcf > 0)
+        pdl_launch(k_gs_cut<D>, grid_for(ncutcf, 128), 128, 0, s2, L, (const int32_t*)d.cutcf_ent[parity].p,
+                   (const double*)d.cutcf_gbc[parity].p, (const double*)d.cutcf_coef[parity].p, ncutcf);
       if (stream) {
         if constexpr (D == 3 && (N == 8 || N == 16)) {
           constexpr int T256 = N == 16 ? 256 : 0;
-          if (T256 && d.n_gs <= c.sms * 4)  // one block per CTA, all resident at once
+          if (d.gs_cf) {
+            if constexpr (N == 8) launch_gs_stream<2, 8, 128, true>(c, Lt, d, parity);
+            else launch_gs_stream<kStreamStages, kStreamCtasPerSm, 0, true>(c, Lt, d, parity);
+          }
+          else if (T256 && d.n_gs <= c.sms * 4)  // one block per CTA, all resident at once
             launch_gs_stream<1, 4, T256>(c, L, d, parity);
           else if (N == 8)  // 512-cell blocks: 128-thread CTAs, eight per SM (40.0 vs 45.1 us per
             launch_gs_stream<2, 8, 128>(c, L, d, parity);  // half-sweep on cfg3's finest level with <2, 2, 256>)
@@ -163,16 +175,16 @@ struct OpsImpl final : Ops {
     }
     return false;
   }
-  template <int ST, int MINB, int TH>
+  template <int ST, int MINB, int TH, bool CF = false>
   void launch_gs_stream(Ctx& c, const LevelView& L, const LevelDev& d, int parity) {
     if constexpr (D == 3 && (N == 8 || N == 16)) {
       using S = Stream3<N, TH>;
-      constexpr size_t smem = (size_t)ST * S::STAGE * sizeof(double);
-      set_smem_attr(c, (const void*)k_gs_stream<N, ST, MINB, TH>, smem);
+      constexpr size_t smem = (size_t)ST * (S::STAGE + (CF ? 6 * S::FH : 0)) * sizeof(double);
+      set_smem_attr(c, (const void*)k_gs_stream<N, ST, MINB, TH, CF>, smem);
       const int grid = std::min(d.n_gs, c.sms * MINB);
       // PDL: the prologue overlaps the previous kernel's drain; parity 1 walks
       // the plan backwards (starts on the blocks the red half-sweep wrote last)
-      pdl_launch_on(k_gs_stream<N, ST, MINB, TH>, grid, S::THR, smem, c.stream, L, parity, c.phi_b.p,
+      pdl_launch_on(k_gs_stream<N, ST, MINB, TH, CF>, grid, S::THR, smem, c.stream, L, parity, c.phi_b.p,
                     (const int4*)d.gs_plan.p, d.n_gs, parity);
     }
   }

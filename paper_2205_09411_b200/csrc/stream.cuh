@@ -73,7 +73,8 @@ __device__ __forceinline__ void cp_async_wait() {
 // ------------------------------------------------------------------ per-block plan
 // Host-built, one int4 pair per lean block of a level (capi.cu upload_stencils):
 // a = {slot, kind | physical-face mask << 8 | srow << 14, nbr(-x), nbr(+x)},
-// b = {nbr(-y), nbr(+y), nbr(-z), nbr(+z)}   (-1 = physical face).
+// b = {nbr(-y), nbr(+y), nbr(-z), nbr(+z)}   (-1 = physical face; -2 - p =
+// coarse-fine face whose cfc page is p, only in the plans of the CF kernels).
 struct BlockPlan {
   int4 a, b;
   __device__ __forceinline__ int slot() const { return a.x; }
@@ -213,15 +214,39 @@ __device__ __forceinline__ void gs_issue_async(const LevelView& L, const BlockPl
   }
 }
 
+// CF kernels: the colour-c halves of the cfc pages of the block's coarse-fine
+// faces (16-B chunks) into the stage's extra 6 FH doubles; returns their mask.
+template <int N, int TH>
+__device__ __forceinline__ void cf_issue_async(const LevelView& L, const BlockPlan& P, int c, double* dst, int t) {
+  using S = Stream3<N, TH>;
+  constexpr int CH = S::FH / 2;
+  for (int u = t; u < 6 * CH; u += S::THR) {
+    const int f = u / CH, ch = u % CH;
+    const int code = P.nbr(f);
+    if (code <= -2)
+      cp_async16(dst + f * S::FH + 2 * ch, L.cfc + (size_t)(-2 - code) * (2 * S::FH) + (size_t)c * S::FH + 2 * ch);
+  }
+}
+__device__ __forceinline__ int cf_mask_of(const BlockPlan& P) {
+  int m = 0;
+#pragma unroll
+  for (int f = 0; f < 6; ++f) m |= (P.nbr(f) <= -2 ? 1 : 0) << f;
+  return m;
+}
+
 // Physical faces: the staged own-colour values become ghosts 2 bc - f1
 // (Dirichlet) or stay f1 (Neumann), mesh.hpp:538-552.
-template <int N>
+// CF: faces in cfmask are coarse-fine -- the staged own value f1 becomes
+// 1/2 c + 3/4 f1 - 1/4 f2 (mesh.hpp:500-535) with c from the staged cfc page
+// (at S::STAGE + dir * FH) and f2 the other-colour value one cell inward.
+template <int N, bool CF = false>
 __device__ __forceinline__ void gs_phys_faces(const LevelView& L, int slot, int pmask, int c, double* st, int t0,
-                                              int nt) {
+                                              int nt, int cfmask = 0) {
   using S = Stream3<N>;
   constexpr int NX = N * N;  // x rows (two sides)
   for (int q = t0; q < NX + 4 * S::FH; q += nt) {
     int dir, i, tj;
+    int ci, e2;  // CF: position in the face's cfc page, entry of f2 in the staged half
     double* h;
     if (q < NX) {
       int side, j, k;
@@ -230,6 +255,8 @@ __device__ __forceinline__ void gs_phys_faces(const LevelView& L, int slot, int 
       i = side ? N - 1 : 0;
       tj = j + N * k;
       h = st + S::OXF + side * N * N + k * N + j;
+      ci = tj >> 1;
+      e2 = ((side ? N - 2 : 1) + N * tj) >> 1;
     } else {
       const int qq = q - NX;
       const int f = qq / S::FH, r = qq % S::FH;  // f: 0 -y, 1 +y, 2 -z, 3 +z
@@ -238,12 +265,21 @@ __device__ __forceinline__ void gs_phys_faces(const LevelView& L, int slot, int 
       if (f < 2) {
         const int j = f ? N - 1 : 0;
         i = 2 * m + ((c + j + a) & 1);
+        e2 = m + S::HN * ((f ? N - 2 : 1) + N * a);
       } else {
         const int k = f == 3 ? N - 1 : 0;
         i = 2 * m + ((c + a + k) & 1);
+        e2 = m + S::HN * (a + N * (f == 3 ? N - 2 : 1));
       }
       tj = i + N * a;
+      ci = r;
       h = st + (f < 2 ? S::OY + f * S::FH : S::OZ + (f - 2) * S::FH) + r;
+    }
+    if (CF && ((cfmask >> dir) & 1)) {
+      const double cv = st[S::STAGE + dir * S::FH + ci];
+      const double f1 = *h, f2 = st[S::OX + e2];
+      *h = 0.5 * cv + 0.75 * f1 - 0.25 * f2;
+      continue;
     }
     if (!((pmask >> dir) & 1) || L.bctype[dir] == 1) continue;
     double bcv = 0.0;
@@ -352,7 +388,8 @@ __device__ __forceinline__ void gs_stream_column(const LevelView& L, const doubl
 // rev: walk the plan backwards.  Alternating the direction between the two
 // half-sweeps makes each sweep start on the blocks the previous one wrote
 // last -- the ones still in the 126 MB L2.
-template <int N, int S_STAGES, int MINB, int TH>
+// CF: the plan may hold blocks with coarse-fine faces (L.cfc set, built).
+template <int N, int S_STAGES, int MINB, int TH, bool CF = false>
 __global__ void __launch_bounds__(Stream3<N, TH>::THR, MINB) k_gs_stream(LevelView L, int parity,
                                                                         const double* __restrict__ phi_b,
                                                                         const int4* __restrict__ plan, int n,
@@ -362,9 +399,10 @@ __global__ void __launch_bounds__(Stream3<N, TH>::THR, MINB) k_gs_stream(LevelVi
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   using S = Stream3<N, TH>;
   constexpr int NI = N * N * N;
+  constexpr int STAGE = S::STAGE + (CF ? 6 * S::FH : 0);
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t full[S_STAGES];
-  __shared__ int meta[S_STAGES][2];
+  __shared__ int meta[S_STAGES][CF ? 3 : 2];
   const int c = parity;
   const int t = threadIdx.x;
   const int G = gridDim.x;
@@ -382,9 +420,13 @@ __global__ void __launch_bounds__(Stream3<N, TH>::THR, MINB) k_gs_stream(LevelVi
   for (int s = 0; s < S_STAGES; ++s) {
     if (s < nmine) {
       const BlockPlan P = R.get(s);
-      if (t == 0) gs_issue<N>(L, P, c, sm + s * S::STAGE, &full[s]);
+      if (t == 0) gs_issue<N>(L, P, c, sm + s * STAGE, &full[s]);
       if (t == 0) meta[s][0] = P.slot(), meta[s][1] = P.a.y;
-      gs_issue_async<N, TH>(L, P, c, sm + s * S::STAGE, t);
+      gs_issue_async<N, TH>(L, P, c, sm + s * STAGE, t);
+      if (CF) {
+        if (t == 0) meta[s][CF ? 2 : 0] = cf_mask_of(P);
+        cf_issue_async<N, TH>(L, P, c, sm + s * STAGE + S::STAGE, t);
+      }
     }
     cp_async_commit();
   }
@@ -404,20 +446,21 @@ __global__ void __launch_bounds__(Stream3<N, TH>::THR, MINB) k_gs_stream(LevelVi
   }
   for (int it = 0; it < nmine; ++it) {
     const int s = it % S_STAGES;
-    double* st = sm + s * S::STAGE;
+    double* st = sm + s * STAGE;
     R.advance(plan, it, nmine, G);
     mbar_wait(&full[s], (uint32_t)((it / S_STAGES) & 1));
     cp_async_wait<S_STAGES - 1>();
     __syncthreads();
     const int slot = meta[s][0], flags = meta[s][1];
     const int kind = flags & 0xff, pmask = (flags >> 8) & 63;
+    const int cfmask = CF ? meta[s][CF ? 2 : 0] : 0;
     if (S_STAGES > 1 && it + 1 < nmine) {  // this thread's g of the next block, in flight during this one
       const double* gsrc = L.rhs + (size_t)meta[(it + 1) % S_STAGES][0] * NI + (size_t)c * S::H + gbase;
 #pragma unroll
       for (int q = 0; q < S::PER; ++q) gnext[q] = gsrc[q * gstep];
     }
-    if (pmask) {  // block-uniform branch
-      gs_phys_faces<N>(L, slot, pmask, c, st, t, blockDim.x);
+    if (pmask | cfmask) {  // block-uniform branch
+      gs_phys_faces<N, CF>(L, slot, pmask, c, st, t, blockDim.x, cfmask);
       __syncthreads();
     }
     gs_stream_column<N, TH>(L, st, c, kind, h2, slot, gcur, t);
@@ -427,6 +470,10 @@ __global__ void __launch_bounds__(Stream3<N, TH>::THR, MINB) k_gs_stream(LevelVi
       if (t == 0) gs_issue<N>(L, pf, c, st, &full[s]);
       if (t == 0) meta[s][0] = pf.slot(), meta[s][1] = pf.a.y;
       gs_issue_async<N, TH>(L, pf, c, st, t);
+      if (CF) {
+        if (t == 0) meta[s][CF ? 2 : 0] = cf_mask_of(pf);
+        cf_issue_async<N, TH>(L, pf, c, st + S::STAGE, t);
+      }
     }
     cp_async_commit();
     if (S_STAGES > 1) {
