@@ -501,7 +501,7 @@ static void upload_stencils(Ctx& c) {
     kindv[(size_t)l] = kind;
     // block classes for the specialised kernels
     {
-      std::vector<int32_t> fast, slow, ufast, uslow, fix[2], gsl, rsl, url, gslow;
+      std::vector<int32_t> fast, slow, ufast, uslow, fix[2], gsl, rsl, url, gslow, rcl, rcslow;
       d.gs_cf = false;
       for (int s = 0; s < d.nb; ++s) {
         if (!own_slot(c, l, s)) continue;
@@ -529,8 +529,10 @@ static void upload_stencils(Ctx& c) {
             const int32_t e[8] = {s, (int32_t)kind[(size_t)s] | (pm << 8) | (sr << 14), ns[0], ns[1], ns[2], ns[3], ns[4], ns[5]};
             gsl.insert(gsl.end(), e, e + 8);
             d.gs_cf = true;
+            if (m.children[(size_t)id * 8] < 0) rcl.insert(rcl.end(), e, e + 8);
           } else {
             gslow.push_back(s);
+            if (m.children[(size_t)id * 8] < 0) rcslow.push_back(s);
           }
         }
         if (no_cf) {
@@ -548,6 +550,7 @@ static void upload_stencils(Ctx& c) {
           rsl.insert(rsl.end(), e, e + 8);
           if (kind[(size_t)s] == pmgdev::KIND_UNIFORM) url.insert(url.end(), e, e + 8);
           if (kind[(size_t)s] != pmgdev::KIND_ALL_INSIDE) gsl.insert(gsl.end(), e, e + 8);
+          if (kind[(size_t)s] != pmgdev::KIND_ALL_INSIDE && m.children[(size_t)id * 8] < 0) rcl.insert(rcl.end(), e, e + 8);
         }
         (no_cf && kind[(size_t)s] == pmgdev::KIND_UNIFORM ? ufast : uslow).push_back(s);
         // cut (non-inside) rows of lean interface blocks, per colour, for k_gs_fix
@@ -576,6 +579,10 @@ static void upload_stencils(Ctx& c) {
       d.slow_list.upload(slow, c.stream);
       d.n_gs_slow = (int)gslow.size();
       d.gs_slow.upload(gslow, c.stream);
+      d.n_rc = (int)rcl.size() / 8;
+      d.rc_plan.upload(rcl, c.stream);
+      d.n_rc_slow = (int)rcslow.size();
+      d.rc_slow.upload(rcslow, c.stream);
       d.n_ufast = (int)ufast.size();
       d.n_uslow = (int)uslow.size();
       d.ufast_list.upload(ufast, c.stream);

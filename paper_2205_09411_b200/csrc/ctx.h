@@ -282,6 +282,11 @@ struct LevelDev {
   bool gs_cf = false;
   DevBuf<int32_t> gs_slow;
   int n_gs_slow = 0;
+  // streaming record (3D N = 8, or N = 16 with coarse-fine faces): the leaf
+  // blocks the column kernel can take (BlockPlan entries with cfc pages), and
+  // the leaf blocks with a cut row on a coarse-fine face (k_record_tile)
+  DevBuf<int32_t> rc_plan, rc_slow;
+  int n_rc = 0, n_rc_slow = 0;
   DevBuf<int32_t> cutcf_ent[2];
   DevBuf<double> cutcf_gbc[2], cutcf_coef[2];
   int n_cutcf[2] = {0, 0};

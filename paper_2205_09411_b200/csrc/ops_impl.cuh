@@ -443,6 +443,55 @@ struct OpsImpl final : Ops {
         return;
       }
     }
+    if constexpr (D == 3 && (N == 8 || N == 16)) {
+      const LevelDev& d = *c.lev[(size_t)l];
+      if ((N == 8 || d.has_cf) && d.n_rc > 0 && L.nb > kSmallLevel) {
+        // N = 8, or coarse-fine faces: the column kernel (k_resid_stream, MODE 1)
+        // over the leaf blocks of rc_plan, coarse-fine ghosts from the staged cfc
+        // pages; the cut rows from their two tables, leaf blocks with a cut row
+        // on a coarse-fine face by k_record_tile.  Partials: [0, G) streaming
+        // CTAs, [G, G + g1) / [.., + g2) the cut-row CTAs, then one per listed
+        // block; folded in that order.
+        constexpr int ST = 2, MINB = N == 8 ? 8 : 1, TTH = N == 8 ? 128 : 512;
+        using Q = QStream3<N, TTH>;
+        constexpr size_t smem = (size_t)ST * (Q::STAGE + 12 * Q::FH) * sizeof(double);
+        set_smem_attr(c, (const void*)k_resid_stream<N, ST, MINB, 1, TTH, true>, smem);
+        const int grid = std::min(d.n_rc, c.sms * MINB);
+        const int nc1 = d.n_cut[0] + d.n_cut[1], nc2 = d.n_cutcf[0] + d.n_cutcf[1];
+        const int g1 = nc1 > 0 ? (int)grid_for(nc1, 256) : 0, g2 = nc2 > 0 ? (int)grid_for(nc2, 256) : 0;
+        const LevelView Lt = Vt(c, l);
+        const bool fork = d.n_rc_slow > 0 || nc1 > 0 || nc2 > 0;
+        if (fork) {
+          PMG_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+          PMG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+        }
+        if (d.n_rc_slow > 0)
+          pdl_launch(k_record_tile<D, N>, d.n_rc_slow, TT::THREADS, 0, c.side, Lt, Vc(c, l), c.phi_b.p,
+                     c.partial.p + grid + g1 + g2, c.rec.p, (unsigned int*)nullptr, d.rc_slow.p);
+        if (nc1 > 0)
+          pdl_launch(k_record_cut<D>, g1, 256, 0, c.side, L, c.phi_b.p, d.cut_ent[0].p, d.cut_gbc[0].p, d.n_cut[0],
+                     d.cut_ent[1].p, d.cut_gbc[1].p, d.n_cut[1], G::NI, c.partial.p + grid);
+        if (nc2 > 0)
+          pdl_launch(k_record_cut<D>, g2, 256, 0, c.side, L, c.phi_b.p, d.cutcf_ent[0].p, d.cutcf_gbc[0].p,
+                     d.n_cutcf[0], d.cutcf_ent[1].p, d.cutcf_gbc[1].p, d.n_cutcf[1], G::NI,
+                     c.partial.p + grid + g1);
+        pdl_launch(k_resid_stream<N, ST, MINB, 1, TTH, true>, grid, Q::THR, smem, c.stream, Lt, Lt, c.phi_b.p,
+                   (const int4*)d.rc_plan.p, d.n_rc, c.partial.p, c.rec.p, (unsigned int*)nullptr);
+        if (fork) {
+          PMG_CUDA(cudaEventRecord(c.ev_join, c.side));
+          PMG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
+        }
+        FinishArgs fin{};
+        if (c.finish_level == l && c.h_out_dev) {
+          fin = FinishArgs{c.rec.p, c.mesh.L, l, c.outbuf.p, c.h_out_dev};
+          c.finished = true;
+        }
+        pdl_launch(k_record_fold, 1, 256, 0, c.stream, (const Rec*)c.partial.p, grid + g1 + g2 + d.n_rc_slow,
+                   c.rec.p + L.level, fin);
+        check();
+        return;
+      }
+    }
     if constexpr (D == 3 && N == 16) {
       const LevelDev& d = *c.lev[(size_t)l];
       if (d.n_rs > 0 && L.nb > kSmallLevel) {

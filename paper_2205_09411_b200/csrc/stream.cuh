@@ -550,33 +550,48 @@ __device__ __forceinline__ void rs_issue_async(const LevelView& L, const BlockPl
   }
 }
 
-template <int N, class S = RStream3<N>>
+// CF: faces in cfmask are coarse-fine -- the staged own value f1 becomes
+// 1/2 c + 3/4 f1 - 1/4 f2 (mesh.hpp:500-535), c from the cfc page staged at
+// S::STAGE + dir * 2 FH, f2 the own other-colour value one cell inward.
+template <int N, class S = RStream3<N>, bool CF = false>
 __device__ __forceinline__ void rs_phys_faces(const LevelView& L, int slot, int pmask, double* st, int t0 = -1,
-                                              int nt = 0) {
+                                              int nt = 0, int cfmask = 0) {
   if (t0 < 0) t0 = threadIdx.x, nt = blockDim.x;
   for (int q = t0; q < 2 * N * N + 8 * S::FH; q += nt) {
     int dir, tj;
+    int cb = 0, e2 = 0;  // CF: colour of the block's own face cell, entry of f2
     double* h;
     if (q < 2 * N * N) {
       const int side = q / (N * N), r = q % (N * N);
       dir = side;
       tj = r % N + N * (r / N);  // j + N k
       h = st + S::OXF + q;
+      cb = ((side ? N - 1 : 0) + r % N + r / N) & 1;
+      e2 = ((side ? N - 2 : 1) + N * tj) >> 1;
     } else {
       const int qq = q - 2 * N * N;
       const int f = qq / (2 * S::FH), cc = (qq / S::FH) % 2, r = qq % S::FH;  // f: -y +y -z +z
       dir = 2 + f;
       const int m = r % S::HN, a = r / S::HN;
       const int side = f & 1;
+      cb = cc;
       if (f < 2) {  // y face: a = k
         const int jb = side ? N - 1 : 0;
         tj = 2 * m + ((cc + jb + a) & 1) + N * a;
         h = st + S::OY + (side * 2 + cc) * S::FH + r;
+        e2 = m + S::HN * ((side ? N - 2 : 1) + N * a);
       } else {  // z face: a = j
         const int kb = side ? N - 1 : 0;
         tj = 2 * m + ((cc + a + kb) & 1) + N * a;
         h = st + S::OZ + (side * 2 + cc) * S::FH + r;
+        e2 = m + S::HN * (a + N * (side ? N - 2 : 1));
       }
+    }
+    if (CF && ((cfmask >> dir) & 1)) {
+      const double cv = st[S::STAGE + dir * 2 * S::FH + cb * S::FH + (tj >> 1)];
+      const double f1 = *h, f2 = st[S::OP + (1 - cb) * S::H + e2];
+      *h = 0.5 * cv + 0.75 * f1 - 0.25 * f2;
+      continue;
     }
     if (!((pmask >> dir) & 1) || L.bctype[dir] == 1) continue;
     double bcv = 0.0;
@@ -809,12 +824,25 @@ struct QStream3 {
   static constexpr int YC = 2 * 2 * N * (HN / 2);  // 16-B chunks of the y layers
 };
 
-template <int N, int TT>
+// CF: the cfc pages (both colours, 2 FH doubles) of the block's coarse-fine
+// faces follow the stage at S::STAGE + dir * 2 FH.
+template <int N, int TT, bool CF = false>
 __device__ __forceinline__ void qs_issue(const LevelView& L, const BlockPlan& P, double* st, uint64_t* bar) {
   using S = QStream3<N, TT>;
   constexpr int NI = N * N * N;
   const double* own = L.phi + (size_t)P.slot() * NI;
-  mbar_arrive_expect_tx(bar, S::TX_BYTES);
+  if (CF) {
+    const int ncf = __popc((unsigned)cf_mask_of(P));
+    mbar_arrive_expect_tx(bar, S::TX_BYTES + (uint32_t)ncf * 2u * S::FH * 8u);
+#pragma unroll
+    for (int f = 0; f < 6; ++f) {
+      const int code = P.nbr(f);
+      if (code <= -2)
+        bulk_g2s(st + S::STAGE + f * 2 * S::FH, L.cfc + (size_t)(-2 - code) * (2 * S::FH), 2 * S::FH * 8, bar);
+    }
+  } else {
+    mbar_arrive_expect_tx(bar, S::TX_BYTES);
+  }
   bulk_g2s(st + S::OP, own, 2 * S::H * 8, bar);
   for (int side = 0; side < 2; ++side) {
     const int ns = P.nbr(4 + side);
@@ -960,7 +988,7 @@ __device__ __forceinline__ void qs_restrict(const LevelView& Lp, int Pp, int cx,
   }
 }
 
-template <int N, int S_STAGES, int MINB, int MODE, int TT>
+template <int N, int S_STAGES, int MINB, int MODE, int TT, bool CF = false>
 __global__ void __launch_bounds__(QStream3<N, TT>::THR, MINB) k_resid_stream(LevelView Lf, LevelView Lp,
                                                                         const double* __restrict__ phi_b,
                                                                         const int4* __restrict__ plan, int n,
@@ -970,10 +998,11 @@ __global__ void __launch_bounds__(QStream3<N, TT>::THR, MINB) k_resid_stream(Lev
   using S = QStream3<N, TT>;
   constexpr int NI = N * N * N, HN = S::HN, H = S::H, FH = S::FH, PER = S::PER, KS = S::KS;
   static_assert(S_STAGES >= 2, "g of block it+1 is read through meta[] one iteration ahead");
-  static_assert(PER * KS == N && PER % 2 == 0 && HN == 8, "columns of whole z pairs; j + 1 is lane + 8");
+  static_assert(PER * KS == N && PER % 2 == 0 && 32 % (2 * HN) == 0, "columns of whole z pairs; j + 1 is lane + HN");
+  constexpr int STAGE = S::STAGE + (CF ? 12 * FH : 0);
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t full[S_STAGES];
-  __shared__ int meta[S_STAGES][2];
+  __shared__ int meta[S_STAGES][CF ? 3 : 2];
   __shared__ double red[72];
   __shared__ bool last;
   __shared__ int4 pring[PlanRing<S_STAGES>::PR * 2];
@@ -992,10 +1021,11 @@ __global__ void __launch_bounds__(QStream3<N, TT>::THR, MINB) k_resid_stream(Lev
     if (s < nmine) {
       const BlockPlan P = R.get(s);
       if (t == 0) {
-        qs_issue<N, TT>(Lf, P, sm + s * S::STAGE, &full[s]);
+        qs_issue<N, TT, CF>(Lf, P, sm + s * STAGE, &full[s]);
         meta[s][0] = P.slot(), meta[s][1] = P.a.y;
+        if (CF) meta[s][CF ? 2 : 0] = cf_mask_of(P);
       }
-      rs_issue_async<N, S>(Lf, P, sm + s * S::STAGE);
+      rs_issue_async<N, S>(Lf, P, sm + s * STAGE);
     }
     cp_async_commit();
   }
@@ -1014,10 +1044,11 @@ __global__ void __launch_bounds__(QStream3<N, TT>::THR, MINB) k_resid_stream(Lev
   double rmx = 0.0, rss = 0.0, rcnt = 0.0;  // MODE 1: this CTA's running totals
   for (int it = 0; it < nmine; ++it) {
     const int s = it % S_STAGES;
-    double* st = sm + s * S::STAGE;
+    double* st = sm + s * STAGE;
     R.advance(plan, it, nmine, G);
     const int slot = meta[s][0], flags = meta[s][1];
     const int kind = flags & 0xff, pmask = (flags >> 8) & 63;
+    const int cfmask = CF ? meta[s][CF ? 2 : 0] : 0;
     // per-block scalars and the special-row kinds, in flight across the wait
     int rr[2][PER];
     if (kind == KIND_IFACE) {
@@ -1046,8 +1077,8 @@ __global__ void __launch_bounds__(QStream3<N, TT>::THR, MINB) k_resid_stream(Lev
 #pragma unroll
         for (int q = 0; q < PER; ++q) gnext[c][q] = gsrc[c * H + q * FH];
     }
-    if (pmask) {  // block-uniform branch
-      rs_phys_faces<N, S>(Lf, slot, pmask, st);
+    if (pmask | cfmask) {  // block-uniform branch
+      rs_phys_faces<N, S, CF>(Lf, slot, pmask, st, -1, 0, cfmask);
       __syncthreads();
     }
     double col[2][PER], res[2][PER], ap[2][PER];
@@ -1069,8 +1100,9 @@ __global__ void __launch_bounds__(QStream3<N, TT>::THR, MINB) k_resid_stream(Lev
     if (it + S_STAGES < nmine) {
       const BlockPlan pf = R.get(it + S_STAGES);
       if (t == 0) {
-        qs_issue<N, TT>(Lf, pf, st, &full[s]);
+        qs_issue<N, TT, CF>(Lf, pf, st, &full[s]);
         meta[s][0] = pf.slot(), meta[s][1] = pf.a.y;
+        if (CF) meta[s][CF ? 2 : 0] = cf_mask_of(pf);
       }
       rs_issue_async<N, S>(Lf, pf, st);
     }
