@@ -172,6 +172,31 @@ static bool cf_streamable(const Ctx& c, int id) {
   return true;
 }
 
+// ... and for the streamed restriction: no cut row within two cells of a
+// coarse-fine face (the 2x2x2 children of a parent with a cut child are
+// gathered by k_restrict_fix, whose entries cannot express such a ghost)
+static bool cf_streamable_r(const Ctx& c, int id) {
+  const HostStencils& st = c.st;
+  if (!stream_dn(c) || !has_cf_face(c, id)) return false;
+  if (!st.valid || !st.boundary[(size_t)id]) return true;
+  const int N = c.N, r0 = st.row_start[(size_t)id];
+  for (int f = 0; f < c.F; ++f) {
+    if (!(c.mesh.nbr[(size_t)id * 6 + f] < 0 && c.mesh.cnbr[(size_t)id * 6 + f] >= 0)) continue;
+    const int ax = f >> 1;
+    for (int w = 0; w < 2; ++w)
+      for (int v = 0; v < N; ++v)
+        for (int u = 0; u < N; ++u) {
+          int q[3];
+          q[ax] = (f & 1) ? N - 1 - w : w;
+          q[ax == 0 ? 1 : 0] = u;
+          q[ax == 2 ? 1 : 2] = v;
+          const int r = st.row_at((size_t)id, (size_t)(q[0] + N * (q[1] + N * q[2])));
+          if (r >= 0 && st.mask[(size_t)(r0 + r)] != PMG_INSIDE) return false;
+        }
+  }
+  return true;
+}
+
 static void build_cut_tables(Ctx& c) {
   const HostMesh& m = c.mesh;
   const HostStencils& st = c.st;
@@ -363,6 +388,7 @@ static void cell_entry(const Ctx& c, int s, int id, int ii, int base, int32_t* e
       e[1 + f] = (int32_t)((size_t)m.slot_of[(size_t)nid] * NI + cs_addr(q[0] + N * (q[1] + N * q[2]), N, D, H));
       continue;
     }
+    require(m.cnbr[(size_t)id * 6 + f] < 0, "gather entry next to a coarse-fine face", PMG_ERR_STATE);
     if (c.bctype[f] == PMG_BC_NEUMANN_ZERO) {
       e[1 + f] = -1;
       continue;
@@ -501,7 +527,7 @@ static void upload_stencils(Ctx& c) {
     kindv[(size_t)l] = kind;
     // block classes for the specialised kernels
     {
-      std::vector<int32_t> fast, slow, ufast, uslow, fix[2], gsl, rsl, url, gslow, rcl, rcslow;
+      std::vector<int32_t> fast, slow, ufast, uslow, fix[2], gsl, rsl, url, gslow, rcl, rcslow, rrl, rrslow;
       d.gs_cf = false;
       for (int s = 0; s < d.nb; ++s) {
         if (!own_slot(c, l, s)) continue;
@@ -510,6 +536,24 @@ static void upload_stencils(Ctx& c) {
         for (int f = 0; f < F; ++f)
           no_cf = no_cf && !(m.nbr[(size_t)id * 6 + f] < 0 && m.cnbr[(size_t)id * 6 + f] >= 0);
         (no_cf ? fast : slow).push_back(s);
+        if (stream_dn(c)) {  // restriction plan: every block (all-inside ones restrict exactly in-stream)
+          if (no_cf || cf_streamable_r(c, id)) {
+            int pm = 0;
+            int32_t ns[6] = {-1, -1, -1, -1, -1, -1};
+            for (int f = 0; f < F; ++f) {
+              const int nid = m.nbr[(size_t)id * 6 + f];
+              if (nid >= 0) ns[f] = m.slot_of[(size_t)nid];
+              else if (m.cnbr[(size_t)id * 6 + f] >= 0) ns[f] = -2 - d.cfoff_host[(size_t)s * F + f] / c.NT;
+              else pm |= 1 << f;
+            }
+            const int sr = srow[(size_t)s] < 0 ? 0 : srow[(size_t)s];
+            require(sr < (1 << 17), "too many interface blocks on one level for the streaming plan");
+            const int32_t e[8] = {s, (int32_t)kind[(size_t)s] | (pm << 8) | (sr << 14), ns[0], ns[1], ns[2], ns[3], ns[4], ns[5]};
+            rrl.insert(rrl.end(), e, e + 8);
+          } else {
+            rrslow.push_back(s);
+          }
+        }
         if (!no_cf && stream_dn(c)) {
           // coarse-fine faces: streamed with the faces' cfc pages as neighbour
           // codes -2 - page (stream.cuh BlockPlan), unless a cut row sits on one
@@ -583,6 +627,10 @@ static void upload_stencils(Ctx& c) {
       d.rc_plan.upload(rcl, c.stream);
       d.n_rc_slow = (int)rcslow.size();
       d.rc_slow.upload(rcslow, c.stream);
+      d.n_rr = (int)rrl.size() / 8;
+      d.rr_plan.upload(rrl, c.stream);
+      d.n_rr_slow = (int)rrslow.size();
+      d.rr_slow.upload(rrslow, c.stream);
       d.n_ufast = (int)ufast.size();
       d.n_uslow = (int)uslow.size();
       d.ufast_list.upload(ufast, c.stream);
@@ -617,6 +665,7 @@ static void upload_stencils(Ctx& c) {
         (void)cz;
         // interface blocks only: all-inside blocks restrict exactly in the stream kernel
         if (!(st.valid && st.boundary[(size_t)id]) || kindv[(size_t)l][(size_t)s] != pmgdev::KIND_IFACE) continue;
+        if (has_cf_face(c, id) && !cf_streamable_r(c, id)) continue;  // restricted by k_restrict_tile
         for (int t = 0; t < HN * HN * HN; ++t) {
           const int ii = t % HN, jj = (t / HN) % HN, kk = t / (HN * HN);
           bool need = false;

@@ -287,6 +287,11 @@ struct LevelDev {
   // the leaf blocks with a cut row on a coarse-fine face (k_record_tile)
   DevBuf<int32_t> rc_plan, rc_slow;
   int n_rc = 0, n_rc_slow = 0;
+  // streaming residual + restriction on the same levels: every block whose
+  // parents with a cut child keep clear of the coarse-fine faces (k_restrict_fix
+  // gathers cannot express those ghosts); the others by k_restrict_tile
+  DevBuf<int32_t> rr_plan, rr_slow;
+  int n_rr = 0, n_rr_slow = 0;
   DevBuf<int32_t> cutcf_ent[2];
   DevBuf<double> cutcf_gbc[2], cutcf_coef[2];
   int n_cutcf[2] = {0, 0};

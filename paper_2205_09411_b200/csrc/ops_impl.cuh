@@ -270,6 +270,46 @@ struct OpsImpl final : Ops {
       check();
       return;
     }
+    if constexpr (D == 3 && (N == 8 || N == 16)) {
+      const LevelDev& d = *c.lev[(size_t)l];
+      if (mode == RM_FUSED && (N == 8 || d.has_cf) && d.n_rr > 0) {
+        // N = 8, or coarse-fine faces: the column kernel (k_resid_stream, MODE 0)
+        // over rr_plan, coarse-fine ghosts from the staged cfc pages; parents
+        // with a cut child by k_restrict_fix, blocks with a cut row near a
+        // coarse-fine face by k_restrict_tile (both only read level l and
+        // write other parent cells), then apply_pins(l-1)
+        constexpr int ST = N == 8 ? 2 : 3, MINB = N == 8 ? 8 : 1, TTH = N == 8 ? 128 : 512;
+        using Q = QStream3<N, TTH>;
+        constexpr size_t smem = (size_t)ST * (Q::STAGE + 12 * Q::FH) * sizeof(double);
+        set_smem_attr(c, (const void*)k_resid_stream<N, ST, MINB, 0, TTH, true>, smem);
+        const int grid = std::min(d.n_rr, c.sms * MINB);
+        const LevelView Lt = Vt(c, l);
+        const bool fork = d.n_rfix > 0 || d.n_rr_slow > 0;
+        if (fork) {
+          PMG_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+          PMG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+        }
+        if (d.n_rr_slow > 0)
+          pdl_launch(k_restrict_tile<D, N, RM_FUSED>, d.n_rr_slow, TT::THREADS, 0, c.side, Lt, Vc(c, l), V(c, l - 1),
+                     c.phi_b.p, (const int32_t*)d.rr_slow.p);
+        if (d.n_rfix > 0)
+          pdl_launch(k_restrict_fix<D, N>, grid_for((long long)d.n_rfix * 8, 128), 128, 0, c.side, Lf, V(c, l - 1),
+                     (const int2*)d.rfix_list.p, (const int32_t*)d.rfix_tab.p, (const double*)d.rfix_gbc.p,
+                     d.n_rfix);
+        pdl_launch(k_resid_stream<N, ST, MINB, 0, TTH, true>, grid, Q::THR, smem, c.stream, Lt, V(c, l - 1),
+                   c.phi_b.p, (const int4*)d.rr_plan.p, d.n_rr, (Rec*)nullptr, (Rec*)nullptr, (unsigned int*)nullptr);
+        if (fork) {
+          PMG_CUDA(cudaEventRecord(c.ev_join, c.side));
+          PMG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
+        }
+        const LevelDev& dp = *c.lev[(size_t)(l - 1)];
+        if (dp.n_pin > 0)  // apply_pins(l-1)
+          pdl_launch_on(k_pin_list, grid_for(dp.n_pin, 256), 256, 0, c.stream, V(c, l - 1).phi, c.phi_b.p,
+                        (const int2*)dp.pin_list.p, dp.n_pin);
+        check();
+        return;
+      }
+    }
     if constexpr (D == 3 && N == 16) {
       const LevelDev& d = *c.lev[(size_t)l];
       if (mode == RM_FUSED && !d.has_cf && d.n_rs == d.n_own) {
@@ -298,11 +338,14 @@ struct OpsImpl final : Ops {
     }
     if constexpr (TILE) {
       if (mode == RM_RES)
-        pdl_launch(k_restrict_tile<D, N, RM_RES>, Lf.nb, TT::THREADS, 0, c.stream, Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
+        pdl_launch(k_restrict_tile<D, N, RM_RES>, Lf.nb, TT::THREADS, 0, c.stream, Lf, Vc(c, l), V(c, l - 1), c.phi_b.p,
+                   (const int32_t*)nullptr);
       else if (mode == RM_RHS)
-        pdl_launch(k_restrict_tile<D, N, RM_RHS>, Lf.nb, TT::THREADS, 0, c.stream, Lf, Vc(c, l), V(c, l - 1), c.phi_b.p);
+        pdl_launch(k_restrict_tile<D, N, RM_RHS>, Lf.nb, TT::THREADS, 0, c.stream, Lf, Vc(c, l), V(c, l - 1), c.phi_b.p,
+                   (const int32_t*)nullptr);
       else
-        pdl_launch(k_restrict_tile<D, N, RM_FUSED>, Lf.nb, TT::THREADS, 0, c.stream, Vt(c, l), Vc(c, l), V(c, l - 1), c.phi_b.p);
+        pdl_launch(k_restrict_tile<D, N, RM_FUSED>, Lf.nb, TT::THREADS, 0, c.stream, Vt(c, l), Vc(c, l), V(c, l - 1), c.phi_b.p,
+                   (const int32_t*)nullptr);
       check();
       return;
     }

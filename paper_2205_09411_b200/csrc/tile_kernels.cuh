@@ -431,9 +431,10 @@ __device__ __forceinline__ void load_both(double* __restrict__ T0, double* __res
 template <int D, int N, int MODE>
 __global__ void __launch_bounds__(Tile<D, N>::THREADS, Tile<D, N>::MINB) k_restrict_tile(LevelView Lf, LevelView Lfc,
                                                                        LevelView Lp,
-                                                                       const double* __restrict__ phi_b) {
+                                                                       const double* __restrict__ phi_b,
+                                                                       const int32_t* __restrict__ list = nullptr) {
   pdl_begin();
-  if (!owned(Lf, blockIdx.x)) return;  // multi-GPU: another rank's block
+  if (!list && !owned(Lf, blockIdx.x)) return;  // multi-GPU: another rank's block (lists hold own blocks)
   using G = Geo<D, N>;
   using TT = Tile<D, N>;
   constexpr int HN = N / 2;
@@ -444,7 +445,7 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS, Tile<D, N>::MINB) k_restr
   constexpr int STEPS = D == 3 ? ((N / 2) + ZG - 1) / ZG : (N + RPS - 1) / RPS;
   __shared__ double T0s[TT::SIZE];
   __shared__ double T1s[TT::SIZE];
-  const int slot = blockIdx.x;
+  const int slot = list ? list[blockIdx.x] : (int)blockIdx.x;
   const size_t base = (size_t)slot * G::NI;
   const uint8_t kind = Lf.kind[slot];
   const int fsr = Lf.srow[slot];
