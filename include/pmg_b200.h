@@ -143,6 +143,12 @@ int pmg_b200_cycle_kernel_count(pmg_b200_ctx* ctx, int kind);
 /* number of refinement levels and blocks per level (after set_mesh) */
 int pmg_b200_n_levels(pmg_b200_ctx* ctx);
 int pmg_b200_level_size(pmg_b200_ctx* ctx, int level);
+/* how the kernels split the blocks of `level` (after the stencils are set):
+ * out[0] blocks, out[1] coarse-fine faces, out[2] blocks of the streaming
+ * GS plan, out[3] blocks left to the block-per-CTA GS kernel (a cut row on a
+ * coarse-fine face), out[4] / out[5] the same for the leaf record, out[6] /
+ * out[7] for residual + restriction.  Diagnostics (tests, profiles). */
+int pmg_b200_level_classes(pmg_b200_ctx* ctx, int level, int32_t* out8);
 int pmg_b200_synchronize(pmg_b200_ctx* ctx);
 /* a page-locked host buffer of at least `bytes`, owned by the context and
  * reused (the C++ drop-in's PHI copies to the host go through it) */

@@ -67,7 +67,7 @@ EXPORTS = [
     "pmg_b200_prolong_correction", "pmg_b200_prolong_full", "pmg_b200_coarse_solve",
     "pmg_b200_set_have_guess", "pmg_b200_coarse_sizes", "pmg_b200_coarse_get",
     "pmg_b200_cycle_kernel_count", "pmg_b200_n_levels", "pmg_b200_level_size",
-    "pmg_b200_synchronize", "pmg_b200_time_op", "pmg_b200_coarse_info",
+    "pmg_b200_synchronize", "pmg_b200_time_op", "pmg_b200_coarse_info", "pmg_b200_level_classes",
     "pmg_b200_set_owned", "pmg_b200_level_field_ptr", "pmg_b200_restrict_only", "pmg_b200_fas_level",
     "pmg_b200_level_record", "pmg_b200_n_leaves", "pmg_b200_face_gradient", "pmg_b200_error_norms",
     "pmg_b200_write_dump", "pmg_b200_stage_field_async", "pmg_b200_commit_staged_field",
@@ -131,6 +131,7 @@ def load():
     lib.pmg_b200_coarse_sizes.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                           C.POINTER(C.c_int32)]
     lib.pmg_b200_coarse_get.argtypes = [vp, i32p, i32p, f64p, f64p, f64p, i32p, i32p]
+    lib.pmg_b200_level_classes.argtypes = [vp, C.c_int, i32p]
     lib.pmg_b200_time_op.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]
     lib.pmg_b200_coarse_info.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_double)]
     lib.pmg_b200_set_owned.argtypes = [vp, C.c_int, C.c_void_p]

@@ -63,6 +63,11 @@ class Case:
     extra: dict = field(default_factory=dict)
 
     @property
+    def refine_lsf(self):
+        """Level set the AMR band follows (the case's own unless extra['refine_lsf'])."""
+        return self.extra.get("refine_lsf", self.lsf)
+
+    @property
     def w_min(self):
         return 1.0 / (self.N * (1 << (self.max_level - 1)))
 
@@ -70,7 +75,7 @@ class Case:
         m = build_uniform(self.dim, self.lo[:self.dim], self.hi[:self.dim], self.N, self.levels)
         if self.amr_band > 0:
             band = self.amr_band
-            lsf = self.lsf
+            lsf = self.refine_lsf
             m.refine_by_criterion(self.max_level,
                                   lambda mesh, b, x: np.abs(lsf_eval(lsf, x)) < band * mesh.dx[b])
         return m
@@ -150,6 +155,13 @@ def get_case(name: str) -> Case:
                                      _sphere((0.7, 0.5, 0.5), 0.15, -1.0)])
         return Case("cfg5", 3, 16, 7, 7, lsf, rhs="gauss", rhs_amp=1e-3, seed=SEED_CFG5,
                     v_cycles=10, notes="3D 1024^3, N=16, two spheres +-1, g ~ N(0,1e-6)")
+    if name == "amrx":
+        # test mesh: the refined band follows a SHIFTED sphere, so coarse-fine
+        # faces cut through the interface of the real one (cut rows on and next
+        # to coarse-fine faces: the block-per-CTA fallbacks of the AMR path)
+        return Case("amrx", 3, 8, 3, 5, _sphere((0.5, 0.5, 0.5), 0.25, 1.0), amr_band=2.0, v_cycles=6,
+                    extra={"refine_lsf": _sphere((0.35, 0.5, 0.5), 0.2, 1.0)},
+                    notes="3D AMR base 32^3 (N=8) -> level 5, band around a shifted sphere")
     # reduced variants for quick parity (same geometry / generator, fewer levels)
     if name.startswith("cfg") and "@" in name:
         base, lv = name.split("@")

@@ -2063,6 +2063,15 @@ int pmg_b200_level_size(pmg_b200_ctx* h, int level) {
   if (!h || !h->c.have_mesh || level < 1 || level > h->c.mesh.L) return 0;
   return h->c.lev[(size_t)level]->nb;
 }
+int pmg_b200_level_classes(pmg_b200_ctx* h, int level, int32_t* out8) {
+  return guard(h, [&](Ctx& c) {
+    need_level(c, level, 1);
+    require(out8 != nullptr, "out8 is null");
+    const LevelDev& d = *c.lev[(size_t)level];
+    const int32_t v[8] = {d.nb, d.n_cf, d.n_gs, d.n_gs_slow, d.n_rc, d.n_rc_slow, d.n_rr, d.n_rr_slow};
+    for (int k = 0; k < 8; ++k) out8[k] = v[k];
+  });
+}
 int pmg_b200_time_op(pmg_b200_ctx* h, int op, int level, int reps, double* ms_avg) {
   return guard(h, [&](Ctx& c) {
     require(c.solver, "solver not created", PMG_ERR_STATE);

@@ -230,6 +230,30 @@ __global__ void __launch_bounds__(kThreads) k_cfold(LevelView L, LevelView Lc) {
   L.cfold[off + tt] = phi_ghost<D, N>(L, Lc, slot, dir, c3[0], c3[1], c3[2], self);
 }
 
+// k_cfold over the level's listed coarse-fine faces (L carries the cfc table).
+template <int D, int N>
+__global__ void __launch_bounds__(256) k_cfold_list(LevelView L, LevelView Lc, const int2* __restrict__ faces,
+                                                    int n_faces) {
+  pdl_begin();
+  using G = Geo<D, N>;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_faces * G::NT) return;
+  const int2 f = faces[t / G::NT];
+  const int tt = t % G::NT;
+  const int slot = f.x, dir = f.y, axis = dir >> 1, side = dir & 1;
+  if (!owned(L, slot)) return;
+  int c3[3] = {0, 0, 0};
+  int u = tt;
+  for (int a = 0; a < D; ++a) {
+    if (a == axis) continue;
+    c3[a] = u % N;
+    u /= N;
+  }
+  c3[axis] = side ? N - 1 : 0;
+  const double self = L.phi[G::addr(slot, c3[0], c3[1], c3[2])];
+  L.cfold[L.cfoff[slot * G::F + dir] + tt] = phi_ghost<D, N>(L, Lc, slot, dir, c3[0], c3[1], c3[2], self);
+}
+
 // The level's cfc table (pmg_dev.cuh LevelView::cfc): one thread per ghost of
 // the listed coarse-fine faces {slot, dir}.  Only level l-1 is read.
 template <int D, int N>

@@ -415,8 +415,10 @@ struct OpsImpl final : Ops {
     check();
   }
   void cfold(Ctx& c, int lc) override {
-    const LevelView& L = V(c, lc);
-    pdl_launch(k_cfold<D, N>, grid_for((long long)L.nb * G::F * G::NT), kThreads, 0, c.stream, L, Vc(c, lc));
+    const LevelDev& d = *c.lev[(size_t)lc];
+    if (d.n_cf == 0) return;
+    pdl_launch(k_cfold_list<D, N>, grid_for((long long)d.n_cf * G::NT, 256), 256, 0, c.stream, Vt(c, lc), Vc(c, lc),
+               (const int2*)d.cf_faces.p, d.n_cf);
     check();
   }
   template <bool FULL>

@@ -381,6 +381,14 @@ class MgSolver:
             self.dev._check(-k)
         return k
 
+    def level_classes(self, level):
+        """How the kernels split the blocks of ``level`` (pmg_b200_level_classes)."""
+        out = np.zeros(8, np.int32)
+        self.dev._check(self.lib.pmg_b200_level_classes(self.h, level, out))
+        keys = ("blocks", "cf_faces", "gs_stream", "gs_tile", "record_stream", "record_tile",
+                "restrict_stream", "restrict_tile")
+        return dict(zip(keys, (int(v) for v in out)))
+
     def coarse_info(self):
         """(iterations, relative residual) of the last BiCGStab coarse solve."""
         it, rel = C.c_int32(), C.c_double()

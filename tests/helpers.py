@@ -16,7 +16,7 @@ def oracle_for_case(case, mesh, which="ref"):
     o = Oracle(case.dim, case.N, case.lo[:case.dim], case.hi[:case.dim], which)
     o.build_uniform(case.levels)
     if case.amr_band > 0:
-        o.refine_band(case.lsf.as_descs(), case.amr_band, case.max_level)
+        o.refine_band(case.refine_lsf.as_descs(), case.amr_band, case.max_level)
     assert o.n_blocks == mesh.n_blocks
     for d in range(2 * case.dim):
         o.set_face_bc(d, 0, 0.0)

@@ -38,7 +38,7 @@ def _same(a, b, what):
                               f"gpu {a[bad][0]!r} oracle {b[bad][0]!r}")
 
 
-@pytest.mark.parametrize("name", ["cfg1@4", "cfg2@3", "cfg3@5", "cfg4@3"])
+@pytest.mark.parametrize("name", ["cfg1@4", "cfg2@3", "cfg3@5", "cfg4@3", "amrx"])
 def test_operators_bit_exact(name):
     case = cfgs.get_case(name)
     mesh = case.build_mesh()
@@ -89,6 +89,21 @@ def test_operators_bit_exact(name):
     cmp(VAR_PHI, "prolong_full", L)
 
 
+def test_amr_block_classes():
+    """cfg3 streams every block; the amrx mesh (coarse-fine faces through the
+    interface) also exercises the block-per-CTA fallbacks."""
+    for name, want_tile in (("cfg3@5", False), ("amrx", True)):
+        case = cfgs.get_case(name)
+        o, dev, sol, mesh, st = setup_pair(case)
+        L = mesh.n_levels
+        cl = sol.level_classes(L)
+        assert cl["blocks"] == len(mesh.level_blocks(L)) and cl["cf_faces"] > 0
+        assert cl["gs_stream"] > 0 and cl["record_stream"] > 0 and cl["restrict_stream"] > 0
+        tiles = cl["gs_tile"], cl["record_tile"], cl["restrict_tile"]
+        assert all(t > 0 for t in tiles) if want_tile else tiles == (0, 0, 0), cl
+        assert cl["restrict_stream"] + cl["restrict_tile"] == cl["blocks"]
+
+
 def _run_cycles(case, which="ref", gpu_stencils=False, threads=1):
     o, dev, sol, mesh, st = setup_pair(case, which=which, gpu_stencils=gpu_stencils, threads=threads)
     D, N = case.dim, case.N
@@ -113,7 +128,7 @@ def _run_cycles(case, which="ref", gpu_stencils=False, threads=1):
     return max_rel_diff(pa, pb), hist
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2@4", "cfg3@5", "cfg4@4"])
+@pytest.mark.parametrize("name", ["cfg1", "cfg2@4", "cfg3@5", "cfg4@4", "amrx"])
 def test_cycles_match_oracle(name):
     case = cfgs.get_case(name)
     rel, hist = _run_cycles(case)
