@@ -162,6 +162,10 @@ def get_case(name: str) -> Case:
         return Case("amrx", 3, 8, 3, 5, _sphere((0.5, 0.5, 0.5), 0.25, 1.0), amr_band=2.0, v_cycles=6,
                     extra={"refine_lsf": _sphere((0.35, 0.5, 0.5), 0.2, 1.0)},
                     notes="3D AMR base 32^3 (N=8) -> level 5, band around a shifted sphere")
+    if name == "amrx16":  # the same with 16^3 blocks (the N = 16 kernels' coarse-fine paths)
+        return Case("amrx16", 3, 16, 2, 4, _sphere((0.5, 0.5, 0.5), 0.25, 1.0), amr_band=2.0, v_cycles=6,
+                    extra={"refine_lsf": _sphere((0.35, 0.5, 0.5), 0.2, 1.0)},
+                    notes="3D AMR base 32^3 (N=16) -> level 4, band around a shifted sphere")
     # reduced variants for quick parity (same geometry / generator, fewer levels)
     if name.startswith("cfg") and "@" in name:
         base, lv = name.split("@")

@@ -54,6 +54,18 @@ struct OpsImpl final : Ops {
   }
 
   void check() { PMG_CUDA(cudaGetLastError()); }
+  // k_resid_stream with coarse-fine support (MODE 0 restriction, 1 record) over `plan`
+  template <int ST, int MINB, int MODE, int TTH>
+  void launch_qs(Ctx& c, int grid, const LevelView& Lf, const LevelView& Lp, const int32_t* plan, int n) {
+    if constexpr (D == 3 && (N == 8 || N == 16)) {
+      using Q = QStream3<N, TTH>;
+      constexpr size_t smem = (size_t)ST * (Q::STAGE + 12 * Q::FH) * sizeof(double);
+      set_smem_attr(c, (const void*)k_resid_stream<N, ST, MINB, MODE, TTH, true>, smem);
+      pdl_launch(k_resid_stream<N, ST, MINB, MODE, TTH, true>, grid, Q::THR, smem, c.stream, Lf, Lp, c.phi_b.p,
+                 (const int4*)plan, n, MODE == 1 ? c.partial.p : (Rec*)nullptr, MODE == 1 ? c.rec.p : (Rec*)nullptr,
+                 (unsigned int*)nullptr);
+    }
+  }
 
   void gs(Ctx& c, int l, int parity) override {
     const LevelView& L = V(c, l);
@@ -278,10 +290,7 @@ struct OpsImpl final : Ops {
         // with a cut child by k_restrict_fix, blocks with a cut row near a
         // coarse-fine face by k_restrict_tile (both only read level l and
         // write other parent cells), then apply_pins(l-1)
-        constexpr int ST = N == 8 ? 2 : 3, MINB = N == 8 ? 8 : 1, TTH = N == 8 ? 128 : 512;
-        using Q = QStream3<N, TTH>;
-        constexpr size_t smem = (size_t)ST * (Q::STAGE + 12 * Q::FH) * sizeof(double);
-        set_smem_attr(c, (const void*)k_resid_stream<N, ST, MINB, 0, TTH, true>, smem);
+        constexpr int MINB = N == 8 ? 8 : 1;
         const int grid = std::min(d.n_rr, c.sms * MINB);
         const LevelView Lt = Vt(c, l);
         const bool fork = d.n_rfix > 0 || d.n_rr_slow > 0;
@@ -296,8 +305,9 @@ struct OpsImpl final : Ops {
           pdl_launch(k_restrict_fix<D, N>, grid_for((long long)d.n_rfix * 8, 128), 128, 0, c.side, Lf, V(c, l - 1),
                      (const int2*)d.rfix_list.p, (const int32_t*)d.rfix_tab.p, (const double*)d.rfix_gbc.p,
                      d.n_rfix);
-        pdl_launch(k_resid_stream<N, ST, MINB, 0, TTH, true>, grid, Q::THR, smem, c.stream, Lt, V(c, l - 1),
-                   c.phi_b.p, (const int4*)d.rr_plan.p, d.n_rr, (Rec*)nullptr, (Rec*)nullptr, (unsigned int*)nullptr);
+        // 128-thread CTAs, eight per SM, two stages (three stages or 64-thread CTAs measured slower)
+        if constexpr (N == 8) launch_qs<2, 8, 0, 128>(c, grid, Lt, V(c, l - 1), d.rr_plan.p, d.n_rr);
+        else launch_qs<3, 1, 0, 512>(c, grid, Lt, V(c, l - 1), d.rr_plan.p, d.n_rr);
         if (fork) {
           PMG_CUDA(cudaEventRecord(c.ev_join, c.side));
           PMG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
@@ -497,10 +507,7 @@ struct OpsImpl final : Ops {
         // on a coarse-fine face by k_record_tile.  Partials: [0, G) streaming
         // CTAs, [G, G + g1) / [.., + g2) the cut-row CTAs, then one per listed
         // block; folded in that order.
-        constexpr int ST = 2, MINB = N == 8 ? 8 : 1, TTH = N == 8 ? 128 : 512;
-        using Q = QStream3<N, TTH>;
-        constexpr size_t smem = (size_t)ST * (Q::STAGE + 12 * Q::FH) * sizeof(double);
-        set_smem_attr(c, (const void*)k_resid_stream<N, ST, MINB, 1, TTH, true>, smem);
+        constexpr int MINB = N == 8 ? 8 : 1;
         const int grid = std::min(d.n_rc, c.sms * MINB);
         const int nc1 = d.n_cut[0] + d.n_cut[1], nc2 = d.n_cutcf[0] + d.n_cutcf[1];
         const int g1 = nc1 > 0 ? (int)grid_for(nc1, 256) : 0, g2 = nc2 > 0 ? (int)grid_for(nc2, 256) : 0;
@@ -520,8 +527,9 @@ struct OpsImpl final : Ops {
           pdl_launch(k_record_cut<D>, g2, 256, 0, c.side, L, c.phi_b.p, d.cutcf_ent[0].p, d.cutcf_gbc[0].p,
                      d.n_cutcf[0], d.cutcf_ent[1].p, d.cutcf_gbc[1].p, d.n_cutcf[1], G::NI,
                      c.partial.p + grid + g1);
-        pdl_launch(k_resid_stream<N, ST, MINB, 1, TTH, true>, grid, Q::THR, smem, c.stream, Lt, Lt, c.phi_b.p,
-                   (const int4*)d.rc_plan.p, d.n_rc, c.partial.p, c.rec.p, (unsigned int*)nullptr);
+        // 128-thread CTAs, eight per SM, two stages (three stages or 64-thread CTAs measured slower)
+        if constexpr (N == 8) launch_qs<2, 8, 1, 128>(c, grid, Lt, Lt, d.rc_plan.p, d.n_rc);
+        else launch_qs<2, 1, 1, 512>(c, grid, Lt, Lt, d.rc_plan.p, d.n_rc);
         if (fork) {
           PMG_CUDA(cudaEventRecord(c.ev_join, c.side));
           PMG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));

@@ -38,7 +38,7 @@ def _same(a, b, what):
                               f"gpu {a[bad][0]!r} oracle {b[bad][0]!r}")
 
 
-@pytest.mark.parametrize("name", ["cfg1@4", "cfg2@3", "cfg3@5", "cfg4@3", "amrx"])
+@pytest.mark.parametrize("name", ["cfg1@4", "cfg2@3", "cfg3@5", "cfg4@3", "amrx", "amrx16"])
 def test_operators_bit_exact(name):
     case = cfgs.get_case(name)
     mesh = case.build_mesh()
@@ -92,7 +92,7 @@ def test_operators_bit_exact(name):
 def test_amr_block_classes():
     """cfg3 streams every block; the amrx mesh (coarse-fine faces through the
     interface) also exercises the block-per-CTA fallbacks."""
-    for name, want_tile in (("cfg3@5", False), ("amrx", True)):
+    for name, want_tile in (("cfg3@5", False), ("amrx", True), ("amrx16", True)):
         case = cfgs.get_case(name)
         o, dev, sol, mesh, st = setup_pair(case)
         L = mesh.n_levels
@@ -128,7 +128,7 @@ def _run_cycles(case, which="ref", gpu_stencils=False, threads=1):
     return max_rel_diff(pa, pb), hist
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2@4", "cfg3@5", "cfg4@4", "amrx"])
+@pytest.mark.parametrize("name", ["cfg1", "cfg2@4", "cfg3@5", "cfg4@4", "amrx", "amrx16"])
 def test_cycles_match_oracle(name):
     case = cfgs.get_case(name)
     rel, hist = _run_cycles(case)
