@@ -143,39 +143,19 @@ static void upload_bc(Ctx& c) {
 // the level's row arrays and the addresses of its 2D neighbour values
 // (same block, same-level neighbour block, or a physical-face code).
 // 3D N = 8 / 16: the streaming GS kernel also takes blocks with coarse-fine
-// faces (their ghosts from the cfc table), unless a cut row sits on such a
-// face (k_gs_cut's gather entries cannot express a coarse-fine ghost)
+// faces (their ghosts from the cfc table), unless a cut row sits near such a
+// face (cf_streamable below)
 static bool stream_dn(const Ctx& c) { return c.dim == 3 && (c.N == 8 || c.N == 16); }
 static bool has_cf_face(const Ctx& c, int id) {
   for (int f = 0; f < c.F; ++f)
     if (c.mesh.nbr[(size_t)id * 6 + f] < 0 && c.mesh.cnbr[(size_t)id * 6 + f] >= 0) return true;
   return false;
 }
+// The criterion: no cut row within two cells of a coarse-fine face -- the
+// 2x2x2 children of a parent with a cut child are gathered by k_restrict_fix,
+// whose entries (like k_gs_cut's) cannot express such a ghost.  One criterion
+// for the GS, record, restriction and FAS plans and the cut-row tables.
 static bool cf_streamable(const Ctx& c, int id) {
-  const HostStencils& st = c.st;
-  if (!stream_dn(c) || !has_cf_face(c, id)) return false;
-  if (!st.valid || !st.boundary[(size_t)id]) return true;
-  const int N = c.N, r0 = st.row_start[(size_t)id];
-  for (int f = 0; f < c.F; ++f) {
-    if (!(c.mesh.nbr[(size_t)id * 6 + f] < 0 && c.mesh.cnbr[(size_t)id * 6 + f] >= 0)) continue;
-    const int ax = f >> 1, fix = (f & 1) ? N - 1 : 0;
-    for (int v = 0; v < N; ++v)
-      for (int u = 0; u < N; ++u) {
-        int q[3];
-        q[ax] = fix;
-        q[ax == 0 ? 1 : 0] = u;
-        q[ax == 2 ? 1 : 2] = v;
-        const int r = st.row_at((size_t)id, (size_t)(q[0] + N * (q[1] + N * q[2])));
-        if (r >= 0 && st.mask[(size_t)(r0 + r)] != PMG_INSIDE) return false;
-      }
-  }
-  return true;
-}
-
-// ... and for the streamed restriction: no cut row within two cells of a
-// coarse-fine face (the 2x2x2 children of a parent with a cut child are
-// gathered by k_restrict_fix, whose entries cannot express such a ghost)
-static bool cf_streamable_r(const Ctx& c, int id) {
   const HostStencils& st = c.st;
   if (!stream_dn(c) || !has_cf_face(c, id)) return false;
   if (!st.valid || !st.boundary[(size_t)id]) return true;
@@ -537,7 +517,7 @@ static void upload_stencils(Ctx& c) {
           no_cf = no_cf && !(m.nbr[(size_t)id * 6 + f] < 0 && m.cnbr[(size_t)id * 6 + f] >= 0);
         (no_cf ? fast : slow).push_back(s);
         if (stream_dn(c)) {  // restriction plan: every block (all-inside ones restrict exactly in-stream)
-          if (no_cf || cf_streamable_r(c, id)) {
+          if (no_cf || cf_streamable(c, id)) {
             int pm = 0;
             int32_t ns[6] = {-1, -1, -1, -1, -1, -1};
             for (int f = 0; f < F; ++f) {
@@ -665,7 +645,7 @@ static void upload_stencils(Ctx& c) {
         (void)cz;
         // interface blocks only: all-inside blocks restrict exactly in the stream kernel
         if (!(st.valid && st.boundary[(size_t)id]) || kindv[(size_t)l][(size_t)s] != pmgdev::KIND_IFACE) continue;
-        if (has_cf_face(c, id) && !cf_streamable_r(c, id)) continue;  // restricted by k_restrict_tile
+        if (has_cf_face(c, id) && !cf_streamable(c, id)) continue;  // restricted by k_restrict_tile
         for (int t = 0; t < HN * HN * HN; ++t) {
           const int ii = t % HN, jj = (t / HN) % HN, kk = t / (HN * HN);
           bool need = false;

@@ -411,9 +411,11 @@ struct OpsImpl final : Ops {
     if constexpr (TILE) {
       if (L.nb > kSmallLevel) {
         if (f)
-          pdl_launch(k_fas_tile<D, N, true>, L.nb, TT::THREADS, 0, c.stream, Vt(c, lc), Vc(c, lc), c.phi_b.p);
+          pdl_launch(k_fas_tile<D, N, true>, L.nb, TT::THREADS, 0, c.stream, Vt(c, lc), Vc(c, lc), c.phi_b.p,
+                     (const int32_t*)nullptr);
         else
-          pdl_launch(k_fas_tile<D, N, false>, L.nb, TT::THREADS, 0, c.stream, L, Vc(c, lc), c.phi_b.p);
+          pdl_launch(k_fas_tile<D, N, false>, L.nb, TT::THREADS, 0, c.stream, L, Vc(c, lc), c.phi_b.p,
+                     (const int32_t*)nullptr);
         check();
         return;
       }

@@ -569,15 +569,16 @@ __global__ void __launch_bounds__(Tile<D, N>::THREADS, Tile<D, N>::MINB) k_restr
 // ------------------------------------------------------------------ FAS + OLD snapshot
 template <int D, int N, bool FAS>
 __global__ void __launch_bounds__(Tile<D, N>::THREADS, Tile<D, N>::MINB) k_fas_tile(LevelView L, LevelView Lc,
-                                                                  const double* __restrict__ phi_b) {
+                                                                  const double* __restrict__ phi_b,
+                                                                  const int32_t* __restrict__ list) {
   pdl_begin();
-  if (!owned(L, blockIdx.x)) return;  // multi-GPU: another rank's block
+  if (!list && !owned(L, blockIdx.x)) return;  // multi-GPU: another rank's block (lists hold own blocks)
   using G = Geo<D, N>;
   using TT = Tile<D, N>;
   using O = Own<D, N>;
   __shared__ double T0[TT::SIZE];
   __shared__ double T1[TT::SIZE];
-  const int slot = blockIdx.x;
+  const int slot = list ? list[blockIdx.x] : (int)blockIdx.x;
   const size_t base = (size_t)slot * G::NI;
   if (!FAS || L.leaf[slot]) {
     for (int ce = threadIdx.x; ce < G::NI; ce += blockDim.x) L.old[base + ce] = L.phi[base + ce];
