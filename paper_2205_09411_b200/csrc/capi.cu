@@ -668,6 +668,8 @@ static void upload_stencils(Ctx& c) {
       LevelDev& d = *c.lev[(size_t)l];
       std::vector<int32_t> pp;
       bool ok = true;
+      d.pp_cf = false;
+      const LevelDev& dpar = *c.lev[(size_t)(l - 1)];
       for (int s = 0; s < d.nb && ok; ++s) {
         if (kindv[(size_t)l][(size_t)s] == pmgdev::KIND_ALL_INSIDE || !own_slot(c, l, s)) continue;
         const int id = m.slots[(size_t)l][(size_t)s];
@@ -679,7 +681,15 @@ static void upload_stencils(Ctx& c) {
           const int dir = 2 * ax + cb;
           const int nid = m.nbr[(size_t)pid * 6 + dir];
           if (nid >= 0) pn[ax] = m.slot_of[(size_t)nid];
-          else if (m.cnbr[(size_t)pid * 6 + dir] >= 0) ok = false;
+          else if (m.cnbr[(size_t)pid * 6 + dir] >= 0) {
+            // the parent's face is coarse-fine: its cfc / cfold page (3D N = 8 / 16 kernels only)
+            if (stream_dn(c)) {
+              pn[ax] = -2 - dpar.cfoff_host[(size_t)m.slot_of[(size_t)pid] * F + dir] / c.NT;
+              d.pp_cf = true;
+            } else {
+              ok = false;
+            }
+          }
           else pn[ax] = -1;
         }
         int edge = 0;  // a face of the fine block without a same-level neighbour

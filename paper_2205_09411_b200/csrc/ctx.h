@@ -255,6 +255,7 @@ struct LevelDev {
   int n_pin = 0;
   DevBuf<int32_t> pp_plan;    // streaming prolongation plan (stream.cuh), -1: level not eligible
   int n_pp = -1;
+  bool pp_cf = false;         // some parent-octant face in pp_plan is coarse-fine (CF kernel)
   DevBuf<int32_t> tab;        // small levels: per-cell row code + neighbour addresses (small.cuh)
   DevBuf<double> tgbc;
   bool has_tab = false;

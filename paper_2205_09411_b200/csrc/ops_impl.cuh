@@ -2,6 +2,7 @@
 // (Dim, N) in ops_<D>_<N>.cu so the variants compile in parallel.
 #pragma once
 #include <algorithm>
+#include <type_traits>
 #include "ctx.h"
 #include "stencil_build.cuh"
 #include "tile_kernels.cuh"
@@ -435,15 +436,33 @@ struct OpsImpl final : Ops {
   }
   template <bool FULL>
   void launch_prolong_stream(Ctx& c, int l) {
-    if constexpr (D == 3 && N == 16) {
+    if constexpr (D == 3 && (N == 8 || N == 16)) {
       const LevelDev& d = *c.lev[(size_t)l];
-      constexpr int ST = 2, MINB = 2;
-      constexpr size_t smem = (size_t)ST * PStream3<N>::STAGE * sizeof(double);
-      set_smem_attr(c, (const void*)k_prolong_stream<N, ST, MINB, FULL>, smem);
-      const int grid = std::min(d.n_pp, c.sms * MINB);
-      pdl_launch_on(k_prolong_stream<N, ST, MINB, FULL>, grid, PStream3<N>::THR, smem, c.stream, 
-          V(c, l), V(c, l - 1), (const int4*)d.pp_plan.p, d.n_pp, FULL ? -1 : c.prolong_dead,
-          1);
+      const int dead = FULL ? -1 : c.prolong_dead;
+      // N = 8: 128-thread CTAs, eight per SM; CF kernel: parents with coarse-fine
+      // faces take their ghosts from level l-1's cfc / cfold pages
+      auto run_cf = [&](auto st, auto minb, auto th) {
+        constexpr int ST = decltype(st)::value, MINB = decltype(minb)::value, TH = decltype(th)::value;
+        using P = PStream3<N, TH>;
+        constexpr size_t smem = (size_t)ST * P::STAGE * sizeof(double);
+        set_smem_attr(c, (const void*)k_prolong_stream<N, ST, MINB, FULL, TH, true>, smem);
+        const int grid = std::min(d.n_pp, c.sms * MINB);
+        pdl_launch_on(k_prolong_stream<N, ST, MINB, FULL, TH, true>, grid, P::THR, smem, c.stream, V(c, l),
+                      Vt(c, l - 1), (const int4*)d.pp_plan.p, d.n_pp, dead, 1);
+      };
+      using I2 = std::integral_constant<int, 2>;
+      if constexpr (N == 8) {
+        run_cf(I2{}, std::integral_constant<int, 8>{}, std::integral_constant<int, 128>{});
+      } else if (d.pp_cf) {
+        run_cf(I2{}, I2{}, std::integral_constant<int, 0>{});
+      } else {
+        constexpr int ST = 2, MINB = 2;
+        constexpr size_t smem = (size_t)ST * PStream3<N>::STAGE * sizeof(double);
+        set_smem_attr(c, (const void*)k_prolong_stream<N, ST, MINB, FULL>, smem);
+        const int grid = std::min(d.n_pp, c.sms * MINB);
+        pdl_launch_on(k_prolong_stream<N, ST, MINB, FULL>, grid, PStream3<N>::THR, smem, c.stream,
+                      V(c, l), V(c, l - 1), (const int4*)d.pp_plan.p, d.n_pp, dead, 1);
+      }
       if (d.n_pin > 0)  // inside cells were interpolated too: restore their pins
         pdl_launch_on(k_pin_list, grid_for(d.n_pin, 256), 256, 0, c.stream, V(c, l).phi, c.phi_b.p,
                                                                   (const int2*)d.pin_list.p, d.n_pin);
@@ -455,12 +474,12 @@ struct OpsImpl final : Ops {
     const LevelView& Lp = V(c, l - 1);
     const LevelView& Lpp = Vc(c, l - 1);
     const unsigned g = grid_for((long long)Lf.nb * G::NI);
-    if constexpr (D == 3 && N == 16) {
+    if constexpr (D == 3 && (N == 8 || N == 16)) {
       const LevelDev& d = *c.lev[(size_t)l];
       // streaming down to 64-block levels too (one block per CTA: 6.9 vs 10.1 us
       // for the generic per-cell kernel's chain of ghost lookups at 64 blocks,
       // but slower at 8)
-      if (Lf.nb > 16 && d.n_pp > 0) {
+      if (Lf.nb > (N == 16 ? 16 : kSmallLevel) && d.n_pp > 0) {
         if (full) launch_prolong_stream<true>(c, l);
         else launch_prolong_stream<false>(c, l);
         check();

@@ -1273,19 +1273,20 @@ __global__ void __launch_bounds__(128) k_gs_cut(LevelView L, const int32_t* __re
 // (physical-face ghosts 2 bc - f1 evaluated for phi and old separately, as the
 // reference's filled ghosts are).  Inside cells are interpolated too and
 // re-pinned by k_pin_list afterwards (they always hold their pin).
-template <int N>
+template <int N, int TH = 0>
 struct PStream3 {
   static constexpr int HN = N / 2;
   static constexpr int H = N * N * N / 2;
   static constexpr int PE = HN + 2, PS = PE * PE * PE;
-  static constexpr int THR = H < 512 ? H : 512;
+  static constexpr int THR = TH ? TH : (H < 512 ? H : 512);
   static constexpr int PER = H / THR;
   static constexpr int OF = 0, ORP = 2 * H, ORO = ORP + PS;
   static constexpr int STAGE = ORO + PS;
 };
 
 // plan entry: {fine slot, parent slot, octant bits, parent neighbour across the
-// octant's outer face per axis (-1 physical), kind, 0}
+// octant's outer face per axis (-1 physical; CF kernels: -2 - p = a coarse-fine
+// face of the parent whose cfc / cfold page is p), kind, edge}
 //
 // Tile element q (natural 10^3 order over the octant and its one-cell halo)
 // of this thread, decoded once per kernel: the thread owns q = t + e*THR.
@@ -1335,9 +1336,9 @@ __device__ __forceinline__ size_t pr_addr(const PElem& E, int oct, int P, const 
     if (nb >= 0) {
       blk = nb;
       v = E.side ? 0 : N - 1;
-    } else {  // physical face: the parent's own boundary cell, made a ghost after the wait
+    } else {  // physical (or coarse-fine) face: the parent's own boundary cell, made a ghost after the wait
       v = E.side ? N - 1 : 0;
-      phys = 1;
+      phys = nb == -1 ? 1 : 2;
     }
     x0 = ax == 0 ? v : x0;
     x1 = ax == 1 ? v : x1;
@@ -1346,10 +1347,10 @@ __device__ __forceinline__ size_t pr_addr(const PElem& E, int oct, int P, const 
   return (size_t)blk * NI + (size_t)(((x0 + x1 + x2) & 1) * H) + (size_t)((x0 + N * (x1 + N * x2)) >> 1);
 }
 
-template <int N, bool FULL, int NE>
+template <int N, bool FULL, int NE, int TH = 0>
 __device__ __forceinline__ void pr_issue_async(const LevelView& Lp, const int4& a, const int4& b, double* st,
                                                const PElem* E) {
-  using S = PStream3<N>;
+  using S = PStream3<N, TH>;
   const int pn[3] = {a.w, b.x, b.y};
 #pragma unroll
   for (int e = 0; e < NE; ++e) {
@@ -1367,12 +1368,15 @@ __device__ __forceinline__ void pr_issue_async(const LevelView& Lp, const int4& 
 // of that colour -- those cells are neither read nor written.
 // rev: walk the plan backwards, so that the first post-smoothing half-sweep
 // (forward) starts on the blocks written last (still in L2).
-template <int N, int S_STAGES, int MINB, bool FULL>
-__global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(LevelView Lf, LevelView Lp,
+// CF: a parent face may be coarse-fine (Lp.cfc set and built): its PHI ghost is
+// 1/2 c + 3/4 f1 - 1/4 f2 from level l-1's cfc page and the two parent cells
+// in the tile, its OLD ghost the cfold snapshot (multigrid.hpp:394-396).
+template <int N, int S_STAGES, int MINB, bool FULL, int TH = 0, bool CF = false>
+__global__ void __launch_bounds__(PStream3<N, TH>::THR, MINB) k_prolong_stream(LevelView Lf, LevelView Lp,
                                                                           const int4* __restrict__ plan, int n,
                                                                           int dead, int rev) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // PDL: prologue before the wait
-  using S = PStream3<N>;
+  using S = PStream3<N, TH>;
   constexpr int NI = N * N * N, HN = S::HN, PE = S::PE;
   constexpr int NE = (S::PS + S::THR - 1) / S::THR;
   extern __shared__ __align__(128) double sm[];
@@ -1417,7 +1421,7 @@ __global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(Level
         bulk_g2s(st + S::OF, Lf.phi + (size_t)a.x * NI, 2 * S::H * 8, &full[s]);
       }
     }
-    pr_issue_async<N, FULL, NE>(Lp, a, b, st, E);
+    pr_issue_async<N, FULL, NE, TH>(Lp, a, b, st, E);
   };
   for (int s = 0; s < S_STAGES; ++s) {
     if (s < nmine) {
@@ -1452,6 +1456,7 @@ __global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(Level
     const int pn[3] = {a.w, b.x, b.y};
     // prep: delta (or phi for FULL) in place of the raw phi tile; physical-face
     // ghosts of phi and old evaluated separately (mesh.hpp:538-552)
+    double dv[NE];  // CF: every element's delta first (coarse-fine ghosts read raw tile values), then the stores
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
       if (E[e].q < 0) continue;
@@ -1459,7 +1464,19 @@ __global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(Level
       double vp = st[S::ORP + q], vo = FULL ? 0.0 : st[S::ORO + q];
       if (E[e].ax >= 0 && ((oct >> E[e].ax) & 1) == E[e].side) {
         const int ax = E[e].ax;
-        if ((ax == 0 ? pn[0] : ax == 1 ? pn[1] : pn[2]) < 0) {
+        const int code = ax == 0 ? pn[0] : ax == 1 ? pn[1] : pn[2];
+        if (CF && code <= -2) {
+          int phys, x0, x1, x2;
+          (void)pr_addr<N>(E[e], oct, P, pn, phys, x0, x1, x2);
+          const int tj = ax == 0 ? x1 + N * x2 : ax == 1 ? x0 + N * x2 : x0 + N * x1;
+          const size_t page = (size_t)(-2 - code) * (N * N);
+          const double cv = Lp.cfc[page + (size_t)(((x0 + x1 + x2) & 1) * (N * N / 2) + (tj >> 1))];
+          // f2: the parent cell one further inward, two tile elements from the ghost
+          const int str = ax == 0 ? 1 : ax == 1 ? PE : PE * PE;
+          const double f2 = st[S::ORP + q + (E[e].side ? -2 * str : 2 * str)];
+          vp = 0.5 * cv + 0.75 * vp - 0.25 * f2;
+          if (!FULL) vo = Lp.cfold[page + tj];
+        } else if (code < 0) {
           const int dir = 2 * ax + E[e].side;
           if (Lp.bctype[dir] != 1) {
             int phys, x0, x1, x2;
@@ -1472,7 +1489,14 @@ __global__ void __launch_bounds__(PStream3<N>::THR, MINB) k_prolong_stream(Level
           }
         }
       }
-      st[S::ORP + q] = FULL ? vp : vp - vo;
+      if (CF) dv[e] = FULL ? vp : vp - vo;
+      else st[S::ORP + q] = FULL ? vp : vp - vo;
+    }
+    if (CF) {
+      __syncthreads();  // all raw reads done
+#pragma unroll
+      for (int e = 0; e < NE; ++e)
+        if (E[e].q >= 0) st[S::ORP + E[e].q] = dv[e];
     }
     __syncthreads();
     const double* Dt = st + S::ORP;
