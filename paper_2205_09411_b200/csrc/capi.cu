@@ -1402,6 +1402,35 @@ static void set_mesh(Ctx& c, int nb, const int32_t* level, const int32_t* coords
         }
     d.n_cf = (int)(cff.size() / 2);
     if (d.n_cf > 0) d.cf_faces.upload(cff, c.stream);
+    // k_cfc_build descriptors, 8 int32 per face: {slot, dir | h0 << 3 | h1 << 4,
+    // cfc offset, coarse slot, the coarse block's same-level neighbours across
+    // the two transverse axes (-/+ of the lower, -/+ of the higher; -1 none)}.
+    // h_a: the fine block lies in the upper half of the coarse block along
+    // transverse axis a, i.e. coarse cell = (h_a N + t_a) >> 1.
+    std::vector<int32_t> cfd;
+    for (int q = 0; q < d.n_cf; ++q) {
+      const int s = cff[(size_t)2 * q], f = cff[(size_t)2 * q + 1];
+      const int id = m.slots[(size_t)l][(size_t)s];
+      const int cid = m.cnbr[(size_t)id * 6 + f];
+      const int ax = f >> 1;
+      int h[2], nn[4], u = 0;
+      for (int a = 0; a < D; ++a) {
+        if (a == ax) continue;
+        const int b = m.coords[(size_t)id * 3 + a] - 2 * m.coords[(size_t)cid * 3 + a];
+        require(b == 0 || b == 1, "coarse neighbour does not cover the fine face", PMG_ERR_TOPOLOGY);
+        h[u] = b;
+        for (int sd = 0; sd < 2; ++sd) {
+          const int nid = m.nbr[(size_t)cid * 6 + 2 * a + sd];
+          nn[2 * u + sd] = nid < 0 ? -1 : m.slot_of[(size_t)nid];
+        }
+        ++u;
+      }
+      for (; u < 2; ++u) h[u] = 0, nn[2 * u] = nn[2 * u + 1] = -1;  // 2D: one transverse axis
+      const int32_t e[8] = {s, f | (h[0] << 3) | (h[1] << 4), cfo[(size_t)s * F + f], m.slot_of[(size_t)cid],
+                            nn[0], nn[1], nn[2], nn[3]};
+      cfd.insert(cfd.end(), e, e + 8);
+    }
+    if (d.n_cf > 0) d.cf_desc.upload(cfd, c.stream);
     d.cfc.alloc((size_t)std::max(n, 1));
     d.cfc_dirty = true;
   }

@@ -273,7 +273,7 @@ struct LevelDev {
   // coarse parts of the coarse-fine ghosts (LevelView::cfc): the level's
   // coarse-fine faces {slot, dir}, the table, and whether level l-1's PHI
   // changed since the table was built
-  DevBuf<int32_t> cf_faces;
+  DevBuf<int32_t> cf_faces, cf_desc;  // cf_desc: 8 int32 per face for k_cfc_build (capi.cu set_mesh)
   int n_cf = 0;
   std::vector<int32_t> cfoff_host;  // cfoff as uploaded (the streaming plans carry the cfc page numbers)
   // streaming GS of blocks with coarse-fine faces (3D N = 8 / 16): they join

@@ -255,27 +255,67 @@ __global__ void __launch_bounds__(256) k_cfold_list(LevelView L, LevelView Lc, c
 }
 
 // The level's cfc table (pmg_dev.cuh LevelView::cfc): one thread per ghost of
-// the listed coarse-fine faces {slot, dir}.  Only level l-1 is read.
+// the listed coarse-fine faces.  Only level l-1 is read.  Each face comes with
+// a host-built descriptor (capi.cu set_mesh: fine slot, dir, page offset,
+// coarse slot, position inside the coarse block, the coarse block's transverse
+// neighbours), so a thread's loads are the descriptor and then the five
+// coarse values: cf_coarse's arithmetic (mesh.hpp:500-531) without its chain
+// of table lookups.  A transverse read that leaves the coarse block across a
+// physical face takes the generic path (val_nocf).
 template <int D, int N>
-__global__ void __launch_bounds__(256) k_cfc_build(LevelView L, LevelView Lc, const int2* __restrict__ faces,
+__global__ void __launch_bounds__(256) k_cfc_build(LevelView L, LevelView Lc, const int4* __restrict__ desc,
                                                    int n_faces, double* __restrict__ out) {
   pdl_begin();
   using G = Geo<D, N>;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_faces * G::NT) return;
-  const int2 f = faces[t / G::NT];
+  const int4 d0 = __ldg(desc + 2 * (t / G::NT)), d1 = __ldg(desc + 2 * (t / G::NT) + 1);
   const int tt = t % G::NT;
-  const int slot = f.x, dir = f.y, axis = dir >> 1, side = dir & 1;
-  int c3[3] = {0, 0, 0};
-  int u = tt;
-  for (int a = 0; a < D; ++a) {
-    if (a == axis) continue;
-    c3[a] = u % N;
-    u /= N;
+  const int dir = d0.y & 7, axis = dir >> 1, side = dir & 1;
+  const int cb = d0.w;
+  const int hb[2] = {(d0.y >> 3) & 1, (d0.y >> 4) & 1};
+  const int nn[4] = {d1.x, d1.y, d1.z, d1.w};
+  int c3[3] = {0, 0, 0};  // the fine block's interior cell next to the ghost
+  int lc[3] = {0, 0, 0};  // the coarse cell behind the ghost
+  int sgn[3] = {0, 0, 0};
+  int ua[3] = {0, 0, 0};  // transverse ordinal of axis a
+  {
+    int u = tt, k = 0;
+    for (int a = 0; a < D; ++a) {
+      if (a == axis) continue;
+      c3[a] = u % N;
+      u /= N;
+      const int gk = hb[k] * N + c3[a];
+      lc[a] = gk >> 1;
+      sgn[a] = (gk & 1) ? 1 : -1;
+      ua[a] = k++;
+    }
   }
   c3[axis] = side ? N - 1 : 0;
-  out[L.cfoff[slot * G::F + dir] + cfc_index<D, N>(axis, c3[0], c3[1], c3[2])] =
-      cf_coarse<D, N>(L, Lc, slot, dir, c3[0], c3[1], c3[2]);
+  lc[axis] = side ? 0 : N - 1;
+  double c = Lc.phi[G::addr(cb, lc[0], lc[1], lc[2])];
+  for (int a = 0; a < D; ++a) {
+    if (a == axis) continue;
+    double v[2];
+#pragma unroll
+    for (int sd = 0; sd < 2; ++sd) {
+      int q[3] = {lc[0], lc[1], lc[2]};
+      q[a] += sd ? 1 : -1;
+      if (q[a] >= 0 && q[a] < N) {
+        v[sd] = Lc.phi[G::addr(cb, q[0], q[1], q[2])];
+      } else {
+        const int ns = nn[2 * ua[a] + sd];
+        if (ns >= 0) {
+          q[a] = sd ? 0 : N - 1;
+          v[sd] = Lc.phi[G::addr(ns, q[0], q[1], q[2])];
+        } else {
+          v[sd] = val_nocf<D, N>(Lc, Lc.phi, cb, q[0], q[1], q[2]);  // physical face of the coarse block
+        }
+      }
+    }
+    c += (double)sgn[a] * (v[1] - v[0]) / 8.0;
+  }
+  out[d0.z + cfc_index<D, N>(axis, c3[0], c3[1], c3[2])] = c;
 }
 
 // ---------------------------------------------------------------- prolongation

@@ -50,7 +50,7 @@ struct OpsImpl final : Ops {
   void cfc_build(Ctx& c, int l) override {
     const LevelDev& d = *c.lev[(size_t)l];
     pdl_launch(k_cfc_build<D, N>, grid_for((long long)d.n_cf * G::NT, 256), 256, 0, c.stream, V(c, l), Vc(c, l),
-               (const int2*)d.cf_faces.p, d.n_cf, d.cfc.p);
+               (const int4*)d.cf_desc.p, d.n_cf, d.cfc.p);
     check();
   }
 
