@@ -122,7 +122,9 @@ struct OpsImpl final : Ops {
         if constexpr (D == 3 && (N == 8 || N == 16)) {
           constexpr int T256 = N == 16 ? 256 : 0;
           if (d.gs_cf) {
-            if constexpr (N == 8) launch_gs_stream<2, 8, 128, true>(c, Lt, d, parity);
+            // ten 128-thread CTAs per SM (20.6 us per finest cfg3 half-sweep; 21.3 with eight,
+            // 21.9 with three stages, 25.9 with 256-thread CTAs, 27.0 with twelve 64-thread CTAs)
+            if constexpr (N == 8) launch_gs_stream<2, 10, 128, true>(c, Lt, d, parity);
             else launch_gs_stream<kStreamStages, kStreamCtasPerSm, 0, true>(c, Lt, d, parity);
           }
           else if (T256 && d.n_gs <= c.sms * 4)  // one block per CTA, all resident at once
