@@ -17,10 +17,13 @@
   §8e); residual-type phases move both colours.  For a rank pair the cells are
   listed in one canonical order, so the sender's gather list is the
   receiver's scatter list (``HaloPlan.pairs``).
-* **Exchange** -- ``exchange()`` packs, sends / receives with
-  ``torch.distributed`` point-to-point calls (NCCL on GPUs, gloo on CPU) and
-  unpacks.  Records are reduced with ``reduce_records()`` in rank order
-  (deterministic).
+* **Exchange** -- the solver's exchange is native (``csrc/dist.h``: the halo
+  plans live on the device, pack / unpack kernels and NCCL run on the
+  context's own stream inside the cycle graph).  ``exchange()`` here is the
+  host-side statement of the same plan over ``torch.distributed``
+  point-to-point calls; the world-size-2 ``gloo`` test drives it on CPU
+  tensors (``tests/test_partition.py``).  Records are reduced with
+  ``reduce_records()`` in rank order (deterministic).
 
 Uniform (dense) levels and AMR levels without coarse-fine faces across a
 partition boundary are supported; a coarse-fine face between two ranks raises
@@ -203,6 +206,10 @@ def exchange(arr, plan: HaloPlan, level: int, colours=(0, 1), group=None):
             w.wait()
     for idx, buf in bufs:
         arr[torch.as_tensor(idx, device=arr.device)] = buf
+    if arr.is_cuda:
+        # the library's kernels run on the context's own non-blocking stream,
+        # which does not wait for torch's: finish the writes before returning
+        torch.cuda.current_stream(arr.device).synchronize()
     return arr
 
 
