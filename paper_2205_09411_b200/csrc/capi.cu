@@ -1131,6 +1131,7 @@ static void enq_dist_cycle(Ctx& c) {
     } else {  // the split level's parents: octants gathered to rank 0, pinned there
       dist_move(c, -1, 0, level_var(c, PMG_VAR_PHI, l - 1));
       dist_move(c, -1, 0, level_var(c, PMG_VAR_RHS, l - 1));
+      phi_written(c, l - 1);
       if (ds.rank == 0) {
         c.ops->pins(c, l - 1);
         enq_fas_level(c, l);
