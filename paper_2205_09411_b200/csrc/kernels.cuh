@@ -6,7 +6,7 @@
 //                   fused; FUSED variant computes r on the fly (residual_level +
 //                   restrict_level in one pass)            multigrid.hpp:374-418,697-722; stencil.hpp:225-237
 //   k_fas           g_c = L_c(phi_c) + R(r), old = phi      multigrid.hpp:383-397
-//   k_cfold         VAR_OLD ghost snapshot on coarse-fine faces (AMR)   multigrid.hpp:394-396
+//   k_cfold_list    VAR_OLD ghost snapshot on coarse-fine faces (AMR)   multigrid.hpp:394-396
 //   k_prolong       phi += interp(phi_c - old_c) / phi = interp(phi_c)  multigrid.hpp:422-438,724-783
 //   k_record        leaf residual max / sum r^2 / count, fixed-order reduction  multigrid.hpp:529-562
 //   k_pins          phi = phi_b at inside rows             stencil.hpp:225-237
@@ -205,32 +205,8 @@ __global__ void __launch_bounds__(kThreads) k_fas(LevelView L, LevelView Lc,
 }
 
 // VAR_OLD ghosts on coarse-fine faces, evaluated right after the fill that
-// precedes the snapshot.  One thread per (block, face, transverse cell).
-template <int D, int N>
-__global__ void __launch_bounds__(kThreads) k_cfold(LevelView L, LevelView Lc) {
-  pdl_begin();
-  using G = Geo<D, N>;
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long long)L.nb * G::F * G::NT) return;
-  const int slot = (int)(t / (G::F * G::NT));
-  const int dir = (int)((t / G::NT) % G::F);
-  const int tt = (int)(t % G::NT);
-  const int off = L.cfoff[slot * G::F + dir];
-  if (off < 0 || !owned(L, slot)) return;
-  const int axis = dir >> 1, side = dir & 1;
-  int c3[3] = {0, 0, 0};
-  int u = tt;
-  for (int a = 0; a < D; ++a) {
-    if (a == axis) continue;
-    c3[a] = u % N;
-    u /= N;
-  }
-  c3[axis] = side ? N - 1 : 0;
-  const double self = L.phi[G::addr(slot, c3[0], c3[1], c3[2])];
-  L.cfold[off + tt] = phi_ghost<D, N>(L, Lc, slot, dir, c3[0], c3[1], c3[2], self);
-}
-
-// k_cfold over the level's listed coarse-fine faces (L carries the cfc table).
+// precedes the snapshot (multigrid.hpp:394-396): one thread per ghost of the
+// level's listed coarse-fine faces; L carries the cfc table.
 template <int D, int N>
 __global__ void __launch_bounds__(256) k_cfold_list(LevelView L, LevelView Lc, const int2* __restrict__ faces,
                                                     int n_faces) {
@@ -271,6 +247,7 @@ __global__ void __launch_bounds__(256) k_cfc_build(LevelView L, LevelView Lc, co
   if (t >= n_faces * G::NT) return;
   const int4 d0 = __ldg(desc + 2 * (t / G::NT)), d1 = __ldg(desc + 2 * (t / G::NT) + 1);
   const int tt = t % G::NT;
+  if (!owned(L, d0.x)) return;  // multi-GPU: another rank's block (its coarse side may not be backed here)
   const int dir = d0.y & 7, axis = dir >> 1, side = dir & 1;
   const int cb = d0.w;
   const int hb[2] = {(d0.y >> 3) & 1, (d0.y >> 4) & 1};
