@@ -21,6 +21,7 @@ using namespace pmgdev;
 // streaming GS pipeline depth and residency (stream.cuh)
 constexpr int kStreamStages = 2;
 constexpr int kStreamCtasPerSm = 2;
+constexpr int kFoldThreads = 512;  // k_record_fold: ~1500 partials at most on the large levels
 
 static inline unsigned grid_for(long long n, int threads = kThreads) {
   return (unsigned)((n + threads - 1) / threads);
@@ -515,7 +516,7 @@ struct OpsImpl final : Ops {
         const int gr = (int)grid_for((long long)L.nb * G::NI, 256);
         pdl_launch(k_record_tab<D, N>, gr, 256, 0, c.stream, L, c.phi_b.p, (const int4*)d.tab.p,
                    (const double*)d.tgbc.p, c.partial.p);
-        pdl_launch(k_record_fold, 1, 256, 0, c.stream, (const Rec*)c.partial.p, gr, c.rec.p + L.level,
+        pdl_launch(k_record_fold, 1, kFoldThreads, 0, c.stream, (const Rec*)c.partial.p, gr, c.rec.p + L.level,
                    FinishArgs{});
         check();
         return;
@@ -562,7 +563,7 @@ struct OpsImpl final : Ops {
           fin = FinishArgs{c.rec.p, c.mesh.L, l, c.outbuf.p, c.h_out_dev};
           c.finished = true;
         }
-        pdl_launch(k_record_fold, 1, 256, 0, c.stream, (const Rec*)c.partial.p, grid + g1 + g2 + d.n_rc_slow,
+        pdl_launch(k_record_fold, 1, kFoldThreads, 0, c.stream, (const Rec*)c.partial.p, grid + g1 + g2 + d.n_rc_slow,
                    c.rec.p + L.level, fin);
         check();
         return;
@@ -602,7 +603,7 @@ struct OpsImpl final : Ops {
           fin = FinishArgs{c.rec.p, c.mesh.L, l, c.outbuf.p, c.h_out_dev};
           c.finished = true;
         }
-        pdl_launch(k_record_fold, 1, 256, 0, c.stream, (const Rec*)c.partial.p,
+        pdl_launch(k_record_fold, 1, kFoldThreads, 0, c.stream, (const Rec*)c.partial.p,
                    grid + gcut + d.n_slow, c.rec.p + L.level, fin);
         check();
         return;
@@ -634,7 +635,7 @@ struct OpsImpl final : Ops {
         fin = FinishArgs{c.rec.p, c.mesh.L, l, c.outbuf.p, c.h_out_dev};
         c.finished = true;
       }
-      pdl_launch(k_record_fold, 1, 256, 0, c.stream, (const Rec*)c.partial.p, d.n_uslow + d.n_ufast,
+      pdl_launch(k_record_fold, 1, kFoldThreads, 0, c.stream, (const Rec*)c.partial.p, d.n_uslow + d.n_ufast,
                  c.rec.p + L.level, fin);
       check();
       return;

@@ -1593,20 +1593,43 @@ struct FinishArgs {
   double* outbuf;     // device: stats[2], diag[2], status
   double* host_out;   // mapped pinned image of outbuf
 };
-static __global__ void __launch_bounds__(256) k_record_fold(const Rec* __restrict__ partial, int n, Rec* out,
-                                                            FinishArgs fin) {
+static __global__ void __launch_bounds__(1024) k_record_fold(const Rec* __restrict__ partial, int n, Rec* out,
+                                                             FinishArgs fin) {
   pdl_begin();
-  __shared__ double red[72];
+  __shared__ double red[3][32];
+  __shared__ double lrec[3][kMaxLevels + 1];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  // the other levels' records for the finish, in flight with the partials
+  if (fin.host_out && (int)threadIdx.x <= fin.nlev && (int)threadIdx.x <= kMaxLevels) {
+    const Rec r = fin.rec[threadIdx.x];
+    lrec[0][threadIdx.x] = r.max;
+    lrec[1][threadIdx.x] = r.sumsq;
+    lrec[2][threadIdx.x] = (double)r.count;
+  }
   double mx = 0.0, ss = 0.0, cc = 0.0;
   for (int b = threadIdx.x; b < n; b += blockDim.x) {
-    mx = fmax(mx, partial[b].max);
-    ss += partial[b].sumsq;
-    cc += (double)partial[b].count;
+    const Rec r = partial[b];
+    mx = fmax(mx, r.max);
+    ss += r.sumsq;
+    cc += (double)r.count;
   }
-  mx = block_max(mx, red);
-  ss = block_sum(ss, red);
-  cc = block_sum(cc, red);
+  // one barrier: warp butterflies, then thread 0 folds the warps in order (fixed order: deterministic)
+  mx = warp_max(mx);
+  ss = warp_sum(ss);
+  cc = warp_sum(cc);
+  if (lane == 0) {
+    red[0][wid] = mx;
+    red[1][wid] = ss;
+    red[2][wid] = cc;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
+    mx = 0.0, ss = 0.0, cc = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      mx = fmax(mx, red[0][w]);
+      ss += red[1][w];
+      cc += red[2][w];
+    }
     out->max = mx;
     out->sumsq = ss;
     out->count = (long long)cc;
@@ -1615,9 +1638,9 @@ static __global__ void __launch_bounds__(256) k_record_fold(const Rec* __restric
       long long c = 0;
       for (int l = 0; l <= fin.nlev; ++l) {
         const bool me = l == fin.level;
-        m = fmax(m, me ? mx : fin.rec[l].max);
-        s += me ? ss : fin.rec[l].sumsq;
-        c += me ? (long long)cc : fin.rec[l].count;
+        m = fmax(m, me ? mx : lrec[0][l]);
+        s += me ? ss : lrec[1][l];
+        c += me ? (long long)cc : (long long)lrec[2][l];
       }
       const double l2 = c > 0 ? sqrt(s / (double)c) : 0.0;
       fin.outbuf[0] = m;
