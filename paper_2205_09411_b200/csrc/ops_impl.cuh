@@ -113,10 +113,15 @@ struct OpsImpl final : Ops {
       if (nfix > 0)
         pdl_launch(k_gs_fix<D, N>, grid_for(nfix, 128), 128, 0, s2, L, Vc(c, l), c.phi_b.p, parity,
                                                            (const int2*)d.fix_list[parity].p, nfix);
-      if (ncut > 0)  // cut rows: disjoint from the streaming kernel's cells and inputs
+      if (ncut > 0 && ncutcf > 0)  // both cut-row tables in one launch
+        pdl_launch(k_gs_cut2<D>, grid_for(ncut + ncutcf, 128), 128, 0, s2, L, (const int32_t*)d.cut_ent[parity].p,
+                   (const double*)d.cut_gbc[parity].p, (const double*)d.cut_coef[parity].p, ncut,
+                   (const int32_t*)d.cutcf_ent[parity].p, (const double*)d.cutcf_gbc[parity].p,
+                   (const double*)d.cutcf_coef[parity].p, ncutcf);
+      else if (ncut > 0)  // cut rows: disjoint from the streaming kernel's cells and inputs
         pdl_launch(k_gs_cut<D>, grid_for(ncut, 128), 128, 0, s2, L, (const int32_t*)d.cut_ent[parity].p,
                    (const double*)d.cut_gbc[parity].p, (const double*)d.cut_coef[parity].p, ncut);
-      if (ncutcf > 0)
+      else if (ncutcf > 0)
         pdl_launch(k_gs_cut<D>, grid_for(ncutcf, 128), 128, 0, s2, L, (const int32_t*)d.cutcf_ent[parity].p,
                    (const double*)d.cutcf_gbc[parity].p, (const double*)d.cutcf_coef[parity].p, ncutcf);
       if (stream) {

@@ -1264,6 +1264,23 @@ __global__ void __launch_bounds__(128) k_gs_cut(LevelView L, const int32_t* __re
   L.phi[a] = v;
 }
 
+// k_gs_cut over two tables (the cut rows of the blocks without / with
+// coarse-fine faces) in one launch.
+template <int D>
+__global__ void __launch_bounds__(128) k_gs_cut2(LevelView L, const int32_t* __restrict__ ent0,
+                                                const double* __restrict__ gbc0, const double* __restrict__ coef0,
+                                                int n0, const int32_t* __restrict__ ent1,
+                                                const double* __restrict__ gbc1, const double* __restrict__ coef1,
+                                                int n1) {
+  pdl_begin();
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n0 + n1) return;
+  const bool first = q < n0;
+  double v;
+  const int a = gs_cut_row<D>(L, first ? ent0 : ent1, first ? gbc0 : gbc1, first ? coef0 : coef1, first ? q : q - n0, v);
+  L.phi[a] = v;
+}
+
 // ------------------------------------------------------------------ prolongation
 // prolong_correction / prolong_full (multigrid.hpp:422-438, 724-783) for 3D
 // fine blocks whose parent octant neighbourhood has no coarse-fine face.  A
