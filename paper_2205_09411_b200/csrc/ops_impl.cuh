@@ -48,11 +48,24 @@ struct OpsImpl final : Ops {
     return v;
   }
   bool cf_table() const override { return TILE; }
-  void cfc_build(Ctx& c, int l) override {
+  void cfc_build(Ctx& c, int l) override { cfc_build_on(c, l, c.stream); }
+  void cfc_build_on(Ctx& c, int l, cudaStream_t s) {
     const LevelDev& d = *c.lev[(size_t)l];
-    pdl_launch(k_cfc_build<D, N>, grid_for((long long)d.n_cf * G::NT, 256), 256, 0, c.stream, V(c, l), Vc(c, l),
+    pdl_launch(k_cfc_build<D, N>, grid_for((long long)d.n_cf * G::NT, 256), 256, 0, s, V(c, l), Vc(c, l),
                (const int4*)d.cf_desc.p, d.n_cf, d.cfc.p);
     check();
+  }
+  // Level l's stale cfc table rebuilt on the forked stream, beside a kernel
+  // that neither writes level l-1 nor reads the table (the caller forks
+  // before and joins after): off the main stream's chain of launches.
+  bool cfc_stale(Ctx& c, int l) {
+    if (l < 2 || l > c.mesh.L) return false;
+    const LevelDev& d = *c.lev[(size_t)l];
+    return d.n_cf > 0 && d.cfc_dirty;
+  }
+  void cfc_build_side(Ctx& c, int l) {
+    cfc_build_on(c, l, c.side);
+    c.lev[(size_t)l]->cfc_dirty = false;
   }
 
   void check() { PMG_CUDA(cudaGetLastError()); }
@@ -302,11 +315,14 @@ struct OpsImpl final : Ops {
         constexpr int MINB = N == 8 ? 8 : 1;
         const int grid = std::min(d.n_rr, c.sms * MINB);
         const LevelView Lt = Vt(c, l);
-        const bool fork = d.n_rfix > 0 || d.n_rr_slow > 0;
+        // level l-1's own table (read next by its FAS pass) depends on level l-2 only
+        const bool pre = cfc_stale(c, l - 1);
+        const bool fork = d.n_rfix > 0 || d.n_rr_slow > 0 || pre;
         if (fork) {
           PMG_CUDA(cudaEventRecord(c.ev_fork, c.stream));
           PMG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
         }
+        if (pre) cfc_build_side(c, l - 1);
         if (d.n_rr_slow > 0)
           pdl_launch(k_restrict_tile<D, N, RM_FUSED>, d.n_rr_slow, TT::THREADS, 0, c.side, Lt, Vc(c, l), V(c, l - 1),
                      c.phi_b.p, (const int32_t*)d.rr_slow.p);
@@ -477,6 +493,21 @@ struct OpsImpl final : Ops {
     }
   }
   void prolong(Ctx& c, int l, bool full) override {
+    // level l's table (read by the sweeps that follow) depends on level l-1,
+    // which the prolongation only reads: rebuilt beside it
+    const bool pre = TILE && cfc_stale(c, l);
+    if (pre) {
+      PMG_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+      PMG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+      cfc_build_side(c, l);
+    }
+    prolong_impl(c, l, full);
+    if (pre) {
+      PMG_CUDA(cudaEventRecord(c.ev_join, c.side));
+      PMG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
+    }
+  }
+  void prolong_impl(Ctx& c, int l, bool full) {
     const LevelView& Lf = V(c, l);
     phi_written(c, l);
     const LevelView& Lp = V(c, l - 1);
