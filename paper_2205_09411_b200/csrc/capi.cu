@@ -938,18 +938,14 @@ static void enq_restrict_only(Ctx& c, int l) {
   }
 }
 // the rest of restrict_level(l): the FAS right-hand side and OLD of level l-1
-static void enq_fas_level(Ctx& c, int l) {
-  c.ops->fas(c, l - 1, true);
-  if (c.lev[(size_t)(l - 1)]->has_cfold) c.ops->cfold(c, l - 1);
-}
+static void enq_fas_level(Ctx& c, int l) { c.ops->fas_cfold(c, l - 1, true); }
 static void enq_restrict_level(Ctx& c, int l) {
   enq_restrict_only(c, l);
   enq_fas_level(c, l);
 }
 static void enq_restrict_level_no_guess(Ctx& c, int l) {
   c.ops->restrict_(c, l, pmgdev::RM_RHS);
-  c.ops->fas(c, l - 1, false);
-  if (c.lev[(size_t)(l - 1)]->has_cfold) c.ops->cfold(c, l - 1);
+  c.ops->fas_cfold(c, l - 1, false);
 }
 static void enq_smooth(Ctx& c, int l, int steps) {
   if (c.ops->smooth(c, l, steps)) return;  // one cooperative launch (coop.cuh)

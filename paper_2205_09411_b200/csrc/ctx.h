@@ -316,6 +316,9 @@ struct Ops {
   virtual void restrict_(Ctx& c, int l, int mode) = 0;
   virtual void fas(Ctx& c, int lc, bool fas) = 0;
   virtual void cfold(Ctx& c, int lc) = 0;
+  // FAS right-hand side / OLD of level lc and, beside it on the forked stream,
+  // the OLD ghost snapshot of its coarse-fine faces (both only read PHI)
+  virtual void fas_cfold(Ctx& c, int lc, bool fas) = 0;
   virtual void cfc_build(Ctx& c, int l) = 0;
   // the block-per-CTA kernels read coarse-fine ghosts from the cfc table, so
   // residual + restriction of a level with coarse-fine faces is one pass

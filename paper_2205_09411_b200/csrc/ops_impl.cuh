@@ -451,12 +451,27 @@ struct OpsImpl final : Ops {
       pdl_launch(k_fas<D, N, false>, g, kThreads, 0, c.stream, L, Vc(c, lc), c.phi_b.p);
     check();
   }
-  void cfold(Ctx& c, int lc) override {
+  void cfold(Ctx& c, int lc) override { cfold_on(c, lc, c.stream); }
+  void cfold_on(Ctx& c, int lc, cudaStream_t s) {
     const LevelDev& d = *c.lev[(size_t)lc];
     if (d.n_cf == 0) return;
-    pdl_launch(k_cfold_list<D, N>, grid_for((long long)d.n_cf * G::NT, 256), 256, 0, c.stream, Vt(c, lc), Vc(c, lc),
+    pdl_launch(k_cfold_list<D, N>, grid_for((long long)d.n_cf * G::NT, 256), 256, 0, s, Vt(c, lc), Vc(c, lc),
                (const int2*)d.cf_faces.p, d.n_cf);
     check();
+  }
+  void fas_cfold(Ctx& c, int lc, bool f) override {
+    const LevelDev& d = *c.lev[(size_t)lc];
+    if (d.n_cf == 0) {
+      fas(c, lc, f);
+      return;
+    }
+    ensure_cfc(c, lc);  // on the main stream, before the fork
+    PMG_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+    PMG_CUDA(cudaStreamWaitEvent(c.side, c.ev_fork, 0));
+    cfold_on(c, lc, c.side);
+    fas(c, lc, f);  // may fork again: the forked stream is in order, its join then covers the snapshot too
+    PMG_CUDA(cudaEventRecord(c.ev_join, c.side));
+    PMG_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
   }
   template <bool FULL>
   void launch_prolong_stream(Ctx& c, int l) {
