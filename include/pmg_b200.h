@@ -145,7 +145,7 @@ int pmg_b200_n_levels(pmg_b200_ctx* ctx);
 int pmg_b200_level_size(pmg_b200_ctx* ctx, int level);
 /* how the kernels split the blocks of `level` (after the stencils are set):
  * out[0] blocks, out[1] coarse-fine faces, out[2] blocks of the streaming
- * GS plan, out[3] blocks left to the block-per-CTA GS kernel (a cut row on a
+ * GS plan, out[3] blocks left to the block-per-CTA GS kernel (a cut row within two cells of a
  * coarse-fine face), out[4] / out[5] the same for the leaf record, out[6] /
  * out[7] for residual + restriction.  Diagnostics (tests, profiles). */
 int pmg_b200_level_classes(pmg_b200_ctx* ctx, int level, int32_t* out8);

@@ -536,7 +536,7 @@ static void upload_stencils(Ctx& c) {
         }
         if (!no_cf && stream_dn(c)) {
           // coarse-fine faces: streamed with the faces' cfc pages as neighbour
-          // codes -2 - page (stream.cuh BlockPlan), unless a cut row sits on one
+          // codes -2 - page (stream.cuh BlockPlan), unless a cut row sits near one (cf_streamable)
           if (kind[(size_t)s] == pmgdev::KIND_ALL_INSIDE) {
             // nothing to sweep
           } else if (cf_streamable(c, id)) {

@@ -278,14 +278,14 @@ struct LevelDev {
   std::vector<int32_t> cfoff_host;  // cfoff as uploaded (the streaming plans carry the cfc page numbers)
   // streaming GS of blocks with coarse-fine faces (3D N = 8 / 16): they join
   // gs_plan with their faces' cfc pages (BlockPlan), their cut rows have
-  // their own k_gs_cut tables, and only blocks with a cut row ON a
+  // their own k_gs_cut tables, and only blocks with a cut row within two cells of a
   // coarse-fine face stay with k_gs_tile (gs_slow)
   bool gs_cf = false;
   DevBuf<int32_t> gs_slow;
   int n_gs_slow = 0;
   // streaming record (3D N = 8, or N = 16 with coarse-fine faces): the leaf
   // blocks the column kernel can take (BlockPlan entries with cfc pages), and
-  // the leaf blocks with a cut row on a coarse-fine face (k_record_tile)
+  // the leaf blocks with a cut row near a coarse-fine face (k_record_tile)
   DevBuf<int32_t> rc_plan, rc_slow;
   int n_rc = 0, n_rc_slow = 0;
   // streaming residual + restriction on the same levels: every block whose

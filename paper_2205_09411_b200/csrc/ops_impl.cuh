@@ -110,7 +110,7 @@ struct OpsImpl final : Ops {
       const bool lean_work = stream || d.n_fast > 0;
       const int ncut = stream ? d.n_cut[parity] : 0;
       // streaming: blocks with coarse-fine faces are in the plan too (gs_cf),
-      // except the few with a cut row on such a face (gs_slow)
+      // except the few with a cut row near such a face (gs_slow)
       const int n_tile = stream ? d.n_gs_slow : d.n_slow;
       const int32_t* tile_list = stream ? d.gs_slow.p : d.slow_list.p;
       const int ncutcf = stream ? d.n_cutcf[parity] : 0;
